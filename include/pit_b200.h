@@ -1,0 +1,207 @@
+/*
+ * pit_b200.h — C ABI of the B200-native PiTSBiCG hot path.
+ *
+ * The reference (/root/reference/proj) exposes this path only as a C++
+ * library API in namespace pit; it has no FFI.  Each entry point below is the
+ * flat-array, status-code replacement of one reference function, so a C++
+ * shim (paper_2203_10148_b200/host/pit_gpu.hpp, shown in INTEGRATION.md) or a
+ * ctypes binding can keep the reference's signatures:
+ *
+ *   pit_apply_F            <- pit::apply_F              include/pit/block_system.hpp:77-78
+ *   pit_assemble_rhs       <- pit::assemble_rhs         include/pit/block_system.hpp:82-83
+ *   pit_apply_G_inverse    <- pit::apply_G_inverse      include/pit/block_system.hpp:88-89
+ *   pit_initial_guess      <- pit::initial_guess        include/pit/solvers.hpp:69-70
+ *   pit_preconditioned_residual
+ *                          <- pit::preconditioned_residual include/pit/solvers.hpp:74-75
+ *   pit_sequential_fine_solve
+ *                          <- pit::sequential_fine_solve include/pit/solvers.hpp:64
+ *   pit_propagate          <- pit::Propagator::propagate / propagate_homogeneous /
+ *                             source_contribution       include/pit/propagator.hpp:38-44
+ *   pit_pitsbicg_solve     <- pit::pitsbicg_solve       include/pit/solvers.hpp:89-90
+ *   pit_parareal_solve     <- pit::parareal_solve       include/pit/solvers.hpp:82-83
+ *   pit_block_inner_product / pit_block_norm_n_inf
+ *                          <- pit::block_inner_product / block_norm_n_inf
+ *                                                       include/pit/block_system.hpp:37-40
+ *   pit_context_create     <- pit::BlockOperatorContext ctor (block_system.hpp:55-72)
+ *                             + Propagator ctors (propagator.hpp:31-36) + SpatialOperator
+ *
+ * Data layout: a block vector is caller-owned contiguous double[N*M],
+ * block-major, x-fastest (the reference's flat convention,
+ * src/dense_oracle.cpp:153-177, src/grid.cpp:35-38).  Host entry points take
+ * host pointers and copy; the *_device variants take device pointers
+ * (cudaMalloc'd, N*M doubles) and a cudaStream_t passed as void*.
+ *
+ * Errors (reference exceptions -> status codes, include/pit/errors.hpp):
+ *   PIT_ERR_INVALID_ARGUMENT  std::invalid_argument (shapes, slab index)
+ *   PIT_ERR_INNER_SOLVE       pit::InnerSolveError (non-finite implicit step)
+ *   PIT_ERR_SLAB              pit::SlabError (lowest failing slab of a fine
+ *                             batch; pit_last_error_slab() gives the index)
+ *   PIT_ERR_CONFIG            pit::ConfigError (solver tolerances)
+ *   PIT_ERR_CUDA              CUDA runtime failure / no device
+ * pit_last_error() returns the message of the last failure on this thread.
+ */
+#ifndef PIT_B200_H
+#define PIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PIT_OK = 0,
+  PIT_ERR_INVALID_ARGUMENT = 1,
+  PIT_ERR_INNER_SOLVE = 2,
+  PIT_ERR_SLAB = 3,
+  PIT_ERR_CONFIG = 4,
+  PIT_ERR_CUDA = 5
+};
+
+enum { PIT_FINE = 0, PIT_COARSE = 1 };
+enum { PIT_SOURCE_NONE = 0, PIT_SOURCE_SEPARABLE = 1 };
+enum { PIT_GUESS_COARSE_SWEEP = 0, PIT_GUESS_ZERO = 1 };
+enum { PIT_CONVERGED = 0, PIT_MAX_ITERATIONS = 1 };
+
+/* Problem description: the 1D operator A (dy/dt = -A y + f) as constant
+ * tridiagonal bands on M interior nodes of [grid_lo, grid_hi] with Dirichlet
+ * walls (assemble_spatial_operator, src/pde.cpp:55-64: lo = -mu/h^2,
+ * diag = 2mu/h^2 + r, up = -mu/h^2; any constant bands are accepted, e.g.
+ * central-difference advection), the partition (T, N), steps per slab for
+ * the fine and coarse propagators, and an optional separable source
+ * f(t, x_i) = amp * sin(omega*t + phase) * shape[i] sampled at step ends
+ * (src/propagator.cpp:61-65). */
+typedef struct pit_problem_desc {
+  int32_t dimension;      /* 1 */
+  int32_t interior;       /* M */
+  double grid_lo, grid_hi;
+  double band_lo, band_diag, band_up;
+  int32_t slab_count;     /* N >= 2 */
+  double total_time;      /* T > 0 */
+  int32_t fine_steps;     /* >= 1 */
+  int32_t coarse_steps;   /* >= 1 */
+  int32_t source_kind;    /* PIT_SOURCE_* */
+  double source_amp, source_omega, source_phase;
+  const double* source_shape; /* [M] host, copied; NULL when no source */
+  const double* initial_value;/* [M] host y0, copied */
+  int32_t device;         /* CUDA ordinal */
+  int32_t fine_mpt, fine_warps;     /* 0 = auto; else points/thread, warps/slab */
+  int32_t coarse_mpt, coarse_warps; /* 0 = auto */
+} pit_problem_desc;
+
+typedef struct pit_context pit_context;
+
+/* Mirrors pit::RunStats (include/pit/executor.hpp:24-30), accumulated. */
+typedef struct pit_run_stats {
+  int64_t fine_applications;
+  int64_t coarse_applications;
+  double fine_parallel_ms;
+  double fine_busy_ms;
+  double coarse_sequential_ms;
+} pit_run_stats;
+
+/* One convergence-history row (include/pit/solvers.hpp:17-24). */
+typedef struct pit_record {
+  int32_t k;
+  double residual_norm;
+  int64_t fine_applications;
+  int64_t coarse_applications;
+  double wall_ms;
+} pit_record;
+
+/* Solver configuration (include/pit/solvers.hpp:36-44). */
+typedef struct pit_solver_config {
+  double tolerance;          /* default 1e-8 */
+  double restart_tolerance;  /* default 1e-12 */
+  int32_t max_iterations;    /* default 200 */
+  int32_t initial_guess;     /* PIT_GUESS_* */
+} pit_solver_config;
+
+typedef struct pit_solve_info {
+  int32_t status;            /* PIT_CONVERGED / PIT_MAX_ITERATIONS */
+  int32_t restarts;
+  int32_t record_count;      /* rows written (<= max_records) */
+  int32_t total_records;     /* rows produced */
+  double min_restart_margin; /* min |<r,r~>|/eps0 at the restart test */
+  pit_run_stats stats;
+} pit_solve_info;
+
+/* Per-role step coefficients of the chunked constant-factor backward-Euler
+ * solve, exported so tests can check that the oracle's own
+ * recipe produces identical bits. */
+typedef struct pit_step_coeffs {
+  int32_t M, mpt, warps, steps;
+  double delta, lam, mu;
+  double dstar, nl, nu, inv, gneg;
+  int32_t K0, R;
+  double invR, invLast;
+  double fl[64], fu[64];
+  double pp[5], qq[5], p32, q32;
+  double plane[32], qlane[32];
+} pit_step_coeffs;
+
+const char* pit_last_error(void);
+int pit_last_error_slab(void);
+const char* pit_version(void);
+int pit_device_count(void);
+
+int pit_context_create(const pit_problem_desc* desc, pit_context** out);
+int pit_context_destroy(pit_context* ctx);
+int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing);
+/* Coefficients for role PIT_FINE / PIT_COARSE (no device needed). */
+int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out);
+/* zc correction vector (first K0 entries used), length M (no device needed). */
+int pit_step_correction(const pit_problem_desc* desc, int role, double* zc_out);
+
+/* ---- host-pointer entry points (copy in, compute, copy out) ---------- */
+int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats);
+int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats);
+int pit_apply_G_inverse(pit_context* ctx, const double* V, double* out, pit_run_stats* stats);
+int pit_initial_guess(pit_context* ctx, int policy, double* out, pit_run_stats* stats);
+int pit_preconditioned_residual(pit_context* ctx, const double* lambda, const double* rhs,
+                                double* out, pit_run_stats* stats);
+int pit_sequential_fine_solve(pit_context* ctx, double* out);
+/* role PIT_FINE/PIT_COARSE; with_source 1 = propagate, 0 = propagate_homogeneous;
+ * in == NULL means the zero field (source_contribution). */
+int pit_propagate(pit_context* ctx, int role, int with_source, const double* in, int slab,
+                  double* out);
+int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, double* out);
+int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out);
+
+/* Full solve.  lambda_out [N*M]; lambda_init optional override [N*M];
+ * first_residual_out optional [N*M]; records optional [max_records]. */
+int pit_pitsbicg_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
+                       double* lambda_out, double* first_residual_out, pit_record* records,
+                       int max_records, pit_solve_info* info);
+int pit_parareal_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
+                       double* lambda_out, double* first_residual_out, pit_record* records,
+                       int max_records, pit_solve_info* info);
+
+/* ---- device-pointer entry points (stream = cudaStream_t or NULL) ----- */
+/* Slab-range forms for slab-sharded multi-GPU drivers: blocks are indexed
+ * globally; the device arrays hold blocks [first, first+count) at offset 0,
+ * halo = block first-1 (NULL when first == 0). */
+int pit_apply_F_device(pit_context* ctx, const double* L, const double* halo, double* out,
+                       int first, int count, void* stream);
+int pit_residual_device(pit_context* ctx, const double* lambda, const double* halo,
+                        const double* rhs, double* out, int first, int count, void* stream);
+int pit_coarse_sweep_device(pit_context* ctx, const double* V, const double* W_prev, double* W,
+                            int first, int count, int with_source, int add_v, void* stream);
+int pit_block_partials_device(pit_context* ctx, const double* a, const double* b, double* partials,
+                              int count, void* stream);
+int pit_sync_status(pit_context* ctx, void* stream);
+int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
+                              const double* lambda_init_dev, double* lambda_dev,
+                              pit_record* records, int max_records, pit_solve_info* info,
+                              void* stream);
+
+/* Seeded inputs (the libstdc++ generators of the reference's tests,
+ * tests/oracles.cpp:108-122): std::mt19937_64 + uniform_real_distribution /
+ * normal_distribution, drawn in order. */
+void pit_seeded_uniform(uint64_t seed, int64_t n, double a, double b, double* out);
+void pit_seeded_normal(uint64_t seed, int64_t n, double mean, double stddev, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

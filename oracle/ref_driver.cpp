@@ -1,0 +1,277 @@
+// ref_driver.cpp — extern "C" driver over the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference sources where they lie (/root/reference/proj/src/*.cpp, minus
+// cli.cpp which needs the absent CLI11.hpp) into oracle/_ref/libpitref.so.
+// It builds BASELINE contexts through the reference's public C++ API
+// (SpatialGrid::make, SpatialOperator, Propagator, BlockOperatorContext) and
+// exposes apply_F / apply_G_inverse / assemble_rhs / initial_guess /
+// sequential_fine_solve / pitsbicg_solve / parareal_solve with flat
+// block-major double arrays, so tests and bench.py can call the reference
+// itself (golden vectors, the CPU baseline, and the loop pin).
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pit/block_system.hpp"
+#include "pit/errors.hpp"
+#include "pit/executor.hpp"
+#include "pit/pde.hpp"
+#include "pit/propagator.hpp"
+#include "pit/solvers.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefCtx {
+  std::unique_ptr<pit::BlockOperatorContext> ctx;
+  int M = 0;
+  int N = 0;
+  std::vector<double> shape;
+};
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const pit::SlabError*>(&e)) return 3;
+  if (dynamic_cast<const pit::InnerSolveError*>(&e)) return 2;
+  if (dynamic_cast<const pit::ConfigError*>(&e)) return 4;
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  return 5;
+}
+
+pit::BlockVector unflat(const RefCtx& r, const double* x) {
+  pit::BlockVector v = r.ctx->zero_vector();
+  for (int n = 0; n < r.N; ++n) {
+    auto vals = v[n].values();
+    std::memcpy(vals.data(), x + static_cast<size_t>(n) * r.M, sizeof(double) * r.M);
+  }
+  return v;
+}
+
+void flat(const RefCtx& r, const pit::BlockVector& v, double* x) {
+  for (int n = 0; n < r.N; ++n) {
+    auto vals = v[n].values();
+    std::memcpy(x + static_cast<size_t>(n) * r.M, vals.data(), sizeof(double) * r.M);
+  }
+}
+
+void copy_history(const pit::ConvergenceHistory& h, int* rec_k, double* rec_res,
+                  long* rec_fine, long* rec_coarse, int max_rec, int* nrec, int* restarts,
+                  int* converged) {
+  const int n = static_cast<int>(h.records.size());
+  *nrec = n;
+  for (int i = 0; i < n && i < max_rec; ++i) {
+    rec_k[i] = h.records[i].k;
+    rec_res[i] = h.records[i].residual_norm;
+    rec_fine[i] = h.records[i].fine_applications;
+    rec_coarse[i] = h.records[i].coarse_applications;
+  }
+  *restarts = h.restarts;
+  *converged = h.status == pit::SolveStatus::Converged ? 1 : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pitref_last_error() { return g_err.c_str(); }
+
+// 1D context on [lo, hi] with M interior points.  When use_bands == 0 the
+// operator comes from assemble_spatial_operator(diffusion, reaction)
+// (pde.cpp:45-64); otherwise a hand-built tridiagonal CSR with the given
+// bands (the route c3's central-difference advection needs, pde.hpp:36-37).
+// Source (has_source): f(t, x_i) = amp * sin(omega*t + phase) * shape[i].
+void* pitref_create_1d(int M, double lo, double hi, double diffusion, double reaction,
+                       int use_bands, double band_lo, double band_diag, double band_up,
+                       int symmetric, int N, double T, int fine_steps, int coarse_steps,
+                       const double* y0, int has_source, const double* shape, double amp,
+                       double omega, double phase) {
+  try {
+    auto r = std::make_unique<RefCtx>();
+    r->M = M;
+    r->N = N;
+    const pit::GridPtr g = pit::SpatialGrid::make(1, lo, hi, M + 2);
+    pit::SpatialOperator op = [&]() {
+      if (!use_bands) {
+        pit::PDECoefficients c;
+        c.diffusion = diffusion;
+        c.reaction = reaction;
+        return pit::assemble_spatial_operator(c, g);
+      }
+      pit::CsrMatrix a;
+      a.n = M;
+      a.row_ptr.push_back(0);
+      for (int i = 0; i < M; ++i) {
+        if (i > 0 && band_lo != 0.0) {
+          a.col.push_back(i - 1);
+          a.val.push_back(band_lo);
+        }
+        a.col.push_back(i);
+        a.val.push_back(band_diag);
+        if (i < M - 1 && band_up != 0.0) {
+          a.col.push_back(i + 1);
+          a.val.push_back(band_up);
+        }
+        a.row_ptr.push_back(static_cast<int>(a.col.size()));
+      }
+      return pit::SpatialOperator(std::move(a), g, symmetric != 0);
+    }();
+    const pit::TimeSlabPartition part(T, N);
+    pit::SourceFn src;
+    if (has_source) {
+      r->shape.assign(shape, shape + M);
+      const double h = g->spacing();
+      const std::vector<double>* sh = &r->shape;
+      src = [sh, lo, h, amp, omega, phase](double t, std::span<const double> x) {
+        const long i = std::lround((x[0] - lo) / h) - 1;
+        return amp * std::sin(omega * t + phase) * (*sh)[static_cast<size_t>(i)];
+      };
+    }
+    pit::Propagator fine(op, part, fine_steps, pit::PropagatorRole::Fine, src);
+    pit::Propagator coarse(op, part, coarse_steps, pit::PropagatorRole::Coarse, src);
+    pit::ScalarField init(g, std::vector<double>(y0, y0 + M));
+    r->ctx = std::make_unique<pit::BlockOperatorContext>(std::move(fine), std::move(coarse),
+                                                         std::move(init));
+    return r.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void pitref_destroy(void* p) { delete static_cast<RefCtx*>(p); }
+
+double pitref_spacing(void* p) {
+  return static_cast<RefCtx*>(p)->ctx->grid_ptr()->spacing();
+}
+
+int pitref_apply_F(void* p, const double* L, double* out, int workers) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    pit::SlabExecutor exec(workers);
+    flat(r, pit::apply_F(*r.ctx, unflat(r, L), exec), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int pitref_apply_G_inverse(void* p, const double* V, double* out) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    flat(r, pit::apply_G_inverse(*r.ctx, unflat(r, V)), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int pitref_assemble_rhs(void* p, double* out, int workers) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    pit::SlabExecutor exec(workers);
+    flat(r, pit::assemble_rhs(*r.ctx, exec), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int pitref_initial_guess(void* p, double* out) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    flat(r, pit::initial_guess(*r.ctx, pit::InitialGuessPolicy::CoarseSweep), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int pitref_sequential_fine(void* p, double* out) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    flat(r, pit::sequential_fine_solve(*r.ctx), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Propagator::propagate / propagate_homogeneous on one field (role 0 fine, 1 coarse).
+int pitref_propagate(void* p, int role, int with_source, const double* in, int slab,
+                     double* out) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    const pit::Propagator& prop = role == 0 ? r.ctx->fine() : r.ctx->coarse();
+    pit::ScalarField f(r.ctx->grid_ptr(), std::vector<double>(in, in + r.M));
+    pit::ScalarField y = with_source ? prop.propagate(f, slab) : prop.propagate_homogeneous(f, slab);
+    std::memcpy(out, y.values().data(), sizeof(double) * r.M);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Signature-compatible with orc_prop_fn (oracle/pit_oracle.h): lets the
+// restated solver loop run on the reference's own propagators.
+int pitref_prop_callback(void* user, int role, int with_source, const double* in, int slab,
+                         double* out) {
+  return pitref_propagate(user, role, with_source, in, slab, out);
+}
+
+static int run_solver(int which, void* p, double tol, double eps0, int max_iter, int zero_guess,
+                      int workers, const double* lambda_init, double* lambda_out,
+                      double* first_residual_out, int* rec_k, double* rec_res, long* rec_fine,
+                      long* rec_coarse, int max_rec, int* nrec, int* restarts, int* converged) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    pit::SlabExecutor exec(workers);
+    pit::SolverConfig cfg;
+    cfg.tolerance = tol;
+    cfg.restart_tolerance = eps0;
+    cfg.max_iterations = max_iter;
+    cfg.initial_guess =
+        zero_guess ? pit::InitialGuessPolicy::Zero : pit::InitialGuessPolicy::CoarseSweep;
+    pit::SolveOptions opt;
+    pit::BlockVector init = r.ctx->zero_vector();
+    if (lambda_init) {
+      init = unflat(r, lambda_init);
+      opt.initial_guess_override = &init;
+    }
+    pit::BlockVector first = r.ctx->zero_vector();
+    if (first_residual_out) opt.first_residual_out = &first;
+    pit::SolveResult res = which == 0 ? pit::pitsbicg_solve(*r.ctx, cfg, exec, opt)
+                                      : pit::parareal_solve(*r.ctx, cfg, exec, opt);
+    flat(r, res.solution, lambda_out);
+    if (first_residual_out) flat(r, first, first_residual_out);
+    copy_history(res.history, rec_k, rec_res, rec_fine, rec_coarse, max_rec, nrec, restarts,
+                 converged);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int pitref_pitsbicg(void* p, double tol, double eps0, int max_iter, int zero_guess, int workers,
+                    const double* lambda_init, double* lambda_out, double* first_residual_out,
+                    int* rec_k, double* rec_res, long* rec_fine, long* rec_coarse, int max_rec,
+                    int* nrec, int* restarts, int* converged) {
+  return run_solver(0, p, tol, eps0, max_iter, zero_guess, workers, lambda_init, lambda_out,
+                    first_residual_out, rec_k, rec_res, rec_fine, rec_coarse, max_rec, nrec,
+                    restarts, converged);
+}
+
+int pitref_parareal(void* p, double tol, double eps0, int max_iter, int zero_guess, int workers,
+                    const double* lambda_init, double* lambda_out, double* first_residual_out,
+                    int* rec_k, double* rec_res, long* rec_fine, long* rec_coarse, int max_rec,
+                    int* nrec, int* restarts, int* converged) {
+  return run_solver(1, p, tol, eps0, max_iter, zero_guess, workers, lambda_init, lambda_out,
+                    first_residual_out, rec_k, rec_res, rec_fine, rec_coarse, max_rec, nrec,
+                    restarts, converged);
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+"""BASELINE.json configurations c1-c4 (1D) as Problem1D instances.
+
+Synthetic inputs follow SURVEY.md §8(d): x_i = (i+1)h on (0,1), h = 1/(M+1);
+seeded draws use std::mt19937_64 with libstdc++ distributions (seed 1234),
+generated once on the host and shared byte-for-byte by the GPU path, the
+oracle and the reference.  No dataset is involved.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .api import (Problem1D, SeparableSource, advection_diffusion_bands,
+                  diffusion_reaction_bands, seeded_normal, seeded_uniform)
+
+SEED = 1234
+
+# name -> (M, N, T, fine_steps, coarse_steps, tol)
+SHAPES = {
+    "c1": (100, 16, 1.0, 100, 1, 1e-10),
+    "c2": (4096, 1024, 1.0, 1000, 1, 1e-10),
+    "c3": (2048, 512, 1.0, 2000, 2, 1e-10),
+    "c4": (8192, 2048, 1.0, 500, 1, 1e-10),
+}
+
+DESCRIPTIONS = {
+    "c1": "1D heat u_t=u_xx, M=100, N=16, T=1, fine 100 BE/slab, coarse 1, y0=sin(pi x)",
+    "c2": "1D heat, M=4096, N=1024, fine 1000 BE/slab, coarse 1, y0=sum_8 N(0,1) sine modes",
+    "c3": "1D adv-diff nu=1e-2 a=1 central, M=2048, N=512, fine 2000 BE/slab, coarse 2",
+    "c4": "1D react-diff r=5 + sin(2pi t)sin(pi x), M=8192, N=2048, fine 500 BE/slab, coarse 1",
+}
+
+
+def tolerance(name: str) -> float:
+    return SHAPES[name][5]
+
+
+def make(name: str, slabs: int | None = None, M: int | None = None) -> Problem1D:
+    """Problem for config `name`.  `slabs` < N keeps the slab length (and so
+    dt and steps/slab) of the full config and shortens T, giving a
+    size-reduced parity case with identical per-slab arithmetic.  `M`
+    overrides the grid (tests only)."""
+    M0, N0, T0, fs, cs, _ = SHAPES[name]
+    M = M0 if M is None else M
+    N = N0 if slabs is None else slabs
+    T = T0 if slabs is None else T0 * slabs / N0
+    h = 1.0 / (M + 1)
+    x = np.array([0.0 + (k + 1) * h for k in range(M)])
+    src = None
+    if name == "c1":
+        bands = diffusion_reaction_bands(1.0, 0.0, h)
+        y0 = np.sin(math.pi * x)
+    elif name == "c2":
+        bands = diffusion_reaction_bands(1.0, 0.0, h)
+        a = seeded_normal(SEED, 8, 0.0, 1.0)
+        y0 = np.zeros(M)
+        for k in range(8):
+            y0 += a[k] * np.sin((k + 1) * math.pi * x)
+    elif name == "c3":
+        bands = advection_diffusion_bands(1e-2, 1.0, h)
+        y0 = np.exp(-200.0 * (x - 0.3) ** 2)
+    elif name == "c4":
+        bands = diffusion_reaction_bands(1.0, 5.0, h)
+        y0 = seeded_uniform(SEED, M, -1.0, 1.0)
+        src = SeparableSource(1.0, 2.0 * math.pi, 0.0, np.sin(math.pi * x))
+    else:
+        raise KeyError(name)
+    return Problem1D(M=M, band_lo=bands[0], band_diag=bands[1], band_up=bands[2], N=N, T=T,
+                     fine_steps=fs, coarse_steps=cs, y0=np.ascontiguousarray(y0), source=src)
+
+
+def gp_steps_per_apply(p: Problem1D) -> int:
+    """Fine gridpoint-steps of one apply_F: M * steps * (N-1)."""
+    return p.M * p.fine_steps * (p.N - 1)

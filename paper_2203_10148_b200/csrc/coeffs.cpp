@@ -1,0 +1,141 @@
+// coeffs.cpp — coefficient recipe of the chunked constant-factor BE step.
+//
+// The step matrix of the reference is I + dt*A, built exactly as
+// ImplicitStepSolver does (src/pde.cpp:103-110: val *= dt, diagonal += 1).
+// For constant tridiagonal bands (lam, delta, mu) it factors as
+//     I + dt*A = Ttilde + sigma e0 e0^T,   Ttilde = (1/inv) (I - nl S)(I - nu S^T)
+// with constant unit-bidiagonal factors (the converged LU of the Toeplitz
+// matrix) and a rank-1 corner correction (Sherman-Morrison).  All derived
+// quantities are evaluated in x87 long double from the double inputs and
+// rounded once; inv is chosen so that the factored operator reproduces the
+// row sum delta + lam + mu exactly, which pins the smooth modes that survive
+// many steps.  Compiled with -ffp-contract=off.
+#include "coeffs.h"
+
+#include <cmath>
+#include <cstring>
+
+namespace pitb {
+
+namespace {
+struct L { int mpt, warps; };
+// fine/coarse layouts compiled into pit_kernels.cu (keep in sync with PIT_LAYOUTS there)
+const L kLayouts[] = {{4, 1},  {4, 2},  {4, 4},  {4, 8},   {4, 16},  {4, 32}, {8, 4},
+                      {8, 8},  {8, 16}, {8, 32}, {16, 4},  {16, 8},  {16, 16}, {16, 32},
+                      {32, 4}, {32, 8}, {32, 16}};
+}  // namespace
+
+bool layout_supported(int mpt, int warps) {
+  for (const L& l : kLayouts)
+    if (l.mpt == mpt && l.warps == warps) return true;
+  return false;
+}
+
+Layout auto_layout(int M, int role) {
+  // fine: 16 points per thread (32 registers of state) once M is large enough,
+  // so four slab CTAs fit per SM; coarse (one persistent CTA): as many
+  // threads as possible, few points each, to shorten the sequential chain.
+  static const L fine[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {32, 16}};
+  static const L coarse[] = {{4, 1}, {4, 2}, {4, 4}, {4, 8}, {4, 16}, {4, 32}, {8, 32}, {16, 32}};
+  const L* list = role == PIT_FINE ? fine : coarse;
+  const int n = 8;
+  for (int i = 0; i < n; ++i)
+    if (32 * list[i].warps * list[i].mpt >= M) return {list[i].mpt, list[i].warps};
+  return {0, 0};
+}
+
+int build_step_coeffs(int M, int mpt, int warps, int steps, double band_lo, double band_diag,
+                      double band_up, double dt, pit_step_coeffs* c, std::vector<double>* zc) {
+  typedef long double ld;
+  std::memset(c, 0, sizeof(*c));
+  if (M < 1 || mpt < 1 || mpt > 32 || warps < 1 || steps < 1) return PIT_ERR_INVALID_ARGUMENT;
+  if (32 * warps * mpt < M) return PIT_ERR_INVALID_ARGUMENT;
+  if (!(dt > 0.0)) return PIT_ERR_INVALID_ARGUMENT;
+  c->M = M;
+  c->mpt = mpt;
+  c->warps = warps;
+  c->steps = steps;
+  c->delta = band_diag * dt + 1.0;
+  c->lam = band_lo * dt;
+  c->mu = band_up * dt;
+  const ld D = c->delta, Lm = c->lam, U = c->mu;
+  const ld disc = D * D - 4.0L * Lm * U;
+  if (!(disc > 0.0L)) return PIT_ERR_INVALID_ARGUMENT;  // not diagonally dominant enough
+  const ld dst = (D + sqrtl(disc)) * 0.5L;
+  c->nl = (double)(-Lm / dst);
+  c->nu = (double)(-U / dst);
+  const ld nl = c->nl, nu = c->nu;
+  c->inv = (double)((1.0L - nl) * (1.0L - nu) / (D + Lm + U));
+  c->dstar = (double)(1.0L / (ld)c->inv);
+
+  std::vector<ld> z((size_t)M);
+  z[0] = 1.0L;
+  for (int i = 1; i < M; ++i) z[i] = nl * z[i - 1];
+  for (int i = M - 2; i >= 0; --i) z[i] = z[i] + nu * z[i + 1];
+  zc->assign((size_t)M, 0.0);
+  for (int i = 0; i < M; ++i) (*zc)[(size_t)i] = (double)z[(size_t)i];
+  {
+    const ld invd = c->inv;
+    const ld sigma = D - 1.0L / invd;
+    const ld a = sigma * invd;
+    c->gneg = (double)(-(a / (1.0L + a * z[0])));
+    const ld thr = fabsl(z[0]) * 8.470329472543003e-22L;  // 2^-70
+    int k0 = 1;
+    for (int i = M - 1; i >= 1; --i) {
+      if (fabsl(z[(size_t)i]) > thr) {
+        k0 = i + 1;
+        break;
+      }
+    }
+    c->K0 = k0;
+  }
+  {
+    ld nlp[65], nup[65];
+    nlp[0] = 1.0L;
+    nup[0] = 1.0L;
+    for (int k = 1; k <= mpt; ++k) {
+      nlp[k] = nlp[k - 1] * nl;
+      nup[k] = nup[k - 1] * nu;
+    }
+    for (int j = 0; j < mpt; ++j) {
+      c->fl[j] = (double)nlp[j + 1];
+      c->fu[j] = (double)nup[mpt - j];
+    }
+    ld pk = nlp[mpt], qk = nup[mpt];
+    for (int k = 0; k < 5; ++k) {
+      c->pp[k] = (double)pk;
+      c->qq[k] = (double)qk;
+      pk = pk * pk;
+      qk = qk * qk;
+    }
+    c->p32 = (double)pk;
+    c->q32 = (double)qk;
+    ld pl = 1.0L, ql = 1.0L;
+    for (int l = 0; l < 32; ++l) {
+      c->plane[l] = (double)pl;
+      c->qlane[31 - l] = (double)ql;
+      pl = pl * nlp[mpt];
+      ql = ql * nup[mpt];
+    }
+  }
+  {
+    const double lg = std::log2(c->dstar);
+    int R = steps;
+    if (lg > 0.0) {
+      const double r = std::floor(512.0 / lg);
+      if (r < (double)steps) R = r < 1.0 ? 1 : (int)r;
+    }
+    c->R = R;
+    const ld invd = c->inv;
+    ld p = 1.0L;
+    for (int k = 0; k < R; ++k) p = p * invd;
+    c->invR = (double)p;
+    const int last = steps % R;
+    p = 1.0L;
+    for (int k = 0; k < last; ++k) p = p * invd;
+    c->invLast = (double)p;
+  }
+  return PIT_OK;
+}
+
+}  // namespace pitb

@@ -1,0 +1,966 @@
+// pit_capi.cu — the C ABI (include/pit_b200.h): device context, the block
+// operators, and the device-resident PiTSBiCG / parareal drivers.
+//
+// The solver drivers restate the reference's control flow op for op
+// (pitsbicg_solve, src/solvers.cpp:116-220; parareal_solve, 73-114): the same
+// branches, restart rules, history rows and cost counters.  All block
+// vectors stay in HBM; per iteration only the per-block reduction partials
+// (N doubles per phase) come back to the host, where they are summed in slab
+// order exactly as block_inner_product does (block_system.cpp:76-87).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "coeffs.h"
+#include "pit_b200.h"
+#include "pit_kernels.cuh"
+
+using namespace pitb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_slab = -1;
+
+int set_err(int code, const std::string& msg, int slab = -1) {
+  g_err = msg;
+  g_err_slab = slab;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return set_err(PIT_ERR_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) +    \
+                                       " at " #expr);                                        \
+  } while (0)
+
+#define PIT_TRY(expr)      \
+  do {                     \
+    int rc_ = (expr);      \
+    if (rc_) return rc_;   \
+  } while (0)
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+struct Role {
+  pit_step_coeffs c{};
+  StepParams P{};
+  double* d_zc = nullptr;
+  double* d_ds = nullptr;
+  int mpt = 0, warps = 0;
+};
+
+}  // namespace
+
+struct pit_context {
+  pit_problem_desc desc{};
+  int M = 0, N = 0;
+  double h = 0, weight = 0;
+  bool has_source = false;
+  Role role[2];
+  double* d_shape = nullptr;
+  double* d_y0 = nullptr;
+  std::vector<double> y0;
+  int* d_status = nullptr;
+  int* h_status = nullptr;       // pinned
+  double* h_partials = nullptr;  // pinned, 3*N
+  double* d_partials = nullptr;  // 3*N
+  cudaStream_t stream = nullptr;
+  // solver work buffers (N*M each), allocated on first solve
+  double* buf[10] = {};
+  size_t nm() const { return (size_t)N * (size_t)M; }
+};
+
+namespace {
+
+int validate_desc(const pit_problem_desc* d) {
+  if (!d) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: null description");
+  if (d->dimension != 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: only dimension 1 is supported");
+  if (d->interior < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "SpatialGrid: points_per_axis must be >= 3");
+  if (!(d->grid_hi > d->grid_lo)) return set_err(PIT_ERR_INVALID_ARGUMENT, "SpatialGrid: empty extent");
+  if (!(d->total_time > 0.0))
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "TimeSlabPartition: T must be positive");
+  if (d->slab_count < 2)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "TimeSlabPartition: need at least 2 slabs");
+  if (d->fine_steps < 1 || d->coarse_steps < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: steps_per_slab must be >= 1");
+  if (!d->initial_value) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: null initial value");
+  if (d->source_kind == PIT_SOURCE_SEPARABLE && !d->source_shape)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: separable source needs a shape");
+  return PIT_OK;
+}
+
+double grid_spacing(const pit_problem_desc* d) {
+  // SpatialGrid: spacing = (hi - lo) / (points_per_axis - 1), points = M + 2 (grid.cpp:19)
+  return (d->grid_hi - d->grid_lo) / static_cast<double>(d->interior + 2 - 1);
+}
+
+int role_coeffs(const pit_problem_desc* d, int role, pit_step_coeffs* c, std::vector<double>* zc,
+                Layout* lay) {
+  const int M = d->interior;
+  const int steps = role == PIT_FINE ? d->fine_steps : d->coarse_steps;
+  // TimeSlabPartition::slab_length() = T/N; Propagator::internal_dt() = slab/steps
+  const double dt = (d->total_time / d->slab_count) / steps;
+  int mpt = role == PIT_FINE ? d->fine_mpt : d->coarse_mpt;
+  int warps = role == PIT_FINE ? d->fine_warps : d->coarse_warps;
+  if (mpt == 0 || warps == 0) {
+    Layout l = auto_layout(M, role);
+    mpt = l.mpt;
+    warps = l.warps;
+  }
+  if (mpt == 0 || !layout_supported(mpt, warps) || 32 * mpt * warps < M)
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_create: no compiled slab layout covers M=" + std::to_string(M));
+  lay->mpt = mpt;
+  lay->warps = warps;
+  if (build_step_coeffs(M, mpt, warps, steps, d->band_lo, d->band_diag, d->band_up, dt, c, zc))
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_create: step matrix I + dt*A is not factorizable with constant "
+                   "factors (needs delta^2 > 4*lam*mu)");
+  return PIT_OK;
+}
+
+void fill_params(const pit_step_coeffs& c, StepParams* P) {
+  P->nl = c.nl;
+  P->nu = c.nu;
+  P->inv = c.inv;
+  P->gneg = c.gneg;
+  P->invR = c.invR;
+  P->invLast = c.invLast;
+  for (int j = 0; j < 32; ++j) {
+    P->fl[j] = j < c.mpt ? c.fl[j] : 0.0;
+    P->fu[j] = j < c.mpt ? c.fu[j] : 0.0;
+    P->plane[j] = c.plane[j];
+    P->qlane[j] = c.qlane[j];
+  }
+  for (int s = 0; s < 5; ++s) {
+    P->pp[s] = c.pp[s];
+    P->qq[s] = c.qq[s];
+  }
+  P->p32 = c.p32;
+  P->q32 = c.q32;
+  P->M = c.M;
+  P->steps = c.steps;
+  P->R = c.R;
+  P->K0 = c.K0;
+}
+
+int check_status(pit_context* ctx, bool fine_batch) {
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const int bad = *ctx->h_status;
+  if (bad != INT_MAX) {
+    *ctx->h_status = INT_MAX;
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(int), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    const std::string what = "implicit step produced non-finite values";
+    if (fine_batch)
+      return set_err(PIT_ERR_SLAB, "slab " + std::to_string(bad) + ": " + what, bad);
+    return set_err(PIT_ERR_INNER_SOLVE, what, bad);
+  }
+  return PIT_OK;
+}
+
+// Fine batch over output blocks [first, first+count) (global indices).
+int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* halo,
+                   const double* rhs, double* out, int first, int count, cudaStream_t st) {
+  Role& R = ctx->role[PIT_FINE];
+  SlabArgs A{};
+  A.mode = mode;
+  A.status = ctx->d_status;
+  const size_t M = ctx->M;
+  int ctas;
+  if (first == 0) {
+    ctas = count - 1;
+    A.in = L;
+    A.in_shift = 0;
+    A.Lsub = L + M;
+    A.rhs = rhs ? rhs + M : nullptr;
+    A.out = out + M;
+    A.slab0 = 0;
+    A.L0 = L;
+    A.rhs0 = rhs;
+    A.out0 = out;
+    if (ctas == 0) {  // single block: block 0 only
+      if (mode == kApplyF)
+        CUDA_TRY(cudaMemcpyAsync(out, L, M * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      else
+        return set_err(PIT_ERR_INVALID_ARGUMENT, "residual over a single block is not supported");
+      return PIT_OK;
+    }
+  } else {
+    if (!halo) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: slab range needs the halo block");
+    ctas = count;
+    A.in = L;
+    A.halo = halo;
+    A.in_shift = -1;
+    A.Lsub = L;
+    A.rhs = rhs;
+    A.out = out;
+    A.slab0 = first - 1;
+  }
+  CUDA_TRY(launch_slab(R.mpt, R.warps, false, R.P, A, ctas, st));
+  return PIT_OK;
+}
+
+// Sequential sweep over output blocks [first, first+count): W_first-1 = W_prev.
+int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, const double* W_prev,
+              double* W, int first, int count, bool add_v, cudaStream_t st) {
+  Role& R = ctx->role[role];
+  const size_t M = ctx->M;
+  SweepArgs A{};
+  A.status = ctx->d_status;
+  if (first == 0) {
+    // block 0: W_0 = V_0 (G^-1) — the caller seeds block 0 otherwise
+    if (add_v && V != W)
+      CUDA_TRY(cudaMemcpyAsync(W, V, M * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    A.start = W;
+    A.V = add_v ? V + M : nullptr;
+    A.W = W + M;
+    A.count = count - 1;
+    A.slab0 = 0;
+  } else {
+    if (!W_prev) return set_err(PIT_ERR_INVALID_ARGUMENT, "coarse sweep: slab range needs W_prev");
+    A.start = W_prev;
+    A.V = add_v ? V : nullptr;
+    A.W = W;
+    A.count = count;
+    A.slab0 = first - 1;
+  }
+  const bool src = with_source && ctx->has_source;
+  CUDA_TRY(launch_sweep(R.mpt, R.warps, src, R.P, A, st));
+  return PIT_OK;
+}
+
+// Sum per-block partials (np per block, component k) in slab order.
+double sum_partials(const double* h, int blocks, int np, int k) {
+  double s = 0.0;
+  for (int n = 0; n < blocks; ++n) s += h[(size_t)n * np + k];
+  return s;
+}
+double max_sqrt_partials(const double* h, int blocks, int np, int k) {
+  double w = 0.0;
+  for (int n = 0; n < blocks; ++n) w = std::max(w, std::sqrt(h[(size_t)n * np + k]));
+  return w;
+}
+
+int fetch_partials(pit_context* ctx, int count) {
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_partials, ctx->d_partials, sizeof(double) * (size_t)count,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PIT_OK;
+}
+
+int ensure_buffers(pit_context* ctx) {
+  if (ctx->buf[0]) return PIT_OK;
+  for (auto& b : ctx->buf) CUDA_TRY(cudaMalloc(&b, ctx->nm() * sizeof(double)));
+  return PIT_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* pit_last_error(void) { return g_err.c_str(); }
+int pit_last_error_slab(void) { return g_err_slab; }
+const char* pit_version(void) { return "pit_b200 0.1 (sm_100a)"; }
+
+int pit_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out) {
+  PIT_TRY(validate_desc(desc));
+  std::vector<double> zc;
+  Layout lay;
+  return role_coeffs(desc, role, out, &zc, &lay);
+}
+
+int pit_step_correction(const pit_problem_desc* desc, int role, double* zc_out) {
+  PIT_TRY(validate_desc(desc));
+  std::vector<double> zc;
+  Layout lay;
+  pit_step_coeffs c;
+  PIT_TRY(role_coeffs(desc, role, &c, &zc, &lay));
+  std::memcpy(zc_out, zc.data(), zc.size() * sizeof(double));
+  return PIT_OK;
+}
+
+int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
+  if (!out) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: null output");
+  *out = nullptr;
+  PIT_TRY(validate_desc(desc));
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(PIT_ERR_CUDA, "no CUDA device: the PiT kernels require a B200 (sm_100a)");
+  if (desc->device < 0 || desc->device >= ndev)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: bad device ordinal");
+  CUDA_TRY(cudaSetDevice(desc->device));
+  auto ctx = new pit_context();
+  ctx->desc = *desc;
+  ctx->desc.source_shape = nullptr;
+  ctx->desc.initial_value = nullptr;
+  ctx->M = desc->interior;
+  ctx->N = desc->slab_count;
+  ctx->h = grid_spacing(desc);
+  ctx->weight = ctx->h;  // inner_product weight h^d, d = 1 (grid.cpp:113-114)
+  ctx->has_source = desc->source_kind == PIT_SOURCE_SEPARABLE;
+  ctx->y0.assign(desc->initial_value, desc->initial_value + ctx->M);
+  auto fail = [&](int rc) {
+    pit_context_destroy(ctx);
+    return rc;
+  };
+  for (int r = 0; r < 2; ++r) {
+    std::vector<double> zc;
+    Layout lay;
+    int rc = role_coeffs(desc, r, &ctx->role[r].c, &zc, &lay);
+    if (rc) return fail(rc);
+    Role& R = ctx->role[r];
+    R.mpt = lay.mpt;
+    R.warps = lay.warps;
+    fill_params(R.c, &R.P);
+    if (cudaMalloc(&R.d_zc, sizeof(double) * zc.size()) != cudaSuccess ||
+        cudaMemcpy(R.d_zc, zc.data(), sizeof(double) * zc.size(), cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+      return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+    R.P.zc = R.d_zc;
+  }
+  if (cudaMalloc(&ctx->d_y0, sizeof(double) * ctx->M) != cudaSuccess ||
+      cudaMemcpy(ctx->d_y0, ctx->y0.data(), sizeof(double) * ctx->M, cudaMemcpyHostToDevice) !=
+          cudaSuccess)
+    return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+  if (ctx->has_source) {
+    if (cudaMalloc(&ctx->d_shape, sizeof(double) * ctx->M) != cudaSuccess ||
+        cudaMemcpy(ctx->d_shape, desc->source_shape, sizeof(double) * ctx->M,
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+    const double slab = desc->total_time / desc->slab_count;
+    for (int r = 0; r < 2; ++r) {
+      Role& R = ctx->role[r];
+      const int steps = R.c.steps;
+      const double dt = slab / steps;
+      // source sampled at step END: t = breakpoint(n) + step*dt (propagator.cpp:56-63)
+      std::vector<double> ds((size_t)ctx->N * steps);
+      for (int n = 0; n < ctx->N; ++n) {
+        const double t0 = n * slab;
+        for (int k = 1; k <= steps; ++k) {
+          const double t = t0 + k * dt;
+          const double sv = desc->source_amp * std::sin(desc->source_omega * t + desc->source_phase);
+          ds[(size_t)n * steps + (k - 1)] = dt * sv;
+        }
+      }
+      if (cudaMalloc(&R.d_ds, sizeof(double) * ds.size()) != cudaSuccess ||
+          cudaMemcpy(R.d_ds, ds.data(), sizeof(double) * ds.size(), cudaMemcpyHostToDevice) !=
+              cudaSuccess)
+        return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+      R.P.ds = R.d_ds;
+      R.P.shape = ctx->d_shape;
+    }
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_status, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_partials, sizeof(double) * 3 * (size_t)ctx->N) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_partials, sizeof(double) * 3 * (size_t)ctx->N) != cudaSuccess)
+    return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+  {
+    const int im = INT_MAX;  // "no failing slab"
+    if (cudaMemcpy(ctx->d_status, &im, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_err(PIT_ERR_CUDA, "pit_context_create: status init failed"));
+  }
+  *out = ctx;
+  return PIT_OK;
+}
+
+int pit_context_destroy(pit_context* ctx) {
+  if (!ctx) return PIT_OK;
+  for (auto& R : ctx->role) {
+    cudaFree(R.d_zc);
+    cudaFree(R.d_ds);
+  }
+  cudaFree(ctx->d_shape);
+  cudaFree(ctx->d_y0);
+  cudaFree(ctx->d_status);
+  cudaFree(ctx->d_partials);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->h_partials) cudaFreeHost(ctx->h_partials);
+  for (auto& b : ctx->buf) cudaFree(b);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PIT_OK;
+}
+
+int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing) {
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (M) *M = ctx->M;
+  if (N) *N = ctx->N;
+  if (spacing) *spacing = ctx->h;
+  return PIT_OK;
+}
+
+// ---- device-pointer entry points ----------------------------------------
+
+int pit_apply_F_device(pit_context* ctx, const double* L, const double* halo, double* out,
+                       int first, int count, void* stream) {
+  if (!ctx || !L || !out || first < 0 || count < 1 || first + count > ctx->N)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: block count does not match the partition");
+  return run_slab_batch(ctx, kApplyF, L, halo, nullptr, out, first, count,
+                        stream ? (cudaStream_t)stream : ctx->stream);
+}
+
+int pit_residual_device(pit_context* ctx, const double* lambda, const double* halo,
+                        const double* rhs, double* out, int first, int count, void* stream) {
+  if (!ctx || !lambda || !rhs || !out || first < 0 || count < 1 || first + count > ctx->N)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "residual: block count does not match the partition");
+  return run_slab_batch(ctx, kResidual, lambda, halo, rhs, out, first, count,
+                        stream ? (cudaStream_t)stream : ctx->stream);
+}
+
+int pit_coarse_sweep_device(pit_context* ctx, const double* V, const double* W_prev, double* W,
+                            int first, int count, int with_source, int add_v, void* stream) {
+  if (!ctx || !W || first < 0 || count < 1 || first + count > ctx->N || (add_v && !V))
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "apply_G_inverse: block count does not match the partition");
+  return run_sweep(ctx, PIT_COARSE, with_source != 0, V, W_prev, W, first, count, add_v != 0,
+                   stream ? (cudaStream_t)stream : ctx->stream);
+}
+
+int pit_block_partials_device(pit_context* ctx, const double* a, const double* b, double* partials,
+                              int count, void* stream) {
+  if (!ctx || !a || !b || !partials || count < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "block partials: bad arguments");
+  const double* A[1] = {a};
+  const double* B[1] = {b};
+  CUDA_TRY(launch_dots(ctx->M, count, ctx->weight, 1, A, B, partials,
+                       stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
+int pit_sync_status(pit_context* ctx, void* stream) {
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return check_status(ctx, true);
+}
+
+// ---- host-pointer entry points -------------------------------------------
+
+namespace {
+
+struct DevVec {
+  double* p = nullptr;
+  ~DevVec() { cudaFree(p); }
+};
+
+int to_device(pit_context* ctx, const double* h, size_t n, DevVec* d) {
+  CUDA_TRY(cudaMalloc(&d->p, n * sizeof(double)));
+  if (h)
+    CUDA_TRY(cudaMemcpyAsync(d->p, h, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  return PIT_OK;
+}
+
+int to_host(pit_context* ctx, const double* d, size_t n, double* h) {
+  CUDA_TRY(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PIT_OK;
+}
+
+void add_fine(pit_context* ctx, pit_run_stats* s, double ms) {
+  if (!s) return;
+  s->fine_applications += ctx->N - 1;
+  s->fine_parallel_ms += ms;
+  s->fine_busy_ms += ms;
+}
+void add_coarse(pit_context* ctx, pit_run_stats* s, double ms) {
+  if (!s) return;
+  s->coarse_applications += ctx->N - 1;
+  s->coarse_sequential_ms += ms;
+}
+
+}  // namespace
+
+int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats) {
+  if (!ctx || !L || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: null argument");
+  const auto t0 = Clock::now();
+  DevVec dL, dO;
+  PIT_TRY(to_device(ctx, L, ctx->nm(), &dL));
+  PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &dO));
+  PIT_TRY(run_slab_batch(ctx, kApplyF, dL.p, nullptr, nullptr, dO.p, 0, ctx->N, ctx->stream));
+  PIT_TRY(check_status(ctx, true));
+  PIT_TRY(to_host(ctx, dO.p, ctx->nm(), out));
+  add_fine(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+
+int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
+  if (!ctx || !rhs) return set_err(PIT_ERR_INVALID_ARGUMENT, "assemble_rhs: null argument");
+  const auto t0 = Clock::now();
+  DevVec d;
+  PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &d));
+  CUDA_TRY(cudaMemsetAsync(d.p, 0, ctx->nm() * sizeof(double), ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(d.p, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  if (ctx->has_source) {
+    Role& R = ctx->role[PIT_FINE];
+    SlabArgs A{};
+    A.mode = kPropagate;
+    A.in = nullptr;
+    A.out = d.p + ctx->M;
+    A.slab0 = 0;
+    A.status = ctx->d_status;
+    CUDA_TRY(launch_slab(R.mpt, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+    PIT_TRY(check_status(ctx, true));
+    add_fine(ctx, stats, ms_since(t0));
+  }
+  return to_host(ctx, d.p, ctx->nm(), rhs);
+}
+
+int pit_apply_G_inverse(pit_context* ctx, const double* V, double* out, pit_run_stats* stats) {
+  if (!ctx || !V || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_G_inverse: null argument");
+  const auto t0 = Clock::now();
+  DevVec d;
+  PIT_TRY(to_device(ctx, V, ctx->nm(), &d));
+  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, d.p, nullptr, d.p, 0, ctx->N, true, ctx->stream));
+  PIT_TRY(check_status(ctx, false));
+  PIT_TRY(to_host(ctx, d.p, ctx->nm(), out));
+  add_coarse(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+
+namespace {
+int initial_guess_dev(pit_context* ctx, int policy, double* d, pit_run_stats* stats) {
+  const auto t0 = Clock::now();
+  CUDA_TRY(cudaMemsetAsync(d, 0, ctx->nm() * sizeof(double), ctx->stream));
+  if (policy == PIT_GUESS_ZERO) return PIT_OK;
+  CUDA_TRY(cudaMemcpyAsync(d, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  PIT_TRY(run_sweep(ctx, PIT_COARSE, true, nullptr, nullptr, d, 0, ctx->N, false, ctx->stream));
+  PIT_TRY(check_status(ctx, false));
+  add_coarse(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
+  const auto t0 = Clock::now();
+  CUDA_TRY(cudaMemsetAsync(d, 0, ctx->nm() * sizeof(double), ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(d, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  if (!ctx->has_source) return PIT_OK;
+  Role& R = ctx->role[PIT_FINE];
+  SlabArgs A{};
+  A.mode = kPropagate;
+  A.out = d + ctx->M;
+  A.status = ctx->d_status;
+  CUDA_TRY(launch_slab(R.mpt, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+  PIT_TRY(check_status(ctx, true));
+  add_fine(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+}  // namespace
+
+int pit_initial_guess(pit_context* ctx, int policy, double* out, pit_run_stats* stats) {
+  if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "initial_guess: null argument");
+  DevVec d;
+  PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &d));
+  PIT_TRY(initial_guess_dev(ctx, policy, d.p, stats));
+  return to_host(ctx, d.p, ctx->nm(), out);
+}
+
+int pit_preconditioned_residual(pit_context* ctx, const double* lambda, const double* rhs,
+                                double* out, pit_run_stats* stats) {
+  if (!ctx || !lambda || !rhs || !out)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "preconditioned_residual: null argument");
+  DevVec dl, db, dr;
+  PIT_TRY(to_device(ctx, lambda, ctx->nm(), &dl));
+  PIT_TRY(to_device(ctx, rhs, ctx->nm(), &db));
+  PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &dr));
+  auto t0 = Clock::now();
+  PIT_TRY(run_slab_batch(ctx, kResidual, dl.p, nullptr, db.p, dr.p, 0, ctx->N, ctx->stream));
+  PIT_TRY(check_status(ctx, true));
+  add_fine(ctx, stats, ms_since(t0));
+  t0 = Clock::now();
+  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, dr.p, nullptr, dr.p, 0, ctx->N, true, ctx->stream));
+  PIT_TRY(check_status(ctx, false));
+  add_coarse(ctx, stats, ms_since(t0));
+  return to_host(ctx, dr.p, ctx->nm(), out);
+}
+
+int pit_sequential_fine_solve(pit_context* ctx, double* out) {
+  if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "sequential_fine_solve: null argument");
+  DevVec d;
+  PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &d));
+  CUDA_TRY(cudaMemsetAsync(d.p, 0, ctx->nm() * sizeof(double), ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(d.p, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  PIT_TRY(run_sweep(ctx, PIT_FINE, true, nullptr, nullptr, d.p, 0, ctx->N, false, ctx->stream));
+  PIT_TRY(check_status(ctx, false));
+  return to_host(ctx, d.p, ctx->nm(), out);
+}
+
+int pit_propagate(pit_context* ctx, int role, int with_source, const double* in, int slab,
+                  double* out) {
+  if (!ctx || !out || (role != PIT_FINE && role != PIT_COARSE))
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: bad argument");
+  if (slab < 0 || slab >= ctx->N)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: slab_index out of range");
+  const size_t M = ctx->M;
+  DevVec di, dout;
+  PIT_TRY(to_device(ctx, in, M, &di));
+  if (!in) CUDA_TRY(cudaMemsetAsync(di.p, 0, M * sizeof(double), ctx->stream));
+  PIT_TRY(to_device(ctx, nullptr, M, &dout));
+  Role& R = ctx->role[role];
+  SweepArgs A{};
+  A.start = di.p;
+  A.W = dout.p;
+  A.count = 1;
+  A.slab0 = slab;
+  A.status = ctx->d_status;
+  const bool src = with_source && ctx->has_source;
+  if (!in && !src) {
+    // source_contribution with f == 0 is exactly zero (propagator.cpp:78)
+    CUDA_TRY(cudaMemsetAsync(dout.p, 0, M * sizeof(double), ctx->stream));
+  } else {
+    CUDA_TRY(launch_sweep(R.mpt, R.warps, src, R.P, A, ctx->stream));
+    PIT_TRY(check_status(ctx, false));
+  }
+  return to_host(ctx, dout.p, M, out);
+}
+
+int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, double* out) {
+  if (!ctx || !a || !b || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "block_inner_product: null");
+  DevVec da, db;
+  PIT_TRY(to_device(ctx, a, ctx->nm(), &da));
+  PIT_TRY(to_device(ctx, b, ctx->nm(), &db));
+  const double* A[1] = {da.p};
+  const double* B[1] = {db.p};
+  CUDA_TRY(launch_dots(ctx->M, ctx->N, ctx->weight, 1, A, B, ctx->d_partials, ctx->stream));
+  PIT_TRY(fetch_partials(ctx, ctx->N));
+  *out = sum_partials(ctx->h_partials, ctx->N, 1, 0);
+  return PIT_OK;
+}
+
+int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out) {
+  if (!ctx || !a || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "block_norm_n_inf: null");
+  DevVec da;
+  PIT_TRY(to_device(ctx, a, ctx->nm(), &da));
+  const double* A[1] = {da.p};
+  CUDA_TRY(launch_dots(ctx->M, ctx->N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
+  PIT_TRY(fetch_partials(ctx, ctx->N));
+  *out = max_sqrt_partials(ctx->h_partials, ctx->N, 1, 0);
+  return PIT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Solvers (device-resident iterates)
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct Recorder {
+  pit_record* rows;
+  int cap;
+  int n = 0;
+  pit_run_stats* stats;
+  Clock::time_point t0;
+  void operator()(int k, double res) {
+    if (n < cap && rows) {
+      rows[n].k = k;
+      rows[n].residual_norm = res;
+      rows[n].fine_applications = stats->fine_applications;
+      rows[n].coarse_applications = stats->coarse_applications;
+      rows[n].wall_ms = ms_since(t0);
+    }
+    ++n;
+  }
+};
+
+int validate_cfg(const pit_solver_config* cfg) {
+  if (!cfg) return set_err(PIT_ERR_INVALID_ARGUMENT, "null solver config");
+  if (!(cfg->tolerance > cfg->restart_tolerance) || !(cfg->restart_tolerance > 0.0))
+    return set_err(PIT_ERR_CONFIG,
+                   "solver tolerances must satisfy tolerance > restart_tolerance > 0");
+  if (cfg->max_iterations < 1) return set_err(PIT_ERR_CONFIG, "max_iterations must be >= 1");
+  return PIT_OK;
+}
+
+// G^-1 F x  ->  out   (F into tmp, then the in-place sweep)
+int apply_GF(pit_context* ctx, const double* x, double* tmp, double* out, pit_run_stats* st) {
+  auto t0 = Clock::now();
+  PIT_TRY(run_slab_batch(ctx, kApplyF, x, nullptr, nullptr, tmp, 0, ctx->N, ctx->stream));
+  PIT_TRY(check_status(ctx, true));
+  add_fine(ctx, st, ms_since(t0));
+  t0 = Clock::now();
+  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, tmp, nullptr, out, 0, ctx->N, true, ctx->stream));
+  PIT_TRY(check_status(ctx, false));
+  add_coarse(ctx, st, ms_since(t0));
+  return PIT_OK;
+}
+
+int precond_residual_dev(pit_context* ctx, const double* lam, const double* rhs, double* out,
+                         pit_run_stats* st) {
+  auto t0 = Clock::now();
+  PIT_TRY(run_slab_batch(ctx, kResidual, lam, nullptr, rhs, out, 0, ctx->N, ctx->stream));
+  PIT_TRY(check_status(ctx, true));
+  add_fine(ctx, st, ms_since(t0));
+  t0 = Clock::now();
+  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, out, nullptr, out, 0, ctx->N, true, ctx->stream));
+  PIT_TRY(check_status(ctx, false));
+  add_coarse(ctx, st, ms_since(t0));
+  return PIT_OK;
+}
+
+int copy_dev(pit_context* ctx, double* dst, const double* src) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, ctx->nm() * sizeof(double), cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  return PIT_OK;
+}
+
+// pitsbicg_solve, src/solvers.cpp:116-220.  lam (device) holds the iterate.
+int pitsbicg_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init, double* lam,
+                 double* first_residual_dev, pit_record* rows, int cap, pit_solve_info* info) {
+  PIT_TRY(ensure_buffers(ctx));
+  const int N = ctx->N, M = ctx->M;
+  const size_t nm = ctx->nm();
+  double *rhs = ctx->buf[1], *r = ctx->buf[2], *rs = ctx->buf[3], *p = ctx->buf[4],
+         *d = ctx->buf[5], *s = ctx->buf[6], *t = ctx->buf[7], *f = ctx->buf[8];
+  pit_solve_info inf{};
+  inf.min_restart_margin = INFINITY;
+  pit_run_stats& st = inf.stats;
+  Recorder rec{rows, cap, 0, &st, Clock::now()};
+  auto finish = [&](int status) {
+    inf.status = status;
+    inf.total_records = rec.n;
+    inf.record_count = std::min(rec.n, cap);
+    if (info) *info = inf;
+    return PIT_OK;
+  };
+  if (!have_init) PIT_TRY(initial_guess_dev(ctx, cfg->initial_guess, lam, &st));
+  PIT_TRY(assemble_rhs_dev(ctx, rhs, &st));
+  PIT_TRY(precond_residual_dev(ctx, lam, rhs, r, &st));
+  if (first_residual_dev) PIT_TRY(copy_dev(ctx, first_residual_dev, r));
+  // ||r|| and <r,r> (= rho of iteration 1, r~ = r) from one partials pass
+  {
+    const double* A[1] = {r};
+    CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
+    PIT_TRY(fetch_partials(ctx, N));
+  }
+  double r_norm = max_sqrt_partials(ctx->h_partials, N, 1, 0);
+  double rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);  // <r, r~> with r~ = r
+  rec(0, r_norm);
+  if (r_norm <= cfg->tolerance) return finish(PIT_CONVERGED);
+  PIT_TRY(copy_dev(ctx, rs, r));
+  PIT_TRY(copy_dev(ctx, p, r));
+
+  for (int k = 1; k <= cfg->max_iterations; ++k) {
+    auto restart = [&]() -> int {
+      PIT_TRY(copy_dev(ctx, rs, r));
+      PIT_TRY(copy_dev(ctx, p, r));
+      ++inf.restarts;
+      rec(k, r_norm);
+      return PIT_OK;
+    };
+    // rho = <r, r~>: the value computed when r (or r~) last changed
+    const double rho = rr_shadow;
+    PIT_TRY(apply_GF(ctx, p, f, d, &st));
+    {
+      const double* A[1] = {d};
+      const double* B[1] = {rs};
+      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, B, ctx->d_partials, ctx->stream));
+      PIT_TRY(fetch_partials(ctx, N));
+    }
+    const double d_dot = sum_partials(ctx->h_partials, N, 1, 0);
+    if (std::abs(d_dot) < 1e-300) {
+      PIT_TRY(restart());
+      // r~ = r: <r, r~> becomes <r, r>
+      const double* A[1] = {r};
+      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
+      PIT_TRY(fetch_partials(ctx, N));
+      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
+      continue;
+    }
+    const double alpha = rho / d_dot;
+    CUDA_TRY(launch_update_s(M, N, ctx->weight, alpha, r, d, s, ctx->d_partials, ctx->stream));
+    PIT_TRY(fetch_partials(ctx, N));
+    const double s_norm = max_sqrt_partials(ctx->h_partials, N, 1, 0);
+    if (s_norm <= cfg->tolerance) {
+      CUDA_TRY(launch_axpy(nm, alpha, p, lam, ctx->stream));
+      std::swap(ctx->buf[2], ctx->buf[6]);  // r = move(s)
+      rec(k, s_norm);
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      return finish(PIT_CONVERGED);
+    }
+    PIT_TRY(apply_GF(ctx, s, f, t, &st));
+    {
+      const double* A[2] = {t, t};
+      const double* B[2] = {t, s};
+      CUDA_TRY(launch_dots(M, N, ctx->weight, 2, A, B, ctx->d_partials, ctx->stream));
+      PIT_TRY(fetch_partials(ctx, 2 * N));
+    }
+    const double tt = sum_partials(ctx->h_partials, N, 2, 0);
+    if (tt < 1e-300) {
+      PIT_TRY(restart());
+      const double* A[1] = {r};
+      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
+      PIT_TRY(fetch_partials(ctx, N));
+      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
+      continue;
+    }
+    const double omega = sum_partials(ctx->h_partials, N, 2, 1) / tt;
+    if (std::abs(omega) < 1e-300) {
+      PIT_TRY(restart());
+      const double* A[1] = {r};
+      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
+      PIT_TRY(fetch_partials(ctx, N));
+      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
+      continue;
+    }
+    // lambda += alpha p; lambda += omega s; s -= omega t; r = move(s)
+    CUDA_TRY(launch_update_lr(M, N, ctx->weight, alpha, omega, p, s, t, rs, lam, r,
+                              ctx->d_partials, ctx->stream));
+    PIT_TRY(fetch_partials(ctx, 2 * N));
+    r_norm = max_sqrt_partials(ctx->h_partials, N, 2, 0);
+    const double rr = sum_partials(ctx->h_partials, N, 2, 0);
+    const double r_dot = sum_partials(ctx->h_partials, N, 2, 1);
+    rec(k, r_norm);
+    if (r_norm <= cfg->tolerance) return finish(PIT_CONVERGED);
+    inf.min_restart_margin = std::min(inf.min_restart_margin, std::abs(r_dot) / cfg->restart_tolerance);
+    if (std::abs(r_dot) <= cfg->restart_tolerance) {
+      PIT_TRY(copy_dev(ctx, rs, r));
+      PIT_TRY(copy_dev(ctx, p, r));
+      ++inf.restarts;
+      rr_shadow = rr;
+    } else {
+      const double beta = (alpha / omega) * (r_dot / rho);
+      CUDA_TRY(launch_update_p(nm, omega, beta, d, r, p, ctx->stream));
+      rr_shadow = r_dot;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return finish(PIT_MAX_ITERATIONS);
+}
+
+// parareal_solve, src/solvers.cpp:73-114.
+int parareal_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init, double* lam,
+                 double* first_residual_dev, pit_record* rows, int cap, pit_solve_info* info) {
+  PIT_TRY(ensure_buffers(ctx));
+  const int N = ctx->N, M = ctx->M;
+  double *rhs = ctx->buf[1], *corr = ctx->buf[2];
+  pit_solve_info inf{};
+  inf.min_restart_margin = INFINITY;
+  pit_run_stats& st = inf.stats;
+  Recorder rec{rows, cap, 0, &st, Clock::now()};
+  if (!have_init) PIT_TRY(initial_guess_dev(ctx, cfg->initial_guess, lam, &st));
+  PIT_TRY(assemble_rhs_dev(ctx, rhs, &st));
+  int status = PIT_MAX_ITERATIONS;
+  for (int k = 0;; ++k) {
+    const pit_run_stats before = st;
+    PIT_TRY(precond_residual_dev(ctx, lam, rhs, corr, &st));
+    if (k == 0 && first_residual_dev) PIT_TRY(copy_dev(ctx, first_residual_dev, corr));
+    const double* A[1] = {corr};
+    CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
+    PIT_TRY(fetch_partials(ctx, N));
+    const double res = max_sqrt_partials(ctx->h_partials, N, 1, 0);
+    const pit_run_stats after = st;
+    st = before;  // the row charges the work spent reaching the current iterate
+    rec(k, res);
+    st = after;
+    if (res <= cfg->tolerance) {
+      status = PIT_CONVERGED;
+      break;
+    }
+    if (k == cfg->max_iterations) break;
+    CUDA_TRY(launch_add(ctx->nm(), corr, lam, ctx->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  inf.status = status;
+  inf.total_records = rec.n;
+  inf.record_count = std::min(rec.n, cap);
+  if (info) *info = inf;
+  return PIT_OK;
+}
+
+int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
+               double* lambda_out, double* first_residual_out, pit_record* records,
+               int max_records, pit_solve_info* info) {
+  if (!ctx || !lambda_out) return set_err(PIT_ERR_INVALID_ARGUMENT, "solve: null argument");
+  PIT_TRY(validate_cfg(cfg));
+  PIT_TRY(ensure_buffers(ctx));
+  double* lam = ctx->buf[0];
+  double* first = first_residual_out ? ctx->buf[9] : nullptr;
+  if (lambda_init)
+    CUDA_TRY(cudaMemcpyAsync(lam, lambda_init, ctx->nm() * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+  if (which == 0)
+    PIT_TRY(pitsbicg_dev(ctx, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
+  else
+    PIT_TRY(parareal_dev(ctx, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
+  PIT_TRY(to_host(ctx, ctx->buf[0], ctx->nm(), lambda_out));
+  if (first_residual_out) PIT_TRY(to_host(ctx, first, ctx->nm(), first_residual_out));
+  return PIT_OK;
+}
+
+}  // namespace
+
+int pit_pitsbicg_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
+                       double* lambda_out, double* first_residual_out, pit_record* records,
+                       int max_records, pit_solve_info* info) {
+  return solve_host(0, ctx, cfg, lambda_init, lambda_out, first_residual_out, records,
+                    max_records, info);
+}
+
+int pit_parareal_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
+                       double* lambda_out, double* first_residual_out, pit_record* records,
+                       int max_records, pit_solve_info* info) {
+  return solve_host(1, ctx, cfg, lambda_init, lambda_out, first_residual_out, records,
+                    max_records, info);
+}
+
+int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
+                              const double* lambda_init_dev, double* lambda_dev,
+                              pit_record* records, int max_records, pit_solve_info* info,
+                              void* stream) {
+  if (!ctx || !lambda_dev) return set_err(PIT_ERR_INVALID_ARGUMENT, "solve: null argument");
+  PIT_TRY(validate_cfg(cfg));
+  if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  if (lambda_init_dev && lambda_init_dev != lambda_dev)
+    CUDA_TRY(cudaMemcpyAsync(lambda_dev, lambda_init_dev, ctx->nm() * sizeof(double),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+  PIT_TRY(pitsbicg_dev(ctx, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
+                       max_records, info));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PIT_OK;
+}
+
+// ---- seeded inputs ---------------------------------------------------------
+
+void pit_seeded_uniform(uint64_t seed, int64_t n, double a, double b, double* out) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(a, b);
+  for (int64_t i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+void pit_seeded_normal(uint64_t seed, int64_t n, double mean, double stddev, double* out) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> dist(mean, stddev);
+  for (int64_t i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+}  // extern "C"

@@ -1,0 +1,375 @@
+// pit_kernels.cu — sm_100a kernels of the PiT hot path.
+//
+//  K1 slab_kernel   apply_F / preconditioned-residual / propagate over a batch
+//                   of slabs, one CTA per slab, state resident in registers
+//                   across all fine steps; HBM traffic only at slab boundaries.
+//                   Replaces block_system.cpp:115-147 (+ the executor fan-out,
+//                   executor.cpp:105-154) and solvers.cpp:66-71's subtraction.
+//  K2 sweep_kernel  the sequential coarse sweep (apply_G_inverse,
+//                   block_system.cpp:174-195; initial_guess, solvers.cpp:49-64;
+//                   sequential_fine_solve, solvers.cpp:40-47) as one persistent
+//                   CTA that keeps W_{n-1} in registers from slab to slab.
+//  K3 vector kernels the BiCGStab block algebra (block_system.cpp:31-87,
+//                   solvers.cpp:159-215) fused into four passes with
+//                   fixed-order per-block reductions.
+#include <cstdint>
+
+#include "pit_kernels.cuh"
+
+namespace pitb {
+
+namespace {
+
+template <int MPT>
+__device__ __forceinline__ void load_field(double (&y)[MPT], const double* __restrict__ src,
+                                           int g0, int M) {
+#pragma unroll
+  for (int j = 0; j < MPT; ++j) y[j] = (src != nullptr && g0 + j < M) ? src[g0 + j] : 0.0;
+}
+
+template <int MPT>
+__device__ __forceinline__ bool all_finite(const double (&y)[MPT], int g0, int M) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < MPT; ++j)
+    if (g0 + j < M && !isfinite(y[j])) ok = false;
+  return ok;
+}
+
+template <int WARPS>
+__device__ __forceinline__ double* zc_smem(StepShared<WARPS>* sh) {
+  return reinterpret_cast<double*>(sh + 1);
+}
+
+template <int MPT, int WARPS, bool SRC>
+struct SlabBounds {
+  static constexpr int kThreads = 32 * WARPS;
+  static constexpr int kRegs = MPT <= 16 ? 64 : 128;
+  static constexpr int kMin0 = 65536 / (kThreads * kRegs);
+  static constexpr int kMin = SRC ? 1 : (kMin0 < 1 ? 1 : (kMin0 > 16 ? 16 : kMin0));
+};
+
+template <int MPT, int WARPS, bool SRC>
+__global__ void __launch_bounds__(32 * WARPS, (SlabBounds<MPT, WARPS, SRC>::kMin))
+    slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
+  double* s_zc = zc_smem<WARPS>(sh);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  const int M = P.M;
+  const int g0 = tid * MPT;
+  for (int i = tid; i < P.K0; i += 32 * WARPS) s_zc[i] = P.zc[i];
+
+  const double* src;
+  if (b + A.in_shift >= 0)
+    src = A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr;
+  else
+    src = A.halo;
+  double y[MPT];
+  load_field<MPT>(y, src, g0, M);
+  double g[MPT];
+  if (SRC) load_field<MPT>(g, P.shape, g0, M);
+  const double plane = P.plane[lane], qlane = P.qlane[lane];
+  const int slab = A.slab0 + b;
+  __syncthreads();
+
+  propagate_slab<MPT, WARPS, SRC>(y, P, plane, qlane, *sh, s_zc, lane, warp, g0,
+                                  SRC ? P.ds + (size_t)slab * P.steps : nullptr, g);
+
+  if (!all_finite<MPT>(y, g0, M)) atomicMin(A.status, slab);
+  const size_t off = (size_t)b * M;
+  double* out = A.out + off;
+  if (A.mode == kApplyF) {
+    const double* Ln = A.Lsub + off;
+#pragma unroll
+    for (int j = 0; j < MPT; ++j)
+      if (g0 + j < M) out[g0 + j] = Ln[g0 + j] - y[j];
+  } else if (A.mode == kResidual) {
+    const double* Ln = A.Lsub + off;
+    const double* Bn = A.rhs + off;
+#pragma unroll
+    for (int j = 0; j < MPT; ++j)
+      if (g0 + j < M) {
+        const double a = Ln[g0 + j] - y[j];
+        out[g0 + j] = Bn[g0 + j] - a;
+      }
+  } else {
+#pragma unroll
+    for (int j = 0; j < MPT; ++j)
+      if (g0 + j < M) out[g0 + j] = y[j];
+  }
+  if (b == 0 && A.out0 != nullptr) {
+    if (A.mode == kApplyF) {
+      for (int i = tid; i < M; i += 32 * WARPS) A.out0[i] = A.L0[i];
+    } else if (A.mode == kResidual) {
+      for (int i = tid; i < M; i += 32 * WARPS) A.out0[i] = A.rhs0[i] - A.L0[i];
+    }
+  }
+}
+
+template <int MPT, int WARPS, bool SRC>
+__global__ void __launch_bounds__(32 * WARPS, 1)
+    sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
+  double* s_zc = zc_smem<WARPS>(sh);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int M = P.M;
+  const int g0 = tid * MPT;
+  for (int i = tid; i < P.K0; i += 32 * WARPS) s_zc[i] = P.zc[i];
+  double y[MPT];
+  load_field<MPT>(y, A.start, g0, M);
+  double g[MPT];
+  if (SRC) load_field<MPT>(g, P.shape, g0, M);
+  const double plane = P.plane[lane], qlane = P.qlane[lane];
+  __syncthreads();
+  bool ok = true;
+  int bad = 0x7fffffff;
+  for (int b = 0; b < A.count; ++b) {
+    const int slab = A.slab0 + b;
+    const size_t off = (size_t)b * M;
+    double v[MPT];
+    load_field<MPT>(v, A.V ? A.V + off : nullptr, g0, M);
+    propagate_slab<MPT, WARPS, SRC>(y, P, plane, qlane, *sh, s_zc, lane, warp, g0,
+                                    SRC ? P.ds + (size_t)slab * P.steps : nullptr, g);
+    if (ok && !all_finite<MPT>(y, g0, M)) {
+      ok = false;
+      bad = slab;
+    }
+    if (A.V) {
+#pragma unroll
+      for (int j = 0; j < MPT; ++j) y[j] = y[j] + v[j];
+    }
+    double* W = A.W + off;
+#pragma unroll
+    for (int j = 0; j < MPT; ++j)
+      if (g0 + j < M) W[g0 + j] = y[j];
+  }
+  if (!ok) atomicMin(A.status, bad);
+}
+
+template <int MPT, int WARPS, bool SRC>
+cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
+  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)P.K0;
+  auto k = slab_kernel<MPT, WARPS, SRC>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<ctas, 32 * WARPS, smem, st>>>(P, A);
+  return cudaGetLastError();
+}
+
+template <int MPT, int WARPS, bool SRC>
+cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
+  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)P.K0;
+  auto k = sweep_kernel<MPT, WARPS, SRC>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<1, 32 * WARPS, smem, st>>>(P, A);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K3 vector kernels
+// ---------------------------------------------------------------------------
+
+// Warp butterfly (shfl_xor 16..1) then warp totals summed in warp order by
+// thread 0.  ws holds kVecThreads/32 doubles.  Result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* ws) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(kFull, v, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    s = ws[0];
+#pragma unroll
+    for (int w = 1; w < kVecThreads / 32; ++w) s = s + ws[w];
+  }
+  return s;
+}
+
+struct DotPtrs {
+  const double* a[3];
+  const double* b[3];
+};
+
+template <int NP>
+__global__ void __launch_bounds__(kVecThreads) dots_kernel(int M, double weight, DotPtrs ptr,
+                                                           double* __restrict__ partials) {
+  __shared__ double ws[NP][kVecThreads / 32];
+  const size_t off = (size_t)blockIdx.x * M;
+  double acc[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) acc[k] = 0.0;
+  for (int i = threadIdx.x; i < M; i += kVecThreads) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) acc[k] = fma(ptr.a[k][off + i], ptr.b[k][off + i], acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double s = block_sum(acc[k], ws[k]);
+    if (threadIdx.x == 0) partials[(size_t)blockIdx.x * NP + k] = weight * s;
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+    update_s_kernel(int M, double weight, double alpha, const double* __restrict__ r,
+                    const double* __restrict__ d, double* __restrict__ s,
+                    double* __restrict__ partials) {
+  __shared__ double ws[kVecThreads / 32];
+  const size_t off = (size_t)blockIdx.x * M;
+  const double na = -alpha;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < M; i += kVecThreads) {
+    const double v = fma(na, d[off + i], r[off + i]);
+    s[off + i] = v;
+    acc = fma(v, v, acc);
+  }
+  const double t = block_sum(acc, ws);
+  if (threadIdx.x == 0) partials[blockIdx.x] = weight * t;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+    update_lr_kernel(int M, double weight, double alpha, double omega,
+                     const double* __restrict__ p, const double* __restrict__ s,
+                     const double* __restrict__ t, const double* __restrict__ rs,
+                     double* __restrict__ lam, double* __restrict__ r,
+                     double* __restrict__ partials) {
+  __shared__ double ws[2][kVecThreads / 32];
+  const size_t off = (size_t)blockIdx.x * M;
+  const double nw = -omega;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int i = threadIdx.x; i < M; i += kVecThreads) {
+    const double sv = s[off + i];
+    double l = lam[off + i];
+    l = fma(alpha, p[off + i], l);
+    l = fma(omega, sv, l);
+    lam[off + i] = l;
+    const double rv = fma(nw, t[off + i], sv);
+    r[off + i] = rv;
+    acc0 = fma(rv, rv, acc0);
+    acc1 = fma(rv, rs[off + i], acc1);
+  }
+  const double a = block_sum(acc0, ws[0]);
+  const double c = block_sum(acc1, ws[1]);
+  if (threadIdx.x == 0) {
+    partials[2 * (size_t)blockIdx.x] = weight * a;
+    partials[2 * (size_t)blockIdx.x + 1] = weight * c;
+  }
+}
+
+__global__ void update_p_kernel(size_t n, double omega, double beta, const double* __restrict__ d,
+                                const double* __restrict__ r, double* __restrict__ p) {
+  const double nw = -omega;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = fma(fma(nw, d[i], p[i]), beta, r[i]);
+}
+
+__global__ void axpy_kernel(size_t n, double a, const double* __restrict__ x,
+                            double* __restrict__ y) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+__global__ void add_kernel(size_t n, const double* __restrict__ x, double* __restrict__ y) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = y[i] + x[i];
+}
+
+int ew_grid(size_t n) {
+  size_t g = (n + 255) / 256;
+  const size_t cap = 148 * 16;
+  return (int)(g < cap ? (g ? g : 1) : cap);
+}
+
+}  // namespace
+
+#define PIT_LAYOUTS(X)                                                                       \
+  X(4, 1) X(4, 2) X(4, 4) X(4, 8) X(4, 16) X(4, 32) X(8, 4) X(8, 8) X(8, 16) X(8, 32) X(16, 4) \
+      X(16, 8) X(16, 16) X(16, 32) X(32, 4) X(32, 8) X(32, 16)
+
+cudaError_t launch_slab(int mpt, int warps, bool src, const StepParams& P, const SlabArgs& A,
+                        int ctas, cudaStream_t st) {
+  if (ctas <= 0) return cudaSuccess;
+#define X(MP, W)                                                               \
+  if (mpt == MP && warps == W)                                                 \
+    return src ? slab_launch<MP, W, true>(P, A, ctas, st)                      \
+               : slab_launch<MP, W, false>(P, A, ctas, st);
+  PIT_LAYOUTS(X)
+#undef X
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_sweep(int mpt, int warps, bool src, const StepParams& P, const SweepArgs& A,
+                         cudaStream_t st) {
+  if (A.count <= 0) return cudaSuccess;
+#define X(MP, W)                                                                             \
+  if (mpt == MP && warps == W)                                                               \
+    return src ? sweep_launch<MP, W, true>(P, A, st) : sweep_launch<MP, W, false>(P, A, st);
+  PIT_LAYOUTS(X)
+#undef X
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_dots(int M, int blocks, double weight, int np, const double* const* a,
+                        const double* const* b, double* partials, cudaStream_t st) {
+  if (blocks <= 0) return cudaSuccess;
+  DotPtrs p{};
+  for (int k = 0; k < np; ++k) {
+    p.a[k] = a[k];
+    p.b[k] = b[k];
+  }
+  switch (np) {
+    case 1: dots_kernel<1><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials); break;
+    case 2: dots_kernel<2><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials); break;
+    case 3: dots_kernel<3><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_s(int M, int blocks, double weight, double alpha, const double* r,
+                            const double* d, double* s, double* partials, cudaStream_t st) {
+  if (blocks <= 0) return cudaSuccess;
+  update_s_kernel<<<blocks, kVecThreads, 0, st>>>(M, weight, alpha, r, d, s, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_lr(int M, int blocks, double weight, double alpha, double omega,
+                             const double* p, const double* s, const double* t, const double* rs,
+                             double* lam, double* r, double* partials, cudaStream_t st) {
+  if (blocks <= 0) return cudaSuccess;
+  update_lr_kernel<<<blocks, kVecThreads, 0, st>>>(M, weight, alpha, omega, p, s, t, rs, lam, r,
+                                                   partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_p(size_t n, double omega, double beta, const double* d, const double* r,
+                            double* p, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  update_p_kernel<<<ew_grid(n), 256, 0, st>>>(n, omega, beta, d, r, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  axpy_kernel<<<ew_grid(n), 256, 0, st>>>(n, a, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add(size_t n, const double* x, double* y, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  add_kernel<<<ew_grid(n), 256, 0, st>>>(n, x, y);
+  return cudaGetLastError();
+}
+
+}  // namespace pitb

@@ -1,0 +1,67 @@
+// pit_kernels.cuh — kernel entry points and host launchers (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pit_step.cuh"
+
+namespace pitb {
+
+enum SlabMode { kApplyF = 0, kResidual = 1, kPropagate = 2 };
+
+// K1: one CTA per slab, all slabs of the batch in parallel.
+struct SlabArgs {
+  const double* in;    // CTA b reads field in + (b + in_shift)*M (nullptr: zero field)
+  const double* halo;  // field used when b + in_shift < 0
+  int in_shift;
+  const double* Lsub;  // kApplyF / kResidual: CTA b subtracts from Lsub + b*M
+  const double* rhs;   // kResidual: rhs + b*M
+  double* out;         // out + b*M
+  int slab0;           // propagation slab index of CTA 0
+  int mode;
+  int* status;         // atomicMin of the first slab with a non-finite result
+  const double* L0;    // block 0 (done by CTA 0 when non-null):
+  const double* rhs0;  //   kApplyF:   out0 = L0
+  double* out0;        //   kResidual: out0 = rhs0 - L0
+};
+
+// K2: one persistent CTA running the sequential sweep
+//   W_b = Prop(W_{b-1}) (+ V_b),  W_{-1} = start
+struct SweepArgs {
+  const double* start;
+  const double* V;  // nullptr: no add
+  double* W;
+  int count;
+  int slab0;
+  int* status;
+};
+
+// Launchers; return cudaErrorInvalidConfiguration for an uncompiled layout.
+cudaError_t launch_slab(int mpt, int warps, bool src, const StepParams& P, const SlabArgs& A,
+                        int ctas, cudaStream_t st);
+cudaError_t launch_sweep(int mpt, int warps, bool src, const StepParams& P, const SweepArgs& A,
+                         cudaStream_t st);
+
+// K3: block-vector algebra, one CTA (kVecThreads) per block, fixed reduction
+// order (oracle/pit_oracle.c orc_block_partial, ORC_MODE_DEVICE).
+constexpr int kVecThreads = 256;
+// partials[b*np + k] = weight * <a_k, b_k> over block b, k < np (np <= 3)
+cudaError_t launch_dots(int M, int blocks, double weight, int np, const double* const* a,
+                        const double* const* b, double* partials, cudaStream_t st);
+// s = r - alpha*d (fma), partials[b] = weight*<s,s>
+cudaError_t launch_update_s(int M, int blocks, double weight, double alpha, const double* r,
+                            const double* d, double* s, double* partials, cudaStream_t st);
+// lam = fma(alpha,p,lam); lam = fma(omega,s,lam); r = fma(-omega,t,s);
+// partials[2b] = weight*<r,r>, partials[2b+1] = weight*<r,rs>
+cudaError_t launch_update_lr(int M, int blocks, double weight, double alpha, double omega,
+                             const double* p, const double* s, const double* t, const double* rs,
+                             double* lam, double* r, double* partials, cudaStream_t st);
+// p = fma(fma(-omega, d, p), beta, r)
+cudaError_t launch_update_p(size_t n, double omega, double beta, const double* d, const double* r,
+                            double* p, cudaStream_t st);
+// y = fma(a, x, y)
+cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st);
+// y = y + x
+cudaError_t launch_add(size_t n, const double* x, double* y, cudaStream_t st);
+
+}  // namespace pitb

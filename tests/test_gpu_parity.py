@@ -1,0 +1,220 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+(device op order, mirrored propagator) — bit for bit — and against the
+reference's golden fixtures; full-size BASELINE shapes through
+size-independent properties."""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from helpers import OracleProblem, modal_heat_1d, rel_block
+from paper_2203_10148_b200 import api, configs
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def same(a, b):
+    return np.array_equal(a, b), float(np.max(np.abs(a - b))) if a.shape == b.shape else None
+
+
+@pytest.fixture(scope="module")
+def c1():
+    p = configs.make("c1")
+    ctx = api.BlockOperatorContext(p)
+    yield p, ctx, OracleProblem(p)
+    ctx.close()
+
+
+def test_c1_operators_bitwise_vs_oracle(c1):
+    p, ctx, o = c1
+    g = gold("c1_reference.npz")
+    probe = g["probe"]
+    assert same(api.apply_F(ctx, probe), o.apply_F(probe))[0]
+    assert same(api.apply_G_inverse(ctx, probe), o.apply_G_inverse(probe))[0]
+    assert same(api.assemble_rhs(ctx), o.assemble_rhs())[0]
+    assert same(api.initial_guess(ctx, api.InitialGuessPolicy.CoarseSweep), o.initial_guess())[0]
+    assert same(api.sequential_fine_solve(ctx), o.sequential_fine())[0]
+    rhs = o.assemble_rhs()
+    assert same(api.preconditioned_residual(ctx, probe, rhs), o.preconditioned_residual(probe, rhs))[0]
+    assert api.block_inner_product(ctx, probe, g["apply_F"]) == o.block_dot(probe, g["apply_F"])
+    assert api.block_norm_n_inf(ctx, probe) == o.block_norm(probe)
+
+
+def test_c1_operators_vs_reference(c1):
+    p, ctx, o = c1
+    g = gold("c1_reference.npz")
+    assert rel_block(api.apply_F(ctx, g["probe"]), g["apply_F"]) < 1e-10
+    assert rel_block(api.apply_G_inverse(ctx, g["probe"]), g["apply_G_inverse"]) < 1e-10
+    assert rel_block(api.sequential_fine_solve(ctx), g["sequential_fine"]) < 1e-10
+
+
+def test_c1_pitsbicg_bitwise_vs_oracle_and_matches_reference(c1):
+    p, ctx, o = c1
+    g = gold("c1_reference.npz")
+    first = np.zeros((p.N, p.M))
+    res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10),
+                             options=api.SolveOptions(first_residual_out=first))
+    r = o.solve(1e-10)
+    assert np.array_equal(res.solution, r["lam"])
+    assert np.array_equal(first, r["first"])
+    assert [(x.k, x.residual_norm, x.fine_applications, x.coarse_applications)
+            for x in res.history.records] == r["rows"]
+    assert res.history.restarts == r["restarts"] == int(g["pitsbicg_restarts"])
+    # against the reference binary: same iterations, every lambda_n within 1e-10
+    hist = g["pitsbicg_hist"]
+    assert [x.k for x in res.history.records] == [int(k) for k in hist[:, 0]]
+    assert res.history.status == api.SolveStatus.Converged
+    assert rel_block(res.solution, g["pitsbicg_lambda"]) < 1e-10
+    lamN = api.fine(ctx).propagate(res.solution[-1], p.N - 1)
+    assert np.linalg.norm(lamN - g["pitsbicg_lambda_N"]) / np.linalg.norm(g["pitsbicg_lambda_N"]) < 1e-10
+
+
+def test_c1_parareal_bitwise_vs_oracle(c1):
+    p, ctx, o = c1
+    g = gold("c1_reference.npz")
+    res = api.parareal_solve(ctx, api.SolverConfig(tolerance=1e-10))
+    r = o.solve(1e-10, which="parareal")
+    assert np.array_equal(res.solution, r["lam"])
+    assert [x.fine_applications for x in res.history.records] == [row[2] for row in r["rows"]]
+    assert rel_block(res.solution, g["parareal_lambda"]) < 1e-10
+
+
+REDUCED = [("c2", 8), ("c3", 6), ("c4", 6)]
+
+
+@pytest.mark.parametrize("name,slabs", REDUCED)
+def test_reduced_operators_bitwise_vs_oracle(name, slabs):
+    p = configs.make(name, slabs=slabs)
+    o = OracleProblem(p)
+    rng = np.random.default_rng(11)
+    L = np.ascontiguousarray(rng.uniform(-1, 1, (p.N, p.M)))
+    with api.BlockOperatorContext(p) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))[0]
+        assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))[0]
+        assert same(api.assemble_rhs(ctx), o.assemble_rhs())[0]
+        assert same(api.initial_guess(ctx, api.InitialGuessPolicy.CoarseSweep), o.initial_guess())[0]
+
+
+@pytest.mark.parametrize("name,slabs", [("c2", 8), ("c3", 8), ("c4", 5)])
+def test_reduced_pitsbicg_bitwise_vs_oracle(name, slabs):
+    p = configs.make(name, slabs=slabs)
+    o = OracleProblem(p)
+    with api.BlockOperatorContext(p) as ctx:
+        res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+    r = o.solve(1e-10)
+    assert [(x.k, x.residual_norm) for x in res.history.records] == [(a[0], a[1]) for a in r["rows"]]
+    assert np.array_equal(res.solution, r["lam"])
+
+
+def test_c3_n16_matches_reference():
+    g = gold("c3_n16_reference.npz")
+    p = configs.make("c3", slabs=16)
+    with api.BlockOperatorContext(p) as ctx:
+        res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+    assert [x.k for x in res.history.records] == [int(k) for k in g["pitsbicg_hist"][:, 0]]
+    assert res.history.restarts == int(g["pitsbicg_restarts"])
+    assert rel_block(res.solution, g["pitsbicg_lambda"]) < 5e-10  # reference inner-solve floor
+
+
+@pytest.mark.parametrize("layout", [(16, 8), (8, 16), (32, 4), (16, 16), (4, 32), (8, 32)])
+def test_fine_layouts_bitwise_vs_oracle(layout):
+    p = configs.make("c2", slabs=4)
+    o = OracleProblem(p, fine_layout=layout)
+    rng = np.random.default_rng(5)
+    L = np.ascontiguousarray(rng.uniform(-1, 1, (p.N, p.M)))
+    with api.BlockOperatorContext(p, fine_layout=layout) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))[0]
+
+
+@pytest.mark.parametrize("M", [1, 2, 31, 100, 333, 1000, 4095])
+def test_ragged_grids_bitwise_vs_oracle(M):
+    p = configs.make("c2", slabs=3, M=M)
+    p.fine_steps = 20
+    o = OracleProblem(p)
+    rng = np.random.default_rng(M)
+    L = np.ascontiguousarray(rng.uniform(-1, 1, (p.N, p.M)))
+    with api.BlockOperatorContext(p) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))[0]
+        assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))[0]
+
+
+# --------------------------------------------------------------------------
+# full BASELINE sizes: size-independent properties
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_continuity_fixed_point(name):
+    # the sequential fine trajectory solves F L = B (test_block_system.cpp:164-174)
+    p = configs.make(name)
+    with api.BlockOperatorContext(p) as ctx:
+        seq = api.sequential_fine_solve(ctx)
+        res = api.apply_F(ctx, seq) - api.assemble_rhs(ctx)
+    norm = max(np.sqrt(p.spacing * np.sum(res * res, axis=1)))
+    if p.source is None:
+        assert norm == 0.0  # same kernel arithmetic on both sides
+    assert norm <= 1e-10
+
+
+def test_full_size_c2_linearity_and_closed_form():
+    p = configs.make("c2")
+    rng = np.random.default_rng(1)
+    x = rng.uniform(-1, 1, (p.N, p.M))
+    y = rng.uniform(-1, 1, (p.N, p.M))
+    with api.BlockOperatorContext(p) as ctx:
+        fx, fy = api.apply_F(ctx, x), api.apply_F(ctx, y)
+        fxy = api.apply_F(ctx, 0.75 * x - 1.25 * y)
+        assert rel_block(fxy, 0.75 * fx - 1.25 * fy) < 1e-12
+        seq = api.sequential_fine_solve(ctx)
+    a = api.seeded_normal(configs.SEED, 8)
+    for n in (1, 100, p.N - 1):
+        exact = modal_heat_1d(p, a, n)
+        err = np.linalg.norm(seq[n] - exact) / np.linalg.norm(exact)
+        assert err < 2e-15 * p.fine_steps * n, (n, err)
+
+
+def test_full_size_c2_pitsbicg_converges():
+    p = configs.make("c2")
+    with api.BlockOperatorContext(p) as ctx:
+        res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+        seq = api.sequential_fine_solve(ctx)
+    assert res.history.status == api.SolveStatus.Converged
+    assert res.history.records[-1].residual_norm <= 1e-10
+    rows = res.history.records
+    for i, row in enumerate(rows):  # (2k+1)(N-1), half-step 2k(N-1) (acceptance.cpp:187-220)
+        full = (2 * row.k + 1) * (p.N - 1)
+        assert row.fine_applications == full or (i == len(rows) - 1 and
+                                                 row.fine_applications == 2 * row.k * (p.N - 1))
+    assert rel_block(res.solution, seq) < 1e-8
+
+
+def test_nonfinite_slab_raises_lowest_slab_error():
+    p = configs.make("c2", slabs=8)
+    L = np.ones((p.N, p.M))
+    L[5, 7] = np.nan
+    L[6, 1] = np.inf
+    with api.BlockOperatorContext(p) as ctx:
+        with pytest.raises(api.SlabError) as e:
+            api.apply_F(ctx, L)
+        assert e.value.slab_index == 5
+        with pytest.raises(api.InnerSolveError):
+            api.apply_G_inverse(ctx, L)
+        # the context survives the failure (executor.cpp:142-152 analogue)
+        assert np.isfinite(api.apply_F(ctx, np.ones((p.N, p.M)))).all()
+
+
+def test_bad_shapes_raise_value_error():
+    p = configs.make("c1")
+    with api.BlockOperatorContext(p) as ctx:
+        with pytest.raises(ValueError):
+            api.apply_F(ctx, np.zeros((p.N - 1, p.M)))
+        with pytest.raises(ValueError):
+            api.fine(ctx).propagate(np.zeros(p.M), p.N)
