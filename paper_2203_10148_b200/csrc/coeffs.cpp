@@ -20,9 +20,9 @@ namespace pitb {
 namespace {
 struct L { int mpt, warps; };
 // fine/coarse layouts compiled into pit_kernels.cu (keep in sync with PIT_LAYOUTS there)
-const L kLayouts[] = {{4, 1},  {4, 2},  {4, 4},  {4, 8},   {4, 16},  {4, 32}, {8, 4},
-                      {8, 8},  {8, 16}, {8, 32}, {16, 4},  {16, 8},  {16, 16}, {16, 32},
-                      {32, 4}, {32, 8}, {32, 16}};
+const L kLayouts[] = {{4, 1},   {4, 2},  {4, 4},  {4, 8},  {4, 16}, {4, 32},  {8, 4},
+                      {8, 8},   {8, 16}, {8, 32}, {16, 2}, {16, 4}, {16, 8},  {16, 16},
+                      {16, 32}, {32, 1}, {32, 2}, {32, 4}, {32, 8}, {32, 16}};
 }  // namespace
 
 bool layout_supported(int mpt, int warps) {
@@ -35,8 +35,8 @@ Layout auto_layout(int M, int role) {
   // fine: 16 points per thread (32 registers of state) once M is large enough,
   // so four slab CTAs fit per SM; coarse (one persistent CTA): as many
   // threads as possible, few points each, to shorten the sequential chain.
-  static const L fine[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {32, 16}};
-  static const L coarse[] = {{4, 1}, {4, 2}, {4, 4}, {4, 8}, {4, 16}, {4, 32}, {8, 32}, {16, 32}};
+  static const L fine[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {32, 4}, {32, 8}, {32, 16}};
+  static const L coarse[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {16, 32}};
   const L* list = role == PIT_FINE ? fine : coarse;
   const int n = 8;
   for (int i = 0; i < n; ++i)
@@ -96,10 +96,6 @@ int build_step_coeffs(int M, int mpt, int warps, int steps, double band_lo, doub
     for (int k = 1; k <= mpt; ++k) {
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
-    }
-    for (int j = 0; j < mpt; ++j) {
-      c->fl[j] = (double)nlp[j + 1];
-      c->fu[j] = (double)nup[mpt - j];
     }
     ld pk = nlp[mpt], qk = nup[mpt];
     for (int k = 0; k < 5; ++k) {

@@ -41,6 +41,19 @@ __device__ __forceinline__ double* zc_smem(StepShared<WARPS>* sh) {
   return reinterpret_cast<double*>(sh + 1);
 }
 
+// Correction vector, zero-padded (see be_solve): narrow path 32*MPT entries,
+// wide path the padded slab length.
+template <int MPT, int WARPS>
+__host__ __device__ constexpr int zc_len_max() { return 32 * WARPS * MPT; }
+__host__ __device__ inline int zc_len(int K0, int mpt, int warps) {
+  return K0 <= 32 * mpt ? 32 * mpt : 32 * warps * mpt;
+}
+template <int MPT, int WARPS>
+__device__ __forceinline__ void load_zc(const StepParams& P, double* s_zc, int tid) {
+  const int n = zc_len(P.K0, MPT, WARPS);
+  for (int i = tid; i < n; i += 32 * WARPS) s_zc[i] = i < P.K0 ? P.zc[i] : 0.0;
+}
+
 template <int MPT, int WARPS, bool SRC>
 struct SlabBounds {
   static constexpr int kThreads = 32 * WARPS;
@@ -59,7 +72,7 @@ __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<MPT, WARPS, SRC>::kMin
   const int b = blockIdx.x;
   const int M = P.M;
   const int g0 = tid * MPT;
-  for (int i = tid; i < P.K0; i += 32 * WARPS) s_zc[i] = P.zc[i];
+  load_zc<MPT, WARPS>(P, s_zc, tid);
 
   const double* src;
   if (b + A.in_shift >= 0)
@@ -117,7 +130,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = P.M;
   const int g0 = tid * MPT;
-  for (int i = tid; i < P.K0; i += 32 * WARPS) s_zc[i] = P.zc[i];
+  load_zc<MPT, WARPS>(P, s_zc, tid);
   double y[MPT];
   load_field<MPT>(y, A.start, g0, M);
   double g[MPT];
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
 
 template <int MPT, int WARPS, bool SRC>
 cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)P.K0;
+  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
   auto k = slab_kernel<MPT, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -163,7 +176,7 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaSt
 
 template <int MPT, int WARPS, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)P.K0;
+  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
   auto k = sweep_kernel<MPT, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -294,8 +307,8 @@ int ew_grid(size_t n) {
 }  // namespace
 
 #define PIT_LAYOUTS(X)                                                                       \
-  X(4, 1) X(4, 2) X(4, 4) X(4, 8) X(4, 16) X(4, 32) X(8, 4) X(8, 8) X(8, 16) X(8, 32) X(16, 4) \
-      X(16, 8) X(16, 16) X(16, 32) X(32, 4) X(32, 8) X(32, 16)
+  X(4, 1) X(4, 2) X(4, 4) X(4, 8) X(4, 16) X(4, 32) X(8, 4) X(8, 8) X(8, 16) X(8, 32) X(16, 2) \
+      X(16, 4) X(16, 8) X(16, 16) X(16, 32) X(32, 1) X(32, 2) X(32, 4) X(32, 8) X(32, 16)
 
 cudaError_t launch_slab(int mpt, int warps, bool src, const StepParams& P, const SlabArgs& A,
                         int ctas, cudaStream_t st) {

@@ -6,8 +6,10 @@
 // (src/pde.cpp:112-130 -> solve_cg/solve_bicgstab, src/sparse.cpp:60-206)
 // with a direct tridiagonal solve:
 //   y <- U^-1 L^-1 y            constant unit-bidiagonal factors nl, nu
-//        (chunked: per-thread sweep, Kogge-Stone warp scan of the chunk
-//         carries, sequential cross-warp carry, fix-up)
+//        (chunked, two passes per direction: a per-thread sweep with zero
+//         carry gives the chunk's end value, a Kogge-Stone warp scan plus a
+//         sequential cross-warp combine gives every chunk its true carry,
+//         and the sweep is rerun from that carry)
 //   y <- y + (gneg*y_0) zc      corner rank-1 (Sherman-Morrison) correction
 // and the diagonal scale inv is deferred: applied as inv^R every R steps
 // (homogeneous propagation) or every step when a source is added.
@@ -23,7 +25,6 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct StepParams {
   double nl, nu, inv, gneg, invR, invLast;
-  double fl[32], fu[32];
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
   int M, steps, R, K0;
@@ -41,73 +42,86 @@ struct StepShared {
   double b;
 };
 
+// d = fma(a, b, d) when p, else d unchanged: one predicated DFMA (no selects).
+__device__ __forceinline__ void fma_if(bool p, double& d, double a, double b) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t}"
+      : "+d"(d)
+      : "d"(a), "d"(b), "r"((unsigned)p));
+}
+
+// s_zc holds the correction vector zero-padded to 32*MPT entries (narrow
+// path, K0 <= 32*MPT: only warp 0 touches it) or to the padded slab length
+// (wide path); fma(c, 0, y) == y, so padding does not change any bit.
 template <int MPT, int WARPS>
 __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P, double plane,
                                          double qlane, StepShared<WARPS>& sh,
                                          const double* __restrict__ s_zc, int lane, int warp,
-                                         int g0) {
-  // ---- forward: L^-1 ----
+                                         int g0, bool ghosts, bool wide) {
+  // ---- forward: L^-1 (pass 1: chunk end with zero carry-in) ----
+  double z = y[0];
 #pragma unroll
-  for (int j = 1; j < MPT; ++j) y[j] = fma(P.nl, y[j - 1], y[j]);
-  double I = y[MPT - 1];
+  for (int j = 1; j < MPT; ++j) z = fma(P.nl, z, y[j]);
+  double I = z;
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const double t = __shfl_up_sync(kFull, I, 1 << s);
-    if (lane >= (1 << s)) I = fma(P.pp[s], t, I);
+    fma_if(lane >= (1 << s), I, P.pp[s], t);
   }
   const double Ip = __shfl_up_sync(kFull, I, 1);
   double Wc = 0.0;
   if (WARPS > 1) {
     if (lane == 31) sh.fw[warp] = I;
     __syncthreads();
-    for (int v = 0; v < warp; ++v) Wc = fma(P.p32, Wc, sh.fw[v]);
+#pragma unroll
+    for (int v = 0; v < WARPS - 1; ++v) fma_if(v < warp, Wc, P.p32, sh.fw[v]);
   }
-  const double Cc = lane == 0 ? Wc : fma(plane, Wc, Ip);
+  double Cc = Wc;
+  if (lane != 0) Cc = fma(plane, Wc, Ip);
+  // pass 2: the chunk's sweep again, from the true carry
+  y[0] = fma(P.nl, Cc, y[0]);
 #pragma unroll
-  for (int j = 0; j < MPT; ++j) y[j] = fma(P.fl[j], Cc, y[j]);
-  if (g0 + MPT > P.M) {
+  for (int j = 1; j < MPT; ++j) y[j] = fma(P.nl, y[j - 1], y[j]);
+  if (ghosts) {
 #pragma unroll
-    for (int j = 0; j < MPT; ++j)
-      if (g0 + j >= P.M) y[j] = 0.0;  // Dirichlet: padded nodes decouple
+    for (int j = 0; j < MPT; ++j) y[j] = (g0 + j < P.M) ? y[j] : 0.0;  // Dirichlet padding
   }
-  // ---- backward: U^-1 ----
+  // ---- backward: U^-1 (pass 1: chunk start with zero carry from the right) ----
+  double h = y[MPT - 1];
 #pragma unroll
-  for (int j = MPT - 2; j >= 0; --j) y[j] = fma(P.nu, y[j + 1], y[j]);
-  double J = y[0];
+  for (int j = MPT - 2; j >= 0; --j) h = fma(P.nu, h, y[j]);
+  double J = h;
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const double t = __shfl_down_sync(kFull, J, 1 << s);
-    if (lane < 32 - (1 << s)) J = fma(P.qq[s], t, J);
+    fma_if(lane < 32 - (1 << s), J, P.qq[s], t);
   }
   const double Jn = __shfl_down_sync(kFull, J, 1);
   double Vc = 0.0;
   if (WARPS > 1) {
     if (lane == 0) sh.bw[warp] = J;
     __syncthreads();
-    for (int v = WARPS - 1; v > warp; --v) Vc = fma(P.q32, Vc, sh.bw[v]);
-  }
-  const double Rc = lane == 31 ? Vc : fma(qlane, Vc, Jn);
 #pragma unroll
-  for (int j = 0; j < MPT; ++j) y[j] = fma(P.fu[j], Rc, y[j]);
+    for (int v = WARPS - 1; v > 0; --v) fma_if(v > warp, Vc, P.q32, sh.bw[v]);
+  }
+  double Rc = Vc;
+  if (lane != 31) Rc = fma(qlane, Vc, Jn);
+  // pass 2
+  y[MPT - 1] = fma(P.nu, Rc, y[MPT - 1]);
+#pragma unroll
+  for (int j = MPT - 2; j >= 0; --j) y[j] = fma(P.nu, y[j + 1], y[j]);
   // ---- corner rank-1 correction ----
-  if (P.K0 <= 32 * MPT) {
+  if (!wide) {
     if (warp == 0) {
       const double c = P.gneg * __shfl_sync(kFull, y[0], 0);
-      if (g0 < P.K0) {
 #pragma unroll
-        for (int j = 0; j < MPT; ++j)
-          if (g0 + j < P.K0) y[j] = fma(c, s_zc[g0 + j], y[j]);
-      }
+      for (int j = 0; j < MPT; ++j) y[j] = fma(c, s_zc[g0 + j], y[j]);
     }
   } else {
     if (warp == 0 && lane == 0) sh.b = y[0];
     __syncthreads();
     const double c = P.gneg * sh.b;
-    if (g0 < P.K0) {
 #pragma unroll
-      for (int j = 0; j < MPT; ++j)
-        if (g0 + j < P.K0) y[j] = fma(c, s_zc[g0 + j], y[j]);
-    }
+    for (int j = 0; j < MPT; ++j) y[j] = fma(c, s_zc[g0 + j], y[j]);
   }
 }
 
@@ -121,13 +135,15 @@ __device__ __forceinline__ void propagate_slab(double (&y)[MPT], const StepParam
                                                const double* __restrict__ s_zc, int lane,
                                                int warp, int g0, const double* __restrict__ ds,
                                                const double (&g)[MPT]) {
+  const bool ghosts = P.M < 32 * WARPS * MPT;
+  const bool wide = P.K0 > 32 * MPT;
   if (SRC) {
     double dsk = ds[0];
     for (int k = 0; k < P.steps; ++k) {
       const double dsn = (k + 1 < P.steps) ? ds[k + 1] : 0.0;
 #pragma unroll
       for (int j = 0; j < MPT; ++j) y[j] = fma(dsk, g[j], y[j]);
-      be_solve<MPT, WARPS>(y, P, plane, qlane, sh, s_zc, lane, warp, g0);
+      be_solve<MPT, WARPS>(y, P, plane, qlane, sh, s_zc, lane, warp, g0, ghosts, wide);
 #pragma unroll
       for (int j = 0; j < MPT; ++j) y[j] = y[j] * P.inv;
       dsk = dsn;
@@ -135,7 +151,7 @@ __device__ __forceinline__ void propagate_slab(double (&y)[MPT], const StepParam
   } else {
     int cnt = 0;
     for (int k = 0; k < P.steps; ++k) {
-      be_solve<MPT, WARPS>(y, P, plane, qlane, sh, s_zc, lane, warp, g0);
+      be_solve<MPT, WARPS>(y, P, plane, qlane, sh, s_zc, lane, warp, g0, ghosts, wide);
       if (++cnt == P.R) {
         cnt = 0;
 #pragma unroll

@@ -11,6 +11,7 @@ from paper_2203_10148_b200 import _lib, api, configs  # noqa: E402
 
 
 def main(name="c2", reps=5, layout=None):
+    reps = int(reps)
     p = configs.make(name)
     fl = tuple(int(v) for v in layout.split(",")) if layout else None
     ctx = api.BlockOperatorContext(p, fine_layout=fl)
@@ -18,7 +19,9 @@ def main(name="c2", reps=5, layout=None):
     dev = torch.device("cuda:0")
     x = torch.tensor(np.random.default_rng(0).uniform(-1, 1, (p.N, p.M)), device=dev)
     out = torch.empty_like(x)
-    st = torch.cuda.current_stream().cuda_stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    st = stream.cuda_stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     gp = configs.gp_steps_per_apply(p)
     for label, fn in (
