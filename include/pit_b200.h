@@ -135,6 +135,7 @@ typedef struct pit_step_coeffs {
   double dstar, nl, nu, inv, gneg;
   int32_t K0, R;
   double invR, invLast;
+  double fl[64], fu[64];
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
 } pit_step_coeffs;

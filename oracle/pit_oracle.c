@@ -79,6 +79,10 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int warps, int steps, double 
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
     }
+    for (int j = 0; j < m; ++j) {
+      s->fl[j] = (double)nlp[j + 1];
+      s->fu[j] = (double)nup[m - j];
+    }
     ld pk = nlp[m], qk = nup[m];
     for (int k = 0; k < 5; ++k) {
       s->pp[k] = (double)pk;
@@ -123,9 +127,10 @@ void orc_stepper_free(orc_stepper* s) {
 
 /* One unscaled solve y <- U^-1 L^-1 b plus the corner correction, on the
  * padded array y[Mp], chunked exactly like the CUDA step (pit_step.cuh
- * be_solve): per direction, pass 1 gives each chunk's end value with zero
- * carry, the warp Kogge-Stone scan + sequential cross-warp combine give the
- * true carries, pass 2 reruns each chunk's sweep from its carry. */
+ * be_solve): per direction, a local sweep with zero carry, the warp
+ * Kogge-Stone scan + sequential cross-warp combine of the chunk end values,
+ * and a fix-up y_j += w_j * carry with w_j = nl^(j+1) (forward) or
+ * nu^(m-j) (backward). */
 static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   const int m = s->m, W = s->warps, T = 32 * W, M = s->M;
   double* Z = scratch;          /* [T] local end values / scan */
@@ -133,12 +138,11 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   double* tot = scratch + 2 * T;/* [W] */
   double* tmp = scratch + 2 * T + W; /* [32] */
 
-  /* forward pass 1 */
+  /* forward local sweeps */
   for (int k = 0; k < T; ++k) {
-    const double* c = y + (size_t)k * m;
-    double z = c[0];
-    for (int j = 1; j < m; ++j) z = fma(s->nl, z, c[j]);
-    Z[k] = z;
+    double* c = y + (size_t)k * m;
+    for (int j = 1; j < m; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
+    Z[k] = c[m - 1];
   }
   /* warp Kogge-Stone inclusive scans */
   for (int w = 0; w < W; ++w) {
@@ -158,20 +162,19 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
       C[k] = (l == 0) ? Wc : fma(s->plane[l], Wc, Z[k - 1]);
     }
   }
-  /* forward pass 2 + Dirichlet ghosts */
+  /* forward fix-ups + Dirichlet ghosts */
   for (int k = 0; k < T; ++k) {
     double* c = y + (size_t)k * m;
-    c[0] = fma(s->nl, C[k], c[0]);
-    for (int j = 1; j < m; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
-    for (int j = 0; j < m; ++j)
+    for (int j = 0; j < m; ++j) {
+      c[j] = fma(s->fl[j], C[k], c[j]);
       if (k * m + j >= M) c[j] = 0.0;
+    }
   }
-  /* backward pass 1 */
+  /* backward local sweeps */
   for (int k = 0; k < T; ++k) {
-    const double* c = y + (size_t)k * m;
-    double h = c[m - 1];
-    for (int j = m - 2; j >= 0; --j) h = fma(s->nu, h, c[j]);
-    Z[k] = h;
+    double* c = y + (size_t)k * m;
+    for (int j = m - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
+    Z[k] = c[0];
   }
   for (int w = 0; w < W; ++w) {
     double* J = Z + 32 * w;
@@ -191,11 +194,9 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
       C[k] = (l == 31) ? Vc : fma(s->qlane[l], Vc, Z[k + 1]);
     }
   }
-  /* backward pass 2 */
   for (int k = 0; k < T; ++k) {
     double* c = y + (size_t)k * m;
-    c[m - 1] = fma(s->nu, C[k], c[m - 1]);
-    for (int j = m - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
+    for (int j = 0; j < m; ++j) c[j] = fma(s->fu[j], C[k], c[j]);
   }
   /* corner rank-1 correction */
   {

@@ -56,6 +56,7 @@ typedef struct orc_stepper {
   double dstar, nl, nu, inv;
   double gneg;             /* -gamma' of the corner rank-1 correction */
   int K0;                  /* correction extent */
+  double fl[ORC_MAX_M], fu[ORC_MAX_M]; /* fix-up weights nl^(j+1), nu^(m-j) */
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
   int R;                   /* rescale period, homogeneous propagation */

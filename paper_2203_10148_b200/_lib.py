@@ -72,7 +72,8 @@ class StepCoeffsC(C.Structure):
                 ("delta", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("dstar", C.c_double), ("nl", C.c_double), ("nu", C.c_double),
                 ("inv", C.c_double), ("gneg", C.c_double), ("K0", C.c_int32), ("R", C.c_int32),
-                ("invR", C.c_double), ("invLast", C.c_double), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
+                ("invR", C.c_double), ("invLast", C.c_double), ("fl", C.c_double * 64),
+                ("fu", C.c_double * 64), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
                 ("qlane", C.c_double * 32)]
 

@@ -35,7 +35,7 @@ Layout auto_layout(int M, int role) {
   // fine: 16 points per thread (32 registers of state) once M is large enough,
   // so four slab CTAs fit per SM; coarse (one persistent CTA): as many
   // threads as possible, few points each, to shorten the sequential chain.
-  static const L fine[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {32, 4}, {32, 8}, {32, 16}};
+  static const L fine[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {32, 16}};
   static const L coarse[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {16, 32}};
   const L* list = role == PIT_FINE ? fine : coarse;
   const int n = 8;
@@ -96,6 +96,10 @@ int build_step_coeffs(int M, int mpt, int warps, int steps, double band_lo, doub
     for (int k = 1; k <= mpt; ++k) {
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
+    }
+    for (int j = 0; j < mpt; ++j) {
+      c->fl[j] = (double)nlp[j + 1];
+      c->fu[j] = (double)nup[mpt - j];
     }
     ld pk = nlp[mpt], qk = nup[mpt];
     for (int k = 0; k < 5; ++k) {

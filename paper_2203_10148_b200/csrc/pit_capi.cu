@@ -143,6 +143,8 @@ void fill_params(const pit_step_coeffs& c, StepParams* P) {
   P->invR = c.invR;
   P->invLast = c.invLast;
   for (int j = 0; j < 32; ++j) {
+    P->fl[j] = j < c.mpt ? c.fl[j] : 0.0;
+    P->fu[j] = j < c.mpt ? c.fu[j] : 0.0;
     P->plane[j] = c.plane[j];
     P->qlane[j] = c.qlane[j];
   }

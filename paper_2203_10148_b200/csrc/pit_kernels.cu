@@ -36,8 +36,8 @@ __device__ __forceinline__ bool all_finite(const double (&y)[MPT], int g0, int M
   return ok;
 }
 
-template <int WARPS>
-__device__ __forceinline__ double* zc_smem(StepShared<WARPS>* sh) {
+template <int MPT, int WARPS>
+__device__ __forceinline__ double* zc_smem(StepShared<MPT, WARPS>* sh) {
   return reinterpret_cast<double*>(sh + 1);
 }
 
@@ -66,13 +66,14 @@ template <int MPT, int WARPS, bool SRC>
 __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<MPT, WARPS, SRC>::kMin))
     slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
-  double* s_zc = zc_smem<WARPS>(sh);
+  StepShared<MPT, WARPS>* sh = reinterpret_cast<StepShared<MPT, WARPS>*>(smem_raw);
+  double* s_zc = zc_smem<MPT, WARPS>(sh);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
   const int M = P.M;
   const int g0 = tid * MPT;
   load_zc<MPT, WARPS>(P, s_zc, tid);
+  init_step_shared<MPT, WARPS>(P, *sh, tid);
 
   const double* src;
   if (b + A.in_shift >= 0)
@@ -83,11 +84,10 @@ __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<MPT, WARPS, SRC>::kMin
   load_field<MPT>(y, src, g0, M);
   double g[MPT];
   if (SRC) load_field<MPT>(g, P.shape, g0, M);
-  const double plane = P.plane[lane], qlane = P.qlane[lane];
   const int slab = A.slab0 + b;
   __syncthreads();
 
-  propagate_slab<MPT, WARPS, SRC>(y, P, plane, qlane, *sh, s_zc, lane, warp, g0,
+  propagate_slab<MPT, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0,
                                   SRC ? P.ds + (size_t)slab * P.steps : nullptr, g);
 
   if (!all_finite<MPT>(y, g0, M)) atomicMin(A.status, slab);
@@ -125,17 +125,17 @@ template <int MPT, int WARPS, bool SRC>
 __global__ void __launch_bounds__(32 * WARPS, 1)
     sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
-  double* s_zc = zc_smem<WARPS>(sh);
+  StepShared<MPT, WARPS>* sh = reinterpret_cast<StepShared<MPT, WARPS>*>(smem_raw);
+  double* s_zc = zc_smem<MPT, WARPS>(sh);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = P.M;
   const int g0 = tid * MPT;
   load_zc<MPT, WARPS>(P, s_zc, tid);
+  init_step_shared<MPT, WARPS>(P, *sh, tid);
   double y[MPT];
   load_field<MPT>(y, A.start, g0, M);
   double g[MPT];
   if (SRC) load_field<MPT>(g, P.shape, g0, M);
-  const double plane = P.plane[lane], qlane = P.qlane[lane];
   __syncthreads();
   bool ok = true;
   int bad = 0x7fffffff;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
     const size_t off = (size_t)b * M;
     double v[MPT];
     load_field<MPT>(v, A.V ? A.V + off : nullptr, g0, M);
-    propagate_slab<MPT, WARPS, SRC>(y, P, plane, qlane, *sh, s_zc, lane, warp, g0,
+    propagate_slab<MPT, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0,
                                     SRC ? P.ds + (size_t)slab * P.steps : nullptr, g);
     if (ok && !all_finite<MPT>(y, g0, M)) {
       ok = false;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
 
 template <int MPT, int WARPS, bool SRC>
 cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
+  const size_t smem = sizeof(StepShared<MPT, WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
   auto k = slab_kernel<MPT, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -176,7 +176,7 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaSt
 
 template <int MPT, int WARPS, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
+  const size_t smem = sizeof(StepShared<MPT, WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
   auto k = sweep_kernel<MPT, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -6,10 +6,9 @@
 // (src/pde.cpp:112-130 -> solve_cg/solve_bicgstab, src/sparse.cpp:60-206)
 // with a direct tridiagonal solve:
 //   y <- U^-1 L^-1 y            constant unit-bidiagonal factors nl, nu
-//        (chunked, two passes per direction: a per-thread sweep with zero
-//         carry gives the chunk's end value, a Kogge-Stone warp scan plus a
-//         sequential cross-warp combine gives every chunk its true carry,
-//         and the sweep is rerun from that carry)
+//        (chunked: per-thread sweep with zero carry, Kogge-Stone warp scan of
+//         the chunk end values plus a sequential cross-warp combine for the
+//         true carries, and a fix-up y_j += w_j * carry)
 //   y <- y + (gneg*y_0) zc      corner rank-1 (Sherman-Morrison) correction
 // and the diagonal scale inv is deferred: applied as inv^R every R steps
 // (homogeneous propagation) or every step when a source is added.
@@ -25,6 +24,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct StepParams {
   double nl, nu, inv, gneg, invR, invLast;
+  double fl[32], fu[32];
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
   int M, steps, R, K0;
@@ -33,82 +33,93 @@ struct StepParams {
   const double* ds;     // [slabs*steps] dt*s(t_k) table (device) or nullptr
 };
 
-// Shared-memory layout used by the step: s_fw[WARPS], s_bw[WARPS], s_b[1]
-// (broadcast), s_zc[K0] (correction vector).
-template <int WARPS>
+// Shared memory of one slab CTA: cross-warp carries, broadcast scalar, and
+// the step's coefficient tables (read with LDS instead of indexed constant
+// loads, which serialise across lanes).  The correction vector follows.
+template <int MPT, int WARPS>
 struct StepShared {
   double fw[WARPS > 1 ? WARPS : 1];
   double bw[WARPS > 1 ? WARPS : 1];
   double b;
+  double pad;
+  double fl[MPT], fu[MPT];     // fix-up weights nl^(j+1), nu^(MPT-j)
+  double plane[32], qlane[32]; // per-lane carry weights p^lane, q^(31-lane)
+  double cf[5][32], cb[5][32]; // Kogge-Stone weights, 0 where a lane keeps its value
 };
 
-// d = fma(a, b, d) when p, else d unchanged: one predicated DFMA (no selects).
-__device__ __forceinline__ void fma_if(bool p, double& d, double a, double b) {
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t}"
-      : "+d"(d)
-      : "d"(a), "d"(b), "r"((unsigned)p));
+template <int MPT, int WARPS>
+__device__ __forceinline__ void init_step_shared(const StepParams& P, StepShared<MPT, WARPS>& sh,
+                                                 int tid) {
+  for (int i = tid; i < 32; i += 32 * WARPS) {
+    sh.plane[i] = P.plane[i];
+    sh.qlane[i] = P.qlane[i];
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      sh.cf[s][i] = i >= (1 << s) ? P.pp[s] : 0.0;
+      sh.cb[s][i] = i < 32 - (1 << s) ? P.qq[s] : 0.0;
+    }
+  }
+  for (int j = tid; j < MPT; j += 32 * WARPS) {
+    sh.fl[j] = P.fl[j];
+    sh.fu[j] = P.fu[j];
+  }
 }
 
 // s_zc holds the correction vector zero-padded to 32*MPT entries (narrow
 // path, K0 <= 32*MPT: only warp 0 touches it) or to the padded slab length
 // (wide path); fma(c, 0, y) == y, so padding does not change any bit.
+// Likewise fma(0, t, I) == I keeps a lane's scan value where the reference
+// scan skips it, and the lane-0 / lane-31 carry uses weight 1 on a zeroed
+// neighbour value.
 template <int MPT, int WARPS>
-__device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P, double plane,
-                                         double qlane, StepShared<WARPS>& sh,
+__device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P,
+                                         StepShared<MPT, WARPS>& sh,
                                          const double* __restrict__ s_zc, int lane, int warp,
                                          int g0, bool ghosts, bool wide) {
-  // ---- forward: L^-1 (pass 1: chunk end with zero carry-in) ----
-  double z = y[0];
+  // ---- forward: L^-1 ----
 #pragma unroll
-  for (int j = 1; j < MPT; ++j) z = fma(P.nl, z, y[j]);
-  double I = z;
+  for (int j = 1; j < MPT; ++j) y[j] = fma(P.nl, y[j - 1], y[j]);
+  double I = y[MPT - 1];
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const double t = __shfl_up_sync(kFull, I, 1 << s);
-    fma_if(lane >= (1 << s), I, P.pp[s], t);
+    I = fma(sh.cf[s][lane], t, I);
   }
-  const double Ip = __shfl_up_sync(kFull, I, 1);
+  double Ip = __shfl_up_sync(kFull, I, 1);
+  Ip = lane == 0 ? 0.0 : Ip;
   double Wc = 0.0;
   if (WARPS > 1) {
     if (lane == 31) sh.fw[warp] = I;
     __syncthreads();
-#pragma unroll
-    for (int v = 0; v < WARPS - 1; ++v) fma_if(v < warp, Wc, P.p32, sh.fw[v]);
+    for (int v = 0; v < warp; ++v) Wc = fma(P.p32, Wc, sh.fw[v]);
   }
-  double Cc = Wc;
-  if (lane != 0) Cc = fma(plane, Wc, Ip);
-  // pass 2: the chunk's sweep again, from the true carry
-  y[0] = fma(P.nl, Cc, y[0]);
+  const double Cc = fma(sh.plane[lane], Wc, Ip);
 #pragma unroll
-  for (int j = 1; j < MPT; ++j) y[j] = fma(P.nl, y[j - 1], y[j]);
+  for (int j = MPT - 1; j >= 0; --j) y[j] = fma(sh.fl[j], Cc, y[j]);
   if (ghosts) {
 #pragma unroll
     for (int j = 0; j < MPT; ++j) y[j] = (g0 + j < P.M) ? y[j] : 0.0;  // Dirichlet padding
   }
-  // ---- backward: U^-1 (pass 1: chunk start with zero carry from the right) ----
-  double h = y[MPT - 1];
+  // ---- backward: U^-1 ----
 #pragma unroll
-  for (int j = MPT - 2; j >= 0; --j) h = fma(P.nu, h, y[j]);
-  double J = h;
+  for (int j = MPT - 2; j >= 0; --j) y[j] = fma(P.nu, y[j + 1], y[j]);
+  double J = y[0];
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const double t = __shfl_down_sync(kFull, J, 1 << s);
-    fma_if(lane < 32 - (1 << s), J, P.qq[s], t);
+    J = fma(sh.cb[s][lane], t, J);
   }
-  const double Jn = __shfl_down_sync(kFull, J, 1);
+  double Jn = __shfl_down_sync(kFull, J, 1);
+  Jn = lane == 31 ? 0.0 : Jn;
   double Vc = 0.0;
   if (WARPS > 1) {
     if (lane == 0) sh.bw[warp] = J;
     __syncthreads();
-#pragma unroll
-    for (int v = WARPS - 1; v > 0; --v) fma_if(v > warp, Vc, P.q32, sh.bw[v]);
+    for (int v = WARPS - 1; v > warp; --v) Vc = fma(P.q32, Vc, sh.bw[v]);
   }
-  double Rc = Vc;
-  if (lane != 31) Rc = fma(qlane, Vc, Jn);
-  // pass 2
-  y[MPT - 1] = fma(P.nu, Rc, y[MPT - 1]);
+  const double Rc = fma(sh.qlane[lane], Vc, Jn);
 #pragma unroll
-  for (int j = MPT - 2; j >= 0; --j) y[j] = fma(P.nu, y[j + 1], y[j]);
+  for (int j = 0; j < MPT; ++j) y[j] = fma(sh.fu[j], Rc, y[j]);
   // ---- corner rank-1 correction ----
   if (!wide) {
     if (warp == 0) {
@@ -130,8 +141,7 @@ __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P, 
 // slab's row of the dt*s(t_k) table; g holds the thread's source shape.
 template <int MPT, int WARPS, bool SRC>
 __device__ __forceinline__ void propagate_slab(double (&y)[MPT], const StepParams& P,
-                                               double plane, double qlane,
-                                               StepShared<WARPS>& sh,
+                                               StepShared<MPT, WARPS>& sh,
                                                const double* __restrict__ s_zc, int lane,
                                                int warp, int g0, const double* __restrict__ ds,
                                                const double (&g)[MPT]) {
@@ -143,7 +153,7 @@ __device__ __forceinline__ void propagate_slab(double (&y)[MPT], const StepParam
       const double dsn = (k + 1 < P.steps) ? ds[k + 1] : 0.0;
 #pragma unroll
       for (int j = 0; j < MPT; ++j) y[j] = fma(dsk, g[j], y[j]);
-      be_solve<MPT, WARPS>(y, P, plane, qlane, sh, s_zc, lane, warp, g0, ghosts, wide);
+      be_solve<MPT, WARPS>(y, P, sh, s_zc, lane, warp, g0, ghosts, wide);
 #pragma unroll
       for (int j = 0; j < MPT; ++j) y[j] = y[j] * P.inv;
       dsk = dsn;
@@ -151,7 +161,7 @@ __device__ __forceinline__ void propagate_slab(double (&y)[MPT], const StepParam
   } else {
     int cnt = 0;
     for (int k = 0; k < P.steps; ++k) {
-      be_solve<MPT, WARPS>(y, P, plane, qlane, sh, s_zc, lane, warp, g0, ghosts, wide);
+      be_solve<MPT, WARPS>(y, P, sh, s_zc, lane, warp, g0, ghosts, wide);
       if (++cnt == P.R) {
         cnt = 0;
 #pragma unroll

@@ -44,6 +44,8 @@ def test_coefficients_bitwise_equal_product(name, role):
             assert getattr(st, f) == getattr(c, f), f
         for f in ("pp", "qq", "plane", "qlane"):
             assert list(getattr(st, f)) == list(getattr(c, f)), f
+        assert list(st.fl)[: c.mpt] == list(c.fl)[: c.mpt]
+        assert list(st.fu)[: c.mpt] == list(c.fu)[: c.mpt]
         assert np.array_equal(np.ctypeslib.as_array(st.zc, (p.M,)), zc)
     finally:
         O.orc().orc_stepper_free(C.byref(st))
