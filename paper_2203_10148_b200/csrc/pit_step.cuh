@@ -42,9 +42,7 @@ struct StepShared {
   double bw[WARPS > 1 ? WARPS : 1];
   double b;
   double pad;
-  double fl[MPT], fu[MPT];     // fix-up weights nl^(j+1), nu^(MPT-j)
   double plane[32], qlane[32]; // per-lane carry weights p^lane, q^(31-lane)
-  double cf[5][32], cb[5][32]; // Kogge-Stone weights, 0 where a lane keeps its value
 };
 
 template <int MPT, int WARPS>
@@ -53,24 +51,37 @@ __device__ __forceinline__ void init_step_shared(const StepParams& P, StepShared
   for (int i = tid; i < 32; i += 32 * WARPS) {
     sh.plane[i] = P.plane[i];
     sh.qlane[i] = P.qlane[i];
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-      sh.cf[s][i] = i >= (1 << s) ? P.pp[s] : 0.0;
-      sh.cb[s][i] = i < 32 - (1 << s) ? P.qq[s] : 0.0;
-    }
   }
-  for (int j = tid; j < MPT; j += 32 * WARPS) {
-    sh.fl[j] = P.fl[j];
-    sh.fu[j] = P.fu[j];
-  }
+}
+
+// Kogge-Stone stage: I += c * I[lane -/+ d] on lanes whose source lane exists
+// (shfl's in-range predicate guards the DFMA; other lanes keep I).
+__device__ __forceinline__ void scan_stage_up(double& I, double c, int d) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, slo, shi;\n\t.reg .f64 t;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "shfl.sync.up.b32 slo|p, lo, %2, 0, -1;\n\t"
+      "shfl.sync.up.b32 shi, hi, %2, 0, -1;\n\t"
+      "mov.b64 t, {slo, shi};\n\t"
+      "@p fma.rn.f64 %0, %1, t, %0;\n\t}"
+      : "+d"(I)
+      : "d"(c), "r"(d));
+}
+__device__ __forceinline__ void scan_stage_down(double& J, double c, int d) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, slo, shi;\n\t.reg .f64 t;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "shfl.sync.down.b32 slo|p, lo, %2, 31, -1;\n\t"
+      "shfl.sync.down.b32 shi, hi, %2, 31, -1;\n\t"
+      "mov.b64 t, {slo, shi};\n\t"
+      "@p fma.rn.f64 %0, %1, t, %0;\n\t}"
+      : "+d"(J)
+      : "d"(c), "r"(d));
 }
 
 // s_zc holds the correction vector zero-padded to 32*MPT entries (narrow
 // path, K0 <= 32*MPT: only warp 0 touches it) or to the padded slab length
 // (wide path); fma(c, 0, y) == y, so padding does not change any bit.
-// Likewise fma(0, t, I) == I keeps a lane's scan value where the reference
-// scan skips it, and the lane-0 / lane-31 carry uses weight 1 on a zeroed
-// neighbour value.
+// The lane-0 / lane-31 carry uses weight 1 on a zeroed neighbour value:
+// fma(1, W, 0) == W.
 template <int MPT, int WARPS>
 __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P,
                                          StepShared<MPT, WARPS>& sh,
@@ -81,10 +92,7 @@ __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P,
   for (int j = 1; j < MPT; ++j) y[j] = fma(P.nl, y[j - 1], y[j]);
   double I = y[MPT - 1];
 #pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const double t = __shfl_up_sync(kFull, I, 1 << s);
-    I = fma(sh.cf[s][lane], t, I);
-  }
+  for (int s = 0; s < 5; ++s) scan_stage_up(I, P.pp[s], 1 << s);
   double Ip = __shfl_up_sync(kFull, I, 1);
   Ip = lane == 0 ? 0.0 : Ip;
   double Wc = 0.0;
@@ -95,7 +103,7 @@ __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P,
   }
   const double Cc = fma(sh.plane[lane], Wc, Ip);
 #pragma unroll
-  for (int j = MPT - 1; j >= 0; --j) y[j] = fma(sh.fl[j], Cc, y[j]);
+  for (int j = MPT - 1; j >= 0; --j) y[j] = fma(P.fl[j], Cc, y[j]);
   if (ghosts) {
 #pragma unroll
     for (int j = 0; j < MPT; ++j) y[j] = (g0 + j < P.M) ? y[j] : 0.0;  // Dirichlet padding
@@ -105,10 +113,7 @@ __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P,
   for (int j = MPT - 2; j >= 0; --j) y[j] = fma(P.nu, y[j + 1], y[j]);
   double J = y[0];
 #pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const double t = __shfl_down_sync(kFull, J, 1 << s);
-    J = fma(sh.cb[s][lane], t, J);
-  }
+  for (int s = 0; s < 5; ++s) scan_stage_down(J, P.qq[s], 1 << s);
   double Jn = __shfl_down_sync(kFull, J, 1);
   Jn = lane == 31 ? 0.0 : Jn;
   double Vc = 0.0;
@@ -119,7 +124,7 @@ __device__ __forceinline__ void be_solve(double (&y)[MPT], const StepParams& P,
   }
   const double Rc = fma(sh.qlane[lane], Vc, Jn);
 #pragma unroll
-  for (int j = 0; j < MPT; ++j) y[j] = fma(sh.fu[j], Rc, y[j]);
+  for (int j = 0; j < MPT; ++j) y[j] = fma(P.fu[j], Rc, y[j]);
   // ---- corner rank-1 correction ----
   if (!wide) {
     if (warp == 0) {
