@@ -85,8 +85,10 @@ typedef struct pit_problem_desc {
   const double* source_shape; /* [M] host, copied; NULL when no source */
   const double* initial_value;/* [M] host y0, copied */
   int32_t device;         /* CUDA ordinal */
-  int32_t fine_mpt, fine_warps;     /* 0 = auto; else points/thread, warps/slab */
-  int32_t coarse_mpt, coarse_warps; /* 0 = auto */
+  /* kernel layout per role: points per thread, sub-chunks per thread (whose
+   * sweeps interleave), warps per slab CTA; all 0 = auto */
+  int32_t fine_mpt, fine_nsub, fine_warps;
+  int32_t coarse_mpt, coarse_nsub, coarse_warps;
 } pit_problem_desc;
 
 typedef struct pit_context pit_context;
@@ -130,12 +132,13 @@ typedef struct pit_solve_info {
  * solve, exported so tests can check that the oracle's own
  * recipe produces identical bits. */
 typedef struct pit_step_coeffs {
-  int32_t M, mpt, warps, steps;
+  int32_t M, mpt, nsub, warps, steps;
   double delta, lam, mu;
   double dstar, nl, nu, inv, gneg;
   int32_t K0, R;
   double invR, invLast;
-  double fl[64], fu[64];
+  double pS, qS;          /* nl^sub, nu^sub, sub = mpt/nsub */
+  double fl[64], fu[64];  /* nl^(j+1), nu^(sub-j), j < sub */
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
 } pit_step_coeffs;

@@ -17,13 +17,15 @@
 /* checks both produce identical bits.                                       */
 /* ------------------------------------------------------------------------ */
 
-int orc_stepper_init(orc_stepper* s, int M, int m, int warps, int steps, double band_lo,
-                     double band_diag, double band_up, double dt) {
+int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int warps, int steps,
+                     double band_lo, double band_diag, double band_up, double dt) {
   typedef long double ld;
   memset(s, 0, sizeof(*s));
-  if (M < 1 || m < 1 || m > ORC_MAX_M || warps < 1 || steps < 1) return -1;
+  if (M < 1 || m < 1 || m > ORC_MAX_M || nsub < 1 || m % nsub || warps < 1 || steps < 1)
+    return -1;
   s->M = M;
   s->m = m;
+  s->nsub = nsub;
   s->warps = warps;
   s->Mp = 32 * warps * m;
   if (s->Mp < M) return -1;
@@ -79,10 +81,13 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int warps, int steps, double 
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
     }
-    for (int j = 0; j < m; ++j) {
+    const int sub = m / nsub;
+    for (int j = 0; j < sub; ++j) {
       s->fl[j] = (double)nlp[j + 1];
-      s->fu[j] = (double)nup[m - j];
+      s->fu[j] = (double)nup[sub - j];
     }
+    s->pS = (double)nlp[sub];
+    s->qS = (double)nup[sub];
     ld pk = nlp[m], qk = nup[m];
     for (int k = 0; k < 5; ++k) {
       s->pp[k] = (double)pk;
@@ -127,22 +132,30 @@ void orc_stepper_free(orc_stepper* s) {
 
 /* One unscaled solve y <- U^-1 L^-1 b plus the corner correction, on the
  * padded array y[Mp], chunked exactly like the CUDA step (pit_step.cuh
- * be_solve): per direction, a local sweep with zero carry, the warp
- * Kogge-Stone scan + sequential cross-warp combine of the chunk end values,
- * and a fix-up y_j += w_j * carry with w_j = nl^(j+1) (forward) or
- * nu^(m-j) (backward). */
+ * be_solve).  Thread k owns m = nsub*sub points as nsub sub-chunks.  Per
+ * direction: local sub-chunk sweeps with zero carry; the thread's end value
+ * combined from its sub-chunks; the warp Kogge-Stone scan + sequential
+ * cross-warp combine give the thread carry; sub-chunk carries; fix-up
+ * y_j += w_j * carry. */
 static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   const int m = s->m, W = s->warps, T = 32 * W, M = s->M;
-  double* Z = scratch;          /* [T] local end values / scan */
-  double* C = scratch + T;      /* [T] carries */
+  const int ns = s->nsub, sub = m / ns;
+  double* Z = scratch;          /* [T] thread end values / scan */
+  double* C = scratch + T;      /* [T] thread carries */
   double* tot = scratch + 2 * T;/* [W] */
   double* tmp = scratch + 2 * T + W; /* [32] */
+  double E[ORC_MAX_M], Cs[ORC_MAX_M];
 
-  /* forward local sweeps */
+  /* forward local sweeps + thread end values */
   for (int k = 0; k < T; ++k) {
     double* c = y + (size_t)k * m;
-    for (int j = 1; j < m; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
-    Z[k] = c[m - 1];
+    for (int q = 0; q < ns; ++q) {
+      double* cq = c + q * sub;
+      for (int j = 1; j < sub; ++j) cq[j] = fma(s->nl, cq[j - 1], cq[j]);
+    }
+    double z = c[sub - 1];
+    for (int q = 1; q < ns; ++q) z = fma(s->pS, z, c[q * sub + sub - 1]);
+    Z[k] = z;
   }
   /* warp Kogge-Stone inclusive scans */
   for (int w = 0; w < W; ++w) {
@@ -162,19 +175,27 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
       C[k] = (l == 0) ? Wc : fma(s->plane[l], Wc, Z[k - 1]);
     }
   }
-  /* forward fix-ups + Dirichlet ghosts */
+  /* sub-chunk carries, forward fix-ups + Dirichlet ghosts */
   for (int k = 0; k < T; ++k) {
     double* c = y + (size_t)k * m;
-    for (int j = 0; j < m; ++j) {
-      c[j] = fma(s->fl[j], C[k], c[j]);
+    for (int q = 0; q < ns; ++q) E[q] = c[q * sub + sub - 1];
+    Cs[0] = C[k];
+    for (int q = 1; q < ns; ++q) Cs[q] = fma(s->pS, Cs[q - 1], E[q - 1]);
+    for (int q = 0; q < ns; ++q)
+      for (int j = 0; j < sub; ++j) c[q * sub + j] = fma(s->fl[j], Cs[q], c[q * sub + j]);
+    for (int j = 0; j < m; ++j)
       if (k * m + j >= M) c[j] = 0.0;
-    }
   }
-  /* backward local sweeps */
+  /* backward local sweeps + thread start values */
   for (int k = 0; k < T; ++k) {
     double* c = y + (size_t)k * m;
-    for (int j = m - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
-    Z[k] = c[0];
+    for (int q = 0; q < ns; ++q) {
+      double* cq = c + q * sub;
+      for (int j = sub - 2; j >= 0; --j) cq[j] = fma(s->nu, cq[j + 1], cq[j]);
+    }
+    double h = c[(ns - 1) * sub];
+    for (int q = ns - 2; q >= 0; --q) h = fma(s->qS, h, c[q * sub]);
+    Z[k] = h;
   }
   for (int w = 0; w < W; ++w) {
     double* J = Z + 32 * w;
@@ -196,7 +217,11 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   }
   for (int k = 0; k < T; ++k) {
     double* c = y + (size_t)k * m;
-    for (int j = 0; j < m; ++j) c[j] = fma(s->fu[j], C[k], c[j]);
+    for (int q = 0; q < ns; ++q) E[q] = c[q * sub];
+    Cs[ns - 1] = C[k];
+    for (int q = ns - 2; q >= 0; --q) Cs[q] = fma(s->qS, Cs[q + 1], E[q + 1]);
+    for (int q = 0; q < ns; ++q)
+      for (int j = 0; j < sub; ++j) c[q * sub + j] = fma(s->fu[j], Cs[q], c[q * sub + j]);
   }
   /* corner rank-1 correction */
   {
@@ -634,7 +659,8 @@ static int orc_1d_prop(void* user, int role, int with_source, const double* in, 
 
 orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double band_up, int N,
                       double total_time, int fine_steps, int coarse_steps, int fine_m,
-                      int fine_warps, int coarse_m, int coarse_warps, const double* y0,
+                      int fine_nsub, int fine_warps, int coarse_m, int coarse_nsub,
+                      int coarse_warps, const double* y0,
                       int has_source, const double* src_shape, double src_amp,
                       double src_omega, double src_phase, int use_thomas, int mode) {
   orc_1d* o = (orc_1d*)calloc(1, sizeof(orc_1d));
@@ -648,10 +674,10 @@ orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double 
   const double slab = total_time / N; /* TimeSlabPartition::slab_length */
   o->dt[0] = slab / fine_steps;       /* Propagator::internal_dt */
   o->dt[1] = slab / coarse_steps;
-  if (orc_stepper_init(&o->st[0], M, fine_m, fine_warps, fine_steps, band_lo, band_diag,
-                       band_up, o->dt[0]) ||
-      orc_stepper_init(&o->st[1], M, coarse_m, coarse_warps, coarse_steps, band_lo, band_diag,
-                       band_up, o->dt[1])) {
+  if (orc_stepper_init(&o->st[0], M, fine_m, fine_nsub, fine_warps, fine_steps, band_lo,
+                       band_diag, band_up, o->dt[0]) ||
+      orc_stepper_init(&o->st[1], M, coarse_m, coarse_nsub, coarse_warps, coarse_steps, band_lo,
+                       band_diag, band_up, o->dt[1])) {
     orc_1d_destroy(o);
     return NULL;
   }

@@ -40,7 +40,8 @@ class ProblemDesc(C.Structure):
                 ("source_kind", C.c_int32), ("source_amp", C.c_double),
                 ("source_omega", C.c_double), ("source_phase", C.c_double),
                 ("source_shape", _dp), ("initial_value", _dp), ("device", C.c_int32),
-                ("fine_mpt", C.c_int32), ("fine_warps", C.c_int32), ("coarse_mpt", C.c_int32),
+                ("fine_mpt", C.c_int32), ("fine_nsub", C.c_int32), ("fine_warps", C.c_int32),
+                ("coarse_mpt", C.c_int32), ("coarse_nsub", C.c_int32),
                 ("coarse_warps", C.c_int32)]
 
 
@@ -68,11 +69,13 @@ class SolveInfoC(C.Structure):
 
 
 class StepCoeffsC(C.Structure):
-    _fields_ = [("M", C.c_int32), ("mpt", C.c_int32), ("warps", C.c_int32), ("steps", C.c_int32),
+    _fields_ = [("M", C.c_int32), ("mpt", C.c_int32), ("nsub", C.c_int32), ("warps", C.c_int32),
+                ("steps", C.c_int32),
                 ("delta", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("dstar", C.c_double), ("nl", C.c_double), ("nu", C.c_double),
                 ("inv", C.c_double), ("gneg", C.c_double), ("K0", C.c_int32), ("R", C.c_int32),
-                ("invR", C.c_double), ("invLast", C.c_double), ("fl", C.c_double * 64),
+                ("invR", C.c_double), ("invLast", C.c_double), ("pS", C.c_double),
+                ("qS", C.c_double), ("fl", C.c_double * 64),
                 ("fu", C.c_double * 64), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
                 ("qlane", C.c_double * 32)]

@@ -132,10 +132,13 @@ class Problem1D:
                                                             self.source.phase)
             d.source_shape = dptr(sh)
         d.device = device
+        # layouts: (points/thread, warps/slab) or (points/thread, sub-chunks, warps/slab)
         if fine_layout:
-            d.fine_mpt, d.fine_warps = fine_layout
+            fl = tuple(fine_layout)
+            d.fine_mpt, d.fine_nsub, d.fine_warps = fl if len(fl) == 3 else (fl[0], 1, fl[1])
         if coarse_layout:
-            d.coarse_mpt, d.coarse_warps = coarse_layout
+            cl = tuple(coarse_layout)
+            d.coarse_mpt, d.coarse_nsub, d.coarse_warps = cl if len(cl) == 3 else (cl[0], 1, cl[1])
         return d, keep
 
 

@@ -18,41 +18,49 @@
 namespace pitb {
 
 namespace {
-struct L { int mpt, warps; };
-// fine/coarse layouts compiled into pit_kernels.cu (keep in sync with PIT_LAYOUTS there)
-const L kLayouts[] = {{4, 1},   {4, 2},  {4, 4},  {4, 8},  {4, 16}, {4, 32},  {8, 4},
-                      {8, 8},   {8, 16}, {8, 32}, {16, 2}, {16, 4}, {16, 8},  {16, 16},
-                      {16, 32}, {32, 1}, {32, 2}, {32, 4}, {32, 8}, {32, 16}};
+struct L { int mpt, nsub, warps; };
+// layouts compiled into pit_kernels.cu (keep in sync with PIT_LAYOUTS there)
+const L kLayouts[] = {{4, 1, 1},   {4, 1, 2},   {4, 1, 4},   {4, 1, 8},  {4, 1, 16},
+                      {4, 1, 32},  {8, 1, 4},   {8, 1, 8},   {8, 1, 16}, {8, 1, 32},
+                      {16, 1, 2},  {16, 1, 4},  {16, 1, 8},  {16, 1, 16}, {16, 1, 32},
+                      {32, 2, 1},  {32, 2, 2},  {32, 2, 4},  {32, 2, 8}, {64, 4, 1},
+                      {64, 4, 2},  {64, 4, 4},  {64, 2, 2},  {64, 4, 8}};
 }  // namespace
 
-bool layout_supported(int mpt, int warps) {
+bool layout_supported(int mpt, int nsub, int warps) {
   for (const L& l : kLayouts)
-    if (l.mpt == mpt && l.warps == warps) return true;
+    if (l.mpt == mpt && l.nsub == nsub && l.warps == warps) return true;
   return false;
 }
 
 Layout auto_layout(int M, int role) {
-  // fine: 16 points per thread (32 registers of state) once M is large enough,
-  // so four slab CTAs fit per SM; coarse (one persistent CTA): as many
-  // threads as possible, few points each, to shorten the sequential chain.
-  static const L fine[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {32, 16}};
-  static const L coarse[] = {{4, 1}, {4, 2}, {4, 4}, {8, 4}, {16, 4}, {16, 8}, {16, 16}, {16, 32}};
+  // fine: 64 points per thread in 4 interleaved sub-chunks of 16 once M is
+  // large (the per-warp scan/sync overhead is amortised over 64 points and the
+  // four chains hide the DFMA latency); coarse (one persistent CTA, latency
+  // bound): many threads with few points each.
+  static const L fine[] = {{4, 1, 1}, {4, 1, 2}, {4, 1, 4}, {8, 1, 4},
+                           {64, 4, 1}, {64, 4, 2}, {64, 4, 4}, {64, 4, 8}};
+  static const L coarse[] = {{4, 1, 1}, {4, 1, 2}, {4, 1, 4}, {8, 1, 4},
+                             {4, 1, 32}, {8, 1, 16}, {8, 1, 32}, {16, 1, 32}};
   const L* list = role == PIT_FINE ? fine : coarse;
-  const int n = 8;
-  for (int i = 0; i < n; ++i)
-    if (32 * list[i].warps * list[i].mpt >= M) return {list[i].mpt, list[i].warps};
-  return {0, 0};
+  for (int i = 0; i < 8; ++i)
+    if (32 * list[i].warps * list[i].mpt >= M) return {list[i].mpt, list[i].nsub, list[i].warps};
+  return {0, 0, 0};
 }
 
-int build_step_coeffs(int M, int mpt, int warps, int steps, double band_lo, double band_diag,
-                      double band_up, double dt, pit_step_coeffs* c, std::vector<double>* zc) {
+int build_step_coeffs(int M, int mpt, int nsub, int warps, int steps, double band_lo,
+                      double band_diag, double band_up, double dt, pit_step_coeffs* c,
+                      std::vector<double>* zc) {
   typedef long double ld;
   std::memset(c, 0, sizeof(*c));
-  if (M < 1 || mpt < 1 || mpt > 32 || warps < 1 || steps < 1) return PIT_ERR_INVALID_ARGUMENT;
+  if (M < 1 || mpt < 1 || mpt > 64 || nsub < 1 || mpt % nsub || mpt / nsub > 32 || warps < 1 ||
+      steps < 1)
+    return PIT_ERR_INVALID_ARGUMENT;
   if (32 * warps * mpt < M) return PIT_ERR_INVALID_ARGUMENT;
   if (!(dt > 0.0)) return PIT_ERR_INVALID_ARGUMENT;
   c->M = M;
   c->mpt = mpt;
+  c->nsub = nsub;
   c->warps = warps;
   c->steps = steps;
   c->delta = band_diag * dt + 1.0;
@@ -97,10 +105,13 @@ int build_step_coeffs(int M, int mpt, int warps, int steps, double band_lo, doub
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
     }
-    for (int j = 0; j < mpt; ++j) {
+    const int sub = mpt / nsub;
+    for (int j = 0; j < sub; ++j) {
       c->fl[j] = (double)nlp[j + 1];
-      c->fu[j] = (double)nup[mpt - j];
+      c->fu[j] = (double)nup[sub - j];
     }
+    c->pS = (double)nlp[sub];
+    c->qS = (double)nup[sub];
     ld pk = nlp[mpt], qk = nup[mpt];
     for (int k = 0; k < 5; ++k) {
       c->pp[k] = (double)pk;

@@ -60,7 +60,7 @@ struct Role {
   StepParams P{};
   double* d_zc = nullptr;
   double* d_ds = nullptr;
-  int mpt = 0, warps = 0;
+  int mpt = 0, nsub = 0, warps = 0;
 };
 
 }  // namespace
@@ -117,18 +117,23 @@ int role_coeffs(const pit_problem_desc* d, int role, pit_step_coeffs* c, std::ve
   // TimeSlabPartition::slab_length() = T/N; Propagator::internal_dt() = slab/steps
   const double dt = (d->total_time / d->slab_count) / steps;
   int mpt = role == PIT_FINE ? d->fine_mpt : d->coarse_mpt;
+  int nsub = role == PIT_FINE ? d->fine_nsub : d->coarse_nsub;
   int warps = role == PIT_FINE ? d->fine_warps : d->coarse_warps;
   if (mpt == 0 || warps == 0) {
     Layout l = auto_layout(M, role);
     mpt = l.mpt;
+    nsub = l.nsub;
     warps = l.warps;
   }
-  if (mpt == 0 || !layout_supported(mpt, warps) || 32 * mpt * warps < M)
+  if (nsub == 0) nsub = 1;
+  if (mpt == 0 || !layout_supported(mpt, nsub, warps) || 32 * mpt * warps < M)
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "pit_context_create: no compiled slab layout covers M=" + std::to_string(M));
   lay->mpt = mpt;
+  lay->nsub = nsub;
   lay->warps = warps;
-  if (build_step_coeffs(M, mpt, warps, steps, d->band_lo, d->band_diag, d->band_up, dt, c, zc))
+  if (build_step_coeffs(M, mpt, nsub, warps, steps, d->band_lo, d->band_diag, d->band_up, dt, c,
+                        zc))
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "pit_context_create: step matrix I + dt*A is not factorizable with constant "
                    "factors (needs delta^2 > 4*lam*mu)");
@@ -142,9 +147,12 @@ void fill_params(const pit_step_coeffs& c, StepParams* P) {
   P->gneg = c.gneg;
   P->invR = c.invR;
   P->invLast = c.invLast;
+  const int sub = c.mpt / c.nsub;
+  P->pS = c.pS;
+  P->qS = c.qS;
   for (int j = 0; j < 32; ++j) {
-    P->fl[j] = j < c.mpt ? c.fl[j] : 0.0;
-    P->fu[j] = j < c.mpt ? c.fu[j] : 0.0;
+    P->fl[j] = j < sub ? c.fl[j] : 0.0;
+    P->fu[j] = j < sub ? c.fu[j] : 0.0;
     P->plane[j] = c.plane[j];
     P->qlane[j] = c.qlane[j];
   }
@@ -216,7 +224,7 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
     A.out = out;
     A.slab0 = first - 1;
   }
-  CUDA_TRY(launch_slab(R.mpt, R.warps, false, R.P, A, ctas, st));
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.warps, false, R.P, A, ctas, st));
   return PIT_OK;
 }
 
@@ -245,7 +253,7 @@ int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, con
     A.slab0 = first - 1;
   }
   const bool src = with_source && ctx->has_source;
-  CUDA_TRY(launch_sweep(R.mpt, R.warps, src, R.P, A, st));
+  CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.warps, src, R.P, A, st));
   return PIT_OK;
 }
 
@@ -337,6 +345,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     if (rc) return fail(rc);
     Role& R = ctx->role[r];
     R.mpt = lay.mpt;
+    R.nsub = lay.nsub;
     R.warps = lay.warps;
     fill_params(R.c, &R.P);
     if (cudaMalloc(&R.d_zc, sizeof(double) * zc.size()) != cudaSuccess ||
@@ -527,7 +536,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
     A.out = d.p + ctx->M;
     A.slab0 = 0;
     A.status = ctx->d_status;
-    CUDA_TRY(launch_slab(R.mpt, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+    CUDA_TRY(launch_slab(R.mpt, R.nsub, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
     PIT_TRY(check_status(ctx, true));
     add_fine(ctx, stats, ms_since(t0));
   }
@@ -569,7 +578,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
   A.mode = kPropagate;
   A.out = d + ctx->M;
   A.status = ctx->d_status;
-  CUDA_TRY(launch_slab(R.mpt, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
   PIT_TRY(check_status(ctx, true));
   add_fine(ctx, stats, ms_since(t0));
   return PIT_OK;
@@ -638,7 +647,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
     // source_contribution with f == 0 is exactly zero (propagator.cpp:78)
     CUDA_TRY(cudaMemsetAsync(dout.p, 0, M * sizeof(double), ctx->stream));
   } else {
-    CUDA_TRY(launch_sweep(R.mpt, R.warps, src, R.P, A, ctx->stream));
+    CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.warps, src, R.P, A, ctx->stream));
     PIT_TRY(check_status(ctx, false));
   }
   return to_host(ctx, dout.p, M, out);

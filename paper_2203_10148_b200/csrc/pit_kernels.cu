@@ -20,31 +20,31 @@ namespace pitb {
 
 namespace {
 
-template <int MPT>
-__device__ __forceinline__ void load_field(double (&y)[MPT], const double* __restrict__ src,
+template <int SUB, int NSUB>
+__device__ __forceinline__ void load_field(double (&y)[NSUB][SUB], const double* __restrict__ src,
                                            int g0, int M) {
 #pragma unroll
-  for (int j = 0; j < MPT; ++j) y[j] = (src != nullptr && g0 + j < M) ? src[g0 + j] : 0.0;
+  for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+    for (int j = 0; j < SUB; ++j) {
+      const int i = g0 + s * SUB + j;
+      y[s][j] = (src != nullptr && i < M) ? src[i] : 0.0;
+    }
 }
 
-template <int MPT>
-__device__ __forceinline__ bool all_finite(const double (&y)[MPT], int g0, int M) {
+template <int SUB, int NSUB>
+__device__ __forceinline__ bool all_finite(const double (&y)[NSUB][SUB], int g0, int M) {
   bool ok = true;
 #pragma unroll
-  for (int j = 0; j < MPT; ++j)
-    if (g0 + j < M && !isfinite(y[j])) ok = false;
+  for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+    for (int j = 0; j < SUB; ++j)
+      if (g0 + s * SUB + j < M && !isfinite(y[s][j])) ok = false;
   return ok;
-}
-
-template <int MPT, int WARPS>
-__device__ __forceinline__ double* zc_smem(StepShared<MPT, WARPS>* sh) {
-  return reinterpret_cast<double*>(sh + 1);
 }
 
 // Correction vector, zero-padded (see be_solve): narrow path 32*MPT entries,
 // wide path the padded slab length.
-template <int MPT, int WARPS>
-__host__ __device__ constexpr int zc_len_max() { return 32 * WARPS * MPT; }
 __host__ __device__ inline int zc_len(int K0, int mpt, int warps) {
   return K0 <= 32 * mpt ? 32 * mpt : 32 * warps * mpt;
 }
@@ -57,61 +57,113 @@ __device__ __forceinline__ void load_zc(const StepParams& P, double* s_zc, int t
 template <int MPT, int WARPS, bool SRC>
 struct SlabBounds {
   static constexpr int kThreads = 32 * WARPS;
-  static constexpr int kRegs = MPT <= 16 ? 64 : 128;
+  static constexpr int kRegs = MPT <= 16 ? 64 : (MPT <= 32 ? 96 : 168);
   static constexpr int kMin0 = 65536 / (kThreads * kRegs);
   static constexpr int kMin = SRC ? 1 : (kMin0 < 1 ? 1 : (kMin0 > 16 ? 16 : kMin0));
 };
 
-template <int MPT, int WARPS, bool SRC>
-__global__ void __launch_bounds__(32 * WARPS, (SlabBounds<MPT, WARPS, SRC>::kMin))
+// Source shape for SRC kernels: read through L1 each step (not held in
+// registers) so MPT=64 layouts do not spill.
+template <int SUB, int NSUB>
+struct ShapeView {
+  const double* __restrict__ g;
+  int g0, M;
+  __device__ double operator()(int s, int j) const {
+    const int i = g0 + s * SUB + j;
+    return i < M ? __ldg(g + i) : 0.0;
+  }
+};
+
+template <int SUB, int NSUB, int WARPS, bool SRC>
+__device__ __forceinline__ void run_slab(double (&y)[NSUB][SUB], const StepParams& P,
+                                         StepShared<WARPS>& sh, const double* s_zc, int lane,
+                                         int warp, int g0, int slab) {
+  constexpr int MPT = SUB * NSUB;
+  const bool ghosts = P.M < 32 * WARPS * MPT;
+  const bool wide = P.K0 > 32 * MPT;
+  if (SRC) {
+    const double* ds = P.ds + (size_t)slab * P.steps;
+    const ShapeView<SUB, NSUB> g{P.shape, g0, P.M};
+    double dsk = ds[0];
+    for (int k = 0; k < P.steps; ++k) {
+      const double dsn = (k + 1 < P.steps) ? ds[k + 1] : 0.0;
+#pragma unroll
+      for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+        for (int j = 0; j < SUB; ++j) y[s][j] = fma(dsk, g(s, j), y[s][j]);
+      be_solve<SUB, NSUB, WARPS>(y, P, sh, s_zc, lane, warp, g0, ghosts, wide);
+#pragma unroll
+      for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+        for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.inv;
+      dsk = dsn;
+    }
+  } else {
+    int cnt = 0;
+    for (int k = 0; k < P.steps; ++k) {
+      be_solve<SUB, NSUB, WARPS>(y, P, sh, s_zc, lane, warp, g0, ghosts, wide);
+      if (++cnt == P.R) {
+        cnt = 0;
+#pragma unroll
+        for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+          for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invR;
+      }
+    }
+    if (cnt) {
+#pragma unroll
+      for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+        for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invLast;
+    }
+  }
+}
+
+template <int SUB, int NSUB, int WARPS, bool SRC>
+__global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSUB, WARPS, SRC>::kMin))
     slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
+  constexpr int MPT = SUB * NSUB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StepShared<MPT, WARPS>* sh = reinterpret_cast<StepShared<MPT, WARPS>*>(smem_raw);
-  double* s_zc = zc_smem<MPT, WARPS>(sh);
+  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
+  double* s_zc = reinterpret_cast<double*>(sh + 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
   const int M = P.M;
   const int g0 = tid * MPT;
   load_zc<MPT, WARPS>(P, s_zc, tid);
-  init_step_shared<MPT, WARPS>(P, *sh, tid);
+  init_step_shared<WARPS>(P, *sh, tid);
 
   const double* src;
   if (b + A.in_shift >= 0)
     src = A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr;
   else
     src = A.halo;
-  double y[MPT];
-  load_field<MPT>(y, src, g0, M);
-  double g[MPT];
-  if (SRC) load_field<MPT>(g, P.shape, g0, M);
+  double y[NSUB][SUB];
+  load_field<SUB, NSUB>(y, src, g0, M);
   const int slab = A.slab0 + b;
   __syncthreads();
 
-  propagate_slab<MPT, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0,
-                                  SRC ? P.ds + (size_t)slab * P.steps : nullptr, g);
+  run_slab<SUB, NSUB, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0, slab);
 
-  if (!all_finite<MPT>(y, g0, M)) atomicMin(A.status, slab);
+  if (!all_finite<SUB, NSUB>(y, g0, M)) atomicMin(A.status, slab);
   const size_t off = (size_t)b * M;
   double* out = A.out + off;
-  if (A.mode == kApplyF) {
-    const double* Ln = A.Lsub + off;
 #pragma unroll
-    for (int j = 0; j < MPT; ++j)
-      if (g0 + j < M) out[g0 + j] = Ln[g0 + j] - y[j];
-  } else if (A.mode == kResidual) {
-    const double* Ln = A.Lsub + off;
-    const double* Bn = A.rhs + off;
+  for (int s = 0; s < NSUB; ++s)
 #pragma unroll
-    for (int j = 0; j < MPT; ++j)
-      if (g0 + j < M) {
-        const double a = Ln[g0 + j] - y[j];
-        out[g0 + j] = Bn[g0 + j] - a;
+    for (int j = 0; j < SUB; ++j) {
+      const int i = g0 + s * SUB + j;
+      if (i < M) {
+        if (A.mode == kApplyF) {
+          out[i] = A.Lsub[off + i] - y[s][j];
+        } else if (A.mode == kResidual) {
+          const double a = A.Lsub[off + i] - y[s][j];
+          out[i] = A.rhs[off + i] - a;
+        } else {
+          out[i] = y[s][j];
+        }
       }
-  } else {
-#pragma unroll
-    for (int j = 0; j < MPT; ++j)
-      if (g0 + j < M) out[g0 + j] = y[j];
-  }
+    }
   if (b == 0 && A.out0 != nullptr) {
     if (A.mode == kApplyF) {
       for (int i = tid; i < M; i += 32 * WARPS) A.out0[i] = A.L0[i];
@@ -121,51 +173,93 @@ __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<MPT, WARPS, SRC>::kMin
   }
 }
 
-template <int MPT, int WARPS, bool SRC>
+// Staging layout of one block in shared memory: thread t's chunk at
+// t*(MPT+1) (odd pitch: a warp reading element e of every chunk hits
+// distinct banks), filled and drained with coalesced global accesses.
+template <int MPT>
+__device__ __forceinline__ int stage_idx(int i) {
+  return (i / MPT) * (MPT + 1) + (i % MPT);
+}
+
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int SUB, int NSUB, int WARPS, bool SRC>
 __global__ void __launch_bounds__(32 * WARPS, 1)
     sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A) {
+  constexpr int MPT = SUB * NSUB;
+  constexpr int T = 32 * WARPS;
+  constexpr int STAGE = T * (MPT + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StepShared<MPT, WARPS>* sh = reinterpret_cast<StepShared<MPT, WARPS>*>(smem_raw);
-  double* s_zc = zc_smem<MPT, WARPS>(sh);
+  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
+  double* s_zc = reinterpret_cast<double*>(sh + 1);
+  double* stage = s_zc + zc_len(P.K0, MPT, WARPS);  // [3][STAGE]: V double buffer + W out
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = P.M;
   const int g0 = tid * MPT;
   load_zc<MPT, WARPS>(P, s_zc, tid);
-  init_step_shared<MPT, WARPS>(P, *sh, tid);
-  double y[MPT];
-  load_field<MPT>(y, A.start, g0, M);
-  double g[MPT];
-  if (SRC) load_field<MPT>(g, P.shape, g0, M);
+  init_step_shared<WARPS>(P, *sh, tid);
+  double y[NSUB][SUB];
+  load_field<SUB, NSUB>(y, A.start, g0, M);
+  auto prefetch = [&](int b) {
+    double* buf = stage + (b & 1) * STAGE;
+    const double* v = A.V + (size_t)b * M;
+    for (int i = tid; i < M; i += T) cp_async8(buf + stage_idx<MPT>(i), v + i);
+    cp_async_commit();
+  };
+  if (A.V) prefetch(0);
   __syncthreads();
   bool ok = true;
   int bad = 0x7fffffff;
+  double* wbuf = stage + 2 * STAGE;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
-    const size_t off = (size_t)b * M;
-    double v[MPT];
-    load_field<MPT>(v, A.V ? A.V + off : nullptr, g0, M);
-    propagate_slab<MPT, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0,
-                                    SRC ? P.ds + (size_t)slab * P.steps : nullptr, g);
-    if (ok && !all_finite<MPT>(y, g0, M)) {
+    if (A.V && b + 1 < A.count) prefetch(b + 1);
+    run_slab<SUB, NSUB, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0, slab);
+    if (ok && !all_finite<SUB, NSUB>(y, g0, M)) {
       ok = false;
       bad = slab;
     }
     if (A.V) {
+      if (b + 1 < A.count)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+      __syncthreads();
+      const double* vb = stage + (b & 1) * STAGE + tid * (MPT + 1);
 #pragma unroll
-      for (int j = 0; j < MPT; ++j) y[j] = y[j] + v[j];
+      for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+        for (int j = 0; j < SUB; ++j) {
+          const int e = s * SUB + j;
+          y[s][j] = y[s][j] + (g0 + e < M ? vb[e] : 0.0);
+        }
     }
-    double* W = A.W + off;
+    double* wb = wbuf + tid * (MPT + 1);
 #pragma unroll
-    for (int j = 0; j < MPT; ++j)
-      if (g0 + j < M) W[g0 + j] = y[j];
+    for (int s = 0; s < NSUB; ++s)
+#pragma unroll
+      for (int j = 0; j < SUB; ++j) wb[s * SUB + j] = y[s][j];
+    __syncthreads();
+    double* W = A.W + (size_t)b * M;
+    for (int i = tid; i < M; i += T) W[i] = wbuf[stage_idx<MPT>(i)];
+    __syncthreads();  // wbuf and the V buffer of slab b are free again
   }
   if (!ok) atomicMin(A.status, bad);
 }
 
-template <int MPT, int WARPS, bool SRC>
+template <int SUB, int NSUB, int WARPS, bool SRC>
 cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<MPT, WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
-  auto k = slab_kernel<MPT, WARPS, SRC>;
+  const size_t smem =
+      sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, SUB * NSUB, WARPS);
+  auto k = slab_kernel<SUB, NSUB, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -174,10 +268,13 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaSt
   return cudaGetLastError();
 }
 
-template <int MPT, int WARPS, bool SRC>
+template <int SUB, int NSUB, int WARPS, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<MPT, WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, MPT, WARPS);
-  auto k = sweep_kernel<MPT, WARPS, SRC>;
+  constexpr int MPT = SUB * NSUB;
+  const size_t smem = sizeof(StepShared<WARPS>) +
+                      sizeof(double) * ((size_t)zc_len(P.K0, MPT, WARPS) +
+                                        3 * (size_t)(32 * WARPS) * (MPT + 1));
+  auto k = sweep_kernel<SUB, NSUB, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -306,28 +403,33 @@ int ew_grid(size_t n) {
 
 }  // namespace
 
-#define PIT_LAYOUTS(X)                                                                       \
-  X(4, 1) X(4, 2) X(4, 4) X(4, 8) X(4, 16) X(4, 32) X(8, 4) X(8, 8) X(8, 16) X(8, 32) X(16, 2) \
-      X(16, 4) X(16, 8) X(16, 16) X(16, 32) X(32, 1) X(32, 2) X(32, 4) X(32, 8) X(32, 16)
+// (points per thread, sub-chunks per thread, warps per slab) compiled here;
+// keep in sync with kLayouts in coeffs.cpp.
+#define PIT_LAYOUTS(X)                                                                    \
+  X(4, 1, 1) X(4, 1, 2) X(4, 1, 4) X(4, 1, 8) X(4, 1, 16) X(4, 1, 32) X(8, 1, 4) X(8, 1, 8) \
+  X(8, 1, 16) X(8, 1, 32) X(16, 1, 2) X(16, 1, 4) X(16, 1, 8) X(16, 1, 16) X(16, 1, 32)     \
+  X(32, 2, 1) X(32, 2, 2) X(32, 2, 4) X(32, 2, 8) X(64, 4, 1) X(64, 4, 2) X(64, 4, 4)       \
+  X(64, 2, 2) X(64, 4, 8)
 
-cudaError_t launch_slab(int mpt, int warps, bool src, const StepParams& P, const SlabArgs& A,
-                        int ctas, cudaStream_t st) {
+cudaError_t launch_slab(int mpt, int nsub, int warps, bool src, const StepParams& P,
+                        const SlabArgs& A, int ctas, cudaStream_t st) {
   if (ctas <= 0) return cudaSuccess;
-#define X(MP, W)                                                               \
-  if (mpt == MP && warps == W)                                                 \
-    return src ? slab_launch<MP, W, true>(P, A, ctas, st)                      \
-               : slab_launch<MP, W, false>(P, A, ctas, st);
+#define X(MP, NS, W)                                                           \
+  if (mpt == MP && nsub == NS && warps == W)                                   \
+    return src ? slab_launch<MP / NS, NS, W, true>(P, A, ctas, st)             \
+               : slab_launch<MP / NS, NS, W, false>(P, A, ctas, st);
   PIT_LAYOUTS(X)
 #undef X
   return cudaErrorInvalidConfiguration;
 }
 
-cudaError_t launch_sweep(int mpt, int warps, bool src, const StepParams& P, const SweepArgs& A,
-                         cudaStream_t st) {
+cudaError_t launch_sweep(int mpt, int nsub, int warps, bool src, const StepParams& P,
+                         const SweepArgs& A, cudaStream_t st) {
   if (A.count <= 0) return cudaSuccess;
-#define X(MP, W)                                                                             \
-  if (mpt == MP && warps == W)                                                               \
-    return src ? sweep_launch<MP, W, true>(P, A, st) : sweep_launch<MP, W, false>(P, A, st);
+#define X(MP, NS, W)                                                           \
+  if (mpt == MP && nsub == NS && warps == W)                                   \
+    return src ? sweep_launch<MP / NS, NS, W, true>(P, A, st)                  \
+               : sweep_launch<MP / NS, NS, W, false>(P, A, st);
   PIT_LAYOUTS(X)
 #undef X
   return cudaErrorInvalidConfiguration;

@@ -125,7 +125,8 @@ def test_c3_n16_matches_reference():
     assert rel_block(res.solution, g["pitsbicg_lambda"]) < 5e-10  # reference inner-solve floor
 
 
-@pytest.mark.parametrize("layout", [(16, 8), (8, 16), (32, 4), (16, 16), (4, 32), (8, 32)])
+@pytest.mark.parametrize("layout", [(16, 1, 8), (8, 1, 16), (32, 2, 4), (16, 1, 16), (4, 1, 32),
+                                    (8, 1, 32), (64, 4, 2), (64, 2, 2), (64, 4, 4)])
 def test_fine_layouts_bitwise_vs_oracle(layout):
     p = configs.make("c2", slabs=4)
     o = OracleProblem(p, fine_layout=layout)

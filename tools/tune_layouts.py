@@ -7,8 +7,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2203_10148_b200 import _lib, api, configs  # noqa: E402
 
-FINE = [(16, 2), (16, 4), (16, 8), (16, 16), (32, 1), (32, 2), (32, 4), (32, 8), (32, 16), (8, 8), (8, 16), (8, 32)]
-COARSE = [(4, 8), (4, 16), (4, 32), (8, 4), (8, 8), (8, 16), (8, 32), (16, 4), (16, 8), (16, 16), (16, 32), (32, 4), (32, 8)]
+FINE = [(16, 1, 4), (16, 1, 8), (16, 1, 16), (32, 2, 1), (32, 2, 2), (32, 2, 4), (32, 2, 8), (64, 4, 1), (64, 4, 2), (64, 4, 4), (64, 4, 8), (64, 2, 2), (8, 1, 8), (8, 1, 16)]
+COARSE = [(4, 1, 8), (4, 1, 16), (4, 1, 32), (8, 1, 4), (8, 1, 8), (8, 1, 16), (8, 1, 32), (16, 1, 4), (16, 1, 8), (16, 1, 16), (16, 1, 32), (32, 2, 4), (32, 2, 8), (64, 4, 2)]
 
 
 def timeit(fn, reps=3):
@@ -37,14 +37,14 @@ def main(names):
         x = torch.tensor(np.random.default_rng(0).uniform(-1, 1, (p.N, p.M)), device="cuda")
         out = torch.empty_like(x)
         for lay in FINE:
-            if 32 * lay[0] * lay[1] < p.M or 32 * lay[0] * lay[1] >= 2 * p.M:
+            if 32 * lay[0] * lay[-1] < p.M or 32 * lay[0] * lay[-1] >= 2 * p.M:
                 continue
-            ctx = api.BlockOperatorContext(p, fine_layout=lay, coarse_layout=(16, 8) if p.M <= 4096 else (16, 16))
+            ctx = api.BlockOperatorContext(p, fine_layout=lay, coarse_layout=None)
             ms = timeit(lambda: L.pit_apply_F_device(ctx.handle, x.data_ptr(), None, out.data_ptr(), 0, p.N, st))
             print(f"{name} fine {lay}: {ms:.3f} ms  {gp / ms / 1e9:.3e} gp-steps/s  {5 * gp / ms / 1e9 / 1e12 * 1e3:.2f} TF", flush=True)
             ctx.close()
         for lay in COARSE:
-            if 32 * lay[0] * lay[1] < p.M or 32 * lay[0] * lay[1] >= 2 * p.M:
+            if 32 * lay[0] * lay[-1] < p.M or 32 * lay[0] * lay[-1] >= 2 * p.M:
                 continue
             ctx = api.BlockOperatorContext(p, coarse_layout=lay)
             ms = timeit(lambda: L.pit_coarse_sweep_device(ctx.handle, x.data_ptr(), None, out.data_ptr(), 0, p.N, 0, 1, st))
