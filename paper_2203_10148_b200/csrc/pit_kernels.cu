@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
-  double* stage = s_zc + zc_len(P.K0, MPT, WARPS);  // [3][STAGE]: V double buffer + W out
+  double* stage = s_zc + zc_len(P.K0, MPT, WARPS);  // [2][STAGE]: V double buffer
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = P.M;
   const int g0 = tid * MPT;
@@ -218,7 +218,6 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   __syncthreads();
   bool ok = true;
   int bad = 0x7fffffff;
-  double* wbuf = stage + 2 * STAGE;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
     if (A.V && b + 1 < A.count) prefetch(b + 1);
@@ -242,6 +241,9 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
           y[s][j] = y[s][j] + (g0 + e < M ? vb[e] : 0.0);
         }
     }
+    // drain W_b through slab b's (now consumed) V buffer: coalesced stores
+    double* wbuf = stage + (b & 1) * STAGE;
+    // (each thread overwrites exactly the V slots it just read)
     double* wb = wbuf + tid * (MPT + 1);
 #pragma unroll
     for (int s = 0; s < NSUB; ++s)
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
     __syncthreads();
     double* W = A.W + (size_t)b * M;
     for (int i = tid; i < M; i += T) W[i] = wbuf[stage_idx<MPT>(i)];
-    __syncthreads();  // wbuf and the V buffer of slab b are free again
+    __syncthreads();  // the buffer is free for the prefetch of slab b+2
   }
   if (!ok) atomicMin(A.status, bad);
 }
@@ -273,7 +275,7 @@ cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t s
   constexpr int MPT = SUB * NSUB;
   const size_t smem = sizeof(StepShared<WARPS>) +
                       sizeof(double) * ((size_t)zc_len(P.K0, MPT, WARPS) +
-                                        3 * (size_t)(32 * WARPS) * (MPT + 1));
+                                        2 * (size_t)(32 * WARPS) * (MPT + 1));
   auto k = sweep_kernel<SUB, NSUB, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -14,7 +14,8 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 st = stream.cuda_stream
 L = _lib.lib()
-ctx = api.BlockOperatorContext(p)
+lay = tuple(int(v) for v in sys.argv[3].split(",")) if len(sys.argv) > 3 else None
+ctx = api.BlockOperatorContext(p, fine_layout=lay)
 x = torch.tensor(np.random.default_rng(0).uniform(-1, 1, (p.N, p.M)), device="cuda")
 out = torch.empty_like(x)
 for _ in range(reps):
