@@ -17,15 +17,16 @@
 /* checks both produce identical bits.                                       */
 /* ------------------------------------------------------------------------ */
 
-int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int warps, int steps,
+int orc_stepper_init(orc_stepper* s, int M, int m, int nseg, int warps, int steps,
                      double band_lo, double band_diag, double band_up, double dt) {
   typedef long double ld;
   memset(s, 0, sizeof(*s));
-  if (M < 1 || m < 1 || m > ORC_MAX_M || nsub < 1 || m % nsub || warps < 1 || steps < 1)
+  if (M < 1 || m < 1 || m > ORC_MAX_M || nseg < 1 || m % nseg || m / nseg > 32 || warps < 1 ||
+      steps < 1)
     return -1;
   s->M = M;
   s->m = m;
-  s->nsub = nsub;
+  s->nseg = nseg;
   s->warps = warps;
   s->Mp = 32 * warps * m;
   if (s->Mp < M) return -1;
@@ -74,21 +75,20 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int warps, int step
   }
   free(z);
   {
-    ld nlp[ORC_MAX_M + 1], nup[ORC_MAX_M + 1];
+    /* chunk = sub points (warp scan multiplier nl^sub); segment = T*sub */
+    const int sub = m / nseg, T = 32 * warps;
+    ld nlp[33], nup[33];
     nlp[0] = 1.0L;
     nup[0] = 1.0L;
-    for (int k = 1; k <= m; ++k) {
+    for (int k = 1; k <= sub; ++k) {
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
     }
-    const int sub = m / nsub;
     for (int j = 0; j < sub; ++j) {
       s->fl[j] = (double)nlp[j + 1];
       s->fu[j] = (double)nup[sub - j];
     }
-    s->pS = (double)nlp[sub];
-    s->qS = (double)nup[sub];
-    ld pk = nlp[m], qk = nup[m];
+    ld pk = nlp[sub], qk = nup[sub];
     for (int k = 0; k < 5; ++k) {
       s->pp[k] = (double)pk;
       s->qq[k] = (double)qk;
@@ -101,9 +101,20 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int warps, int step
     for (int l = 0; l < 32; ++l) {
       s->plane[l] = (double)pl;
       s->qlane[31 - l] = (double)ql;
-      pl = pl * nlp[m];
-      ql = ql * nup[m];
+      pl = pl * nlp[sub];
+      ql = ql * nup[sub];
     }
+    s->ppos = (double*)calloc((size_t)T, sizeof(double));
+    s->qpos = (double*)calloc((size_t)T, sizeof(double));
+    ld pt = 1.0L, qt = 1.0L;
+    for (int t = 0; t < T; ++t) {
+      s->ppos[t] = (double)pt;
+      s->qpos[T - 1 - t] = (double)qt;
+      pt = pt * nlp[sub];
+      qt = qt * nup[sub];
+    }
+    s->Pseg = (double)pt;
+    s->Qseg = (double)qt;
   }
   {
     double lg = log2(s->dstar);
@@ -127,101 +138,98 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int warps, int step
 
 void orc_stepper_free(orc_stepper* s) {
   free(s->zc);
-  s->zc = NULL;
+  free(s->ppos);
+  free(s->qpos);
+  s->zc = s->ppos = s->qpos = NULL;
 }
 
 /* One unscaled solve y <- U^-1 L^-1 b plus the corner correction, on the
  * padded array y[Mp], chunked exactly like the CUDA step (pit_step.cuh
- * be_solve).  Thread k owns m = nsub*sub points as nsub sub-chunks.  Per
- * direction: local sub-chunk sweeps with zero carry; the thread's end value
- * combined from its sub-chunks; the warp Kogge-Stone scan + sequential
- * cross-warp combine give the thread carry; sub-chunk carries; fix-up
- * y_j += w_j * carry. */
+ * be_solve).  The padded slab is nseg segments of lseg = T*sub points;
+ * thread k owns chunk k (sub points) of every segment.  Per direction and
+ * segment: chunk sweeps with zero carry; warp Kogge-Stone scan + sequential
+ * cross-warp combine; segment totals chained segment to segment; chunk carry
+ * = local carry + pos_k * segment carry; fix-up y_j += w_j * carry. */
 static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
-  const int m = s->m, W = s->warps, T = 32 * W, M = s->M;
-  const int ns = s->nsub, sub = m / ns;
-  double* Z = scratch;          /* [T] thread end values / scan */
-  double* C = scratch + T;      /* [T] thread carries */
+  const int W = s->warps, T = 32 * W, M = s->M;
+  const int ns = s->nseg, sub = s->m / ns, lseg = T * sub;
+  double* Z = scratch;          /* [T] chunk end values / scan */
+  double* C = scratch + T;      /* [T] local carries */
   double* tot = scratch + 2 * T;/* [W] */
   double* tmp = scratch + 2 * T + W; /* [32] */
-  double E[ORC_MAX_M], Cs[ORC_MAX_M];
 
-  /* forward local sweeps + thread end values */
-  for (int k = 0; k < T; ++k) {
-    double* c = y + (size_t)k * m;
-    for (int q = 0; q < ns; ++q) {
-      double* cq = c + q * sub;
-      for (int j = 1; j < sub; ++j) cq[j] = fma(s->nl, cq[j - 1], cq[j]);
+  /* ---- forward ---- */
+  double S = 0.0; /* segment carry-in */
+  for (int q = 0; q < ns; ++q) {
+    double* seg = y + (size_t)q * lseg;
+    for (int k = 0; k < T; ++k) {
+      double* c = seg + (size_t)k * sub;
+      for (int j = 1; j < sub; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
+      Z[k] = c[sub - 1];
     }
-    double z = c[sub - 1];
-    for (int q = 1; q < ns; ++q) z = fma(s->pS, z, c[q * sub + sub - 1]);
-    Z[k] = z;
-  }
-  /* warp Kogge-Stone inclusive scans */
-  for (int w = 0; w < W; ++w) {
-    double* I = Z + 32 * w;
-    for (int st = 0; st < 5; ++st) {
-      int off = 1 << st;
-      for (int l = 0; l < 32; ++l) tmp[l] = (l >= off) ? fma(s->pp[st], I[l - off], I[l]) : I[l];
-      memcpy(I, tmp, 32 * sizeof(double));
+    for (int w = 0; w < W; ++w) {
+      double* I = Z + 32 * w;
+      for (int st = 0; st < 5; ++st) {
+        int off = 1 << st;
+        for (int l = 0; l < 32; ++l) tmp[l] = (l >= off) ? fma(s->pp[st], I[l - off], I[l]) : I[l];
+        memcpy(I, tmp, 32 * sizeof(double));
+      }
+      tot[w] = I[31];
     }
-    tot[w] = I[31];
-  }
-  for (int w = 0; w < W; ++w) {
-    double Wc = 0.0;
-    for (int v = 0; v < w; ++v) Wc = fma(s->p32, Wc, tot[v]);
-    for (int l = 0; l < 32; ++l) {
-      int k = 32 * w + l;
-      C[k] = (l == 0) ? Wc : fma(s->plane[l], Wc, Z[k - 1]);
+    for (int w = 0; w < W; ++w) {
+      double Wc = 0.0;
+      for (int v = 0; v < w; ++v) Wc = fma(s->p32, Wc, tot[v]);
+      for (int l = 0; l < 32; ++l) {
+        int k = 32 * w + l;
+        C[k] = (l == 0) ? Wc : fma(s->plane[l], Wc, Z[k - 1]);
+      }
     }
-  }
-  /* sub-chunk carries, forward fix-ups + Dirichlet ghosts */
-  for (int k = 0; k < T; ++k) {
-    double* c = y + (size_t)k * m;
-    for (int q = 0; q < ns; ++q) E[q] = c[q * sub + sub - 1];
-    Cs[0] = C[k];
-    for (int q = 1; q < ns; ++q) Cs[q] = fma(s->pS, Cs[q - 1], E[q - 1]);
-    for (int q = 0; q < ns; ++q)
-      for (int j = 0; j < sub; ++j) c[q * sub + j] = fma(s->fl[j], Cs[q], c[q * sub + j]);
-    for (int j = 0; j < m; ++j)
-      if (k * m + j >= M) c[j] = 0.0;
-  }
-  /* backward local sweeps + thread start values */
-  for (int k = 0; k < T; ++k) {
-    double* c = y + (size_t)k * m;
-    for (int q = 0; q < ns; ++q) {
-      double* cq = c + q * sub;
-      for (int j = sub - 2; j >= 0; --j) cq[j] = fma(s->nu, cq[j + 1], cq[j]);
+    double segtot = 0.0;
+    for (int v = 0; v < W; ++v) segtot = fma(s->p32, segtot, tot[v]);
+    if (q > 0) { /* S = S_q, chained from segment q-1 (computed below) */ }
+    for (int k = 0; k < T; ++k) {
+      double* c = seg + (size_t)k * sub;
+      const double Ck = fma(s->ppos[k], S, C[k]);
+      for (int j = 0; j < sub; ++j) c[j] = fma(s->fl[j], Ck, c[j]);
     }
-    double h = c[(ns - 1) * sub];
-    for (int q = ns - 2; q >= 0; --q) h = fma(s->qS, h, c[q * sub]);
-    Z[k] = h;
+    S = fma(s->Pseg, S, segtot); /* carry into segment q+1 */
   }
-  for (int w = 0; w < W; ++w) {
-    double* J = Z + 32 * w;
-    for (int st = 0; st < 5; ++st) {
-      int off = 1 << st;
-      for (int l = 0; l < 32; ++l)
-        tmp[l] = (l < 32 - off) ? fma(s->qq[st], J[l + off], J[l]) : J[l];
-      memcpy(J, tmp, 32 * sizeof(double));
+  for (int i = M; i < ns * lseg; ++i) y[i] = 0.0; /* Dirichlet padding */
+  /* ---- backward ---- */
+  S = 0.0;
+  for (int q = ns - 1; q >= 0; --q) {
+    double* seg = y + (size_t)q * lseg;
+    for (int k = 0; k < T; ++k) {
+      double* c = seg + (size_t)k * sub;
+      for (int j = sub - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
+      Z[k] = c[0];
     }
-    tot[w] = J[0];
-  }
-  for (int w = 0; w < W; ++w) {
-    double Vc = 0.0;
-    for (int v = W - 1; v > w; --v) Vc = fma(s->q32, Vc, tot[v]);
-    for (int l = 0; l < 32; ++l) {
-      int k = 32 * w + l;
-      C[k] = (l == 31) ? Vc : fma(s->qlane[l], Vc, Z[k + 1]);
+    for (int w = 0; w < W; ++w) {
+      double* J = Z + 32 * w;
+      for (int st = 0; st < 5; ++st) {
+        int off = 1 << st;
+        for (int l = 0; l < 32; ++l)
+          tmp[l] = (l < 32 - off) ? fma(s->qq[st], J[l + off], J[l]) : J[l];
+        memcpy(J, tmp, 32 * sizeof(double));
+      }
+      tot[w] = J[0];
     }
-  }
-  for (int k = 0; k < T; ++k) {
-    double* c = y + (size_t)k * m;
-    for (int q = 0; q < ns; ++q) E[q] = c[q * sub];
-    Cs[ns - 1] = C[k];
-    for (int q = ns - 2; q >= 0; --q) Cs[q] = fma(s->qS, Cs[q + 1], E[q + 1]);
-    for (int q = 0; q < ns; ++q)
-      for (int j = 0; j < sub; ++j) c[q * sub + j] = fma(s->fu[j], Cs[q], c[q * sub + j]);
+    for (int w = 0; w < W; ++w) {
+      double Vc = 0.0;
+      for (int v = W - 1; v > w; --v) Vc = fma(s->q32, Vc, tot[v]);
+      for (int l = 0; l < 32; ++l) {
+        int k = 32 * w + l;
+        C[k] = (l == 31) ? Vc : fma(s->qlane[l], Vc, Z[k + 1]);
+      }
+    }
+    double segtot = 0.0;
+    for (int v = W - 1; v >= 0; --v) segtot = fma(s->q32, segtot, tot[v]);
+    for (int k = 0; k < T; ++k) {
+      double* c = seg + (size_t)k * sub;
+      const double Rk = fma(s->qpos[k], S, C[k]);
+      for (int j = 0; j < sub; ++j) c[j] = fma(s->fu[j], Rk, c[j]);
+    }
+    S = fma(s->Qseg, S, segtot);
   }
   /* corner rank-1 correction */
   {
@@ -659,7 +667,7 @@ static int orc_1d_prop(void* user, int role, int with_source, const double* in, 
 
 orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double band_up, int N,
                       double total_time, int fine_steps, int coarse_steps, int fine_m,
-                      int fine_nsub, int fine_warps, int coarse_m, int coarse_nsub,
+                      int fine_nseg, int fine_warps, int coarse_m, int coarse_nseg,
                       int coarse_warps, const double* y0,
                       int has_source, const double* src_shape, double src_amp,
                       double src_omega, double src_phase, int use_thomas, int mode) {
@@ -674,9 +682,9 @@ orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double 
   const double slab = total_time / N; /* TimeSlabPartition::slab_length */
   o->dt[0] = slab / fine_steps;       /* Propagator::internal_dt */
   o->dt[1] = slab / coarse_steps;
-  if (orc_stepper_init(&o->st[0], M, fine_m, fine_nsub, fine_warps, fine_steps, band_lo,
+  if (orc_stepper_init(&o->st[0], M, fine_m, fine_nseg, fine_warps, fine_steps, band_lo,
                        band_diag, band_up, o->dt[0]) ||
-      orc_stepper_init(&o->st[1], M, coarse_m, coarse_nsub, coarse_warps, coarse_steps, band_lo,
+      orc_stepper_init(&o->st[1], M, coarse_m, coarse_nseg, coarse_warps, coarse_steps, band_lo,
                        band_diag, band_up, o->dt[1])) {
     orc_1d_destroy(o);
     return NULL;

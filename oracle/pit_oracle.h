@@ -49,7 +49,7 @@ enum { ORC_FINE = 0, ORC_COARSE = 1 };
 typedef struct orc_stepper {
   int M;          /* interior points */
   int m;          /* points per thread */
-  int nsub;       /* sub-chunks per thread (sub = m / nsub points each) */
+  int nseg;       /* strided segments (thread chunk = sub = m / nseg points per segment) */
   int warps;      /* warps per slab CTA */
   int Mp;         /* padded length = 32*warps*m */
   int steps;      /* BE steps per slab */
@@ -57,16 +57,18 @@ typedef struct orc_stepper {
   double dstar, nl, nu, inv;
   double gneg;             /* -gamma' of the corner rank-1 correction */
   int K0;                  /* correction extent */
-  double pS, qS;           /* nl^sub, nu^sub */
+  double Pseg, Qseg;       /* nl^lseg, nu^lseg, lseg = 32*warps*sub */
   double fl[ORC_MAX_M], fu[ORC_MAX_M]; /* fix-up weights nl^(j+1), nu^(sub-j), j < sub */
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
   int R;                   /* rescale period, homogeneous propagation */
   double invR, invLast;    /* inv^R, inv^(steps % R) */
   double* zc;              /* [M] correction vector z' (entries >= K0 unused) */
+  double* ppos;            /* [32*warps] nl^(t*sub) */
+  double* qpos;            /* [32*warps] nu^((T-1-t)*sub) */
 } orc_stepper;
 
-int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int warps, int steps,
+int orc_stepper_init(orc_stepper* s, int M, int m, int nseg, int warps, int steps,
                      double band_lo, double band_diag, double band_up, double dt);
 void orc_stepper_free(orc_stepper* s);
 
@@ -143,7 +145,7 @@ void orc_problem_delete(orc_problem* p);
 typedef struct orc_1d orc_1d;
 orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double band_up, int N,
                       double total_time, int fine_steps, int coarse_steps, int fine_m,
-                      int fine_nsub, int fine_warps, int coarse_m, int coarse_nsub,
+                      int fine_nseg, int fine_warps, int coarse_m, int coarse_nseg,
                       int coarse_warps, const double* y0,
                       int has_source, const double* src_shape, double src_amp,
                       double src_omega, double src_phase, int use_thomas, int mode);

@@ -20,80 +20,76 @@ namespace pitb {
 
 namespace {
 
-template <int SUB, int NSUB>
-__device__ __forceinline__ void load_field(double (&y)[NSUB][SUB], const double* __restrict__ src,
+// Thread-owned point i of y[s][j]: s*LSEG + g0 + j, LSEG = 32*WARPS*SUB.
+template <int SUB, int NSEG, int WARPS>
+__device__ __forceinline__ void load_field(double (&y)[NSEG][SUB], const double* __restrict__ src,
                                            int g0, int M) {
+  constexpr int LSEG = 32 * WARPS * SUB;
 #pragma unroll
-  for (int s = 0; s < NSUB; ++s)
+  for (int s = 0; s < NSEG; ++s)
 #pragma unroll
     for (int j = 0; j < SUB; ++j) {
-      const int i = g0 + s * SUB + j;
+      const int i = s * LSEG + g0 + j;
       y[s][j] = (src != nullptr && i < M) ? src[i] : 0.0;
     }
 }
 
-template <int SUB, int NSUB>
-__device__ __forceinline__ bool all_finite(const double (&y)[NSUB][SUB], int g0, int M) {
+template <int SUB, int NSEG, int WARPS>
+__device__ __forceinline__ bool all_finite(const double (&y)[NSEG][SUB], int g0, int M) {
+  constexpr int LSEG = 32 * WARPS * SUB;
   bool ok = true;
 #pragma unroll
-  for (int s = 0; s < NSUB; ++s)
+  for (int s = 0; s < NSEG; ++s)
 #pragma unroll
     for (int j = 0; j < SUB; ++j)
-      if (g0 + s * SUB + j < M && !isfinite(y[s][j])) ok = false;
+      if (s * LSEG + g0 + j < M && !isfinite(y[s][j])) ok = false;
   return ok;
 }
 
-// Correction vector, zero-padded (see be_solve): narrow path 32*MPT entries,
+// Correction vector, zero-padded (see be_solve): narrow path 32*SUB entries,
 // wide path the padded slab length.
-__host__ __device__ inline int zc_len(int K0, int mpt, int warps) {
-  return K0 <= 32 * mpt ? 32 * mpt : 32 * warps * mpt;
+__host__ __device__ inline int zc_len(int K0, int sub, int nseg, int warps) {
+  return K0 <= 32 * sub ? 32 * sub : 32 * warps * sub * nseg;
 }
-template <int MPT, int WARPS>
+template <int SUB, int NSEG, int WARPS>
 __device__ __forceinline__ void load_zc(const StepParams& P, double* s_zc, int tid) {
-  const int n = zc_len(P.K0, MPT, WARPS);
+  const int n = zc_len(P.K0, SUB, NSEG, WARPS);
   for (int i = tid; i < n; i += 32 * WARPS) s_zc[i] = i < P.K0 ? P.zc[i] : 0.0;
 }
 
 template <int MPT, int WARPS, bool SRC>
 struct SlabBounds {
   static constexpr int kThreads = 32 * WARPS;
-  static constexpr int kRegs = MPT <= 16 ? 64 : (MPT <= 32 ? 96 : 168);
+  static constexpr int kRegs = MPT <= 16 ? 64 : (MPT <= 32 ? 128 : 168);
   static constexpr int kMin0 = 65536 / (kThreads * kRegs);
   static constexpr int kMin = SRC ? 1 : (kMin0 < 1 ? 1 : (kMin0 > 16 ? 16 : kMin0));
 };
 
-// Source shape for SRC kernels: read through L1 each step (not held in
-// registers) so MPT=64 layouts do not spill.
-template <int SUB, int NSUB>
-struct ShapeView {
-  const double* __restrict__ g;
-  int g0, M;
-  __device__ double operator()(int s, int j) const {
-    const int i = g0 + s * SUB + j;
-    return i < M ? __ldg(g + i) : 0.0;
-  }
-};
-
-template <int SUB, int NSUB, int WARPS, bool SRC>
-__device__ __forceinline__ void run_slab(double (&y)[NSUB][SUB], const StepParams& P,
-                                         StepShared<WARPS>& sh, const double* s_zc, int lane,
-                                         int warp, int g0, int slab) {
-  constexpr int MPT = SUB * NSUB;
-  const bool ghosts = P.M < 32 * WARPS * MPT;
-  const bool wide = P.K0 > 32 * MPT;
+template <int SUB, int NSEG, int WARPS, bool SRC>
+__device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParams& P,
+                                         const StepLane& L, StepShared<NSEG, WARPS>& sh,
+                                         const double* s_zc, int lane, int warp, int g0,
+                                         int slab) {
+  constexpr int LSEG = 32 * WARPS * SUB;
+  const bool ghosts = P.M < NSEG * LSEG;
+  const bool wide = P.K0 > 32 * SUB;
   if (SRC) {
+    // separable source y += dt*s(t_k) g(x): g read through L1 each step (not
+    // held in registers, so wide layouts do not spill)
     const double* ds = P.ds + (size_t)slab * P.steps;
-    const ShapeView<SUB, NSUB> g{P.shape, g0, P.M};
     double dsk = ds[0];
     for (int k = 0; k < P.steps; ++k) {
       const double dsn = (k + 1 < P.steps) ? ds[k + 1] : 0.0;
 #pragma unroll
-      for (int s = 0; s < NSUB; ++s)
+      for (int s = 0; s < NSEG; ++s)
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) y[s][j] = fma(dsk, g(s, j), y[s][j]);
-      be_solve<SUB, NSUB, WARPS>(y, P, sh, s_zc, lane, warp, g0, ghosts, wide);
+        for (int j = 0; j < SUB; ++j) {
+          const int i = s * LSEG + g0 + j;
+          y[s][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[s][j]);
+        }
+      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide);
 #pragma unroll
-      for (int s = 0; s < NSUB; ++s)
+      for (int s = 0; s < NSEG; ++s)
 #pragma unroll
         for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.inv;
       dsk = dsn;
@@ -101,58 +97,70 @@ __device__ __forceinline__ void run_slab(double (&y)[NSUB][SUB], const StepParam
   } else {
     int cnt = 0;
     for (int k = 0; k < P.steps; ++k) {
-      be_solve<SUB, NSUB, WARPS>(y, P, sh, s_zc, lane, warp, g0, ghosts, wide);
+      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide);
       if (++cnt == P.R) {
         cnt = 0;
 #pragma unroll
-        for (int s = 0; s < NSUB; ++s)
+        for (int s = 0; s < NSEG; ++s)
 #pragma unroll
           for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invR;
       }
     }
     if (cnt) {
 #pragma unroll
-      for (int s = 0; s < NSUB; ++s)
+      for (int s = 0; s < NSEG; ++s)
 #pragma unroll
         for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invLast;
     }
   }
 }
 
-template <int SUB, int NSUB, int WARPS, bool SRC>
-__global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSUB, WARPS, SRC>::kMin))
+template <int SUB, int NSEG, int WARPS>
+__device__ __forceinline__ StepLane step_lane(const StepParams& P,
+                                              const StepShared<NSEG, WARPS>& sh, int tid) {
+  StepLane L;
+  L.plane = sh.plane[tid & 31];
+  L.qlane = sh.qlane[tid & 31];
+  L.ppos = P.ppos[tid];
+  L.qpos = P.qpos[tid];
+  return L;
+}
+
+template <int SUB, int NSEG, int WARPS, bool SRC>
+__global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSEG, WARPS, SRC>::kMin))
     slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
-  constexpr int MPT = SUB * NSUB;
+  constexpr int LSEG = 32 * WARPS * SUB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
+  auto* sh = reinterpret_cast<StepShared<NSEG, WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
   const int M = P.M;
-  const int g0 = tid * MPT;
-  load_zc<MPT, WARPS>(P, s_zc, tid);
-  init_step_shared<WARPS>(P, *sh, tid);
+  const int g0 = tid * SUB;
+  load_zc<SUB, NSEG, WARPS>(P, s_zc, tid);
+  init_step_shared<NSEG, WARPS>(P, *sh, tid);
 
   const double* src;
   if (b + A.in_shift >= 0)
     src = A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr;
   else
     src = A.halo;
-  double y[NSUB][SUB];
-  load_field<SUB, NSUB>(y, src, g0, M);
+  double y[NSEG][SUB];
+  load_field<SUB, NSEG, WARPS>(y, src, g0, M);
   const int slab = A.slab0 + b;
   __syncthreads();
+  const StepLane L = step_lane<SUB, NSEG, WARPS>(P, *sh, tid);
 
-  run_slab<SUB, NSUB, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0, slab);
+  run_slab<SUB, NSEG, WARPS, SRC>(y, P, L, *sh, s_zc, lane, warp, g0, slab);
 
-  if (!all_finite<SUB, NSUB>(y, g0, M)) atomicMin(A.status, slab);
+  if (!all_finite<SUB, NSEG, WARPS>(y, g0, M)) atomicMin(A.status, slab);
   const size_t off = (size_t)b * M;
   double* out = A.out + off;
 #pragma unroll
-  for (int s = 0; s < NSUB; ++s)
+  for (int s = 0; s < NSEG; ++s)
 #pragma unroll
     for (int j = 0; j < SUB; ++j) {
-      const int i = g0 + s * SUB + j;
+      const int i = s * LSEG + g0 + j;
       if (i < M) {
         if (A.mode == kApplyF) {
           out[i] = A.Lsub[off + i] - y[s][j];
@@ -173,12 +181,16 @@ __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSUB, WARPS, SRC
   }
 }
 
-// Staging layout of one block in shared memory: thread t's chunk at
-// t*(MPT+1) (odd pitch: a warp reading element e of every chunk hits
+// Staging layout of one block in shared memory: thread t's MPT values at
+// t*(MPT+1) (odd pitch: a warp reading element e of every thread hits
 // distinct banks), filled and drained with coalesced global accesses.
-template <int MPT>
+template <int SUB, int NSEG, int WARPS>
 __device__ __forceinline__ int stage_idx(int i) {
-  return (i / MPT) * (MPT + 1) + (i % MPT);
+  constexpr int LSEG = 32 * WARPS * SUB;
+  constexpr int MPT = SUB * NSEG;
+  const int s = i / LSEG, r = i - s * LSEG;
+  const int t = r / SUB, j = r - t * SUB;
+  return t * (MPT + 1) + s * SUB + j;
 }
 
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
@@ -191,77 +203,77 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int SUB, int NSUB, int WARPS, bool SRC>
+template <int SUB, int NSEG, int WARPS, bool SRC>
 __global__ void __launch_bounds__(32 * WARPS, 1)
     sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A) {
-  constexpr int MPT = SUB * NSUB;
+  constexpr int MPT = SUB * NSEG;
   constexpr int T = 32 * WARPS;
   constexpr int STAGE = T * (MPT + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  StepShared<WARPS>* sh = reinterpret_cast<StepShared<WARPS>*>(smem_raw);
+  auto* sh = reinterpret_cast<StepShared<NSEG, WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
-  double* stage = s_zc + zc_len(P.K0, MPT, WARPS);  // [2][STAGE]: V double buffer
+  double* stage = s_zc + zc_len(P.K0, SUB, NSEG, WARPS);  // [2][STAGE]: V double buffer
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = P.M;
-  const int g0 = tid * MPT;
-  load_zc<MPT, WARPS>(P, s_zc, tid);
-  init_step_shared<WARPS>(P, *sh, tid);
-  double y[NSUB][SUB];
-  load_field<SUB, NSUB>(y, A.start, g0, M);
+  const int g0 = tid * SUB;
+  load_zc<SUB, NSEG, WARPS>(P, s_zc, tid);
+  init_step_shared<NSEG, WARPS>(P, *sh, tid);
+  double y[NSEG][SUB];
+  load_field<SUB, NSEG, WARPS>(y, A.start, g0, M);
   auto prefetch = [&](int b) {
     double* buf = stage + (b & 1) * STAGE;
     const double* v = A.V + (size_t)b * M;
-    for (int i = tid; i < M; i += T) cp_async8(buf + stage_idx<MPT>(i), v + i);
+    for (int i = tid; i < M; i += T) cp_async8(buf + stage_idx<SUB, NSEG, WARPS>(i), v + i);
     cp_async_commit();
   };
   if (A.V) prefetch(0);
   __syncthreads();
+  const StepLane L = step_lane<SUB, NSEG, WARPS>(P, *sh, tid);
   bool ok = true;
   int bad = 0x7fffffff;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
     if (A.V && b + 1 < A.count) prefetch(b + 1);
-    run_slab<SUB, NSUB, WARPS, SRC>(y, P, *sh, s_zc, lane, warp, g0, slab);
-    if (ok && !all_finite<SUB, NSUB>(y, g0, M)) {
+    run_slab<SUB, NSEG, WARPS, SRC>(y, P, L, *sh, s_zc, lane, warp, g0, slab);
+    if (ok && !all_finite<SUB, NSEG, WARPS>(y, g0, M)) {
       ok = false;
       bad = slab;
     }
+    double* buf = stage + (b & 1) * STAGE + tid * (MPT + 1);
     if (A.V) {
       if (b + 1 < A.count)
         cp_async_wait<1>();
       else
         cp_async_wait<0>();
       __syncthreads();
-      const double* vb = stage + (b & 1) * STAGE + tid * (MPT + 1);
 #pragma unroll
-      for (int s = 0; s < NSUB; ++s)
+      for (int s = 0; s < NSEG; ++s)
 #pragma unroll
         for (int j = 0; j < SUB; ++j) {
-          const int e = s * SUB + j;
-          y[s][j] = y[s][j] + (g0 + e < M ? vb[e] : 0.0);
+          const double v = (s * 32 * WARPS * SUB + g0 + j < M) ? buf[s * SUB + j] : 0.0;
+          y[s][j] = y[s][j] + v;
         }
     }
-    // drain W_b through slab b's (now consumed) V buffer: coalesced stores
-    double* wbuf = stage + (b & 1) * STAGE;
-    // (each thread overwrites exactly the V slots it just read)
-    double* wb = wbuf + tid * (MPT + 1);
+    // drain W_b through slab b's (consumed) V buffer with coalesced stores;
+    // each thread overwrites exactly the slots it just read
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s)
+    for (int s = 0; s < NSEG; ++s)
 #pragma unroll
-      for (int j = 0; j < SUB; ++j) wb[s * SUB + j] = y[s][j];
+      for (int j = 0; j < SUB; ++j) buf[s * SUB + j] = y[s][j];
     __syncthreads();
+    const double* wbuf = stage + (b & 1) * STAGE;
     double* W = A.W + (size_t)b * M;
-    for (int i = tid; i < M; i += T) W[i] = wbuf[stage_idx<MPT>(i)];
+    for (int i = tid; i < M; i += T) W[i] = wbuf[stage_idx<SUB, NSEG, WARPS>(i)];
     __syncthreads();  // the buffer is free for the prefetch of slab b+2
   }
   if (!ok) atomicMin(A.status, bad);
 }
 
-template <int SUB, int NSUB, int WARPS, bool SRC>
+template <int SUB, int NSEG, int WARPS, bool SRC>
 cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
   const size_t smem =
-      sizeof(StepShared<WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, SUB * NSUB, WARPS);
-  auto k = slab_kernel<SUB, NSUB, WARPS, SRC>;
+      sizeof(StepShared<NSEG, WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, SUB, NSEG, WARPS);
+  auto k = slab_kernel<SUB, NSEG, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -270,13 +282,13 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaSt
   return cudaGetLastError();
 }
 
-template <int SUB, int NSUB, int WARPS, bool SRC>
+template <int SUB, int NSEG, int WARPS, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
-  constexpr int MPT = SUB * NSUB;
-  const size_t smem = sizeof(StepShared<WARPS>) +
-                      sizeof(double) * ((size_t)zc_len(P.K0, MPT, WARPS) +
+  constexpr int MPT = SUB * NSEG;
+  const size_t smem = sizeof(StepShared<NSEG, WARPS>) +
+                      sizeof(double) * ((size_t)zc_len(P.K0, SUB, NSEG, WARPS) +
                                         2 * (size_t)(32 * WARPS) * (MPT + 1));
-  auto k = sweep_kernel<SUB, NSUB, WARPS, SRC>;
+  auto k = sweep_kernel<SUB, NSEG, WARPS, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -405,13 +417,14 @@ int ew_grid(size_t n) {
 
 }  // namespace
 
-// (points per thread, sub-chunks per thread, warps per slab) compiled here;
-// keep in sync with kLayouts in coeffs.cpp.
+// (points per thread, segments, warps per slab) compiled here (points per
+// thread = SUB * segments); keep in sync with kLayouts in coeffs.cpp.
 #define PIT_LAYOUTS(X)                                                                    \
   X(4, 1, 1) X(4, 1, 2) X(4, 1, 4) X(4, 1, 8) X(4, 1, 16) X(4, 1, 32) X(8, 1, 4) X(8, 1, 8) \
   X(8, 1, 16) X(8, 1, 32) X(16, 1, 2) X(16, 1, 4) X(16, 1, 8) X(16, 1, 16) X(16, 1, 32)     \
-  X(32, 2, 1) X(32, 2, 2) X(32, 2, 4) X(32, 2, 8) X(64, 4, 1) X(64, 4, 2) X(64, 4, 4)       \
-  X(64, 2, 2) X(64, 4, 8)
+  X(16, 2, 4) X(16, 2, 8) X(16, 4, 2) X(16, 4, 4) X(32, 2, 2) X(32, 2, 4) X(32, 4, 1)      \
+  X(32, 4, 2) X(32, 4, 4) X(64, 4, 1) X(64, 4, 2) X(16, 4, 8) X(8, 4, 8) X(16, 2, 16)      \
+  X(32, 4, 8)
 
 cudaError_t launch_slab(int mpt, int nsub, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st) {

@@ -1,18 +1,24 @@
 // pit_step.cuh — one backward-Euler step (I + dt*A) y' = y for a slab whose
-// M-point state lives in registers across a CTA of 32*WARPS threads.  Each
-// thread owns MPT = NSUB*SUB contiguous points, split into NSUB sub-chunks
-// of SUB points whose sweeps run interleaved (instruction-level parallelism
-// across the sub-chunk chains).  DESIGN.md §3.
+// M-point state lives in registers across a CTA of T = 32*WARPS threads.
+// DESIGN.md §3.
+//
+// Layout: the (padded) slab is split into NSEG super-segments of
+// Lseg = T*SUB points; thread t owns chunk t (SUB contiguous points) of every
+// segment: point s*Lseg + t*SUB + j sits in y[s][j].  The NSEG segments are
+// swept, scanned and fixed up side by side, so every phase has NSEG-way
+// instruction-level parallelism, and the corner correction touches only
+// segment 0.
 //
 // Replaces, per slab and step, the reference's ImplicitStepSolver::solve
 // (src/pde.cpp:112-130 -> solve_cg/solve_bicgstab, src/sparse.cpp:60-206)
 // with a direct tridiagonal solve:
-//   y <- U^-1 L^-1 y            constant unit-bidiagonal factors nl, nu,
-//        chunked: per-sub-chunk sweeps with zero carry, the thread's end
-//        value combined from its sub-chunks, a Kogge-Stone warp scan plus a
-//        sequential cross-warp combine for the true thread carries, the
-//        sub-chunk carries, and a fix-up y_j += w_j * carry
-//   y <- y + (gneg*y_0) zc      corner rank-1 (Sherman-Morrison) correction
+//   y <- U^-1 L^-1 y     constant unit-bidiagonal factors nl, nu; per
+//        direction: chunk sweeps with zero carry; Kogge-Stone warp scans and a
+//        sequential cross-warp combine give each chunk its carry within its
+//        segment; the segment totals are chained segment to segment; the
+//        chunk carry adds the segment carry-in (weight nl^(t*SUB)); fix-up
+//        y_j += w_j * carry
+//   y <- y + (gneg*y_0) zc   corner rank-1 (Sherman-Morrison) correction
 // and the diagonal scale inv is deferred: applied as inv^R every R steps
 // (homogeneous propagation) or every step when a source is added.
 // Every multiply-add is an explicit fma(); oracle/pit_oracle.c
@@ -27,31 +33,33 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct StepParams {
   double nl, nu, inv, gneg, invR, invLast;
-  double pS, qS;            // nl^SUB, nu^SUB (sub-chunk carry weights)
+  double Pseg, Qseg;        // nl^Lseg, nu^Lseg (segment-to-segment carry weights)
   double fl[32], fu[32];    // fix-up weights nl^(j+1), nu^(SUB-j), j < SUB
-  double pp[5], qq[5], p32, q32;  // Kogge-Stone weights, powers of nl^MPT / nu^MPT
+  double pp[5], qq[5], p32, q32;  // Kogge-Stone weights: powers of nl^SUB / nu^SUB
   double plane[32], qlane[32];
   int M, steps, R, K0;
   const double* zc;     // [K0] correction vector (device)
+  const double* ppos;   // [T] nl^(t*SUB)  (device)
+  const double* qpos;   // [T] nu^((T-1-t)*SUB)  (device)
   const double* shape;  // [M] source shape g(x_i) (device) or nullptr
   const double* ds;     // [slabs*steps] dt*s(t_k) table (device) or nullptr
 };
 
-// Shared memory of one slab CTA: cross-warp carries, broadcast scalar and the
-// per-lane carry weights (read with LDS: an indexed constant load would
-// serialise across lanes).  The correction vector follows the struct.
-template <int WARPS>
+// Shared memory of one slab CTA: per-segment cross-warp totals, broadcast
+// scalar and the per-lane carry weights (read with LDS: an indexed constant
+// load would serialise across lanes).  The correction vector follows.
+template <int NSEG, int WARPS>
 struct StepShared {
-  double fw[WARPS > 1 ? WARPS : 1];
-  double bw[WARPS > 1 ? WARPS : 1];
+  double fw[NSEG][WARPS > 1 ? WARPS : 1];
+  double bw[NSEG][WARPS > 1 ? WARPS : 1];
   double b;
   double pad;
   double plane[32], qlane[32];  // p^lane, q^(31-lane)
 };
 
-template <int WARPS>
-__device__ __forceinline__ void init_step_shared(const StepParams& P, StepShared<WARPS>& sh,
-                                                 int tid) {
+template <int NSEG, int WARPS>
+__device__ __forceinline__ void init_step_shared(const StepParams& P,
+                                                 StepShared<NSEG, WARPS>& sh, int tid) {
   for (int i = tid; i < 32; i += 32 * WARPS) {
     sh.plane[i] = P.plane[i];
     sh.qlane[i] = P.qlane[i];
@@ -81,92 +89,147 @@ __device__ __forceinline__ void scan_stage_down(double& J, double c, int d) {
       : "d"(c), "r"(d));
 }
 
-// s_zc holds the correction vector zero-padded to 32*MPT entries (narrow
-// path, K0 <= 32*MPT: only warp 0 touches it) or to the padded slab length
-// (wide path); fma(c, 0, y) == y, so padding does not change any bit.
-// The lane-0 / lane-31 carry uses weight 1 on a zeroed neighbour value:
-// fma(1, W, 0) == W.
-template <int SUB, int NSUB, int WARPS>
-__device__ __forceinline__ void be_solve(double (&y)[NSUB][SUB], const StepParams& P,
-                                         StepShared<WARPS>& sh,
+// Per-thread constants of the step (registers, loaded once per kernel).
+struct StepLane {
+  double plane, qlane, ppos, qpos;
+};
+
+// s_zc holds the correction vector zero-padded to 32*SUB entries (narrow
+// path, K0 <= 32*SUB: warp 0 of segment 0 only) or to the padded slab length
+// (wide path); fma(c, 0, y) == y, so padding does not change any bit.  The
+// lane-0 / lane-31 carry uses weight 1 on a zeroed neighbour value, and
+// segment 0 (NSEG-1 backward) adds a zero segment carry-in: both exact.
+template <int SUB, int NSEG, int WARPS>
+__device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParams& P,
+                                         const StepLane& L, StepShared<NSEG, WARPS>& sh,
                                          const double* __restrict__ s_zc, int lane, int warp,
                                          int g0, bool ghosts, bool wide) {
+  constexpr int LSEG = 32 * WARPS * SUB;
   // ---- forward: L^-1 ----
 #pragma unroll
   for (int j = 1; j < SUB; ++j)
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s) y[s][j] = fma(P.nl, y[s][j - 1], y[s][j]);
-  double I = y[0][SUB - 1];
+    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nl, y[s][j - 1], y[s][j]);
+  double I[NSEG], Ip[NSEG], Wc[NSEG], Tot[NSEG];
 #pragma unroll
-  for (int s = 1; s < NSUB; ++s) I = fma(P.pS, I, y[s][SUB - 1]);
+  for (int s = 0; s < NSEG; ++s) I[s] = y[s][SUB - 1];
 #pragma unroll
-  for (int s = 0; s < 5; ++s) scan_stage_up(I, P.pp[s], 1 << s);
-  double Ip = __shfl_up_sync(kFull, I, 1);
-  Ip = lane == 0 ? 0.0 : Ip;
-  double Wc = 0.0;
-  if (WARPS > 1) {
-    if (lane == 31) sh.fw[warp] = I;
-    __syncthreads();
-    for (int v = 0; v < warp; ++v) Wc = fma(P.p32, Wc, sh.fw[v]);
+  for (int st = 0; st < 5; ++st)
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) scan_stage_up(I[s], P.pp[st], 1 << st);
+#pragma unroll
+  for (int s = 0; s < NSEG; ++s) {
+    Ip[s] = __shfl_up_sync(kFull, I[s], 1);
+    Ip[s] = lane == 0 ? 0.0 : Ip[s];
+    Wc[s] = 0.0;
   }
-  double Cs[NSUB];
-  Cs[0] = fma(sh.plane[lane], Wc, Ip);
+  if (WARPS > 1) {
+    if (lane == 31) {
 #pragma unroll
-  for (int s = 1; s < NSUB; ++s) Cs[s] = fma(P.pS, Cs[s - 1], y[s - 1][SUB - 1]);
+      for (int s = 0; s < NSEG; ++s) sh.fw[s][warp] = I[s];
+    }
+    __syncthreads();
+    for (int v = 0; v < warp; ++v)
 #pragma unroll
-  for (int j = SUB - 1; j >= 0; --j)
+      for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.p32, Wc[s], sh.fw[s][v]);
+    if (NSEG > 1) {
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s) y[s][j] = fma(P.fl[j], Cs[s], y[s][j]);
+      for (int s = 0; s < NSEG - 1; ++s) Tot[s] = 0.0;
+#pragma unroll
+      for (int v = 0; v < WARPS; ++v)
+#pragma unroll
+        for (int s = 0; s < NSEG - 1; ++s) Tot[s] = fma(P.p32, Tot[s], sh.fw[s][v]);
+    }
+  } else if (NSEG > 1) {
+#pragma unroll
+    for (int s = 0; s < NSEG - 1; ++s) Tot[s] = __shfl_sync(kFull, I[s], 31);
+  }
+  {
+    double S = 0.0;  // segment carry-in
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) {
+      if (s > 0) S = fma(P.Pseg, S, Tot[s - 1]);
+      double C = fma(L.plane, Wc[s], Ip[s]);
+      C = fma(L.ppos, S, C);
+#pragma unroll
+      for (int j = SUB - 1; j >= 0; --j) y[s][j] = fma(P.fl[j], C, y[s][j]);
+    }
+  }
   if (ghosts) {
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s)
+    for (int s = 0; s < NSEG; ++s)
 #pragma unroll
       for (int j = 0; j < SUB; ++j)
-        y[s][j] = (g0 + s * SUB + j < P.M) ? y[s][j] : 0.0;  // Dirichlet padding
+        y[s][j] = (s * LSEG + g0 + j < P.M) ? y[s][j] : 0.0;  // Dirichlet padding
   }
   // ---- backward: U^-1 ----
 #pragma unroll
   for (int j = SUB - 2; j >= 0; --j)
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s) y[s][j] = fma(P.nu, y[s][j + 1], y[s][j]);
-  double J = y[NSUB - 1][0];
+    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nu, y[s][j + 1], y[s][j]);
 #pragma unroll
-  for (int s = NSUB - 2; s >= 0; --s) J = fma(P.qS, J, y[s][0]);
+  for (int s = 0; s < NSEG; ++s) I[s] = y[s][0];
 #pragma unroll
-  for (int s = 0; s < 5; ++s) scan_stage_down(J, P.qq[s], 1 << s);
-  double Jn = __shfl_down_sync(kFull, J, 1);
-  Jn = lane == 31 ? 0.0 : Jn;
-  double Vc = 0.0;
-  if (WARPS > 1) {
-    if (lane == 0) sh.bw[warp] = J;
-    __syncthreads();
-    for (int v = WARPS - 1; v > warp; --v) Vc = fma(P.q32, Vc, sh.bw[v]);
+  for (int st = 0; st < 5; ++st)
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) scan_stage_down(I[s], P.qq[st], 1 << st);
+#pragma unroll
+  for (int s = 0; s < NSEG; ++s) {
+    Ip[s] = __shfl_down_sync(kFull, I[s], 1);
+    Ip[s] = lane == 31 ? 0.0 : Ip[s];
+    Wc[s] = 0.0;
   }
-  double Rs[NSUB];
-  Rs[NSUB - 1] = fma(sh.qlane[lane], Vc, Jn);
+  if (WARPS > 1) {
+    if (lane == 0) {
 #pragma unroll
-  for (int s = NSUB - 2; s >= 0; --s) Rs[s] = fma(P.qS, Rs[s + 1], y[s + 1][0]);
+      for (int s = 0; s < NSEG; ++s) sh.bw[s][warp] = I[s];
+    }
+    __syncthreads();
+    for (int v = WARPS - 1; v > warp; --v)
 #pragma unroll
-  for (int j = 0; j < SUB; ++j)
+      for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.q32, Wc[s], sh.bw[s][v]);
+    if (NSEG > 1) {
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s) y[s][j] = fma(P.fu[j], Rs[s], y[s][j]);
+      for (int s = 1; s < NSEG; ++s) Tot[s] = 0.0;
+#pragma unroll
+      for (int v = WARPS - 1; v >= 0; --v)
+#pragma unroll
+        for (int s = 1; s < NSEG; ++s) Tot[s] = fma(P.q32, Tot[s], sh.bw[s][v]);
+    }
+  } else if (NSEG > 1) {
+#pragma unroll
+    for (int s = 1; s < NSEG; ++s) Tot[s] = __shfl_sync(kFull, I[s], 0);
+  }
+  {
+    double S = 0.0;  // segment carry from the right
+#pragma unroll
+    for (int s = NSEG - 1; s >= 0; --s) {
+      if (s < NSEG - 1) S = fma(P.Qseg, S, Tot[s + 1]);
+      double R = fma(L.qlane, Wc[s], Ip[s]);
+      R = fma(L.qpos, S, R);
+#pragma unroll
+      for (int j = 0; j < SUB; ++j) y[s][j] = fma(P.fu[j], R, y[s][j]);
+    }
+  }
   // ---- corner rank-1 correction ----
   if (!wide) {
     if (warp == 0) {
       const double c = P.gneg * __shfl_sync(kFull, y[0][0], 0);
+      if (g0 < P.K0) {
 #pragma unroll
-      for (int s = 0; s < NSUB; ++s)
-#pragma unroll
-        for (int j = 0; j < SUB; ++j) y[s][j] = fma(c, s_zc[g0 + s * SUB + j], y[s][j]);
+        for (int j = 0; j < SUB; ++j) y[0][j] = fma(c, s_zc[g0 + j], y[0][j]);
+      }
     }
   } else {
     if (warp == 0 && lane == 0) sh.b = y[0][0];
     __syncthreads();
     const double c = P.gneg * sh.b;
 #pragma unroll
-    for (int s = 0; s < NSUB; ++s)
+    for (int s = 0; s < NSEG; ++s)
+      if (s * LSEG + g0 < P.K0) {
 #pragma unroll
-      for (int j = 0; j < SUB; ++j) y[s][j] = fma(c, s_zc[g0 + s * SUB + j], y[s][j]);
+        for (int j = 0; j < SUB; ++j) y[s][j] = fma(c, s_zc[s * LSEG + g0 + j], y[s][j]);
+      }
   }
 }
 

@@ -35,16 +35,16 @@ class OrcHistory(C.Structure):
 
 
 class OrcStepper(C.Structure):
-    _fields_ = [("M", C.c_int), ("m", C.c_int), ("nsub", C.c_int), ("warps", C.c_int),
+    _fields_ = [("M", C.c_int), ("m", C.c_int), ("nseg", C.c_int), ("warps", C.c_int),
                 ("Mp", C.c_int),
                 ("steps", C.c_int), ("delta", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("dstar", C.c_double), ("nl", C.c_double), ("nu", C.c_double), ("inv", C.c_double),
-                ("gneg", C.c_double), ("K0", C.c_int), ("pS", C.c_double), ("qS", C.c_double),
+                ("gneg", C.c_double), ("K0", C.c_int), ("Pseg", C.c_double), ("Qseg", C.c_double),
                 ("fl", C.c_double * 64),
                 ("fu", C.c_double * 64), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
                 ("qlane", C.c_double * 32), ("R", C.c_int), ("invR", C.c_double),
-                ("invLast", C.c_double), ("zc", _dp)]
+                ("invLast", C.c_double), ("zc", _dp), ("ppos", _dp), ("qpos", _dp)]
 
 
 def ensure_built() -> None:

@@ -126,7 +126,7 @@ def test_c3_n16_matches_reference():
 
 
 @pytest.mark.parametrize("layout", [(16, 1, 8), (8, 1, 16), (32, 2, 4), (16, 1, 16), (4, 1, 32),
-                                    (8, 1, 32), (64, 4, 2), (64, 2, 2), (64, 4, 4)])
+                                    (8, 1, 32), (64, 4, 2), (32, 4, 4), (16, 4, 8), (16, 2, 8)])
 def test_fine_layouts_bitwise_vs_oracle(layout):
     p = configs.make("c2", slabs=4)
     o = OracleProblem(p, fine_layout=layout)
@@ -136,14 +136,16 @@ def test_fine_layouts_bitwise_vs_oracle(layout):
         assert same(api.apply_F(ctx, L), o.apply_F(L))[0]
 
 
-@pytest.mark.parametrize("M", [1, 2, 31, 100, 333, 1000, 4095])
-def test_ragged_grids_bitwise_vs_oracle(M):
+@pytest.mark.parametrize("M,layout", [(1, None), (2, None), (31, None), (100, None), (333, None),
+                                      (1000, None), (4095, None), (1500, (8, 4, 8)),
+                                      (3000, (32, 4, 4)), (700, (16, 4, 2))])
+def test_ragged_grids_bitwise_vs_oracle(M, layout):
     p = configs.make("c2", slabs=3, M=M)
     p.fine_steps = 20
-    o = OracleProblem(p)
+    o = OracleProblem(p, fine_layout=layout)
     rng = np.random.default_rng(M)
     L = np.ascontiguousarray(rng.uniform(-1, 1, (p.N, p.M)))
-    with api.BlockOperatorContext(p) as ctx:
+    with api.BlockOperatorContext(p, fine_layout=layout) as ctx:
         assert same(api.apply_F(ctx, L), o.apply_F(L))[0]
         assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))[0]
 
