@@ -147,9 +147,10 @@ void orc_stepper_free(orc_stepper* s) {
  * padded array y[Mp], chunked exactly like the CUDA step (pit_step.cuh
  * be_solve).  The padded slab is nseg segments of lseg = T*sub points;
  * thread k owns chunk k (sub points) of every segment.  Per direction and
- * segment: chunk sweeps with zero carry; warp Kogge-Stone scan + sequential
- * cross-warp combine; segment totals chained segment to segment; chunk carry
- * = local carry + pos_k * segment carry; fix-up y_j += w_j * carry. */
+ * segment: pass 1 sweeps each chunk with zero carry (end value only); warp
+ * Kogge-Stone scan + sequential cross-warp combine; segment totals chained
+ * segment to segment; chunk carry = local carry + pos_k * segment carry;
+ * pass 2 reruns the chunk's sweep from its carry. */
 static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   const int W = s->warps, T = 32 * W, M = s->M;
   const int ns = s->nseg, sub = s->m / ns, lseg = T * sub;
@@ -162,10 +163,11 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   double S = 0.0; /* segment carry-in */
   for (int q = 0; q < ns; ++q) {
     double* seg = y + (size_t)q * lseg;
-    for (int k = 0; k < T; ++k) {
-      double* c = seg + (size_t)k * sub;
-      for (int j = 1; j < sub; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
-      Z[k] = c[sub - 1];
+    for (int k = 0; k < T; ++k) { /* pass 1: end value with zero carry */
+      const double* c = seg + (size_t)k * sub;
+      double z = c[0];
+      for (int j = 1; j < sub; ++j) z = fma(s->nl, z, c[j]);
+      Z[k] = z;
     }
     for (int w = 0; w < W; ++w) {
       double* I = Z + 32 * w;
@@ -186,11 +188,11 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     }
     double segtot = 0.0;
     for (int v = 0; v < W; ++v) segtot = fma(s->p32, segtot, tot[v]);
-    if (q > 0) { /* S = S_q, chained from segment q-1 (computed below) */ }
-    for (int k = 0; k < T; ++k) {
+    for (int k = 0; k < T; ++k) { /* pass 2 from the true carry */
       double* c = seg + (size_t)k * sub;
       const double Ck = fma(s->ppos[k], S, C[k]);
-      for (int j = 0; j < sub; ++j) c[j] = fma(s->fl[j], Ck, c[j]);
+      c[0] = fma(s->nl, Ck, c[0]);
+      for (int j = 1; j < sub; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
     }
     S = fma(s->Pseg, S, segtot); /* carry into segment q+1 */
   }
@@ -199,10 +201,11 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   S = 0.0;
   for (int q = ns - 1; q >= 0; --q) {
     double* seg = y + (size_t)q * lseg;
-    for (int k = 0; k < T; ++k) {
-      double* c = seg + (size_t)k * sub;
-      for (int j = sub - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
-      Z[k] = c[0];
+    for (int k = 0; k < T; ++k) { /* pass 1: start value with zero carry */
+      const double* c = seg + (size_t)k * sub;
+      double h = c[sub - 1];
+      for (int j = sub - 2; j >= 0; --j) h = fma(s->nu, h, c[j]);
+      Z[k] = h;
     }
     for (int w = 0; w < W; ++w) {
       double* J = Z + 32 * w;
@@ -224,10 +227,11 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     }
     double segtot = 0.0;
     for (int v = W - 1; v >= 0; --v) segtot = fma(s->q32, segtot, tot[v]);
-    for (int k = 0; k < T; ++k) {
+    for (int k = 0; k < T; ++k) { /* pass 2 from the true carry */
       double* c = seg + (size_t)k * sub;
       const double Rk = fma(s->qpos[k], S, C[k]);
-      for (int j = 0; j < sub; ++j) c[j] = fma(s->fu[j], Rk, c[j]);
+      c[sub - 1] = fma(s->nu, Rk, c[sub - 1]);
+      for (int j = sub - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
     }
     S = fma(s->Qseg, S, segtot);
   }

@@ -13,11 +13,11 @@
 // (src/pde.cpp:112-130 -> solve_cg/solve_bicgstab, src/sparse.cpp:60-206)
 // with a direct tridiagonal solve:
 //   y <- U^-1 L^-1 y     constant unit-bidiagonal factors nl, nu; per
-//        direction: chunk sweeps with zero carry; Kogge-Stone warp scans and a
-//        sequential cross-warp combine give each chunk its carry within its
-//        segment; the segment totals are chained segment to segment; the
-//        chunk carry adds the segment carry-in (weight nl^(t*SUB)); fix-up
-//        y_j += w_j * carry
+//        direction: chunk sweeps with zero carry (end value only); Kogge-Stone
+//        warp scans and a sequential cross-warp combine give each chunk its
+//        carry within its segment; the segment totals are chained segment to
+//        segment; the chunk carry adds the segment carry-in (weight
+//        nl^(t*SUB)); the chunk sweep is rerun from that carry
 //   y <- y + (gneg*y_0) zc   corner rank-1 (Sherman-Morrison) correction
 // and the diagonal scale inv is deferred: applied as inv^R every R steps
 // (homogeneous propagation) or every step when a source is added.
@@ -55,6 +55,7 @@ struct StepShared {
   double b;
   double pad;
   double plane[32], qlane[32];  // p^lane, q^(31-lane)
+  double cf[5][32], cb[5][32];  // Kogge-Stone weights, 0 where a lane has no source lane
 };
 
 template <int NSEG, int WARPS>
@@ -63,30 +64,12 @@ __device__ __forceinline__ void init_step_shared(const StepParams& P,
   for (int i = tid; i < 32; i += 32 * WARPS) {
     sh.plane[i] = P.plane[i];
     sh.qlane[i] = P.qlane[i];
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+      sh.cf[st][i] = i >= (1 << st) ? P.pp[st] : 0.0;
+      sh.cb[st][i] = i < 32 - (1 << st) ? P.qq[st] : 0.0;
+    }
   }
-}
-
-// Kogge-Stone stage: I += c * I[lane -/+ d] on lanes whose source lane exists
-// (shfl's in-range predicate guards the DFMA; other lanes keep I).
-__device__ __forceinline__ void scan_stage_up(double& I, double c, int d) {
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, slo, shi;\n\t.reg .f64 t;\n\t"
-      "mov.b64 {lo, hi}, %0;\n\t"
-      "shfl.sync.up.b32 slo|p, lo, %2, 0, -1;\n\t"
-      "shfl.sync.up.b32 shi, hi, %2, 0, -1;\n\t"
-      "mov.b64 t, {slo, shi};\n\t"
-      "@p fma.rn.f64 %0, %1, t, %0;\n\t}"
-      : "+d"(I)
-      : "d"(c), "r"(d));
-}
-__device__ __forceinline__ void scan_stage_down(double& J, double c, int d) {
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, slo, shi;\n\t.reg .f64 t;\n\t"
-      "mov.b64 {lo, hi}, %0;\n\t"
-      "shfl.sync.down.b32 slo|p, lo, %2, 31, -1;\n\t"
-      "shfl.sync.down.b32 shi, hi, %2, 31, -1;\n\t"
-      "mov.b64 t, {slo, shi};\n\t"
-      "@p fma.rn.f64 %0, %1, t, %0;\n\t}"
-      : "+d"(J)
-      : "d"(c), "r"(d));
 }
 
 // Per-thread constants of the step (registers, loaded once per kernel).
@@ -94,6 +77,13 @@ struct StepLane {
   double plane, qlane, ppos, qpos;
 };
 
+// One step.  Per direction: pass 1 runs each chunk's sweep with zero carry
+// (only the end value is kept); Kogge-Stone warp scans (per-lane weights
+// from shared memory, zero where a lane has no source lane: fma(0, t, I) ==
+// I) and the cross-warp combine give each chunk its carry within the
+// segment; the segment totals are chained segment to segment; pass 2 reruns
+// each chunk's sweep from its true carry.  No per-point constants are
+// needed, and the NSEG chunk sweeps of a thread interleave.
 // s_zc holds the correction vector zero-padded to 32*SUB entries (narrow
 // path, K0 <= 32*SUB: warp 0 of segment 0 only) or to the padded slab length
 // (wide path); fma(c, 0, y) == y, so padding does not change any bit.  The
@@ -105,18 +95,20 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
                                          const double* __restrict__ s_zc, int lane, int warp,
                                          int g0, bool ghosts, bool wide) {
   constexpr int LSEG = 32 * WARPS * SUB;
+  double I[NSEG], Ip[NSEG], Wc[NSEG], Tot[NSEG];
   // ---- forward: L^-1 ----
+#pragma unroll
+  for (int s = 0; s < NSEG; ++s) I[s] = y[s][0];
 #pragma unroll
   for (int j = 1; j < SUB; ++j)
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nl, y[s][j - 1], y[s][j]);
-  double I[NSEG], Ip[NSEG], Wc[NSEG], Tot[NSEG];
+    for (int s = 0; s < NSEG; ++s) I[s] = fma(P.nl, I[s], y[s][j]);
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s) I[s] = y[s][SUB - 1];
+  for (int st = 0; st < 5; ++st) {
+    const double c = sh.cf[st][lane];
 #pragma unroll
-  for (int st = 0; st < 5; ++st)
-#pragma unroll
-    for (int s = 0; s < NSEG; ++s) scan_stage_up(I[s], P.pp[st], 1 << st);
+    for (int s = 0; s < NSEG; ++s) I[s] = fma(c, __shfl_up_sync(kFull, I[s], 1 << st), I[s]);
+  }
 #pragma unroll
   for (int s = 0; s < NSEG; ++s) {
     Ip[s] = __shfl_up_sync(kFull, I[s], 1);
@@ -151,10 +143,13 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
       if (s > 0) S = fma(P.Pseg, S, Tot[s - 1]);
       double C = fma(L.plane, Wc[s], Ip[s]);
       C = fma(L.ppos, S, C);
-#pragma unroll
-      for (int j = SUB - 1; j >= 0; --j) y[s][j] = fma(P.fl[j], C, y[s][j]);
+      y[s][0] = fma(P.nl, C, y[s][0]);
     }
   }
+#pragma unroll
+  for (int j = 1; j < SUB; ++j)
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nl, y[s][j - 1], y[s][j]);
   if (ghosts) {
 #pragma unroll
     for (int s = 0; s < NSEG; ++s)
@@ -164,15 +159,17 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
   }
   // ---- backward: U^-1 ----
 #pragma unroll
+  for (int s = 0; s < NSEG; ++s) I[s] = y[s][SUB - 1];
+#pragma unroll
   for (int j = SUB - 2; j >= 0; --j)
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nu, y[s][j + 1], y[s][j]);
+    for (int s = 0; s < NSEG; ++s) I[s] = fma(P.nu, I[s], y[s][j]);
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s) I[s] = y[s][0];
+  for (int st = 0; st < 5; ++st) {
+    const double c = sh.cb[st][lane];
 #pragma unroll
-  for (int st = 0; st < 5; ++st)
-#pragma unroll
-    for (int s = 0; s < NSEG; ++s) scan_stage_down(I[s], P.qq[st], 1 << st);
+    for (int s = 0; s < NSEG; ++s) I[s] = fma(c, __shfl_down_sync(kFull, I[s], 1 << st), I[s]);
+  }
 #pragma unroll
   for (int s = 0; s < NSEG; ++s) {
     Ip[s] = __shfl_down_sync(kFull, I[s], 1);
@@ -207,10 +204,13 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
       if (s < NSEG - 1) S = fma(P.Qseg, S, Tot[s + 1]);
       double R = fma(L.qlane, Wc[s], Ip[s]);
       R = fma(L.qpos, S, R);
-#pragma unroll
-      for (int j = 0; j < SUB; ++j) y[s][j] = fma(P.fu[j], R, y[s][j]);
+      y[s][SUB - 1] = fma(P.nu, R, y[s][SUB - 1]);
     }
   }
+#pragma unroll
+  for (int j = SUB - 2; j >= 0; --j)
+#pragma unroll
+    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nu, y[s][j + 1], y[s][j]);
   // ---- corner rank-1 correction ----
   if (!wide) {
     if (warp == 0) {
