@@ -201,6 +201,10 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                               pit_record* records, int max_records, pit_solve_info* info,
                               void* stream);
 
+/* Measured FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA):
+ * the roofline denominator for the FP64-pipe-bound fine propagator. */
+int pit_measure_fp64_peak(int device, double* tflops);
+
 /* Seeded inputs (the libstdc++ generators of the reference's tests,
  * tests/oracles.cpp:108-122): std::mt19937_64 + uniform_real_distribution /
  * normal_distribution, drawn in order. */

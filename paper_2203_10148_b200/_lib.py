@@ -89,7 +89,7 @@ EXPORTS = [
     "pit_propagate", "pit_block_inner_product", "pit_block_norm_n_inf", "pit_pitsbicg_solve",
     "pit_parareal_solve", "pit_apply_F_device", "pit_residual_device", "pit_coarse_sweep_device",
     "pit_block_partials_device", "pit_sync_status", "pit_pitsbicg_solve_device",
-    "pit_seeded_uniform", "pit_seeded_normal",
+    "pit_seeded_uniform", "pit_seeded_normal", "pit_measure_fp64_peak",
 ]
 
 _lib = None
@@ -133,6 +133,7 @@ def lib():
     L.pit_sync_status.argtypes = [vp, vp]
     L.pit_pitsbicg_solve_device.argtypes = [vp, C.POINTER(SolverConfigC), vp, vp,
                                             C.POINTER(RecordC), C.c_int, C.POINTER(SolveInfoC), vp]
+    L.pit_measure_fp64_peak.argtypes = [C.c_int, _dp]
     L.pit_seeded_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]
     L.pit_seeded_uniform.restype = None
     L.pit_seeded_normal.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]

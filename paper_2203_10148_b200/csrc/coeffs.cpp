@@ -24,7 +24,8 @@ const L kLayouts[] = {{4, 1, 1},  {4, 1, 2},  {4, 1, 4},  {4, 1, 8},  {4, 1, 16}
                       {8, 1, 4},  {8, 1, 8},  {8, 1, 16}, {8, 1, 32}, {16, 1, 2}, {16, 1, 4},
                       {16, 1, 8}, {16, 1, 16}, {16, 1, 32}, {16, 2, 4}, {16, 2, 8}, {16, 4, 2},
                       {16, 4, 4}, {32, 2, 2}, {32, 2, 4}, {32, 4, 1}, {32, 4, 2}, {32, 4, 4},
-                      {64, 4, 1}, {64, 4, 2}, {16, 4, 8}, {8, 4, 8},  {16, 2, 16}, {32, 4, 8}};
+                      {64, 4, 1}, {64, 4, 2}, {16, 4, 8}, {8, 4, 8},  {16, 2, 16}, {32, 4, 8},
+                      {64, 4, 4}};
 }  // namespace
 
 bool layout_supported(int mpt, int nseg, int warps) {
@@ -34,12 +35,12 @@ bool layout_supported(int mpt, int nseg, int warps) {
 }
 
 Layout auto_layout(int M, int role) {
-  // fine: 32 points per thread as 4 strided segments of 8 (the four segment
+  // fine: 64 points per thread as 4 strided segments of 16 (the four segment
   // sweeps and scans interleave, hiding DFMA / shuffle latency, and the
-  // per-warp scan cost is amortised over 32 points); coarse (one persistent
+  // per-warp scan cost is amortised over 64 points); coarse (one persistent
   // CTA, latency bound): many threads, few points each.
   static const L fine[] = {{4, 1, 1}, {4, 1, 2}, {4, 1, 4}, {8, 1, 4},
-                           {32, 4, 2}, {32, 4, 4}, {32, 4, 4}, {32, 4, 4}};
+                           {64, 4, 1}, {64, 4, 2}, {64, 4, 4}, {32, 4, 8}};
   static const L coarse[] = {{4, 1, 1}, {4, 1, 2}, {4, 1, 4}, {8, 1, 4},
                              {4, 1, 32}, {8, 1, 16}, {8, 1, 32}, {16, 1, 32}};
   const L* list = role == PIT_FINE ? fine : coarse;

@@ -82,6 +82,10 @@ struct pit_context {
   cudaStream_t stream = nullptr;
   // solver work buffers (N*M each), allocated on first solve
   double* buf[10] = {};
+  // host-entry scratch (see to_device)
+  double* scratch[3] = {};
+  size_t scratch_n[3] = {};
+  bool scratch_busy[3] = {};
   size_t nm() const { return (size_t)N * (size_t)M; }
 };
 
@@ -436,6 +440,7 @@ int pit_context_destroy(pit_context* ctx) {
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_partials) cudaFreeHost(ctx->h_partials);
   for (auto& b : ctx->buf) cudaFree(b);
+  for (auto& b : ctx->scratch) cudaFree(b);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PIT_OK;
@@ -497,17 +502,42 @@ int pit_sync_status(pit_context* ctx, void* stream) {
 
 namespace {
 
+// Scratch device vectors for the host-pointer entry points: the context keeps
+// up to three N*M buffers (allocated on first use) so repeated calls do not
+// pay cudaMalloc/cudaFree.
 struct DevVec {
   double* p = nullptr;
-  ~DevVec() { cudaFree(p); }
 };
 
 int to_device(pit_context* ctx, const double* h, size_t n, DevVec* d) {
-  CUDA_TRY(cudaMalloc(&d->p, n * sizeof(double)));
+  int slot = -1;
+  for (int i = 0; i < 3; ++i)
+    if (!ctx->scratch_busy[i]) {
+      slot = i;
+      break;
+    }
+  if (slot < 0) return set_err(PIT_ERR_INVALID_ARGUMENT, "internal: scratch exhausted");
+  if (ctx->scratch_n[slot] < n) {
+    cudaFree(ctx->scratch[slot]);
+    ctx->scratch[slot] = nullptr;
+    ctx->scratch_n[slot] = 0;
+    CUDA_TRY(cudaMalloc(&ctx->scratch[slot], n * sizeof(double)));
+    ctx->scratch_n[slot] = n;
+  }
+  ctx->scratch_busy[slot] = true;
+  d->p = ctx->scratch[slot];
   if (h)
     CUDA_TRY(cudaMemcpyAsync(d->p, h, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   return PIT_OK;
 }
+
+// Releases all scratch slots when the entry point returns.
+struct ScratchScope {
+  pit_context* ctx;
+  ~ScratchScope() {
+    for (auto& b : ctx->scratch_busy) b = false;
+  }
+};
 
 int to_host(pit_context* ctx, const double* d, size_t n, double* h) {
   CUDA_TRY(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -531,6 +561,7 @@ void add_coarse(pit_context* ctx, pit_run_stats* s, double ms) {
 
 int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats) {
   if (!ctx || !L || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: null argument");
+  ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
   DevVec dL, dO;
   PIT_TRY(to_device(ctx, L, ctx->nm(), &dL));
@@ -544,6 +575,7 @@ int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* s
 
 int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
   if (!ctx || !rhs) return set_err(PIT_ERR_INVALID_ARGUMENT, "assemble_rhs: null argument");
+  ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
   DevVec d;
   PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &d));
@@ -567,6 +599,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
 
 int pit_apply_G_inverse(pit_context* ctx, const double* V, double* out, pit_run_stats* stats) {
   if (!ctx || !V || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_G_inverse: null argument");
+  ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
   DevVec d;
   PIT_TRY(to_device(ctx, V, ctx->nm(), &d));
@@ -609,6 +642,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
 
 int pit_initial_guess(pit_context* ctx, int policy, double* out, pit_run_stats* stats) {
   if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "initial_guess: null argument");
+  ScratchScope scope_{ctx};
   DevVec d;
   PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &d));
   PIT_TRY(initial_guess_dev(ctx, policy, d.p, stats));
@@ -619,6 +653,7 @@ int pit_preconditioned_residual(pit_context* ctx, const double* lambda, const do
                                 double* out, pit_run_stats* stats) {
   if (!ctx || !lambda || !rhs || !out)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "preconditioned_residual: null argument");
+  ScratchScope scope_{ctx};
   DevVec dl, db, dr;
   PIT_TRY(to_device(ctx, lambda, ctx->nm(), &dl));
   PIT_TRY(to_device(ctx, rhs, ctx->nm(), &db));
@@ -636,6 +671,7 @@ int pit_preconditioned_residual(pit_context* ctx, const double* lambda, const do
 
 int pit_sequential_fine_solve(pit_context* ctx, double* out) {
   if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "sequential_fine_solve: null argument");
+  ScratchScope scope_{ctx};
   DevVec d;
   PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &d));
   CUDA_TRY(cudaMemsetAsync(d.p, 0, ctx->nm() * sizeof(double), ctx->stream));
@@ -650,6 +686,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
                   double* out) {
   if (!ctx || !out || (role != PIT_FINE && role != PIT_COARSE))
     return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: bad argument");
+  ScratchScope scope_{ctx};
   if (slab < 0 || slab >= ctx->N)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: slab_index out of range");
   const size_t M = ctx->M;
@@ -677,6 +714,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
 
 int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, double* out) {
   if (!ctx || !a || !b || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "block_inner_product: null");
+  ScratchScope scope_{ctx};
   DevVec da, db;
   PIT_TRY(to_device(ctx, a, ctx->nm(), &da));
   PIT_TRY(to_device(ctx, b, ctx->nm(), &db));
@@ -690,6 +728,7 @@ int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, 
 
 int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out) {
   if (!ctx || !a || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "block_norm_n_inf: null");
+  ScratchScope scope_{ctx};
   DevVec da;
   PIT_TRY(to_device(ctx, a, ctx->nm(), &da));
   const double* A[1] = {da.p};
@@ -977,6 +1016,13 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
   PIT_TRY(pitsbicg_dev(ctx, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
                        max_records, info));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PIT_OK;
+}
+
+int pit_measure_fp64_peak(int device, double* tflops) {
+  if (!tflops) return set_err(PIT_ERR_INVALID_ARGUMENT, "null output");
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(measure_fp64_peak(tflops));
   return PIT_OK;
 }
 

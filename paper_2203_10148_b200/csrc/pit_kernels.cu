@@ -424,7 +424,7 @@ int ew_grid(size_t n) {
   X(8, 1, 16) X(8, 1, 32) X(16, 1, 2) X(16, 1, 4) X(16, 1, 8) X(16, 1, 16) X(16, 1, 32)     \
   X(16, 2, 4) X(16, 2, 8) X(16, 4, 2) X(16, 4, 4) X(32, 2, 2) X(32, 2, 4) X(32, 4, 1)      \
   X(32, 4, 2) X(32, 4, 4) X(64, 4, 1) X(64, 4, 2) X(16, 4, 8) X(8, 4, 8) X(16, 2, 16)      \
-  X(32, 4, 8)
+  X(32, 4, 8) X(64, 4, 4)
 
 cudaError_t launch_slab(int mpt, int nsub, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st) {
@@ -448,6 +448,47 @@ cudaError_t launch_sweep(int mpt, int nsub, int warps, bool src, const StepParam
   PIT_LAYOUTS(X)
 #undef X
   return cudaErrorInvalidConfiguration;
+}
+
+// FP64 pipe probe for the roofline denominator: 8 independent DFMA chains per
+// thread, 8 x 256-thread CTAs per SM.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters, double a) {
+  double v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = fma(v[k], a, 1e-9);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += v[k];
+  if (s == 1.2345) out[0] = s;
+}
+
+cudaError_t measure_fp64_peak(double* tflops) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 64);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int grid = sms * 8, iters = 40000;
+  fp64_probe_kernel<<<grid, 256>>>(d, 100, 1.0000001);
+  cudaEventRecord(e0);
+  fp64_probe_kernel<<<grid, 256>>>(d, iters, 1.0000001);
+  cudaEventRecord(e1);
+  e = cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *tflops = 2.0 * 8 * iters * (double)grid * 256 / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return e;
 }
 
 cudaError_t launch_dots(int M, int blocks, double weight, int np, const double* const* a,

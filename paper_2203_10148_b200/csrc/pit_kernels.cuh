@@ -63,5 +63,7 @@ cudaError_t launch_update_p(size_t n, double omega, double beta, const double* d
 cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st);
 // y = y + x
 cudaError_t launch_add(size_t n, const double* x, double* y, cudaStream_t st);
+// measured FP64 DFMA throughput of the current device (TFLOP/s)
+cudaError_t measure_fp64_peak(double* tflops);
 
 }  // namespace pitb
