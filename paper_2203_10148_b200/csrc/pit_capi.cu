@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -82,6 +83,7 @@ struct pit_context {
   cudaStream_t stream = nullptr;
   // solver work buffers (N*M each), allocated on first solve
   double* buf[10] = {};
+  int stagger = 0, stagger_mod = 1, sms = 148;  // slab-kernel phase offset (see SlabArgs)
   // host-entry scratch (see to_device)
   double* scratch[3] = {};
   size_t scratch_n[3] = {};
@@ -229,6 +231,9 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
     A.out = out;
     A.slab0 = first - 1;
   }
+  A.stagger = ctx->stagger;
+  A.stagger_mod = ctx->stagger_mod;
+  A.sms = ctx->sms;
   CUDA_TRY(launch_slab(R.mpt, R.nseg, R.warps, false, R.P, A, ctas, st));
   return PIT_OK;
 }
@@ -411,6 +416,9 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
       R.P.shape = ctx->d_shape;
     }
   }
+  cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, desc->device);
+  if (const char* e = std::getenv("PIT_STAGGER")) ctx->stagger = std::atoi(e);
+  if (const char* e = std::getenv("PIT_STAGGER_MOD")) ctx->stagger_mod = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_status, sizeof(int)) != cudaSuccess ||

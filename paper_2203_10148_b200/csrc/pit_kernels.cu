@@ -150,6 +150,16 @@ __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSEG, WARPS, SRC
   const int slab = A.slab0 + b;
   __syncthreads();
   const StepLane L = step_lane<SUB, NSEG, WARPS>(P, *sh, tid);
+  if (A.stagger > 0) {
+    // Offset the step phase of co-resident CTAs (same SM: block ids that
+    // differ by a multiple of the SM count) so their latency-bound scan
+    // phases overlap other CTAs' DFMA-bound sweeps.
+    const long long wait = (long long)((b / A.sms) % A.stagger_mod) * A.stagger;
+    const long long t0 = clock64();
+    while (clock64() - t0 < wait) {
+    }
+    __syncthreads();
+  }
 
   run_slab<SUB, NSEG, WARPS, SRC>(y, P, L, *sh, s_zc, lane, warp, g0, slab);
 
