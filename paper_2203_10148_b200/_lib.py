@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpit_b200.so")
+LIB_PATH = os.environ.get("PIT_LIB") or os.path.join(HERE, "libpit_b200.so")
 
 PIT_OK = 0
 PIT_ERR_INVALID_ARGUMENT = 1

@@ -417,6 +417,10 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     }
   }
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, desc->device);
+#ifdef PIT_PHASE_TIMING
+  cudaMalloc(&ctx->role[PIT_FINE].P.timing, 32 * sizeof(long long));
+  cudaMemset(ctx->role[PIT_FINE].P.timing, 0, 32 * sizeof(long long));
+#endif
   if (const char* e = std::getenv("PIT_STAGGER")) ctx->stagger = std::atoi(e);
   if (const char* e = std::getenv("PIT_STAGGER_MOD")) ctx->stagger_mod = std::max(1, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -1025,6 +1029,20 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                        max_records, info));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return PIT_OK;
+}
+
+// instrumented builds only: per-phase cycle totals of CTA 0 (warps 0, 1)
+extern "C" int pit_debug_phase_timing(pit_context* ctx, long long* out32) {
+#ifdef PIT_PHASE_TIMING
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(out32, ctx->role[PIT_FINE].P.timing, 32 * sizeof(long long),
+                      cudaMemcpyDeviceToHost));
+  return PIT_OK;
+#else
+  (void)ctx;
+  (void)out32;
+  return set_err(PIT_ERR_INVALID_ARGUMENT, "not an instrumented build");
+#endif
 }
 
 int pit_measure_fp64_peak(int device, double* tflops) {

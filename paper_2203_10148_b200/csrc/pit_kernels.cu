@@ -73,6 +73,13 @@ __device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParam
   constexpr int LSEG = 32 * WARPS * SUB;
   const bool ghosts = P.M < NSEG * LSEG;
   const bool wide = P.K0 > 32 * SUB;
+#ifdef PIT_PHASE_TIMING
+  long long ph_acc[16] = {};
+  long long ph_t = clock64();
+#define PIT_TIMING_ARGS , ph_acc, ph_t
+#else
+#define PIT_TIMING_ARGS
+#endif
   if (SRC) {
     // separable source y += dt*s(t_k) g(x): g read through L1 each step (not
     // held in registers, so wide layouts do not spill)
@@ -87,7 +94,7 @@ __device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParam
           const int i = s * LSEG + g0 + j;
           y[s][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[s][j]);
         }
-      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide);
+      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide PIT_TIMING_ARGS);
 #pragma unroll
       for (int s = 0; s < NSEG; ++s)
 #pragma unroll
@@ -97,7 +104,7 @@ __device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParam
   } else {
     int cnt = 0;
     for (int k = 0; k < P.steps; ++k) {
-      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide);
+      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide PIT_TIMING_ARGS);
       if (++cnt == P.R) {
         cnt = 0;
 #pragma unroll
@@ -105,6 +112,7 @@ __device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParam
 #pragma unroll
           for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invR;
       }
+      PIT_PHASE(9);
     }
     if (cnt) {
 #pragma unroll
@@ -113,6 +121,10 @@ __device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParam
         for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invLast;
     }
   }
+#ifdef PIT_PHASE_TIMING
+  if (P.timing && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && warp < 2)
+    for (int k = 0; k < 16; ++k) P.timing[warp * 16 + k] = ph_acc[k];
+#endif
 }
 
 template <int SUB, int NSEG, int WARPS>

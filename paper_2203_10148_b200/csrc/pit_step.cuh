@@ -43,7 +43,21 @@ struct StepParams {
   const double* qpos;   // [T] nu^((T-1-t)*SUB)  (device)
   const double* shape;  // [M] source shape g(x_i) (device) or nullptr
   const double* ds;     // [slabs*steps] dt*s(t_k) table (device) or nullptr
+  long long* timing;    // PIT_PHASE_TIMING builds only: [2 warps][16 phases] cycles
 };
+
+#ifdef PIT_PHASE_TIMING
+#define PIT_PHASE(k)                          \
+  do {                                        \
+    const long long now_ = clock64();         \
+    ph_acc[k] += now_ - ph_t;                 \
+    ph_t = now_;                              \
+  } while (0)
+#else
+#define PIT_PHASE(k) \
+  do {               \
+  } while (0)
+#endif
 
 // Shared memory of one slab CTA: per-segment cross-warp totals, broadcast
 // scalar and the per-lane carry weights (read with LDS: an indexed constant
@@ -93,7 +107,11 @@ template <int SUB, int NSEG, int WARPS>
 __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParams& P,
                                          const StepLane& L, StepShared<NSEG, WARPS>& sh,
                                          const double* __restrict__ s_zc, int lane, int warp,
-                                         int g0, bool ghosts, bool wide) {
+                                         int g0, bool ghosts, bool wide
+#ifdef PIT_PHASE_TIMING
+                                         , long long (&ph_acc)[16], long long& ph_t
+#endif
+) {
   constexpr int LSEG = 32 * WARPS * SUB;
   double I[NSEG], Ip[NSEG], Wc[NSEG], Tot[NSEG];
   // ---- forward: L^-1 ----
@@ -103,6 +121,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
   for (int j = 1; j < SUB; ++j)
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(P.nl, I[s], y[s][j]);
+  PIT_PHASE(0);
 #pragma unroll
   for (int st = 0; st < 5; ++st) {
     const double c = sh.cf[st][lane];
@@ -115,6 +134,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
     Ip[s] = lane == 0 ? 0.0 : Ip[s];
     Wc[s] = 0.0;
   }
+  PIT_PHASE(1);
   if (WARPS > 1) {
     if (lane == 31) {
 #pragma unroll
@@ -136,6 +156,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
 #pragma unroll
     for (int s = 0; s < NSEG - 1; ++s) Tot[s] = __shfl_sync(kFull, I[s], 31);
   }
+  PIT_PHASE(2);
   {
     double S = 0.0;  // segment carry-in
 #pragma unroll
@@ -157,6 +178,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
       for (int j = 0; j < SUB; ++j)
         y[s][j] = (s * LSEG + g0 + j < P.M) ? y[s][j] : 0.0;  // Dirichlet padding
   }
+  PIT_PHASE(3);
   // ---- backward: U^-1 ----
 #pragma unroll
   for (int s = 0; s < NSEG; ++s) I[s] = y[s][SUB - 1];
@@ -164,6 +186,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
   for (int j = SUB - 2; j >= 0; --j)
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(P.nu, I[s], y[s][j]);
+  PIT_PHASE(4);
 #pragma unroll
   for (int st = 0; st < 5; ++st) {
     const double c = sh.cb[st][lane];
@@ -176,6 +199,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
     Ip[s] = lane == 31 ? 0.0 : Ip[s];
     Wc[s] = 0.0;
   }
+  PIT_PHASE(5);
   if (WARPS > 1) {
     if (lane == 0) {
 #pragma unroll
@@ -197,6 +221,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
 #pragma unroll
     for (int s = 1; s < NSEG; ++s) Tot[s] = __shfl_sync(kFull, I[s], 0);
   }
+  PIT_PHASE(6);
   {
     double S = 0.0;  // segment carry from the right
 #pragma unroll
@@ -211,6 +236,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
   for (int j = SUB - 2; j >= 0; --j)
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nu, y[s][j + 1], y[s][j]);
+  PIT_PHASE(7);
   // ---- corner rank-1 correction ----
   if (!wide) {
     if (warp == 0) {
@@ -231,6 +257,7 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
         for (int j = 0; j < SUB; ++j) y[s][j] = fma(c, s_zc[s * LSEG + g0 + j], y[s][j]);
       }
   }
+  PIT_PHASE(8);
 }
 
 }  // namespace pitb
