@@ -85,11 +85,11 @@ typedef struct pit_problem_desc {
   const double* source_shape; /* [M] host, copied; NULL when no source */
   const double* initial_value;/* [M] host y0, copied */
   int32_t device;         /* CUDA ordinal */
-  /* kernel layout per role: points per thread, strided segments per slab
-   * (each thread holds mpt/nseg points of every segment), warps per slab
-   * CTA; all 0 = auto */
-  int32_t fine_mpt, fine_nseg, fine_warps;
-  int32_t coarse_mpt, coarse_nseg, coarse_warps;
+  /* kernel layout per role: points per thread, contiguous sub-chunks per
+   * thread chunk, strided segments per slab, warps per slab CTA
+   * (sub-chunk length = mpt / (nsub*nseg)); all 0 = auto */
+  int32_t fine_mpt, fine_nsub, fine_nseg, fine_warps;
+  int32_t coarse_mpt, coarse_nsub, coarse_nseg, coarse_warps;
 } pit_problem_desc;
 
 typedef struct pit_context pit_context;
@@ -133,13 +133,16 @@ typedef struct pit_solve_info {
  * solve, exported so tests can check that the oracle's own
  * recipe produces identical bits. */
 typedef struct pit_step_coeffs {
-  int32_t M, mpt, nseg, warps, steps;
+  int32_t M, mpt, nsub, nseg, warps, steps;
   double delta, lam, mu;
   double dstar, nl, nu, inv, gneg;
   int32_t K0, R;
   double invR, invLast;
-  double Pseg, Qseg;      /* nl^lseg, nu^lseg, lseg = 32*warps*sub, sub = mpt/nseg */
-  double fl[64], fu[64];  /* nl^(j+1), nu^(sub-j), j < sub */
+  double pS, qS;          /* nl^sub, nu^sub, sub = mpt/(nsub*nseg) */
+  double Pseg, Qseg;      /* nl^lseg, nu^lseg, lseg = 32*warps*nsub*sub */
+  double nlpow[32];       /* nl^j, j < sub  (narrow corner) */
+  double pw[8];           /* nl^(u*sub), u < nsub (narrow corner) */
+  int32_t narrow;         /* corner correction in geometric form */
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
 } pit_step_coeffs;
@@ -156,8 +159,10 @@ int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing);
 int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out);
 /* zc correction vector (first K0 entries used), length M (no device needed). */
 int pit_step_correction(const pit_problem_desc* desc, int role, double* zc_out);
-/* per-thread segment-carry weights, length 32*warps each (no device needed). */
-int pit_step_positions(const pit_problem_desc* desc, int role, double* ppos_out, double* qpos_out);
+/* per-thread weights, length 32*warps each (no device needed): segment-carry
+ * weights nl^(t*ch), nu^((T-1-t)*ch) and narrow-corner weights zc_0 nl^(t*ch). */
+int pit_step_positions(const pit_problem_desc* desc, int role, double* ppos_out, double* qpos_out,
+                       double* zt_out);
 
 /* ---- host-pointer entry points (copy in, compute, copy out) ---------- */
 int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats);

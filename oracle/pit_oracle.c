@@ -17,15 +17,16 @@
 /* checks both produce identical bits.                                       */
 /* ------------------------------------------------------------------------ */
 
-int orc_stepper_init(orc_stepper* s, int M, int m, int nseg, int warps, int steps,
+int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int nseg, int warps, int steps,
                      double band_lo, double band_diag, double band_up, double dt) {
   typedef long double ld;
   memset(s, 0, sizeof(*s));
-  if (M < 1 || m < 1 || m > ORC_MAX_M || nseg < 1 || m % nseg || m / nseg > 32 || warps < 1 ||
-      steps < 1)
+  if (M < 1 || m < 1 || m > ORC_MAX_M || nsub < 1 || nsub > 8 || nseg < 1 || m % (nsub * nseg) ||
+      m / (nsub * nseg) > 32 || warps < 1 || steps < 1)
     return -1;
   s->M = M;
   s->m = m;
+  s->nsub = nsub;
   s->nseg = nseg;
   s->warps = warps;
   s->Mp = 32 * warps * m;
@@ -73,22 +74,24 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int nseg, int warps, int step
     }
     s->K0 = k0;
   }
+  const ld z0 = z[0];
   free(z);
   {
-    /* chunk = sub points (warp scan multiplier nl^sub); segment = T*sub */
-    const int sub = m / nseg, T = 32 * warps;
-    ld nlp[33], nup[33];
+    /* sub-chunk = sub points; thread chunk = ch = nsub*sub (warp scan
+     * multiplier nl^ch); segment = T*ch */
+    const int sub = m / (nsub * nseg), ch = nsub * sub, T = 32 * warps;
+    ld nlp[65], nup[65];
     nlp[0] = 1.0L;
     nup[0] = 1.0L;
-    for (int k = 1; k <= sub; ++k) {
+    for (int k = 1; k <= 64; ++k) {
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
     }
-    for (int j = 0; j < sub; ++j) {
-      s->fl[j] = (double)nlp[j + 1];
-      s->fu[j] = (double)nup[sub - j];
-    }
-    ld pk = nlp[sub], qk = nup[sub];
+    for (int j = 0; j < sub; ++j) s->nlpow[j] = (double)nlp[j];
+    for (int u = 0; u < nsub; ++u) s->pw[u] = (double)nlp[u * sub];
+    s->pS = (double)nlp[sub];
+    s->qS = (double)nup[sub];
+    ld pk = nlp[ch], qk = nup[ch];
     for (int k = 0; k < 5; ++k) {
       s->pp[k] = (double)pk;
       s->qq[k] = (double)qk;
@@ -101,20 +104,24 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int nseg, int warps, int step
     for (int l = 0; l < 32; ++l) {
       s->plane[l] = (double)pl;
       s->qlane[31 - l] = (double)ql;
-      pl = pl * nlp[sub];
-      ql = ql * nup[sub];
+      pl = pl * nlp[ch];
+      ql = ql * nup[ch];
     }
     s->ppos = (double*)calloc((size_t)T, sizeof(double));
     s->qpos = (double*)calloc((size_t)T, sizeof(double));
+    s->zt = (double*)calloc((size_t)T, sizeof(double));
     ld pt = 1.0L, qt = 1.0L;
     for (int t = 0; t < T; ++t) {
       s->ppos[t] = (double)pt;
       s->qpos[T - 1 - t] = (double)qt;
-      pt = pt * nlp[sub];
-      qt = qt * nup[sub];
+      s->zt[t] = (double)(z0 * pt);
+      pt = pt * nlp[ch];
+      qt = qt * nup[ch];
     }
     s->Pseg = (double)pt;
     s->Qseg = (double)qt;
+    const ld decay = powl(fabsl(nl * nu), (ld)(M - s->K0));
+    s->narrow = (s->K0 <= 32 * ch && decay < 7.7e-34L) ? 1 : 0;
   }
   {
     double lg = log2(s->dstar);
@@ -140,33 +147,42 @@ void orc_stepper_free(orc_stepper* s) {
   free(s->zc);
   free(s->ppos);
   free(s->qpos);
-  s->zc = s->ppos = s->qpos = NULL;
+  free(s->zt);
+  s->zc = s->ppos = s->qpos = s->zt = NULL;
 }
 
 /* One unscaled solve y <- U^-1 L^-1 b plus the corner correction, on the
  * padded array y[Mp], chunked exactly like the CUDA step (pit_step.cuh
- * be_solve).  The padded slab is nseg segments of lseg = T*sub points;
- * thread k owns chunk k (sub points) of every segment.  Per direction and
- * segment: pass 1 sweeps each chunk with zero carry (end value only); warp
- * Kogge-Stone scan + sequential cross-warp combine; segment totals chained
- * segment to segment; chunk carry = local carry + pos_k * segment carry;
- * pass 2 reruns the chunk's sweep from its carry. */
+ * be_solve).  The padded slab is nseg segments of lseg = T*ch points; thread
+ * k owns chunk k (ch = nsub*sub contiguous points) of every segment, split
+ * into nsub sub-chunks.  Per direction and segment: pass 1 sweeps each
+ * sub-chunk with zero carry (end value only); the chunk end combines its
+ * sub-chunks; warp Kogge-Stone scan + sequential cross-warp combine; segment
+ * totals chained segment to segment; chunk carry = local carry + pos_k *
+ * segment carry; sub-chunk carries; pass 2 reruns each sub-chunk's sweep. */
 static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   const int W = s->warps, T = 32 * W, M = s->M;
-  const int ns = s->nseg, sub = s->m / ns, lseg = T * sub;
+  const int nu_ = s->nsub, ns = s->nseg, sub = s->m / (nu_ * ns), ch = nu_ * sub, lseg = T * ch;
   double* Z = scratch;          /* [T] chunk end values / scan */
   double* C = scratch + T;      /* [T] local carries */
   double* tot = scratch + 2 * T;/* [W] */
   double* tmp = scratch + 2 * T + W; /* [32] */
+  double E[8];
 
   /* ---- forward ---- */
   double S = 0.0; /* segment carry-in */
   for (int q = 0; q < ns; ++q) {
     double* seg = y + (size_t)q * lseg;
-    for (int k = 0; k < T; ++k) { /* pass 1: end value with zero carry */
-      const double* c = seg + (size_t)k * sub;
-      double z = c[0];
-      for (int j = 1; j < sub; ++j) z = fma(s->nl, z, c[j]);
+    for (int k = 0; k < T; ++k) { /* pass 1 */
+      const double* c = seg + (size_t)k * ch;
+      for (int u = 0; u < nu_; ++u) {
+        const double* cu = c + u * sub;
+        double z = cu[0];
+        for (int j = 1; j < sub; ++j) z = fma(s->nl, z, cu[j]);
+        E[u] = z;
+      }
+      double z = E[0];
+      for (int u = 1; u < nu_; ++u) z = fma(s->pS, z, E[u]);
       Z[k] = z;
     }
     for (int w = 0; w < W; ++w) {
@@ -188,11 +204,22 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     }
     double segtot = 0.0;
     for (int v = 0; v < W; ++v) segtot = fma(s->p32, segtot, tot[v]);
-    for (int k = 0; k < T; ++k) { /* pass 2 from the true carry */
-      double* c = seg + (size_t)k * sub;
-      const double Ck = fma(s->ppos[k], S, C[k]);
-      c[0] = fma(s->nl, Ck, c[0]);
-      for (int j = 1; j < sub; ++j) c[j] = fma(s->nl, c[j - 1], c[j]);
+    for (int k = 0; k < T; ++k) { /* pass 2 from the true carries */
+      double* c = seg + (size_t)k * ch;
+      for (int u = 0; u < nu_; ++u) { /* sub-chunk end values with zero carry */
+        const double* cu = c + u * sub;
+        double z = cu[0];
+        for (int j = 1; j < sub; ++j) z = fma(s->nl, z, cu[j]);
+        E[u] = z;
+      }
+      double Ck = fma(s->ppos[k], S, C[k]);
+      for (int u = 0; u < nu_; ++u) {
+        double* cu = c + u * sub;
+        const double Cu = Ck;
+        if (u + 1 < nu_) Ck = fma(s->pS, Ck, E[u]);
+        cu[0] = fma(s->nl, Cu, cu[0]);
+        for (int j = 1; j < sub; ++j) cu[j] = fma(s->nl, cu[j - 1], cu[j]);
+      }
     }
     S = fma(s->Pseg, S, segtot); /* carry into segment q+1 */
   }
@@ -201,10 +228,16 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
   S = 0.0;
   for (int q = ns - 1; q >= 0; --q) {
     double* seg = y + (size_t)q * lseg;
-    for (int k = 0; k < T; ++k) { /* pass 1: start value with zero carry */
-      const double* c = seg + (size_t)k * sub;
-      double h = c[sub - 1];
-      for (int j = sub - 2; j >= 0; --j) h = fma(s->nu, h, c[j]);
+    for (int k = 0; k < T; ++k) { /* pass 1 */
+      const double* c = seg + (size_t)k * ch;
+      for (int u = 0; u < nu_; ++u) {
+        const double* cu = c + u * sub;
+        double h = cu[sub - 1];
+        for (int j = sub - 2; j >= 0; --j) h = fma(s->nu, h, cu[j]);
+        E[u] = h;
+      }
+      double h = E[nu_ - 1];
+      for (int u = nu_ - 2; u >= 0; --u) h = fma(s->qS, h, E[u]);
       Z[k] = h;
     }
     for (int w = 0; w < W; ++w) {
@@ -227,18 +260,42 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     }
     double segtot = 0.0;
     for (int v = W - 1; v >= 0; --v) segtot = fma(s->q32, segtot, tot[v]);
-    for (int k = 0; k < T; ++k) { /* pass 2 from the true carry */
-      double* c = seg + (size_t)k * sub;
-      const double Rk = fma(s->qpos[k], S, C[k]);
-      c[sub - 1] = fma(s->nu, Rk, c[sub - 1]);
-      for (int j = sub - 2; j >= 0; --j) c[j] = fma(s->nu, c[j + 1], c[j]);
+    for (int k = 0; k < T; ++k) { /* pass 2 */
+      double* c = seg + (size_t)k * ch;
+      for (int u = 0; u < nu_; ++u) {
+        const double* cu = c + u * sub;
+        double h = cu[sub - 1];
+        for (int j = sub - 2; j >= 0; --j) h = fma(s->nu, h, cu[j]);
+        E[u] = h;
+      }
+      double Rk = fma(s->qpos[k], S, C[k]);
+      for (int u = nu_ - 1; u >= 0; --u) {
+        double* cu = c + u * sub;
+        const double Ru = Rk;
+        if (u > 0) Rk = fma(s->qS, Rk, E[u]);
+        cu[sub - 1] = fma(s->nu, Ru, cu[sub - 1]);
+        for (int j = sub - 2; j >= 0; --j) cu[j] = fma(s->nu, cu[j + 1], cu[j]);
+      }
     }
     S = fma(s->Qseg, S, segtot);
   }
   /* corner rank-1 correction */
   {
-    double cc = s->gneg * y[0];
-    for (int i = 0; i < s->K0; ++i) y[i] = fma(cc, s->zc[i], y[i]);
+    const double cc = s->gneg * y[0];
+    if (s->narrow) {
+      for (int k = 0; k < 32 && k * ch < s->K0; ++k) {
+        const double a = cc * s->zt[k];
+        for (int u = 0; u < nu_; ++u) {
+          const double au = a * s->pw[u];
+          for (int j = 0; j < sub; ++j) {
+            double* v = y + (size_t)k * ch + u * sub + j;
+            *v = fma(au, s->nlpow[j], *v);
+          }
+        }
+      }
+    } else {
+      for (int i = 0; i < s->K0; ++i) y[i] = fma(cc, s->zc[i], y[i]);
+    }
   }
 }
 
@@ -671,8 +728,8 @@ static int orc_1d_prop(void* user, int role, int with_source, const double* in, 
 
 orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double band_up, int N,
                       double total_time, int fine_steps, int coarse_steps, int fine_m,
-                      int fine_nseg, int fine_warps, int coarse_m, int coarse_nseg,
-                      int coarse_warps, const double* y0,
+                      int fine_nsub, int fine_nseg, int fine_warps, int coarse_m,
+                      int coarse_nsub, int coarse_nseg, int coarse_warps, const double* y0,
                       int has_source, const double* src_shape, double src_amp,
                       double src_omega, double src_phase, int use_thomas, int mode) {
   orc_1d* o = (orc_1d*)calloc(1, sizeof(orc_1d));
@@ -686,10 +743,10 @@ orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double 
   const double slab = total_time / N; /* TimeSlabPartition::slab_length */
   o->dt[0] = slab / fine_steps;       /* Propagator::internal_dt */
   o->dt[1] = slab / coarse_steps;
-  if (orc_stepper_init(&o->st[0], M, fine_m, fine_nseg, fine_warps, fine_steps, band_lo,
-                       band_diag, band_up, o->dt[0]) ||
-      orc_stepper_init(&o->st[1], M, coarse_m, coarse_nseg, coarse_warps, coarse_steps, band_lo,
-                       band_diag, band_up, o->dt[1])) {
+  if (orc_stepper_init(&o->st[0], M, fine_m, fine_nsub, fine_nseg, fine_warps, fine_steps,
+                       band_lo, band_diag, band_up, o->dt[0]) ||
+      orc_stepper_init(&o->st[1], M, coarse_m, coarse_nsub, coarse_nseg, coarse_warps,
+                       coarse_steps, band_lo, band_diag, band_up, o->dt[1])) {
     orc_1d_destroy(o);
     return NULL;
   }

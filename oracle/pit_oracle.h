@@ -49,7 +49,8 @@ enum { ORC_FINE = 0, ORC_COARSE = 1 };
 typedef struct orc_stepper {
   int M;          /* interior points */
   int m;          /* points per thread */
-  int nseg;       /* strided segments (thread chunk = sub = m / nseg points per segment) */
+  int nsub;       /* contiguous sub-chunks per thread chunk */
+  int nseg;       /* strided segments; sub = m / (nsub*nseg) */
   int warps;      /* warps per slab CTA */
   int Mp;         /* padded length = 32*warps*m */
   int steps;      /* BE steps per slab */
@@ -57,18 +58,22 @@ typedef struct orc_stepper {
   double dstar, nl, nu, inv;
   double gneg;             /* -gamma' of the corner rank-1 correction */
   int K0;                  /* correction extent */
-  double Pseg, Qseg;       /* nl^lseg, nu^lseg, lseg = 32*warps*sub */
-  double fl[ORC_MAX_M], fu[ORC_MAX_M]; /* fix-up weights nl^(j+1), nu^(sub-j), j < sub */
+  double pS, qS;           /* nl^sub, nu^sub */
+  double Pseg, Qseg;       /* nl^lseg, nu^lseg, lseg = 32*warps*nsub*sub */
+  double nlpow[32];        /* nl^j, j < sub (narrow corner) */
+  double pw[8];            /* nl^(u*sub), u < nsub (narrow corner) */
+  int narrow;              /* corner in geometric form */
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
   int R;                   /* rescale period, homogeneous propagation */
   double invR, invLast;    /* inv^R, inv^(steps % R) */
   double* zc;              /* [M] correction vector z' (entries >= K0 unused) */
-  double* ppos;            /* [32*warps] nl^(t*sub) */
-  double* qpos;            /* [32*warps] nu^((T-1-t)*sub) */
+  double* ppos;            /* [32*warps] nl^(t*ch), ch = nsub*sub */
+  double* qpos;            /* [32*warps] nu^((T-1-t)*ch) */
+  double* zt;              /* [32*warps] zc_0 nl^(t*ch) */
 } orc_stepper;
 
-int orc_stepper_init(orc_stepper* s, int M, int m, int nseg, int warps, int steps,
+int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int nseg, int warps, int steps,
                      double band_lo, double band_diag, double band_up, double dt);
 void orc_stepper_free(orc_stepper* s);
 
@@ -145,8 +150,8 @@ void orc_problem_delete(orc_problem* p);
 typedef struct orc_1d orc_1d;
 orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double band_up, int N,
                       double total_time, int fine_steps, int coarse_steps, int fine_m,
-                      int fine_nseg, int fine_warps, int coarse_m, int coarse_nseg,
-                      int coarse_warps, const double* y0,
+                      int fine_nsub, int fine_nseg, int fine_warps, int coarse_m,
+                      int coarse_nsub, int coarse_nseg, int coarse_warps, const double* y0,
                       int has_source, const double* src_shape, double src_amp,
                       double src_omega, double src_phase, int use_thomas, int mode);
 void orc_1d_destroy(orc_1d* o);

@@ -40,9 +40,9 @@ class ProblemDesc(C.Structure):
                 ("source_kind", C.c_int32), ("source_amp", C.c_double),
                 ("source_omega", C.c_double), ("source_phase", C.c_double),
                 ("source_shape", _dp), ("initial_value", _dp), ("device", C.c_int32),
-                ("fine_mpt", C.c_int32), ("fine_nseg", C.c_int32), ("fine_warps", C.c_int32),
-                ("coarse_mpt", C.c_int32), ("coarse_nseg", C.c_int32),
-                ("coarse_warps", C.c_int32)]
+                ("fine_mpt", C.c_int32), ("fine_nsub", C.c_int32), ("fine_nseg", C.c_int32),
+                ("fine_warps", C.c_int32), ("coarse_mpt", C.c_int32), ("coarse_nsub", C.c_int32),
+                ("coarse_nseg", C.c_int32), ("coarse_warps", C.c_int32)]
 
 
 class RunStatsC(C.Structure):
@@ -69,14 +69,16 @@ class SolveInfoC(C.Structure):
 
 
 class StepCoeffsC(C.Structure):
-    _fields_ = [("M", C.c_int32), ("mpt", C.c_int32), ("nseg", C.c_int32), ("warps", C.c_int32),
+    _fields_ = [("M", C.c_int32), ("mpt", C.c_int32), ("nsub", C.c_int32), ("nseg", C.c_int32),
+                ("warps", C.c_int32),
                 ("steps", C.c_int32),
                 ("delta", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("dstar", C.c_double), ("nl", C.c_double), ("nu", C.c_double),
                 ("inv", C.c_double), ("gneg", C.c_double), ("K0", C.c_int32), ("R", C.c_int32),
-                ("invR", C.c_double), ("invLast", C.c_double), ("Pseg", C.c_double),
-                ("Qseg", C.c_double), ("fl", C.c_double * 64),
-                ("fu", C.c_double * 64), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
+                ("invR", C.c_double), ("invLast", C.c_double), ("pS", C.c_double),
+                ("qS", C.c_double), ("Pseg", C.c_double), ("Qseg", C.c_double),
+                ("nlpow", C.c_double * 32), ("pw", C.c_double * 8), ("narrow", C.c_int32),
+                ("pp", C.c_double * 5), ("qq", C.c_double * 5),
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
                 ("qlane", C.c_double * 32)]
 
@@ -112,7 +114,7 @@ def lib():
     L.pit_context_shape.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]
     L.pit_step_coefficients.argtypes = [C.POINTER(ProblemDesc), C.c_int, C.POINTER(StepCoeffsC)]
     L.pit_step_correction.argtypes = [C.POINTER(ProblemDesc), C.c_int, _dp]
-    L.pit_step_positions.argtypes = [C.POINTER(ProblemDesc), C.c_int, _dp, _dp]
+    L.pit_step_positions.argtypes = [C.POINTER(ProblemDesc), C.c_int, _dp, _dp, _dp]
     st = C.POINTER(RunStatsC)
     L.pit_apply_F.argtypes = [vp, _dp, _dp, st]
     L.pit_assemble_rhs.argtypes = [vp, _dp, st]

@@ -132,14 +132,22 @@ class Problem1D:
                                                             self.source.phase)
             d.source_shape = dptr(sh)
         d.device = device
-        # layouts: (points/thread, warps/slab) or (points/thread, segments, warps/slab)
+        # layouts: (points/thread, warps/slab) or
+        # (points/thread, sub-chunks/thread, segments/slab, warps/slab)
         if fine_layout:
-            fl = tuple(fine_layout)
-            d.fine_mpt, d.fine_nseg, d.fine_warps = fl if len(fl) == 3 else (fl[0], 1, fl[1])
+            d.fine_mpt, d.fine_nsub, d.fine_nseg, d.fine_warps = _layout4(fine_layout)
         if coarse_layout:
-            cl = tuple(coarse_layout)
-            d.coarse_mpt, d.coarse_nseg, d.coarse_warps = cl if len(cl) == 3 else (cl[0], 1, cl[1])
+            d.coarse_mpt, d.coarse_nsub, d.coarse_nseg, d.coarse_warps = _layout4(coarse_layout)
         return d, keep
+
+
+def _layout4(lay):
+    lay = tuple(lay)
+    if len(lay) == 2:
+        return lay[0], 1, 1, lay[1]
+    if len(lay) == 4:
+        return lay
+    raise ValueError("layout must be (mpt, warps) or (mpt, nsub, nseg, warps)")
 
 
 def diffusion_reaction_bands(diffusion: float, reaction: float, h: float):
@@ -169,13 +177,13 @@ def step_coefficients(problem: Problem1D, role: int = _lib.PIT_FINE, fine_layout
 
 def step_positions(problem: Problem1D, role: int = _lib.PIT_FINE, fine_layout=None,
                    coarse_layout=None):
-    """Per-thread segment-carry weights (ppos, qpos) of one role."""
+    """Per-thread weights (ppos, qpos, zt) of one role."""
     c, _ = step_coefficients(problem, role, fine_layout, coarse_layout)
     d, keep = problem.desc(0, fine_layout, coarse_layout)
     T = 32 * c.warps
-    pp, qp = np.zeros(T), np.zeros(T)
-    _check(_lib.lib().pit_step_positions(C.byref(d), role, dptr(pp), dptr(qp)))
-    return pp, qp
+    pp, qp, zt = np.zeros(T), np.zeros(T), np.zeros(T)
+    _check(_lib.lib().pit_step_positions(C.byref(d), role, dptr(pp), dptr(qp), dptr(zt)))
+    return pp, qp, zt
 
 
 # ---------------------------------------------------------------------------

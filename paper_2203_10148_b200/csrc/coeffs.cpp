@@ -18,51 +18,51 @@
 namespace pitb {
 
 namespace {
-struct L { int mpt, nseg, warps; };
+struct L { int mpt, nsub, nseg, warps; };
 // layouts compiled into pit_kernels.cu (keep in sync with PIT_LAYOUTS there)
-const L kLayouts[] = {{4, 1, 1},  {4, 1, 2},  {4, 1, 4},  {4, 1, 8},  {4, 1, 16}, {4, 1, 32},
-                      {8, 1, 4},  {8, 1, 8},  {8, 1, 16}, {8, 1, 32}, {16, 1, 2}, {16, 1, 4},
-                      {16, 1, 8}, {16, 1, 16}, {16, 1, 32}, {16, 2, 4}, {16, 2, 8}, {16, 4, 2},
-                      {16, 4, 4}, {32, 2, 2}, {32, 2, 4}, {32, 4, 1}, {32, 4, 2}, {32, 4, 4},
-                      {64, 4, 1}, {64, 4, 2}, {16, 4, 8}, {8, 4, 8},  {16, 2, 16}, {32, 4, 8},
-                      {64, 4, 4}};
+const L kLayouts[] = {
+    {4, 1, 1, 1},   {4, 1, 1, 2},   {4, 1, 1, 4},  {4, 1, 1, 8},  {4, 1, 1, 16}, {4, 1, 1, 32},
+    {8, 1, 1, 4},   {8, 1, 1, 8},   {8, 1, 1, 16}, {8, 1, 1, 32}, {16, 1, 1, 4}, {16, 1, 1, 8},
+    {16, 1, 1, 16}, {16, 1, 1, 32}, {32, 2, 1, 4}, {32, 2, 1, 8}, {32, 1, 2, 4}, {32, 2, 2, 4},
+    {64, 2, 2, 1},  {64, 2, 2, 2},  {64, 2, 2, 4}, {64, 4, 1, 2}, {64, 1, 4, 2}, {64, 4, 1, 1},
+    {64, 4, 1, 4},  {64, 1, 2, 2},  {32, 2, 2, 8}, {64, 2, 2, 8}, {16, 2, 1, 16}, {16, 2, 2, 8}};
 }  // namespace
 
-bool layout_supported(int mpt, int nseg, int warps) {
+bool layout_supported(int mpt, int nsub, int nseg, int warps) {
   for (const L& l : kLayouts)
-    if (l.mpt == mpt && l.nseg == nseg && l.warps == warps) return true;
+    if (l.mpt == mpt && l.nsub == nsub && l.nseg == nseg && l.warps == warps) return true;
   return false;
 }
 
 Layout auto_layout(int M, int role) {
-  // fine: 64 points per thread as 4 strided segments of 16 (the four segment
-  // sweeps and scans interleave, hiding DFMA / shuffle latency, and the
-  // per-warp scan cost is amortised over 64 points); coarse (one persistent
-  // CTA, latency bound): many threads, few points each.
-  static const L fine[] = {{4, 1, 1}, {4, 1, 2}, {4, 1, 4}, {8, 1, 4},
-                           {64, 4, 1}, {64, 4, 2}, {64, 4, 4}, {32, 4, 8}};
-  static const L coarse[] = {{4, 1, 1}, {4, 1, 2}, {4, 1, 4}, {8, 1, 4},
-                             {4, 1, 32}, {8, 1, 16}, {8, 1, 32}, {16, 1, 32}};
+  // fine: 64 points per thread = 2 strided segments x 2 contiguous sub-chunks
+  // of 16 (four interleaved chains; two warp scans per direction); coarse
+  // (one persistent CTA, latency bound): many threads, few points each.
+  static const L fine[] = {{4, 1, 1, 1},  {4, 1, 1, 2},  {4, 1, 1, 4},  {8, 1, 1, 4},
+                           {64, 2, 2, 1}, {64, 2, 2, 2}, {64, 2, 2, 4}, {64, 2, 2, 8}};
+  static const L coarse[] = {{4, 1, 1, 1},  {4, 1, 1, 2},  {4, 1, 1, 4},  {8, 1, 1, 4},
+                             {16, 1, 1, 4}, {16, 1, 1, 8}, {16, 1, 1, 16}, {16, 1, 1, 32}};
   const L* list = role == PIT_FINE ? fine : coarse;
   for (int i = 0; i < 8; ++i)
-    if (32 * list[i].warps * list[i].mpt >= M) return {list[i].mpt, list[i].nseg, list[i].warps};
-  if (role == PIT_FINE && M <= 32 * 8 * 32) return {32, 4, 8};
-  return {0, 0, 0};
+    if (32 * list[i].warps * list[i].mpt >= M)
+      return {list[i].mpt, list[i].nsub, list[i].nseg, list[i].warps};
+  return {0, 0, 0, 0};
 }
 
-int build_step_coeffs(int M, int mpt, int nseg, int warps, int steps, double band_lo,
+int build_step_coeffs(int M, int mpt, int nsub, int nseg, int warps, int steps, double band_lo,
                       double band_diag, double band_up, double dt, pit_step_coeffs* c,
                       std::vector<double>* zc, std::vector<double>* ppos,
-                      std::vector<double>* qpos) {
+                      std::vector<double>* qpos, std::vector<double>* zt) {
   typedef long double ld;
   std::memset(c, 0, sizeof(*c));
-  if (M < 1 || mpt < 1 || mpt > 64 || nseg < 1 || mpt % nseg || mpt / nseg > 32 || warps < 1 ||
-      steps < 1)
+  if (M < 1 || mpt < 1 || mpt > 64 || nsub < 1 || nsub > 8 || nseg < 1 || mpt % (nsub * nseg) ||
+      mpt / (nsub * nseg) > 32 || warps < 1 || steps < 1)
     return PIT_ERR_INVALID_ARGUMENT;
   if (32 * warps * mpt < M) return PIT_ERR_INVALID_ARGUMENT;
   if (!(dt > 0.0)) return PIT_ERR_INVALID_ARGUMENT;
   c->M = M;
   c->mpt = mpt;
+  c->nsub = nsub;
   c->nseg = nseg;
   c->warps = warps;
   c->steps = steps;
@@ -101,21 +101,21 @@ int build_step_coeffs(int M, int mpt, int nseg, int warps, int steps, double ban
     c->K0 = k0;
   }
   {
-    // chunk = sub points; the warp scan combines chunks (p = nl^sub), the
-    // segment chain combines segments of lseg = 32*warps*sub points.
-    const int sub = mpt / nseg, T = 32 * warps, lseg = T * sub;
-    ld nlp[33], nup[33];
+    // sub-chunk = sub points; thread chunk = ch = nsub*sub points (warp scan
+    // multiplier nl^ch); segment = lseg = T*ch points.
+    const int sub = mpt / (nsub * nseg), ch = nsub * sub, T = 32 * warps, lseg = T * ch;
+    ld nlp[65], nup[65];
     nlp[0] = 1.0L;
     nup[0] = 1.0L;
-    for (int k = 1; k <= sub; ++k) {
+    for (int k = 1; k <= 64; ++k) {
       nlp[k] = nlp[k - 1] * nl;
       nup[k] = nup[k - 1] * nu;
     }
-    for (int j = 0; j < sub; ++j) {
-      c->fl[j] = (double)nlp[j + 1];
-      c->fu[j] = (double)nup[sub - j];
-    }
-    ld pk = nlp[sub], qk = nup[sub];
+    for (int j = 0; j < sub; ++j) c->nlpow[j] = (double)nlp[j];
+    for (int u = 0; u < nsub; ++u) c->pw[u] = (double)nlp[u * sub];
+    c->pS = (double)nlp[sub];
+    c->qS = (double)nup[sub];
+    ld pk = nlp[ch], qk = nup[ch];
     for (int k = 0; k < 5; ++k) {
       c->pp[k] = (double)pk;
       c->qq[k] = (double)qk;
@@ -128,20 +128,26 @@ int build_step_coeffs(int M, int mpt, int nseg, int warps, int steps, double ban
     for (int l = 0; l < 32; ++l) {
       c->plane[l] = (double)pl;
       c->qlane[31 - l] = (double)ql;
-      pl = pl * nlp[sub];
-      ql = ql * nup[sub];
+      pl = pl * nlp[ch];
+      ql = ql * nup[ch];
     }
     ppos->assign((size_t)T, 0.0);
     qpos->assign((size_t)T, 0.0);
+    zt->assign((size_t)T, 0.0);
     ld pt = 1.0L, qt = 1.0L;
     for (int t = 0; t < T; ++t) {
       (*ppos)[(size_t)t] = (double)pt;
       (*qpos)[(size_t)(T - 1 - t)] = (double)qt;
-      pt = pt * nlp[sub];
-      qt = qt * nup[sub];
+      (*zt)[(size_t)t] = (double)(z[0] * pt);
+      pt = pt * nlp[ch];
+      qt = qt * nup[ch];
     }
-    c->Pseg = (double)pt;  // nl^(T*sub) = nl^lseg
+    c->Pseg = (double)pt;  // nl^(T*ch) = nl^lseg
     c->Qseg = (double)qt;
+    // narrow corner: every point below K0 in warp 0's chunks of segment 0,
+    // and zc geometric there to double precision ((nl nu)^(M-K0) negligible)
+    const ld decay = powl(fabsl(nl * nu), (ld)(M - c->K0));
+    c->narrow = (c->K0 <= 32 * ch && decay < 7.7e-34L /* 2^-110 */) ? 1 : 0;
     (void)lseg;
   }
   {

@@ -60,9 +60,9 @@ struct Role {
   pit_step_coeffs c{};
   StepParams P{};
   double* d_zc = nullptr;
-  double* d_pos = nullptr;  // [2*T]: ppos then qpos
+  double* d_pos = nullptr;  // [3*T]: ppos, qpos, zt
   double* d_ds = nullptr;
-  int mpt = 0, nseg = 0, warps = 0;
+  int mpt = 0, nsub = 0, nseg = 0, warps = 0;
 };
 
 }  // namespace
@@ -118,29 +118,34 @@ double grid_spacing(const pit_problem_desc* d) {
 }
 
 int role_coeffs(const pit_problem_desc* d, int role, pit_step_coeffs* c, std::vector<double>* zc,
-                Layout* lay, std::vector<double>* ppos, std::vector<double>* qpos) {
+                Layout* lay, std::vector<double>* ppos, std::vector<double>* qpos,
+                std::vector<double>* zt) {
   const int M = d->interior;
   const int steps = role == PIT_FINE ? d->fine_steps : d->coarse_steps;
   // TimeSlabPartition::slab_length() = T/N; Propagator::internal_dt() = slab/steps
   const double dt = (d->total_time / d->slab_count) / steps;
   int mpt = role == PIT_FINE ? d->fine_mpt : d->coarse_mpt;
+  int nsub = role == PIT_FINE ? d->fine_nsub : d->coarse_nsub;
   int nseg = role == PIT_FINE ? d->fine_nseg : d->coarse_nseg;
   int warps = role == PIT_FINE ? d->fine_warps : d->coarse_warps;
   if (mpt == 0 || warps == 0) {
     Layout l = auto_layout(M, role);
     mpt = l.mpt;
+    nsub = l.nsub;
     nseg = l.nseg;
     warps = l.warps;
   }
   if (nseg == 0) nseg = 1;
-  if (mpt == 0 || !layout_supported(mpt, nseg, warps) || 32 * mpt * warps < M)
+  if (nsub == 0) nsub = 1;
+  if (mpt == 0 || !layout_supported(mpt, nsub, nseg, warps) || 32 * mpt * warps < M)
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "pit_context_create: no compiled slab layout covers M=" + std::to_string(M));
   lay->mpt = mpt;
+  lay->nsub = nsub;
   lay->nseg = nseg;
   lay->warps = warps;
-  if (build_step_coeffs(M, mpt, nseg, warps, steps, d->band_lo, d->band_diag, d->band_up, dt, c,
-                        zc, ppos, qpos))
+  if (build_step_coeffs(M, mpt, nsub, nseg, warps, steps, d->band_lo, d->band_diag, d->band_up,
+                        dt, c, zc, ppos, qpos, zt))
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "pit_context_create: step matrix I + dt*A is not factorizable with constant "
                    "factors (needs delta^2 > 4*lam*mu)");
@@ -154,12 +159,15 @@ void fill_params(const pit_step_coeffs& c, StepParams* P) {
   P->gneg = c.gneg;
   P->invR = c.invR;
   P->invLast = c.invLast;
-  const int sub = c.mpt / c.nseg;
+  const int sub = c.mpt / (c.nsub * c.nseg);
+  P->pS = c.pS;
+  P->qS = c.qS;
   P->Pseg = c.Pseg;
   P->Qseg = c.Qseg;
+  P->narrow = c.narrow;
+  for (int u = 0; u < 8; ++u) P->pw[u] = u < c.nsub ? c.pw[u] : 0.0;
   for (int j = 0; j < 32; ++j) {
-    P->fl[j] = j < sub ? c.fl[j] : 0.0;
-    P->fu[j] = j < sub ? c.fu[j] : 0.0;
+    P->nlpow[j] = j < sub ? c.nlpow[j] : 0.0;
     P->plane[j] = c.plane[j];
     P->qlane[j] = c.qlane[j];
   }
@@ -234,7 +242,7 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
   A.stagger = ctx->stagger;
   A.stagger_mod = ctx->stagger_mod;
   A.sms = ctx->sms;
-  CUDA_TRY(launch_slab(R.mpt, R.nseg, R.warps, false, R.P, A, ctas, st));
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, false, R.P, A, ctas, st));
   return PIT_OK;
 }
 
@@ -263,7 +271,7 @@ int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, con
     A.slab0 = first - 1;
   }
   const bool src = with_source && ctx->has_source;
-  CUDA_TRY(launch_sweep(R.mpt, R.nseg, R.warps, src, R.P, A, st));
+  CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, st));
   return PIT_OK;
 }
 
@@ -309,30 +317,31 @@ int pit_device_count(void) {
 
 int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out) {
   PIT_TRY(validate_desc(desc));
-  std::vector<double> zc, ppos, qpos;
+  std::vector<double> zc, ppos, qpos, zt;
   Layout lay;
-  return role_coeffs(desc, role, out, &zc, &lay, &ppos, &qpos);
+  return role_coeffs(desc, role, out, &zc, &lay, &ppos, &qpos, &zt);
 }
 
 int pit_step_correction(const pit_problem_desc* desc, int role, double* zc_out) {
   PIT_TRY(validate_desc(desc));
-  std::vector<double> zc, ppos, qpos;
+  std::vector<double> zc, ppos, qpos, zt;
   Layout lay;
   pit_step_coeffs c;
-  PIT_TRY(role_coeffs(desc, role, &c, &zc, &lay, &ppos, &qpos));
+  PIT_TRY(role_coeffs(desc, role, &c, &zc, &lay, &ppos, &qpos, &zt));
   std::memcpy(zc_out, zc.data(), zc.size() * sizeof(double));
   return PIT_OK;
 }
 
 int pit_step_positions(const pit_problem_desc* desc, int role, double* ppos_out,
-                       double* qpos_out) {
+                       double* qpos_out, double* zt_out) {
   PIT_TRY(validate_desc(desc));
-  std::vector<double> zc, ppos, qpos;
+  std::vector<double> zc, ppos, qpos, zt;
   Layout lay;
   pit_step_coeffs c;
-  PIT_TRY(role_coeffs(desc, role, &c, &zc, &lay, &ppos, &qpos));
+  PIT_TRY(role_coeffs(desc, role, &c, &zc, &lay, &ppos, &qpos, &zt));
   std::memcpy(ppos_out, ppos.data(), ppos.size() * sizeof(double));
   std::memcpy(qpos_out, qpos.data(), qpos.size() * sizeof(double));
+  if (zt_out) std::memcpy(zt_out, zt.data(), zt.size() * sizeof(double));
   return PIT_OK;
 }
 
@@ -361,12 +370,13 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     return rc;
   };
   for (int r = 0; r < 2; ++r) {
-    std::vector<double> zc, ppos, qpos;
+    std::vector<double> zc, ppos, qpos, zt;
     Layout lay;
-    int rc = role_coeffs(desc, r, &ctx->role[r].c, &zc, &lay, &ppos, &qpos);
+    int rc = role_coeffs(desc, r, &ctx->role[r].c, &zc, &lay, &ppos, &qpos, &zt);
     if (rc) return fail(rc);
     Role& R = ctx->role[r];
     R.mpt = lay.mpt;
+    R.nsub = lay.nsub;
     R.nseg = lay.nseg;
     R.warps = lay.warps;
     fill_params(R.c, &R.P);
@@ -377,12 +387,14 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     R.P.zc = R.d_zc;
     std::vector<double> pos(ppos);
     pos.insert(pos.end(), qpos.begin(), qpos.end());
+    pos.insert(pos.end(), zt.begin(), zt.end());
     if (cudaMalloc(&R.d_pos, sizeof(double) * pos.size()) != cudaSuccess ||
         cudaMemcpy(R.d_pos, pos.data(), sizeof(double) * pos.size(), cudaMemcpyHostToDevice) !=
             cudaSuccess)
       return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
     R.P.ppos = R.d_pos;
     R.P.qpos = R.d_pos + ppos.size();
+    R.P.zt = R.d_pos + 2 * ppos.size();
   }
   if (cudaMalloc(&ctx->d_y0, sizeof(double) * ctx->M) != cudaSuccess ||
       cudaMemcpy(ctx->d_y0, ctx->y0.data(), sizeof(double) * ctx->M, cudaMemcpyHostToDevice) !=
@@ -602,7 +614,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
     A.out = d.p + ctx->M;
     A.slab0 = 0;
     A.status = ctx->d_status;
-    CUDA_TRY(launch_slab(R.mpt, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+    CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
     PIT_TRY(check_status(ctx, true));
     add_fine(ctx, stats, ms_since(t0));
   }
@@ -645,7 +657,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
   A.mode = kPropagate;
   A.out = d + ctx->M;
   A.status = ctx->d_status;
-  CUDA_TRY(launch_slab(R.mpt, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
   PIT_TRY(check_status(ctx, true));
   add_fine(ctx, stats, ms_since(t0));
   return PIT_OK;
@@ -718,7 +730,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
     // source_contribution with f == 0 is exactly zero (propagator.cpp:78)
     CUDA_TRY(cudaMemsetAsync(dout.p, 0, M * sizeof(double), ctx->stream));
   } else {
-    CUDA_TRY(launch_sweep(R.mpt, R.nseg, R.warps, src, R.P, A, ctx->stream));
+    CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, ctx->stream));
     PIT_TRY(check_status(ctx, false));
   }
   return to_host(ctx, dout.p, M, out);

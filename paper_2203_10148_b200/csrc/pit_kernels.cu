@@ -20,41 +20,40 @@ namespace pitb {
 
 namespace {
 
-// Thread-owned point i of y[s][j]: s*LSEG + g0 + j, LSEG = 32*WARPS*SUB.
-template <int SUB, int NSEG, int WARPS>
-__device__ __forceinline__ void load_field(double (&y)[NSEG][SUB], const double* __restrict__ src,
-                                           int g0, int M) {
-  constexpr int LSEG = 32 * WARPS * SUB;
+template <class S>
+__device__ __forceinline__ void load_field(double (&y)[S::NC][S::SUB],
+                                           const double* __restrict__ src, int tid, int M) {
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s)
+  for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-    for (int j = 0; j < SUB; ++j) {
-      const int i = s * LSEG + g0 + j;
-      y[s][j] = (src != nullptr && i < M) ? src[i] : 0.0;
+    for (int j = 0; j < S::SUB; ++j) {
+      const int i = S::point(tid, c, j);
+      y[c][j] = (src != nullptr && i < M) ? src[i] : 0.0;
     }
 }
 
-template <int SUB, int NSEG, int WARPS>
-__device__ __forceinline__ bool all_finite(const double (&y)[NSEG][SUB], int g0, int M) {
-  constexpr int LSEG = 32 * WARPS * SUB;
+template <class S>
+__device__ __forceinline__ bool all_finite(const double (&y)[S::NC][S::SUB], int tid, int M) {
   bool ok = true;
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s)
+  for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-    for (int j = 0; j < SUB; ++j)
-      if (s * LSEG + g0 + j < M && !isfinite(y[s][j])) ok = false;
+    for (int j = 0; j < S::SUB; ++j)
+      if (S::point(tid, c, j) < M && !isfinite(y[c][j])) ok = false;
   return ok;
 }
 
-// Correction vector, zero-padded (see be_solve): narrow path 32*SUB entries,
-// wide path the padded slab length.
-__host__ __device__ inline int zc_len(int K0, int sub, int nseg, int warps) {
-  return K0 <= 32 * sub ? 32 * sub : 32 * warps * sub * nseg;
+// Table-form correction vector in shared memory (wide path only): slot layout,
+// zero beyond K0.
+template <class S>
+__host__ __device__ inline int zc_smem_len(int narrow) {
+  return narrow ? 0 : S::T * (S::MPT + 1);
 }
-template <int SUB, int NSEG, int WARPS>
+template <class S>
 __device__ __forceinline__ void load_zc(const StepParams& P, double* s_zc, int tid) {
-  const int n = zc_len(P.K0, SUB, NSEG, WARPS);
-  for (int i = tid; i < n; i += 32 * WARPS) s_zc[i] = i < P.K0 ? P.zc[i] : 0.0;
+  if (P.narrow) return;
+  const int n = S::NSEG * S::LSEG;
+  for (int i = tid; i < n; i += S::T) s_zc[S::slot_of_point(i)] = i < P.K0 ? P.zc[i] : 0.0;
 }
 
 template <int MPT, int WARPS, bool SRC>
@@ -65,14 +64,23 @@ struct SlabBounds {
   static constexpr int kMin = SRC ? 1 : (kMin0 < 1 ? 1 : (kMin0 > 16 ? 16 : kMin0));
 };
 
-template <int SUB, int NSEG, int WARPS, bool SRC>
-__device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParams& P,
-                                         const StepLane& L, StepShared<NSEG, WARPS>& sh,
-                                         const double* s_zc, int lane, int warp, int g0,
-                                         int slab) {
-  constexpr int LSEG = 32 * WARPS * SUB;
-  const bool ghosts = P.M < NSEG * LSEG;
-  const bool wide = P.K0 > 32 * SUB;
+template <class S>
+__device__ __forceinline__ StepLane step_lane(const StepParams& P,
+                                              const StepShared<S::NSEG, S::WARPS>& sh, int tid) {
+  StepLane L;
+  L.plane = sh.plane[tid & 31];
+  L.qlane = sh.qlane[tid & 31];
+  L.ppos = P.ppos[tid];
+  L.qpos = P.qpos[tid];
+  L.zt = P.narrow ? P.zt[tid] : 0.0;
+  return L;
+}
+
+template <class S, bool SRC>
+__device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepParams& P,
+                                         const StepLane& L, StepShared<S::NSEG, S::WARPS>& sh,
+                                         const double* s_zc, int tid, int slab) {
+  const bool ghosts = P.M < S::NSEG * S::LSEG;
 #ifdef PIT_PHASE_TIMING
   long long ph_acc[16] = {};
   long long ph_t = clock64();
@@ -88,84 +96,70 @@ __device__ __forceinline__ void run_slab(double (&y)[NSEG][SUB], const StepParam
     for (int k = 0; k < P.steps; ++k) {
       const double dsn = (k + 1 < P.steps) ? ds[k + 1] : 0.0;
 #pragma unroll
-      for (int s = 0; s < NSEG; ++s)
+      for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) {
-          const int i = s * LSEG + g0 + j;
-          y[s][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[s][j]);
+        for (int j = 0; j < S::SUB; ++j) {
+          const int i = S::point(tid, c, j);
+          y[c][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[c][j]);
         }
-      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide PIT_TIMING_ARGS);
+      be_solve<S>(y, P, L, sh, s_zc, tid, ghosts PIT_TIMING_ARGS);
 #pragma unroll
-      for (int s = 0; s < NSEG; ++s)
+      for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.inv;
+        for (int j = 0; j < S::SUB; ++j) y[c][j] = y[c][j] * P.inv;
       dsk = dsn;
     }
   } else {
     int cnt = 0;
     for (int k = 0; k < P.steps; ++k) {
-      be_solve<SUB, NSEG, WARPS>(y, P, L, sh, s_zc, lane, warp, g0, ghosts, wide PIT_TIMING_ARGS);
+      be_solve<S>(y, P, L, sh, s_zc, tid, ghosts PIT_TIMING_ARGS);
       if (++cnt == P.R) {
         cnt = 0;
 #pragma unroll
-        for (int s = 0; s < NSEG; ++s)
+        for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-          for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invR;
+          for (int j = 0; j < S::SUB; ++j) y[c][j] = y[c][j] * P.invR;
       }
       PIT_PHASE(9);
     }
     if (cnt) {
 #pragma unroll
-      for (int s = 0; s < NSEG; ++s)
+      for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) y[s][j] = y[s][j] * P.invLast;
+        for (int j = 0; j < S::SUB; ++j) y[c][j] = y[c][j] * P.invLast;
     }
   }
 #ifdef PIT_PHASE_TIMING
-  if (P.timing && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && warp < 2)
-    for (int k = 0; k < 16; ++k) P.timing[warp * 16 + k] = ph_acc[k];
+  if (P.timing && blockIdx.x == 0 && (tid & 31) == 0 && (tid >> 5) < 2)
+    for (int k = 0; k < 16; ++k) P.timing[(tid >> 5) * 16 + k] = ph_acc[k];
 #endif
 }
 
-template <int SUB, int NSEG, int WARPS>
-__device__ __forceinline__ StepLane step_lane(const StepParams& P,
-                                              const StepShared<NSEG, WARPS>& sh, int tid) {
-  StepLane L;
-  L.plane = sh.plane[tid & 31];
-  L.qlane = sh.qlane[tid & 31];
-  L.ppos = P.ppos[tid];
-  L.qpos = P.qpos[tid];
-  return L;
-}
-
-template <int SUB, int NSEG, int WARPS, bool SRC>
-__global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSEG, WARPS, SRC>::kMin))
+template <class S, bool SRC>
+__global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin))
     slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
-  constexpr int LSEG = 32 * WARPS * SUB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sh = reinterpret_cast<StepShared<NSEG, WARPS>*>(smem_raw);
+  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int b = blockIdx.x;
   const int M = P.M;
-  const int g0 = tid * SUB;
-  load_zc<SUB, NSEG, WARPS>(P, s_zc, tid);
-  init_step_shared<NSEG, WARPS>(P, *sh, tid);
+  load_zc<S>(P, s_zc, tid);
+  init_step_shared<S::NSEG, S::WARPS>(P, *sh, tid);
 
   const double* src;
   if (b + A.in_shift >= 0)
     src = A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr;
   else
     src = A.halo;
-  double y[NSEG][SUB];
-  load_field<SUB, NSEG, WARPS>(y, src, g0, M);
+  double y[S::NC][S::SUB];
+  load_field<S>(y, src, tid, M);
   const int slab = A.slab0 + b;
   __syncthreads();
-  const StepLane L = step_lane<SUB, NSEG, WARPS>(P, *sh, tid);
+  const StepLane L = step_lane<S>(P, *sh, tid);
   if (A.stagger > 0) {
-    // Offset the step phase of co-resident CTAs (same SM: block ids that
-    // differ by a multiple of the SM count) so their latency-bound scan
-    // phases overlap other CTAs' DFMA-bound sweeps.
+    // Offset the step phase of co-resident CTAs (block ids differing by a
+    // multiple of the SM count) — tuning knob, off by default.
     const long long wait = (long long)((b / A.sms) % A.stagger_mod) * A.stagger;
     const long long t0 = clock64();
     while (clock64() - t0 < wait) {
@@ -173,46 +167,34 @@ __global__ void __launch_bounds__(32 * WARPS, (SlabBounds<SUB * NSEG, WARPS, SRC
     __syncthreads();
   }
 
-  run_slab<SUB, NSEG, WARPS, SRC>(y, P, L, *sh, s_zc, lane, warp, g0, slab);
+  run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab);
 
-  if (!all_finite<SUB, NSEG, WARPS>(y, g0, M)) atomicMin(A.status, slab);
+  if (!all_finite<S>(y, tid, M)) atomicMin(A.status, slab);
   const size_t off = (size_t)b * M;
   double* out = A.out + off;
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s)
+  for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-    for (int j = 0; j < SUB; ++j) {
-      const int i = s * LSEG + g0 + j;
+    for (int j = 0; j < S::SUB; ++j) {
+      const int i = S::point(tid, c, j);
       if (i < M) {
         if (A.mode == kApplyF) {
-          out[i] = A.Lsub[off + i] - y[s][j];
+          out[i] = A.Lsub[off + i] - y[c][j];
         } else if (A.mode == kResidual) {
-          const double a = A.Lsub[off + i] - y[s][j];
+          const double a = A.Lsub[off + i] - y[c][j];
           out[i] = A.rhs[off + i] - a;
         } else {
-          out[i] = y[s][j];
+          out[i] = y[c][j];
         }
       }
     }
   if (b == 0 && A.out0 != nullptr) {
     if (A.mode == kApplyF) {
-      for (int i = tid; i < M; i += 32 * WARPS) A.out0[i] = A.L0[i];
+      for (int i = tid; i < M; i += S::T) A.out0[i] = A.L0[i];
     } else if (A.mode == kResidual) {
-      for (int i = tid; i < M; i += 32 * WARPS) A.out0[i] = A.rhs0[i] - A.L0[i];
+      for (int i = tid; i < M; i += S::T) A.out0[i] = A.rhs0[i] - A.L0[i];
     }
   }
-}
-
-// Staging layout of one block in shared memory: thread t's MPT values at
-// t*(MPT+1) (odd pitch: a warp reading element e of every thread hits
-// distinct banks), filled and drained with coalesced global accesses.
-template <int SUB, int NSEG, int WARPS>
-__device__ __forceinline__ int stage_idx(int i) {
-  constexpr int LSEG = 32 * WARPS * SUB;
-  constexpr int MPT = SUB * NSEG;
-  const int s = i / LSEG, r = i - s * LSEG;
-  const int t = r / SUB, j = r - t * SUB;
-  return t * (MPT + 1) + s * SUB + j;
 }
 
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
@@ -225,43 +207,43 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int SUB, int NSEG, int WARPS, bool SRC>
-__global__ void __launch_bounds__(32 * WARPS, 1)
+// K2: one persistent CTA.  V_b prefetched with cp.async into the odd-pitch
+// slot layout (coalesced global reads), W_b drained through the consumed V
+// buffer with coalesced stores.
+template <class S, bool SRC>
+__global__ void __launch_bounds__(S::T, 1)
     sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A) {
-  constexpr int MPT = SUB * NSEG;
-  constexpr int T = 32 * WARPS;
-  constexpr int STAGE = T * (MPT + 1);
+  constexpr int STAGE = S::T * (S::MPT + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sh = reinterpret_cast<StepShared<NSEG, WARPS>*>(smem_raw);
+  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
-  double* stage = s_zc + zc_len(P.K0, SUB, NSEG, WARPS);  // [2][STAGE]: V double buffer
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* stage = s_zc + zc_smem_len<S>(P.narrow);  // [2][STAGE]: V double buffer
+  const int tid = threadIdx.x;
   const int M = P.M;
-  const int g0 = tid * SUB;
-  load_zc<SUB, NSEG, WARPS>(P, s_zc, tid);
-  init_step_shared<NSEG, WARPS>(P, *sh, tid);
-  double y[NSEG][SUB];
-  load_field<SUB, NSEG, WARPS>(y, A.start, g0, M);
+  load_zc<S>(P, s_zc, tid);
+  init_step_shared<S::NSEG, S::WARPS>(P, *sh, tid);
+  double y[S::NC][S::SUB];
+  load_field<S>(y, A.start, tid, M);
   auto prefetch = [&](int b) {
     double* buf = stage + (b & 1) * STAGE;
     const double* v = A.V + (size_t)b * M;
-    for (int i = tid; i < M; i += T) cp_async8(buf + stage_idx<SUB, NSEG, WARPS>(i), v + i);
+    for (int i = tid; i < M; i += S::T) cp_async8(buf + S::slot_of_point(i), v + i);
     cp_async_commit();
   };
   if (A.V) prefetch(0);
   __syncthreads();
-  const StepLane L = step_lane<SUB, NSEG, WARPS>(P, *sh, tid);
+  const StepLane L = step_lane<S>(P, *sh, tid);
   bool ok = true;
   int bad = 0x7fffffff;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
     if (A.V && b + 1 < A.count) prefetch(b + 1);
-    run_slab<SUB, NSEG, WARPS, SRC>(y, P, L, *sh, s_zc, lane, warp, g0, slab);
-    if (ok && !all_finite<SUB, NSEG, WARPS>(y, g0, M)) {
+    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab);
+    if (ok && !all_finite<S>(y, tid, M)) {
       ok = false;
       bad = slab;
     }
-    double* buf = stage + (b & 1) * STAGE + tid * (MPT + 1);
+    double* buf = stage + (b & 1) * STAGE;
     if (A.V) {
       if (b + 1 < A.count)
         cp_async_wait<1>();
@@ -269,53 +251,51 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
         cp_async_wait<0>();
       __syncthreads();
 #pragma unroll
-      for (int s = 0; s < NSEG; ++s)
+      for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) {
-          const double v = (s * 32 * WARPS * SUB + g0 + j < M) ? buf[s * SUB + j] : 0.0;
-          y[s][j] = y[s][j] + v;
+        for (int j = 0; j < S::SUB; ++j) {
+          const double v = S::point(tid, c, j) < M ? buf[S::slot(tid, c, j)] : 0.0;
+          y[c][j] = y[c][j] + v;
         }
     }
-    // drain W_b through slab b's (consumed) V buffer with coalesced stores;
-    // each thread overwrites exactly the slots it just read
+    // drain W_b through slab b's (consumed) V buffer; each thread overwrites
+    // exactly the slots it just read
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s)
+    for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-      for (int j = 0; j < SUB; ++j) buf[s * SUB + j] = y[s][j];
+      for (int j = 0; j < S::SUB; ++j) buf[S::slot(tid, c, j)] = y[c][j];
     __syncthreads();
-    const double* wbuf = stage + (b & 1) * STAGE;
     double* W = A.W + (size_t)b * M;
-    for (int i = tid; i < M; i += T) W[i] = wbuf[stage_idx<SUB, NSEG, WARPS>(i)];
+    for (int i = tid; i < M; i += S::T) W[i] = buf[S::slot_of_point(i)];
     __syncthreads();  // the buffer is free for the prefetch of slab b+2
   }
   if (!ok) atomicMin(A.status, bad);
 }
 
-template <int SUB, int NSEG, int WARPS, bool SRC>
+template <class S, bool SRC>
 cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
   const size_t smem =
-      sizeof(StepShared<NSEG, WARPS>) + sizeof(double) * (size_t)zc_len(P.K0, SUB, NSEG, WARPS);
-  auto k = slab_kernel<SUB, NSEG, WARPS, SRC>;
+      sizeof(StepShared<S::NSEG, S::WARPS>) + sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
+  auto k = slab_kernel<S, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<ctas, 32 * WARPS, smem, st>>>(P, A);
+  k<<<ctas, S::T, smem, st>>>(P, A);
   return cudaGetLastError();
 }
 
-template <int SUB, int NSEG, int WARPS, bool SRC>
+template <class S, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
-  constexpr int MPT = SUB * NSEG;
-  const size_t smem = sizeof(StepShared<NSEG, WARPS>) +
-                      sizeof(double) * ((size_t)zc_len(P.K0, SUB, NSEG, WARPS) +
-                                        2 * (size_t)(32 * WARPS) * (MPT + 1));
-  auto k = sweep_kernel<SUB, NSEG, WARPS, SRC>;
+  const size_t smem = sizeof(StepShared<S::NSEG, S::WARPS>) +
+                      sizeof(double) * ((size_t)zc_smem_len<S>(P.narrow) +
+                                        2 * (size_t)S::T * (S::MPT + 1));
+  auto k = sweep_kernel<S, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<1, 32 * WARPS, smem, st>>>(P, A);
+  k<<<1, S::T, smem, st>>>(P, A);
   return cudaGetLastError();
 }
 
@@ -439,34 +419,37 @@ int ew_grid(size_t n) {
 
 }  // namespace
 
-// (points per thread, segments, warps per slab) compiled here (points per
-// thread = SUB * segments); keep in sync with kLayouts in coeffs.cpp.
-#define PIT_LAYOUTS(X)                                                                    \
-  X(4, 1, 1) X(4, 1, 2) X(4, 1, 4) X(4, 1, 8) X(4, 1, 16) X(4, 1, 32) X(8, 1, 4) X(8, 1, 8) \
-  X(8, 1, 16) X(8, 1, 32) X(16, 1, 2) X(16, 1, 4) X(16, 1, 8) X(16, 1, 16) X(16, 1, 32)     \
-  X(16, 2, 4) X(16, 2, 8) X(16, 4, 2) X(16, 4, 4) X(32, 2, 2) X(32, 2, 4) X(32, 4, 1)      \
-  X(32, 4, 2) X(32, 4, 4) X(64, 4, 1) X(64, 4, 2) X(16, 4, 8) X(8, 4, 8) X(16, 2, 16)      \
-  X(32, 4, 8) X(64, 4, 4)
+// Layouts (points per thread, sub-chunks, segments, warps per slab) compiled
+// here; SUB = points / (sub-chunks * segments).  Keep in sync with kLayouts
+// in coeffs.cpp.
+#define PIT_LAYOUTS(X)                                                                       \
+  X(4, 1, 1, 1) X(4, 1, 1, 2) X(4, 1, 1, 4) X(4, 1, 1, 8) X(4, 1, 1, 16) X(4, 1, 1, 32)        \
+  X(8, 1, 1, 4) X(8, 1, 1, 8) X(8, 1, 1, 16) X(8, 1, 1, 32) X(16, 1, 1, 4) X(16, 1, 1, 8)    \
+  X(16, 1, 1, 16) X(16, 1, 1, 32) X(32, 2, 1, 4) X(32, 2, 1, 8) X(32, 1, 2, 4) X(32, 2, 2, 4) \
+  X(64, 2, 2, 1) X(64, 2, 2, 2) X(64, 2, 2, 4) X(64, 4, 1, 2) X(64, 1, 4, 2) X(64, 4, 1, 1)  \
+  X(64, 4, 1, 4) X(64, 1, 2, 2) X(32, 2, 2, 8) X(64, 2, 2, 8) X(16, 2, 1, 16) X(16, 2, 2, 8)
 
-cudaError_t launch_slab(int mpt, int nsub, int warps, bool src, const StepParams& P,
+#define PIT_SHAPE(MP, NU, NS, W) Shape<(MP) / ((NU) * (NS)), NU, NS, W>
+
+cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st) {
   if (ctas <= 0) return cudaSuccess;
-#define X(MP, NS, W)                                                           \
-  if (mpt == MP && nsub == NS && warps == W)                                   \
-    return src ? slab_launch<MP / NS, NS, W, true>(P, A, ctas, st)             \
-               : slab_launch<MP / NS, NS, W, false>(P, A, ctas, st);
+#define X(MP, NU, NS, W)                                                        \
+  if (mpt == MP && nsub == NU && nseg == NS && warps == W)                      \
+    return src ? slab_launch<PIT_SHAPE(MP, NU, NS, W), true>(P, A, ctas, st)    \
+               : slab_launch<PIT_SHAPE(MP, NU, NS, W), false>(P, A, ctas, st);
   PIT_LAYOUTS(X)
 #undef X
   return cudaErrorInvalidConfiguration;
 }
 
-cudaError_t launch_sweep(int mpt, int nsub, int warps, bool src, const StepParams& P,
+cudaError_t launch_sweep(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                          const SweepArgs& A, cudaStream_t st) {
   if (A.count <= 0) return cudaSuccess;
-#define X(MP, NS, W)                                                           \
-  if (mpt == MP && nsub == NS && warps == W)                                   \
-    return src ? sweep_launch<MP / NS, NS, W, true>(P, A, st)                  \
-               : sweep_launch<MP / NS, NS, W, false>(P, A, st);
+#define X(MP, NU, NS, W)                                                        \
+  if (mpt == MP && nsub == NU && nseg == NS && warps == W)                      \
+    return src ? sweep_launch<PIT_SHAPE(MP, NU, NS, W), true>(P, A, st)         \
+               : sweep_launch<PIT_SHAPE(MP, NU, NS, W), false>(P, A, st);
   PIT_LAYOUTS(X)
 #undef X
   return cudaErrorInvalidConfiguration;

@@ -40,9 +40,9 @@ struct SweepArgs {
 };
 
 // Launchers; return cudaErrorInvalidConfiguration for an uncompiled layout.
-cudaError_t launch_slab(int mpt, int nsub, int warps, bool src, const StepParams& P,
+cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st);
-cudaError_t launch_sweep(int mpt, int nsub, int warps, bool src, const StepParams& P,
+cudaError_t launch_sweep(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                          const SweepArgs& A, cudaStream_t st);
 
 // K3: block-vector algebra, one CTA (kVecThreads) per block, fixed reduction

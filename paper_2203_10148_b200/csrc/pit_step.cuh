@@ -2,23 +2,28 @@
 // M-point state lives in registers across a CTA of T = 32*WARPS threads.
 // DESIGN.md §3.
 //
-// Layout: the (padded) slab is split into NSEG super-segments of
-// Lseg = T*SUB points; thread t owns chunk t (SUB contiguous points) of every
-// segment: point s*Lseg + t*SUB + j sits in y[s][j].  The NSEG segments are
-// swept, scanned and fixed up side by side, so every phase has NSEG-way
-// instruction-level parallelism, and the corner correction touches only
-// segment 0.
+// Layout (Shape<SUB, NSUB, NSEG, WARPS>): the padded slab is NSEG strided
+// segments of LSEG = T*NSUB*SUB points; in every segment thread t owns the
+// contiguous chunk [t*NSUB*SUB, (t+1)*NSUB*SUB), split into NSUB sub-chunks
+// of SUB points.  Register y[c][j], c = s*NSUB + u, holds point
+//     s*LSEG + t*NSUB*SUB + u*SUB + j.
+// The NSEG*NSUB sub-chunk sweeps of a thread run interleaved (ILP); each
+// segment needs one warp scan per direction (its sub-chunks are combined
+// inside the thread first), so NSEG trades shuffles for shorter chains.
 //
 // Replaces, per slab and step, the reference's ImplicitStepSolver::solve
 // (src/pde.cpp:112-130 -> solve_cg/solve_bicgstab, src/sparse.cpp:60-206)
 // with a direct tridiagonal solve:
-//   y <- U^-1 L^-1 y     constant unit-bidiagonal factors nl, nu; per
-//        direction: chunk sweeps with zero carry (end value only); Kogge-Stone
+//   y <- U^-1 L^-1 y     constant unit-bidiagonal factors nl, nu.  Per
+//        direction: pass 1 sweeps every sub-chunk with zero carry (end value
+//        only); the thread's chunk end combines its sub-chunks; Kogge-Stone
 //        warp scans and a sequential cross-warp combine give each chunk its
-//        carry within its segment; the segment totals are chained segment to
-//        segment; the chunk carry adds the segment carry-in (weight
-//        nl^(t*SUB)); the chunk sweep is rerun from that carry
-//   y <- y + (gneg*y_0) zc   corner rank-1 (Sherman-Morrison) correction
+//        carry within its segment; segment totals are chained segment to
+//        segment; sub-chunk carries follow; pass 2 reruns every sub-chunk's
+//        sweep from its true carry.
+//   y <- y + (gneg*y_0) zc   corner rank-1 (Sherman-Morrison) correction:
+//        narrow form zc_i = zc_0 nl^i on the chunks of segment 0 that start
+//        below K0 (fine propagators), table form otherwise (coarse).
 // and the diagonal scale inv is deferred: applied as inv^R every R steps
 // (homogeneous propagation) or every step when a source is added.
 // Every multiply-add is an explicit fma(); oracle/pit_oracle.c
@@ -33,25 +38,29 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct StepParams {
   double nl, nu, inv, gneg, invR, invLast;
-  double Pseg, Qseg;        // nl^Lseg, nu^Lseg (segment-to-segment carry weights)
-  double fl[32], fu[32];    // fix-up weights nl^(j+1), nu^(SUB-j), j < SUB
-  double pp[5], qq[5], p32, q32;  // Kogge-Stone weights: powers of nl^SUB / nu^SUB
+  double pS, qS;            // nl^SUB, nu^SUB        (sub-chunk carry weights)
+  double Pseg, Qseg;        // nl^LSEG, nu^LSEG      (segment carry weights)
+  double nlpow[32];         // nl^j, j < SUB         (narrow corner)
+  double pw[8];             // nl^(u*SUB), u < NSUB  (narrow corner)
+  double pp[5], qq[5], p32, q32;  // Kogge-Stone weights: powers of nl^(NSUB*SUB)
   double plane[32], qlane[32];
   int M, steps, R, K0;
-  const double* zc;     // [K0] correction vector (device)
-  const double* ppos;   // [T] nl^(t*SUB)  (device)
-  const double* qpos;   // [T] nu^((T-1-t)*SUB)  (device)
+  int narrow;               // corner in geometric form on segment 0 only
+  const double* zc;     // [K0] correction vector (device), table form
+  const double* zt;     // [T] zc_0 * nl^(t*NSUB*SUB), narrow form
+  const double* ppos;   // [T] nl^(t*NSUB*SUB)  (device)
+  const double* qpos;   // [T] nu^((T-1-t)*NSUB*SUB)  (device)
   const double* shape;  // [M] source shape g(x_i) (device) or nullptr
   const double* ds;     // [slabs*steps] dt*s(t_k) table (device) or nullptr
   long long* timing;    // PIT_PHASE_TIMING builds only: [2 warps][16 phases] cycles
 };
 
 #ifdef PIT_PHASE_TIMING
-#define PIT_PHASE(k)                          \
-  do {                                        \
-    const long long now_ = clock64();         \
-    ph_acc[k] += now_ - ph_t;                 \
-    ph_t = now_;                              \
+#define PIT_PHASE(k)                  \
+  do {                                \
+    const long long now_ = clock64(); \
+    ph_acc[k] += now_ - ph_t;         \
+    ph_t = now_;                      \
   } while (0)
 #else
 #define PIT_PHASE(k) \
@@ -59,9 +68,32 @@ struct StepParams {
   } while (0)
 #endif
 
+template <int SUB_, int NSUB_, int NSEG_, int WARPS_>
+struct Shape {
+  static constexpr int SUB = SUB_, NSUB = NSUB_, NSEG = NSEG_, WARPS = WARPS_;
+  static constexpr int T = 32 * WARPS;
+  static constexpr int NC = NSUB * NSEG;  // sub-chunks per thread
+  static constexpr int CH = NSUB * SUB;   // thread chunk length within a segment
+  static constexpr int MPT = NC * SUB;    // points per thread
+  static constexpr int LSEG = T * CH;     // segment length
+  // global point of register y[c][j] for thread t
+  __host__ __device__ static constexpr int point(int t, int c, int j) {
+    return (c / NSUB) * LSEG + t * CH + (c % NSUB) * SUB + j;
+  }
+  // shared-memory slot of the same point: thread-major, odd pitch MPT+1
+  __host__ __device__ static constexpr int slot(int t, int c, int j) {
+    return t * (MPT + 1) + c * SUB + j;
+  }
+  __host__ __device__ static int slot_of_point(int i) {
+    const int s = i / LSEG, r = i - s * LSEG;
+    const int t = r / CH, q = r - t * CH;
+    return t * (MPT + 1) + s * CH + q;
+  }
+};
+
 // Shared memory of one slab CTA: per-segment cross-warp totals, broadcast
-// scalar and the per-lane carry weights (read with LDS: an indexed constant
-// load would serialise across lanes).  The correction vector follows.
+// scalar and per-lane weights (read with LDS; an indexed constant load would
+// serialise across lanes).  The table-form correction vector follows.
 template <int NSEG, int WARPS>
 struct StepShared {
   double fw[NSEG][WARPS > 1 ? WARPS : 1];
@@ -88,45 +120,45 @@ __device__ __forceinline__ void init_step_shared(const StepParams& P,
 
 // Per-thread constants of the step (registers, loaded once per kernel).
 struct StepLane {
-  double plane, qlane, ppos, qpos;
+  double plane, qlane, ppos, qpos, zt;
 };
 
-// One step.  Per direction: pass 1 runs each chunk's sweep with zero carry
-// (only the end value is kept); Kogge-Stone warp scans (per-lane weights
-// from shared memory, zero where a lane has no source lane: fma(0, t, I) ==
-// I) and the cross-warp combine give each chunk its carry within the
-// segment; the segment totals are chained segment to segment; pass 2 reruns
-// each chunk's sweep from its true carry.  No per-point constants are
-// needed, and the NSEG chunk sweeps of a thread interleave.
-// s_zc holds the correction vector zero-padded to 32*SUB entries (narrow
-// path, K0 <= 32*SUB: warp 0 of segment 0 only) or to the padded slab length
-// (wide path); fma(c, 0, y) == y, so padding does not change any bit.  The
-// lane-0 / lane-31 carry uses weight 1 on a zeroed neighbour value, and
-// segment 0 (NSEG-1 backward) adds a zero segment carry-in: both exact.
-template <int SUB, int NSEG, int WARPS>
-__device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParams& P,
-                                         const StepLane& L, StepShared<NSEG, WARPS>& sh,
-                                         const double* __restrict__ s_zc, int lane, int warp,
-                                         int g0, bool ghosts, bool wide
+// One step (see the file comment).  The lane-0 / lane-31 carry uses weight 1
+// on a zeroed neighbour value, segment 0 (NSEG-1 backward) adds a zero
+// segment carry-in, the Kogge-Stone weight is 0 on lanes without a source
+// lane, and the table-form correction vector is zero-padded: every such
+// extra term is an exact no-op (fma(w, 0, x) == x, fma(0, t, x) == x).
+template <class S>
+__device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepParams& P,
+                                         const StepLane& L, StepShared<S::NSEG, S::WARPS>& sh,
+                                         const double* __restrict__ s_zc, int tid, bool ghosts
 #ifdef PIT_PHASE_TIMING
                                          , long long (&ph_acc)[16], long long& ph_t
 #endif
 ) {
-  constexpr int LSEG = 32 * WARPS * SUB;
+  constexpr int SUB = S::SUB, NSUB = S::NSUB, NSEG = S::NSEG, WARPS = S::WARPS, NC = S::NC;
+  const int lane = tid & 31, warp = tid >> 5;
+  double E[NC];
   double I[NSEG], Ip[NSEG], Wc[NSEG], Tot[NSEG];
-  // ---- forward: L^-1 ----
+  // ---- forward: L^-1, pass 1 ----
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s) I[s] = y[s][0];
+  for (int c = 0; c < NC; ++c) E[c] = y[c][0];
 #pragma unroll
   for (int j = 1; j < SUB; ++j)
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) I[s] = fma(P.nl, I[s], y[s][j]);
+    for (int c = 0; c < NC; ++c) E[c] = fma(P.nl, E[c], y[c][j]);
+#pragma unroll
+  for (int s = 0; s < NSEG; ++s) {
+    I[s] = E[s * NSUB];
+#pragma unroll
+    for (int u = 1; u < NSUB; ++u) I[s] = fma(P.pS, I[s], E[s * NSUB + u]);
+  }
   PIT_PHASE(0);
 #pragma unroll
   for (int st = 0; st < 5; ++st) {
-    const double c = sh.cf[st][lane];
+    const double cw = sh.cf[st][lane];
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) I[s] = fma(c, __shfl_up_sync(kFull, I[s], 1 << st), I[s]);
+    for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_up_sync(kFull, I[s], 1 << st), I[s]);
   }
 #pragma unroll
   for (int s = 0; s < NSEG; ++s) {
@@ -158,40 +190,51 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
   }
   PIT_PHASE(2);
   {
-    double S = 0.0;  // segment carry-in
+    double Sg = 0.0;  // segment carry-in
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) {
-      if (s > 0) S = fma(P.Pseg, S, Tot[s - 1]);
+      if (s > 0) Sg = fma(P.Pseg, Sg, Tot[s - 1]);
       double C = fma(L.plane, Wc[s], Ip[s]);
-      C = fma(L.ppos, S, C);
-      y[s][0] = fma(P.nl, C, y[s][0]);
+      C = fma(L.ppos, Sg, C);
+#pragma unroll
+      for (int u = 0; u < NSUB; ++u) {
+        const int c = s * NSUB + u;
+        const double Cu = C;
+        if (u + 1 < NSUB) C = fma(P.pS, C, E[c]);
+        y[c][0] = fma(P.nl, Cu, y[c][0]);
+      }
     }
   }
 #pragma unroll
   for (int j = 1; j < SUB; ++j)
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nl, y[s][j - 1], y[s][j]);
+    for (int c = 0; c < NC; ++c) y[c][j] = fma(P.nl, y[c][j - 1], y[c][j]);
   if (ghosts) {
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s)
+    for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int j = 0; j < SUB; ++j)
-        y[s][j] = (s * LSEG + g0 + j < P.M) ? y[s][j] : 0.0;  // Dirichlet padding
+      for (int j = 0; j < SUB; ++j) y[c][j] = (S::point(tid, c, j) < P.M) ? y[c][j] : 0.0;
   }
   PIT_PHASE(3);
-  // ---- backward: U^-1 ----
+  // ---- backward: U^-1, pass 1 ----
 #pragma unroll
-  for (int s = 0; s < NSEG; ++s) I[s] = y[s][SUB - 1];
+  for (int c = 0; c < NC; ++c) E[c] = y[c][SUB - 1];
 #pragma unroll
   for (int j = SUB - 2; j >= 0; --j)
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) I[s] = fma(P.nu, I[s], y[s][j]);
+    for (int c = 0; c < NC; ++c) E[c] = fma(P.nu, E[c], y[c][j]);
+#pragma unroll
+  for (int s = 0; s < NSEG; ++s) {
+    I[s] = E[s * NSUB + NSUB - 1];
+#pragma unroll
+    for (int u = NSUB - 2; u >= 0; --u) I[s] = fma(P.qS, I[s], E[s * NSUB + u]);
+  }
   PIT_PHASE(4);
 #pragma unroll
   for (int st = 0; st < 5; ++st) {
-    const double c = sh.cb[st][lane];
+    const double cw = sh.cb[st][lane];
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) I[s] = fma(c, __shfl_down_sync(kFull, I[s], 1 << st), I[s]);
+    for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_down_sync(kFull, I[s], 1 << st), I[s]);
   }
 #pragma unroll
   for (int s = 0; s < NSEG; ++s) {
@@ -223,38 +266,49 @@ __device__ __forceinline__ void be_solve(double (&y)[NSEG][SUB], const StepParam
   }
   PIT_PHASE(6);
   {
-    double S = 0.0;  // segment carry from the right
+    double Sg = 0.0;  // segment carry from the right
 #pragma unroll
     for (int s = NSEG - 1; s >= 0; --s) {
-      if (s < NSEG - 1) S = fma(P.Qseg, S, Tot[s + 1]);
+      if (s < NSEG - 1) Sg = fma(P.Qseg, Sg, Tot[s + 1]);
       double R = fma(L.qlane, Wc[s], Ip[s]);
-      R = fma(L.qpos, S, R);
-      y[s][SUB - 1] = fma(P.nu, R, y[s][SUB - 1]);
+      R = fma(L.qpos, Sg, R);
+#pragma unroll
+      for (int u = NSUB - 1; u >= 0; --u) {
+        const int c = s * NSUB + u;
+        const double Ru = R;
+        if (u > 0) R = fma(P.qS, R, E[c]);
+        y[c][SUB - 1] = fma(P.nu, Ru, y[c][SUB - 1]);
+      }
     }
   }
 #pragma unroll
   for (int j = SUB - 2; j >= 0; --j)
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s) y[s][j] = fma(P.nu, y[s][j + 1], y[s][j]);
+    for (int c = 0; c < NC; ++c) y[c][j] = fma(P.nu, y[c][j + 1], y[c][j]);
   PIT_PHASE(7);
   // ---- corner rank-1 correction ----
-  if (!wide) {
+  if (P.narrow) {
     if (warp == 0) {
-      const double c = P.gneg * __shfl_sync(kFull, y[0][0], 0);
-      if (g0 < P.K0) {
+      const double cc = P.gneg * __shfl_sync(kFull, y[0][0], 0);
+      if (tid * S::CH < P.K0) {
+        const double a = cc * L.zt;
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) y[0][j] = fma(c, s_zc[g0 + j], y[0][j]);
+        for (int u = 0; u < NSUB; ++u) {
+          const double au = a * P.pw[u];
+#pragma unroll
+          for (int j = 0; j < SUB; ++j) y[u][j] = fma(au, P.nlpow[j], y[u][j]);
+        }
       }
     }
   } else {
-    if (warp == 0 && lane == 0) sh.b = y[0][0];
+    if (tid == 0) sh.b = y[0][0];
     __syncthreads();
-    const double c = P.gneg * sh.b;
+    const double cc = P.gneg * sh.b;
 #pragma unroll
-    for (int s = 0; s < NSEG; ++s)
-      if (s * LSEG + g0 < P.K0) {
+    for (int c = 0; c < NC; ++c)
+      if ((c / NSUB) * S::LSEG + tid * S::CH < P.K0) {
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) y[s][j] = fma(c, s_zc[s * LSEG + g0 + j], y[s][j]);
+        for (int j = 0; j < SUB; ++j) y[c][j] = fma(cc, s_zc[S::slot(tid, c, j)], y[c][j]);
       }
   }
   PIT_PHASE(8);

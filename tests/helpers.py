@@ -29,7 +29,7 @@ class OracleProblem:
             self._keep.append(shape)
         self.o = self.lib.orc_1d_create(
             p.M, p.spacing, p.band_lo, p.band_diag, p.band_up, p.N, p.T, p.fine_steps,
-            p.coarse_steps, fc.mpt, fc.nseg, fc.warps, cc.mpt, cc.nseg, cc.warps,
+            p.coarse_steps, fc.mpt, fc.nsub, fc.nseg, fc.warps, cc.mpt, cc.nsub, cc.nseg, cc.warps,
             O.ptr(self._keep[0]),
             1 if src else 0, O.ptr(shape) if src else None, src.amp if src else 0.0,
             src.omega if src else 0.0, src.phase if src else 0.0, 1 if use_thomas else 0, mode)

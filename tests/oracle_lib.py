@@ -35,16 +35,17 @@ class OrcHistory(C.Structure):
 
 
 class OrcStepper(C.Structure):
-    _fields_ = [("M", C.c_int), ("m", C.c_int), ("nseg", C.c_int), ("warps", C.c_int),
+    _fields_ = [("M", C.c_int), ("m", C.c_int), ("nsub", C.c_int), ("nseg", C.c_int), ("warps", C.c_int),
                 ("Mp", C.c_int),
                 ("steps", C.c_int), ("delta", C.c_double), ("lam", C.c_double), ("mu", C.c_double),
                 ("dstar", C.c_double), ("nl", C.c_double), ("nu", C.c_double), ("inv", C.c_double),
-                ("gneg", C.c_double), ("K0", C.c_int), ("Pseg", C.c_double), ("Qseg", C.c_double),
-                ("fl", C.c_double * 64),
-                ("fu", C.c_double * 64), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
+                ("gneg", C.c_double), ("K0", C.c_int), ("pS", C.c_double), ("qS", C.c_double),
+                ("Pseg", C.c_double), ("Qseg", C.c_double), ("nlpow", C.c_double * 32),
+                ("pw", C.c_double * 8), ("narrow", C.c_int), ("pp", C.c_double * 5), ("qq", C.c_double * 5),
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
                 ("qlane", C.c_double * 32), ("R", C.c_int), ("invR", C.c_double),
-                ("invLast", C.c_double), ("zc", _dp), ("ppos", _dp), ("qpos", _dp)]
+                ("invLast", C.c_double), ("zc", _dp), ("ppos", _dp), ("qpos", _dp),
+                ("zt", _dp)]
 
 
 def ensure_built() -> None:
@@ -66,7 +67,8 @@ def orc():
         ensure_built()
         lib = C.CDLL(ORACLE_SO)
         lib.orc_stepper_init.argtypes = [C.POINTER(OrcStepper), C.c_int, C.c_int, C.c_int, C.c_int,
-                                         C.c_int, C.c_double, C.c_double, C.c_double, C.c_double]
+                                         C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                         C.c_double]
         lib.orc_stepper_free.argtypes = [C.POINTER(OrcStepper)]
         lib.orc_stepper_propagate.argtypes = [C.POINTER(OrcStepper), _dp, _dp, _dp, _dp]
         lib.orc_thomas_propagate.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
@@ -74,8 +76,9 @@ def orc():
         lib.orc_1d_create.restype = C.c_void_p
         lib.orc_1d_create.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                       C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
-                                      C.c_int, C.c_int, C.c_int, C.c_int, _dp, C.c_int, _dp,
-                                      C.c_double, C.c_double, C.c_double, C.c_int, C.c_int]
+                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp,
+                                      C.c_int, _dp, C.c_double, C.c_double, C.c_double, C.c_int,
+                                      C.c_int]
         lib.orc_1d_destroy.argtypes = [C.c_void_p]
         lib.orc_1d_problem.restype = C.c_void_p
         lib.orc_1d_problem.argtypes = [C.c_void_p]

@@ -125,8 +125,9 @@ def test_c3_n16_matches_reference():
     assert rel_block(res.solution, g["pitsbicg_lambda"]) < 5e-10  # reference inner-solve floor
 
 
-@pytest.mark.parametrize("layout", [(16, 1, 8), (8, 1, 16), (32, 2, 4), (16, 1, 16), (4, 1, 32),
-                                    (8, 1, 32), (64, 4, 2), (32, 4, 4), (16, 4, 8), (16, 2, 8)])
+@pytest.mark.parametrize("layout", [(16, 1, 1, 8), (8, 1, 1, 16), (32, 2, 1, 4), (16, 1, 1, 16),
+                                    (4, 1, 1, 32), (8, 1, 1, 32), (64, 2, 2, 2), (64, 4, 1, 2),
+                                    (64, 1, 4, 2), (64, 1, 2, 2), (32, 2, 2, 4), (16, 2, 2, 8)])
 def test_fine_layouts_bitwise_vs_oracle(layout):
     p = configs.make("c2", slabs=4)
     o = OracleProblem(p, fine_layout=layout)
@@ -137,8 +138,9 @@ def test_fine_layouts_bitwise_vs_oracle(layout):
 
 
 @pytest.mark.parametrize("M,layout", [(1, None), (2, None), (31, None), (100, None), (333, None),
-                                      (1000, None), (4095, None), (1500, (8, 4, 8)),
-                                      (3000, (32, 4, 4)), (700, (16, 4, 2))])
+                                      (1000, None), (4095, None), (1500, (32, 2, 2, 4)),
+                                      (3000, (64, 1, 4, 2)), (700, (16, 2, 2, 8)),
+                                      (2500, (64, 2, 2, 2))])
 def test_ragged_grids_bitwise_vs_oracle(M, layout):
     p = configs.make("c2", slabs=3, M=M)
     p.fine_steps = 20

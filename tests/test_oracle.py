@@ -34,24 +34,25 @@ def test_coefficients_bitwise_equal_product(name, role):
     steps = p.fine_steps if role == 0 else p.coarse_steps
     dt = (p.T / p.N) / steps
     st = O.OrcStepper()
-    assert O.orc().orc_stepper_init(C.byref(st), p.M, c.mpt, c.nseg, c.warps, steps, p.band_lo,
-                                    p.band_diag, p.band_up, dt) == 0
+    assert O.orc().orc_stepper_init(C.byref(st), p.M, c.mpt, c.nsub, c.nseg, c.warps, steps,
+                                    p.band_lo, p.band_diag, p.band_up, dt) == 0
     try:
         for f in ("delta", "lam", "mu", "dstar", "nl", "nu", "inv", "gneg", "invR", "invLast",
-                  "p32", "q32", "Pseg", "Qseg"):
+                  "p32", "q32", "pS", "qS", "Pseg", "Qseg"):
             assert getattr(st, f) == getattr(c, f), f
-        for f in ("K0", "R"):
+        for f in ("K0", "R", "narrow"):
             assert getattr(st, f) == getattr(c, f), f
         for f in ("pp", "qq", "plane", "qlane"):
             assert list(getattr(st, f)) == list(getattr(c, f)), f
-        sub = c.mpt // c.nseg
-        assert list(st.fl)[:sub] == list(c.fl)[:sub]
-        assert list(st.fu)[:sub] == list(c.fu)[:sub]
+        sub = c.mpt // (c.nsub * c.nseg)
+        assert list(st.nlpow)[:sub] == list(c.nlpow)[:sub]
+        assert list(st.pw)[: c.nsub] == list(c.pw)[: c.nsub]
         assert np.array_equal(np.ctypeslib.as_array(st.zc, (p.M,)), zc)
-        pp, qp = api.step_positions(p, role)
+        pp, qp, zt = api.step_positions(p, role)
         T = 32 * c.warps
         assert np.array_equal(np.ctypeslib.as_array(st.ppos, (T,)), pp)
         assert np.array_equal(np.ctypeslib.as_array(st.qpos, (T,)), qp)
+        assert np.array_equal(np.ctypeslib.as_array(st.zt, (T,)), zt)
     finally:
         O.orc().orc_stepper_free(C.byref(st))
 
@@ -232,8 +233,9 @@ def test_loop_pin_bitwise(which):
 # algorithm cross-checks
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("layout", [(8, 1, 16), (16, 1, 8), (4, 1, 32), (32, 2, 4), (64, 4, 2),
-                                    (32, 4, 4), (16, 4, 8), (16, 2, 8)])
+@pytest.mark.parametrize("layout", [(8, 1, 1, 16), (16, 1, 1, 8), (4, 1, 1, 32), (32, 2, 1, 4),
+                                    (64, 2, 2, 2), (64, 4, 1, 2), (64, 1, 4, 2), (64, 1, 2, 2),
+                                    (32, 2, 2, 4), (16, 2, 2, 8)])
 def test_chunked_stepper_layout_independent_to_rounding(layout):
     p = configs.make("c2", slabs=2)
     rng = np.random.default_rng(3)
@@ -242,7 +244,7 @@ def test_chunked_stepper_layout_independent_to_rounding(layout):
     dt = (p.T / p.N) / p.fine_steps
     st = O.OrcStepper()
     lib = O.orc()
-    assert lib.orc_stepper_init(C.byref(st), p.M, c.mpt, c.nseg, c.warps, 50, p.band_lo,
+    assert lib.orc_stepper_init(C.byref(st), p.M, c.mpt, c.nsub, c.nseg, c.warps, 50, p.band_lo,
                                 p.band_diag, p.band_up, dt) == 0
     out = np.zeros(p.M)
     lib.orc_stepper_propagate(C.byref(st), O.ptr(x), None, None, O.ptr(out))

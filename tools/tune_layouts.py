@@ -7,8 +7,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2203_10148_b200 import _lib, api, configs  # noqa: E402
 
-FINE = [(16, 1, 8), (32, 2, 4), (32, 4, 4), (64, 4, 2), (16, 2, 8), (16, 4, 8), (32, 4, 2), (32, 2, 2), (64, 4, 1), (32, 4, 1), (16, 4, 4), (16, 2, 4), (32, 4, 8), (16, 2, 16)]
-COARSE = [(4, 1, 16), (4, 1, 32), (8, 1, 8), (8, 1, 16), (16, 1, 8), (16, 1, 16), (16, 2, 8), (16, 4, 4), (32, 4, 4), (16, 4, 8), (32, 4, 8), (16, 2, 16), (32, 2, 4), (64, 4, 2)]
+FINE = [(16, 1, 1, 8), (64, 2, 2, 2), (64, 4, 1, 2), (64, 1, 4, 2), (64, 1, 2, 2), (32, 2, 2, 4), (32, 2, 1, 4), (32, 1, 2, 4), (16, 2, 2, 8), (64, 2, 2, 1), (64, 4, 1, 1), (64, 2, 2, 4), (64, 4, 1, 4), (32, 2, 2, 8), (64, 2, 2, 8)]
+COARSE = [(4, 1, 1, 16), (4, 1, 1, 32), (8, 1, 1, 8), (8, 1, 1, 16), (8, 1, 1, 32), (16, 1, 1, 8), (16, 1, 1, 16), (16, 1, 1, 32), (32, 2, 1, 4), (32, 2, 1, 8), (16, 2, 1, 16), (64, 2, 2, 2), (32, 2, 2, 4), (32, 2, 2, 8)]
 
 
 def timeit(fn, reps=3):
