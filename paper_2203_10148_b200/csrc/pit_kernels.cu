@@ -427,7 +427,8 @@ int ew_grid(size_t n) {
   X(8, 1, 1, 4) X(8, 1, 1, 8) X(8, 1, 1, 16) X(8, 1, 1, 32) X(16, 1, 1, 4) X(16, 1, 1, 8)    \
   X(16, 1, 1, 16) X(16, 1, 1, 32) X(32, 2, 1, 4) X(32, 2, 1, 8) X(32, 1, 2, 4) X(32, 2, 2, 4) \
   X(64, 2, 2, 1) X(64, 2, 2, 2) X(64, 2, 2, 4) X(64, 4, 1, 2) X(64, 1, 4, 2) X(64, 4, 1, 1)  \
-  X(64, 4, 1, 4) X(64, 1, 2, 2) X(32, 2, 2, 8) X(64, 2, 2, 8) X(16, 2, 1, 16) X(16, 2, 2, 8)
+  X(64, 4, 1, 4) X(64, 1, 2, 2) X(32, 2, 2, 8) X(64, 2, 2, 8) X(16, 2, 1, 16) X(16, 2, 2, 8)   \
+  X(64, 4, 1, 8)
 
 #define PIT_SHAPE(MP, NU, NS, W) Shape<(MP) / ((NU) * (NS)), NU, NS, W>
 
