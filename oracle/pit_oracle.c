@@ -212,7 +212,7 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
         for (int j = 1; j < sub; ++j) z = fma(s->nl, z, cu[j]);
         E[u] = z;
       }
-      double Ck = fma(s->ppos[k], S, C[k]);
+      double Ck = q > 0 ? fma(s->ppos[k], S, C[k]) : C[k];
       for (int u = 0; u < nu_; ++u) {
         double* cu = c + u * sub;
         const double Cu = Ck;
@@ -268,7 +268,7 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
         for (int j = sub - 2; j >= 0; --j) h = fma(s->nu, h, cu[j]);
         E[u] = h;
       }
-      double Rk = fma(s->qpos[k], S, C[k]);
+      double Rk = q < ns - 1 ? fma(s->qpos[k], S, C[k]) : C[k];
       for (int u = nu_ - 1; u >= 0; --u) {
         double* cu = c + u * sub;
         const double Ru = Rk;

@@ -68,11 +68,9 @@ template <class S>
 __device__ __forceinline__ StepLane step_lane(const StepParams& P,
                                               const StepShared<S::NSEG, S::WARPS>& sh, int tid) {
   StepLane L;
-  L.plane = sh.plane[tid & 31];
-  L.qlane = sh.qlane[tid & 31];
-  L.ppos = P.ppos[tid];
-  L.qpos = P.qpos[tid];
-  L.zt = P.narrow ? P.zt[tid] : 0.0;
+  L.ppos = S::NSEG > 1 ? P.ppos[tid] : 0.0;
+  L.qpos = S::NSEG > 1 ? P.qpos[tid] : 0.0;
+  (void)sh;
   return L;
 }
 

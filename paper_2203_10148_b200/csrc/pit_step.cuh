@@ -120,12 +120,11 @@ __device__ __forceinline__ void init_step_shared(const StepParams& P,
 
 // Per-thread constants of the step (registers, loaded once per kernel).
 struct StepLane {
-  double plane, qlane, ppos, qpos, zt;
+  double ppos, qpos;
 };
 
 // One step (see the file comment).  The lane-0 / lane-31 carry uses weight 1
-// on a zeroed neighbour value, segment 0 (NSEG-1 backward) adds a zero
-// segment carry-in, the Kogge-Stone weight is 0 on lanes without a source
+// on a zeroed neighbour value, the Kogge-Stone weight is 0 on lanes without a source
 // lane, and the table-form correction vector is zero-padded: every such
 // extra term is an exact no-op (fma(w, 0, x) == x, fma(0, t, x) == x).
 template <class S>
@@ -193,9 +192,11 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     double Sg = 0.0;  // segment carry-in
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) {
-      if (s > 0) Sg = fma(P.Pseg, Sg, Tot[s - 1]);
-      double C = fma(L.plane, Wc[s], Ip[s]);
-      C = fma(L.ppos, Sg, C);
+      double C = fma(sh.plane[lane], Wc[s], Ip[s]);
+      if (s > 0) {  // segment 0 has no segment carry-in
+        Sg = fma(P.Pseg, Sg, Tot[s - 1]);
+        C = fma(L.ppos, Sg, C);
+      }
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
         const int c = s * NSUB + u;
@@ -269,9 +270,11 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     double Sg = 0.0;  // segment carry from the right
 #pragma unroll
     for (int s = NSEG - 1; s >= 0; --s) {
-      if (s < NSEG - 1) Sg = fma(P.Qseg, Sg, Tot[s + 1]);
-      double R = fma(L.qlane, Wc[s], Ip[s]);
-      R = fma(L.qpos, Sg, R);
+      double R = fma(sh.qlane[lane], Wc[s], Ip[s]);
+      if (s < NSEG - 1) {  // the last segment has no carry from the right
+        Sg = fma(P.Qseg, Sg, Tot[s + 1]);
+        R = fma(L.qpos, Sg, R);
+      }
 #pragma unroll
       for (int u = NSUB - 1; u >= 0; --u) {
         const int c = s * NSUB + u;
@@ -291,7 +294,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     if (warp == 0) {
       const double cc = P.gneg * __shfl_sync(kFull, y[0][0], 0);
       if (tid * S::CH < P.K0) {
-        const double a = cc * L.zt;
+        const double a = cc * P.zt[tid];
 #pragma unroll
         for (int u = 0; u < NSUB; ++u) {
           const double au = a * P.pw[u];
