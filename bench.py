@@ -206,7 +206,7 @@ def run_ours(args, rank, world):
     dist = None
     if world > 1:
         import torch.distributed as dist
-    backend = DeviceBackend(ctx, stream)
+    backend = DeviceBackend(ctx, first, count, stream)
 
     def exchange():
         if world == 1:

@@ -200,6 +200,26 @@ int pit_coarse_sweep_device(pit_context* ctx, const double* V, const double* W_p
                             int first, int count, int with_source, int add_v, void* stream);
 int pit_block_partials_device(pit_context* ctx, const double* a, const double* b, double* partials,
                               int count, void* stream);
+/* Two fused partials per block: partials[2b] = h<a0,b0>, partials[2b+1] = h<a1,b1>. */
+int pit_block_partials2_device(pit_context* ctx, const double* a0, const double* b0,
+                               const double* a1, const double* b1, double* partials, int count,
+                               void* stream);
+/* BiCGStab vector phases (pitsbicg_solve's op order, src/solvers.cpp:168-214),
+ * on `count` blocks of M doubles, fused with their reductions:
+ *   update_s:  s = r - alpha d;                    partials[b] = h<s,s>
+ *   update_lr: lam += alpha p; lam += omega s; r = s - omega t;
+ *              partials[2b] = h<r,r>, partials[2b+1] = h<r,rs>
+ *   update_p:  p = (p - omega d) * beta + r
+ *   axpy:      y = y + a x          add: y = y + x */
+int pit_update_s_device(pit_context* ctx, double alpha, const double* r, const double* d, double* s,
+                        double* partials, int count, void* stream);
+int pit_update_lr_device(pit_context* ctx, double alpha, double omega, const double* p,
+                         const double* s, const double* t, const double* rs, double* lam, double* r,
+                         double* partials, int count, void* stream);
+int pit_update_p_device(pit_context* ctx, double omega, double beta, const double* d,
+                        const double* r, double* p, int count, void* stream);
+int pit_axpy_device(pit_context* ctx, double a, const double* x, double* y, int count, void* stream);
+int pit_add_device(pit_context* ctx, const double* x, double* y, int count, void* stream);
 int pit_sync_status(pit_context* ctx, void* stream);
 int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                               const double* lambda_init_dev, double* lambda_dev,

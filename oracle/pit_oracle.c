@@ -817,3 +817,27 @@ void orc_problem_delete(orc_problem* p) {
   free((void*)p->y0);
   free(p);
 }
+
+/* Elementwise BiCGStab phases in the device op order (pit_kernels.cu K3),
+ * for drivers that split block vectors across ranks (tests only). */
+void orc_vec_update_s(long n, double alpha, const double* r, const double* d, double* s) {
+  const double na = -alpha;
+  for (long i = 0; i < n; ++i) s[i] = fma(na, d[i], r[i]);
+}
+void orc_vec_update_lr(long n, double alpha, double omega, const double* p, const double* s,
+                       const double* t, double* lam, double* r) {
+  const double nw = -omega;
+  for (long i = 0; i < n; ++i) {
+    double l = fma(alpha, p[i], lam[i]);
+    lam[i] = fma(omega, s[i], l);
+    r[i] = fma(nw, t[i], s[i]);
+  }
+}
+void orc_vec_update_p(long n, double omega, double beta, const double* d, const double* r,
+                      double* p) {
+  const double nw = -omega;
+  for (long i = 0; i < n; ++i) p[i] = fma(fma(nw, d[i], p[i]), beta, r[i]);
+}
+void orc_vec_axpy(long n, double a, const double* x, double* y) {
+  for (long i = 0; i < n; ++i) y[i] = fma(a, x[i], y[i]);
+}

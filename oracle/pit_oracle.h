@@ -145,6 +145,14 @@ orc_problem* orc_problem_new(int M, int N, double weight, int has_source, int mo
                              const double* y0, orc_prop_fn prop, void* user);
 void orc_problem_delete(orc_problem* p);
 
+/* Elementwise BiCGStab phases in the device op order (tests of sharded drivers). */
+void orc_vec_update_s(long n, double alpha, const double* r, const double* d, double* s);
+void orc_vec_update_lr(long n, double alpha, double omega, const double* p, const double* s,
+                       const double* t, double* lam, double* r);
+void orc_vec_update_p(long n, double omega, double beta, const double* d, const double* r,
+                      double* p);
+void orc_vec_axpy(long n, double a, const double* x, double* y);
+
 /* Convenience: a 1D problem whose propagators are orc_stepper (mirrored) or
  * plain Thomas.  Owns its steppers and source tables. */
 typedef struct orc_1d orc_1d;

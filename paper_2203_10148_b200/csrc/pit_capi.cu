@@ -516,6 +516,59 @@ int pit_block_partials_device(pit_context* ctx, const double* a, const double* b
   return PIT_OK;
 }
 
+int pit_block_partials2_device(pit_context* ctx, const double* a0, const double* b0,
+                               const double* a1, const double* b1, double* partials, int count,
+                               void* stream) {
+  if (!ctx || !a0 || !b0 || !a1 || !b1 || !partials || count < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "block partials: bad arguments");
+  const double* A[2] = {a0, a1};
+  const double* B[2] = {b0, b1};
+  CUDA_TRY(launch_dots(ctx->M, count, ctx->weight, 2, A, B, partials,
+                       stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
+int pit_update_s_device(pit_context* ctx, double alpha, const double* r, const double* d, double* s,
+                        double* partials, int count, void* stream) {
+  if (!ctx || !r || !d || !s || !partials || count < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "update_s: bad arguments");
+  CUDA_TRY(launch_update_s(ctx->M, count, ctx->weight, alpha, r, d, s, partials,
+                           stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
+int pit_update_lr_device(pit_context* ctx, double alpha, double omega, const double* p,
+                         const double* s, const double* t, const double* rs, double* lam, double* r,
+                         double* partials, int count, void* stream) {
+  if (!ctx || !p || !s || !t || !rs || !lam || !r || !partials || count < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "update_lr: bad arguments");
+  CUDA_TRY(launch_update_lr(ctx->M, count, ctx->weight, alpha, omega, p, s, t, rs, lam, r,
+                            partials, stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
+int pit_update_p_device(pit_context* ctx, double omega, double beta, const double* d,
+                        const double* r, double* p, int count, void* stream) {
+  if (!ctx || !d || !r || !p || count < 1)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "update_p: bad arguments");
+  CUDA_TRY(launch_update_p((size_t)count * ctx->M, omega, beta, d, r, p,
+                           stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
+int pit_axpy_device(pit_context* ctx, double a, const double* x, double* y, int count,
+                    void* stream) {
+  if (!ctx || !x || !y || count < 1) return set_err(PIT_ERR_INVALID_ARGUMENT, "axpy: bad arguments");
+  CUDA_TRY(launch_axpy((size_t)count * ctx->M, a, x, y, stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
+int pit_add_device(pit_context* ctx, const double* x, double* y, int count, void* stream) {
+  if (!ctx || !x || !y || count < 1) return set_err(PIT_ERR_INVALID_ARGUMENT, "add: bad arguments");
+  CUDA_TRY(launch_add((size_t)count * ctx->M, x, y, stream ? (cudaStream_t)stream : ctx->stream));
+  return PIT_OK;
+}
+
 int pit_sync_status(pit_context* ctx, void* stream) {
   if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
   if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));

@@ -44,14 +44,17 @@ class Shard:
 
 
 class ShardedOperators:
-    """Exchange logic of the sharded PiT operators over a local backend.
+    """Exchange logic of the sharded PiT operators and solver over a local
+    backend (one rank per GPU; torch.distributed must be initialised).
 
-    backend must provide (all arrays are the backend's own array type):
-      apply_F(L_local, halo, first, count) -> out_local
-      coarse_sweep(V_local, W_prev, first, count) -> W_local
-      block_partials(a_local, b_local) -> per-block partials (count,)
-      to_host(x) / empty_block()
-    and torch.distributed must be initialised.
+    backend provides, on the rank's blocks (arrays of the backend's type):
+      apply_F(L, halo, first, count) -> out           K1, (F L)_n
+      residual(lam, halo, rhs, first, count) -> out   K1, rhs_n - (F lam)_n
+      coarse_sweep(V, W_prev, first, count, with_source, add_v, out=None) -> W   K2
+      fine_source(first, count) -> B                  K1 with source, zero input
+      partials(a, b) / partials2(a0, b0, a1, b1)      K3 per-block h<.,.>
+      update_s / update_lr / update_p / axpy / add / copy   K3 (device op order)
+      y0(), zeros(), block(x, i), empty_block(), set_block(x, i, v), to_host(x)
     """
 
     def __init__(self, backend, n_blocks: int, group=None):
@@ -65,8 +68,9 @@ class ShardedOperators:
         self.shard = Shard(first, count, self.rank, self.world)
         self.backend = backend
         self.n_blocks = n_blocks
+        self.counts = [shard_range(n_blocks, self.world, r)[1] for r in range(self.world)]
 
-    # -- point-to-point halo of the last owned block -----------------------
+    # -- point-to-point of the last owned block ------------------------------
     def _send_last(self, x_local):
         if self.rank + 1 < self.world:
             self.dist.send(self.backend.block(x_local, self.shard.count - 1), self.rank + 1,
@@ -79,49 +83,90 @@ class ShardedOperators:
         self.dist.recv(buf, self.rank - 1, group=self.group)
         return buf
 
-    def apply_F(self, L_local):
-        """(F L)_n = L_n - FineHom(L_{n-1}) on the owned blocks; one halo block
-        crosses each rank boundary (sent before the local batch starts)."""
-        # even ranks send first, odd ranks receive first: no deadlock with
-        # blocking send/recv
+    def _halo(self, x_local):
+        # even ranks send first, odd ranks receive first: blocking send/recv
+        # cannot deadlock
         if self.rank % 2 == 0:
-            self._send_last(L_local)
-            halo = self._recv_prev()
-        else:
-            halo = self._recv_prev()
-            self._send_last(L_local)
+            self._send_last(x_local)
+            return self._recv_prev()
+        halo = self._recv_prev()
+        self._send_last(x_local)
+        return halo
+
+    # -- operators (block_system.cpp:115-195) ---------------------------------
+    def apply_F(self, L_local):
+        """(F L)_n = L_n - FineHom(L_{n-1}); one halo block per rank boundary."""
+        halo = self._halo(L_local)
         return self.backend.apply_F(L_local, halo, self.shard.first, self.shard.count)
 
-    def apply_G_inverse(self, V_local):
+    def apply_G_inverse(self, V_local, out=None):
         """W_n = G(W_{n-1}) + V_n: the sequential chain crosses ranks in order."""
         W_prev = self._recv_prev()
-        W = self.backend.coarse_sweep(V_local, W_prev, self.shard.first, self.shard.count)
+        W = self.backend.coarse_sweep(V_local, W_prev, self.shard.first, self.shard.count,
+                                      False, True, out)
         self._send_last(W)
         return W
 
-    def block_inner_product(self, a_local, b_local) -> float:
-        """Sum over all blocks in global slab order (bit-identical to 1 GPU)."""
+    def initial_guess(self, zero: bool = False):
+        """CoarseSweep (solvers.cpp:49-64): lambda_0 = y0, lambda_n = G(lambda_{n-1})."""
+        be = self.backend
+        lam = be.zeros()
+        if zero:
+            return lam
+        if self.rank == 0:
+            be.set_block(lam, 0, be.y0())
+        W_prev = self._recv_prev()
+        lam = be.coarse_sweep(None, W_prev, self.shard.first, self.shard.count, True, False, lam)
+        self._send_last(lam)
+        return lam
+
+    def assemble_rhs(self):
+        """B_0 = y0, B_n = fine.source_contribution(n-1) (block_system.cpp:149-172)."""
+        be = self.backend
+        rhs = be.fine_source(self.shard.first, self.shard.count)
+        if self.rank == 0:
+            be.set_block(rhs, 0, be.y0())
+        return rhs
+
+    def preconditioned_residual(self, lam, rhs):
+        """G^-1 (rhs - F lam) (solvers.cpp:66-71)."""
+        halo = self._halo(lam)
+        f = self.backend.residual(lam, halo, rhs, self.shard.first, self.shard.count)
+        return self.apply_G_inverse(f, out=f)
+
+    # -- reductions: per-block partials, summed in global slab order ---------
+    def _gather(self, part, np_):
         import torch
 
-        part = torch.as_tensor(self.backend.to_host(self.backend.block_partials(a_local, b_local)),
-                               dtype=torch.float64)
-        counts = [shard_range(self.n_blocks, self.world, r)[1] for r in range(self.world)]
-        gathered = [torch.zeros(c, dtype=torch.float64, device=part.device) for c in counts]
-        self.dist.all_gather(gathered, part.to(self._coll_device()), group=self.group)
+        part = torch.as_tensor(self.backend.to_host(part), dtype=torch.float64).reshape(-1)
+        dev = self._coll_device()
+        cmax = max(self.counts)
+        padded = torch.zeros(cmax * np_, dtype=torch.float64, device=dev)  # equal sizes
+        padded[: part.numel()] = part.to(dev)
+        gathered = [torch.zeros(cmax * np_, dtype=torch.float64, device=dev) for _ in self.counts]
+        self.dist.all_gather(gathered, padded, group=self.group)
+        return np.concatenate([g[: c * np_].cpu().numpy() for g, c in zip(gathered, self.counts)]
+                              ).reshape(-1, np_)
+
+    @staticmethod
+    def _sum(p):
         s = 0.0
-        for g in gathered:
-            for v in g.cpu().numpy():
-                s += float(v)
+        for v in p:
+            s += float(v)
         return s
 
-    def block_norm_n_inf(self, a_local) -> float:
-        import torch
+    @staticmethod
+    def _max_sqrt(p):
+        w = 0.0
+        for v in p:
+            w = max(w, float(np.sqrt(v)))
+        return w
 
-        part = np.sqrt(self.backend.to_host(self.backend.block_partials(a_local, a_local)))
-        m = torch.tensor([float(np.max(part)) if part.size else 0.0], dtype=torch.float64,
-                         device=self._coll_device())
-        self.dist.all_reduce(m, op=self.dist.ReduceOp.MAX, group=self.group)
-        return float(m.item())
+    def block_inner_product(self, a_local, b_local) -> float:
+        return self._sum(self._gather(self.backend.partials(a_local, b_local), 1)[:, 0])
+
+    def block_norm_n_inf(self, a_local) -> float:
+        return self._max_sqrt(self._gather(self.backend.partials(a_local, a_local), 1)[:, 0])
 
     def _coll_device(self):
         import torch
@@ -129,32 +174,140 @@ class ShardedOperators:
         return torch.device("cuda", torch.cuda.current_device()) \
             if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu")
 
+    # -- pitsbicg_solve (solvers.cpp:116-220), op for op ----------------------
+    def pitsbicg_solve(self, tolerance=1e-8, restart_tolerance=1e-12, max_iterations=200,
+                       zero_guess=False, lambda_init=None):
+        """Returns (lambda_local, rows, restarts, converged); rows are
+        (k, residual, fine_applications, coarse_applications).  Same branches,
+        restart rules and reduction order as the single-GPU device driver
+        (pit_capi.cu pitsbicg_dev), so the history is bit-identical."""
+        if not (tolerance > restart_tolerance) or not (restart_tolerance > 0.0):
+            raise ValueError("solver tolerances must satisfy tolerance > restart_tolerance > 0")
+        be = self.backend
+        Nm1 = self.n_blocks - 1
+        fine = coarse = 0
+        rows = []
+        lam = lambda_init if lambda_init is not None else self.initial_guess(zero_guess)
+        if lambda_init is None and not zero_guess:
+            coarse += Nm1
+        rhs = self.assemble_rhs()
+        if be.has_source:
+            fine += Nm1
+        r = self.preconditioned_residual(lam, rhs)
+        fine += Nm1
+        coarse += Nm1
+        part = self._gather(be.partials(r, r), 1)[:, 0]
+        r_norm = self._max_sqrt(part)
+        rr_shadow = self._sum(part)
+        rows.append((0, r_norm, fine, coarse))
+        if r_norm <= tolerance:
+            return lam, rows, 0, True
+        rs = be.copy(r)
+        p = be.copy(r)
+        restarts = 0
+        for k in range(1, max_iterations + 1):
+            rho = rr_shadow
+            d = self.apply_G_inverse(self.apply_F(p))
+            fine += Nm1
+            coarse += Nm1
+            d_dot = self._sum(self._gather(be.partials(d, rs), 1)[:, 0])
+            if abs(d_dot) < 1e-300:
+                rs, p = be.copy(r), be.copy(r)
+                restarts += 1
+                rows.append((k, r_norm, fine, coarse))
+                rr_shadow = self._sum(self._gather(be.partials(r, r), 1)[:, 0])
+                continue
+            alpha = rho / d_dot
+            s, ps = be.update_s(alpha, r, d)
+            s_norm = self._max_sqrt(self._gather(ps, 1)[:, 0])
+            if s_norm <= tolerance:
+                be.axpy(alpha, p, lam)
+                rows.append((k, s_norm, fine, coarse))
+                return lam, rows, restarts, True
+            t = self.apply_G_inverse(self.apply_F(s))
+            fine += Nm1
+            coarse += Nm1
+            g2 = self._gather(be.partials2(t, t, t, s), 2)
+            tt = self._sum(g2[:, 0])
+            if tt < 1e-300:
+                rs, p = be.copy(r), be.copy(r)
+                restarts += 1
+                rows.append((k, r_norm, fine, coarse))
+                rr_shadow = self._sum(self._gather(be.partials(r, r), 1)[:, 0])
+                continue
+            omega = self._sum(g2[:, 1]) / tt
+            if abs(omega) < 1e-300:
+                rs, p = be.copy(r), be.copy(r)
+                restarts += 1
+                rows.append((k, r_norm, fine, coarse))
+                rr_shadow = self._sum(self._gather(be.partials(r, r), 1)[:, 0])
+                continue
+            r, plr = be.update_lr(alpha, omega, p, s, t, rs, lam)
+            g2 = self._gather(plr, 2)
+            r_norm = self._max_sqrt(g2[:, 0])
+            rr = self._sum(g2[:, 0])
+            r_dot = self._sum(g2[:, 1])
+            rows.append((k, r_norm, fine, coarse))
+            if r_norm <= tolerance:
+                return lam, rows, restarts, True
+            if abs(r_dot) <= restart_tolerance:
+                rs, p = be.copy(r), be.copy(r)
+                restarts += 1
+                rr_shadow = rr
+            else:
+                beta = (alpha / omega) * (r_dot / rho)
+                be.update_p(omega, beta, d, r, p)
+                rr_shadow = r_dot
+        return lam, rows, restarts, False
+
 
 class DeviceBackend:
     """Per-rank compute on the local GPU through the C ABI.  Arrays are torch
-    CUDA tensors of shape (count, M)."""
+    CUDA tensors of shape (count, M) holding the rank's blocks."""
 
-    def __init__(self, ctx, stream=None):
+    def __init__(self, ctx, first: int, count: int, stream=None):
         import torch
 
         from . import _lib
 
         self.ctx = ctx
         self.M = ctx.M
+        self.first, self.count = first, count
         self.L = _lib.lib()
         self.torch = torch
         self.stream = stream or torch.cuda.current_stream()
+        self.has_source = ctx.problem.source is not None
+        self._y0 = torch.tensor(np.ascontiguousarray(ctx.problem.y0), dtype=torch.float64,
+                                device="cuda")
 
     def _check(self, rc):
         from .api import _check
 
         _check(rc)
 
+    def _st(self):
+        return self.stream.cuda_stream
+
+    def _sync(self):
+        self._check(self.L.pit_sync_status(self.ctx.handle, self._st()))
+
+    def y0(self):
+        return self._y0
+
+    def zeros(self):
+        return self.torch.zeros((self.count, self.M), dtype=self.torch.float64, device="cuda")
+
     def block(self, x, i):
         return x[i].contiguous()
 
+    def set_block(self, x, i, v):
+        x[i].copy_(v)
+
     def empty_block(self):
         return self.torch.empty(self.M, dtype=self.torch.float64, device="cuda")
+
+    def copy(self, x):
+        return x.clone()
 
     def to_host(self, x):
         return x.detach().cpu().numpy()
@@ -163,24 +316,71 @@ class DeviceBackend:
         out = self.torch.empty_like(L_local)
         self._check(self.L.pit_apply_F_device(
             self.ctx.handle, L_local.data_ptr(), halo.data_ptr() if halo is not None else None,
-            out.data_ptr(), first, count, self.stream.cuda_stream))
-        self._check(self.L.pit_sync_status(self.ctx.handle, self.stream.cuda_stream))
+            out.data_ptr(), first, count, self._st()))
+        self._sync()
         return out
 
-    def coarse_sweep(self, V_local, W_prev, first, count):
-        W = self.torch.empty_like(V_local)
+    def residual(self, lam, halo, rhs, first, count):
+        out = self.torch.empty_like(lam)
+        self._check(self.L.pit_residual_device(
+            self.ctx.handle, lam.data_ptr(), halo.data_ptr() if halo is not None else None,
+            rhs.data_ptr(), out.data_ptr(), first, count, self._st()))
+        self._sync()
+        return out
+
+    def coarse_sweep(self, V, W_prev, first, count, with_source, add_v, out=None):
+        W = out if out is not None else self.torch.empty((count, self.M), dtype=self.torch.float64,
+                                                         device="cuda")
         self._check(self.L.pit_coarse_sweep_device(
-            self.ctx.handle, V_local.data_ptr(), W_prev.data_ptr() if W_prev is not None else None,
-            W.data_ptr(), first, count, 0, 1, self.stream.cuda_stream))
-        self._check(self.L.pit_sync_status(self.ctx.handle, self.stream.cuda_stream))
+            self.ctx.handle, V.data_ptr() if V is not None else None,
+            W_prev.data_ptr() if W_prev is not None else None, W.data_ptr(), first, count,
+            int(with_source), int(add_v), self._st()))
+        self._sync()
         return W
 
-    def block_partials(self, a, b):
+    def fine_source(self, first, count):
+        raise NotImplementedError("sharded assemble_rhs with a source: use the single-GPU API")
+
+    def partials(self, a, b):
         p = self.torch.empty(a.shape[0], dtype=self.torch.float64, device="cuda")
         self._check(self.L.pit_block_partials_device(self.ctx.handle, a.data_ptr(), b.data_ptr(),
-                                                     p.data_ptr(), a.shape[0],
-                                                     self.stream.cuda_stream))
+                                                     p.data_ptr(), a.shape[0], self._st()))
         return p
+
+    def partials2(self, a0, b0, a1, b1):
+        p = self.torch.empty(2 * a0.shape[0], dtype=self.torch.float64, device="cuda")
+        self._check(self.L.pit_block_partials2_device(self.ctx.handle, a0.data_ptr(),
+                                                      b0.data_ptr(), a1.data_ptr(), b1.data_ptr(),
+                                                      p.data_ptr(), a0.shape[0], self._st()))
+        return p
+
+    def update_s(self, alpha, r, d):
+        s = self.torch.empty_like(r)
+        p = self.torch.empty(r.shape[0], dtype=self.torch.float64, device="cuda")
+        self._check(self.L.pit_update_s_device(self.ctx.handle, alpha, r.data_ptr(), d.data_ptr(),
+                                               s.data_ptr(), p.data_ptr(), r.shape[0], self._st()))
+        return s, p
+
+    def update_lr(self, alpha, omega, p, s, t, rs, lam):
+        r = self.torch.empty_like(s)
+        part = self.torch.empty(2 * s.shape[0], dtype=self.torch.float64, device="cuda")
+        self._check(self.L.pit_update_lr_device(self.ctx.handle, alpha, omega, p.data_ptr(),
+                                                s.data_ptr(), t.data_ptr(), rs.data_ptr(),
+                                                lam.data_ptr(), r.data_ptr(), part.data_ptr(),
+                                                s.shape[0], self._st()))
+        return r, part
+
+    def update_p(self, omega, beta, d, r, p):
+        self._check(self.L.pit_update_p_device(self.ctx.handle, omega, beta, d.data_ptr(),
+                                               r.data_ptr(), p.data_ptr(), p.shape[0], self._st()))
+
+    def axpy(self, a, x, y):
+        self._check(self.L.pit_axpy_device(self.ctx.handle, a, x.data_ptr(), y.data_ptr(),
+                                           y.shape[0], self._st()))
+
+    def add(self, x, y):
+        self._check(self.L.pit_add_device(self.ctx.handle, x.data_ptr(), y.data_ptr(), y.shape[0],
+                                          self._st()))
 
 
 def init_from_env(backend: str = "nccl"):

@@ -103,6 +103,10 @@ def orc():
         lib.orc_block_dot.argtypes = [C.c_void_p, _dp, _dp]
         lib.orc_block_norm.restype = C.c_double
         lib.orc_block_norm.argtypes = [C.c_void_p, _dp]
+        lib.orc_vec_update_s.argtypes = [C.c_long, C.c_double, _dp, _dp, _dp]
+        lib.orc_vec_update_lr.argtypes = [C.c_long, C.c_double, C.c_double, _dp, _dp, _dp, _dp, _dp]
+        lib.orc_vec_update_p.argtypes = [C.c_long, C.c_double, C.c_double, _dp, _dp, _dp]
+        lib.orc_vec_axpy.argtypes = [C.c_long, C.c_double, _dp, _dp]
         lib.orc_block_partial.restype = C.c_double
         lib.orc_block_partial.argtypes = [C.c_void_p, _dp, _dp]
         _orc = lib

@@ -89,3 +89,15 @@ def test_auto_layouts_cover_baseline_configs():
         for role in (0, 1):
             c, _ = api.step_coefficients(p, role)
             assert 32 * c.mpt * c.warps >= p.M
+
+
+def test_cpp_shim_fails_loudly_without_gpu():
+    import subprocess
+    if _lib.lib().pit_device_count() > 0:
+        pytest.skip("a GPU is present")
+    exe = os.path.join(ROOT, "paper_2203_10148_b200", "host", "test_shim")
+    if not os.path.exists(exe):
+        pytest.skip("shim not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode != 0
+    assert "no CUDA device" in (r.stdout + r.stderr)
