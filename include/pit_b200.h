@@ -220,6 +220,10 @@ int pit_update_p_device(pit_context* ctx, double omega, double beta, const doubl
                         const double* r, double* p, int count, void* stream);
 int pit_axpy_device(pit_context* ctx, double a, const double* x, double* y, int count, void* stream);
 int pit_add_device(pit_context* ctx, const double* x, double* y, int count, void* stream);
+/* assemble_rhs blocks [first, first+count) without block 0's y0:
+ * out_n = fine.source_contribution(n-1) for n >= 1, zero for n = 0 and when
+ * the problem has no source (block_system.cpp:149-172). */
+int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, void* stream);
 int pit_sync_status(pit_context* ctx, void* stream);
 int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                               const double* lambda_init_dev, double* lambda_dev,

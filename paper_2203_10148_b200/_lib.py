@@ -92,6 +92,7 @@ EXPORTS = [
     "pit_parareal_solve", "pit_apply_F_device", "pit_residual_device", "pit_coarse_sweep_device",
     "pit_block_partials_device", "pit_block_partials2_device", "pit_update_s_device",
     "pit_update_lr_device", "pit_update_p_device", "pit_axpy_device", "pit_add_device",
+    "pit_fine_source_device",
     "pit_sync_status", "pit_pitsbicg_solve_device",
     "pit_seeded_uniform", "pit_seeded_normal", "pit_measure_fp64_peak",
 ]
@@ -141,6 +142,7 @@ def lib():
     L.pit_update_p_device.argtypes = [vp, C.c_double, C.c_double, vp, vp, vp, C.c_int, vp]
     L.pit_axpy_device.argtypes = [vp, C.c_double, vp, vp, C.c_int, vp]
     L.pit_add_device.argtypes = [vp, vp, vp, C.c_int, vp]
+    L.pit_fine_source_device.argtypes = [vp, vp, C.c_int, C.c_int, vp]
     L.pit_sync_status.argtypes = [vp, vp]
     L.pit_pitsbicg_solve_device.argtypes = [vp, C.POINTER(SolverConfigC), vp, vp,
                                             C.POINTER(RecordC), C.c_int, C.POINTER(SolveInfoC), vp]

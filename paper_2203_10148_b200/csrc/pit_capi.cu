@@ -569,6 +569,23 @@ int pit_add_device(pit_context* ctx, const double* x, double* y, int count, void
   return PIT_OK;
 }
 
+int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, void* stream) {
+  if (!ctx || !out || first < 0 || count < 1 || first + count > ctx->N)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "assemble_rhs: block count does not match the partition");
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)count * ctx->M * sizeof(double), st));
+  if (!ctx->has_source) return PIT_OK;
+  Role& R = ctx->role[PIT_FINE];
+  SlabArgs A{};
+  A.mode = kPropagate;
+  A.status = ctx->d_status;
+  const int skip = first == 0 ? 1 : 0;  // block 0 is y0, set by the caller
+  A.out = out + (size_t)skip * ctx->M;
+  A.slab0 = first + skip - 1;
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, count - skip, st));
+  return PIT_OK;
+}
+
 int pit_sync_status(pit_context* ctx, void* stream) {
   if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
   if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));

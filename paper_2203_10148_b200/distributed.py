@@ -339,7 +339,11 @@ class DeviceBackend:
         return W
 
     def fine_source(self, first, count):
-        raise NotImplementedError("sharded assemble_rhs with a source: use the single-GPU API")
+        out = self.torch.empty((count, self.M), dtype=self.torch.float64, device="cuda")
+        self._check(self.L.pit_fine_source_device(self.ctx.handle, out.data_ptr(), first, count,
+                                                  self._st()))
+        self._sync()
+        return out
 
     def partials(self, a, b):
         p = self.torch.empty(a.shape[0], dtype=self.torch.float64, device="cuda")

@@ -277,3 +277,29 @@ def test_sharded_device_driver_matches_device_solver():
         assert restarts == res.history.restarts
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_device_driver_with_source_matches_device_solver():
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2203_10148_b200.distributed import DeviceBackend, ShardedOperators
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        p = configs.make("c4", slabs=5)
+        with api.BlockOperatorContext(p) as ctx:
+            res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+            ops = ShardedOperators(DeviceBackend(ctx, 0, p.N), p.N)
+            lam, rows, restarts, conv = ops.pitsbicg_solve(tolerance=1e-10)
+        assert np.array_equal(lam.cpu().numpy(), res.solution)
+        assert [(r[0], r[1], r[2], r[3]) for r in rows] == \
+            [(x.k, x.residual_norm, x.fine_applications, x.coarse_applications)
+             for x in res.history.records]
+    finally:
+        dist.destroy_process_group()
