@@ -430,8 +430,10 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
   }
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, desc->device);
 #ifdef PIT_PHASE_TIMING
-  cudaMalloc(&ctx->role[PIT_FINE].P.timing, 32 * sizeof(long long));
-  cudaMemset(ctx->role[PIT_FINE].P.timing, 0, 32 * sizeof(long long));
+  for (int r = 0; r < 2; ++r) {
+    cudaMalloc(&ctx->role[r].P.timing, 32 * sizeof(long long));
+    cudaMemset(ctx->role[r].P.timing, 0, 32 * sizeof(long long));
+  }
 #endif
   if (const char* e = std::getenv("PIT_STAGGER")) ctx->stagger = std::atoi(e);
   if (const char* e = std::getenv("PIT_STAGGER_MOD")) ctx->stagger_mod = std::max(1, std::atoi(e));
@@ -1114,14 +1116,15 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
 }
 
 // instrumented builds only: per-phase cycle totals of CTA 0 (warps 0, 1)
-extern "C" int pit_debug_phase_timing(pit_context* ctx, long long* out32) {
+extern "C" int pit_debug_phase_timing(pit_context* ctx, int role, long long* out32) {
 #ifdef PIT_PHASE_TIMING
   CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(out32, ctx->role[PIT_FINE].P.timing, 32 * sizeof(long long),
+  CUDA_TRY(cudaMemcpy(out32, ctx->role[role].P.timing, 32 * sizeof(long long),
                       cudaMemcpyDeviceToHost));
   return PIT_OK;
 #else
   (void)ctx;
+  (void)role;
   (void)out32;
   return set_err(PIT_ERR_INVALID_ARGUMENT, "not an instrumented build");
 #endif

@@ -129,7 +129,7 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
   }
 #ifdef PIT_PHASE_TIMING
   if (P.timing && blockIdx.x == 0 && (tid & 31) == 0 && (tid >> 5) < 2)
-    for (int k = 0; k < 16; ++k) P.timing[(tid >> 5) * 16 + k] = ph_acc[k];
+    for (int k = 0; k < 10; ++k) P.timing[(tid >> 5) * 16 + k] += ph_acc[k];
 #endif
 }
 
@@ -236,7 +236,13 @@ __global__ void __launch_bounds__(S::T, 1)
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
     if (A.V && b + 1 < A.count) prefetch(b + 1);
+#ifdef PIT_PHASE_TIMING
+    const long long sw0 = clock64();
+#endif
     run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab);
+#ifdef PIT_PHASE_TIMING
+    const long long sw1 = clock64();
+#endif
     if (ok && !all_finite<S>(y, tid, M)) {
       ok = false;
       bad = slab;
@@ -266,6 +272,12 @@ __global__ void __launch_bounds__(S::T, 1)
     double* W = A.W + (size_t)b * M;
     for (int i = tid; i < M; i += S::T) W[i] = buf[S::slot_of_point(i)];
     __syncthreads();  // the buffer is free for the prefetch of slab b+2
+#ifdef PIT_PHASE_TIMING
+    if (P.timing && (tid & 31) == 0 && (tid >> 5) < 2) {
+      P.timing[(tid >> 5) * 16 + 10] += sw1 - sw0;        // propagation
+      P.timing[(tid >> 5) * 16 + 11] += clock64() - sw1;  // V add + W store
+    }
+#endif
   }
   if (!ok) atomicMin(A.status, bad);
 }
