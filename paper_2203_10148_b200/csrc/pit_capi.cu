@@ -84,6 +84,13 @@ struct pit_context {
   // solver work buffers (N*M each), allocated on first solve
   double* buf[10] = {};
   int stagger = 0, stagger_mod = 1, sms = 148;  // slab-kernel phase offset (see SlabArgs)
+  // K1 piece scheduling (SlabArgs::state): 0 = from occupancy, 1 = off, n = forced
+  int pieces = 0;
+  double* d_state = nullptr;
+  size_t state_n = 0;
+  int* d_sched = nullptr;
+  size_t sched_n = 0;
+  long long* d_trace = nullptr;  // PIT_PHASE_TIMING builds: K1 unit trace
   // host-entry scratch (see to_device)
   double* scratch[3] = {};
   size_t scratch_n[3] = {};
@@ -201,6 +208,33 @@ int check_status(pit_context* ctx, bool fine_batch) {
   return PIT_OK;
 }
 
+// State and scheduler buffers for K1 piece scheduling (grow-only; the
+// launcher decides whether the batch is cut into pieces at all).
+int attach_pieces(pit_context* ctx, SlabArgs* A, int ctas) {
+  if (ctx->pieces == 1 || ctas <= 0) return PIT_OK;
+  const Role& R = ctx->role[PIT_FINE];  // K1 runs the fine propagator
+  const size_t padded = (size_t)R.mpt * 32 * R.warps;  // state in register order
+  const size_t ns = (size_t)ctas * padded, nq = 2 + (size_t)(kMaxPieces - 1) * ctas;
+  if (ctx->state_n < ns) {
+    cudaFree(ctx->d_state);
+    ctx->d_state = nullptr;
+    ctx->state_n = 0;
+    CUDA_TRY(cudaMalloc(&ctx->d_state, ns * sizeof(double)));
+    ctx->state_n = ns;
+  }
+  if (ctx->sched_n < nq) {
+    cudaFree(ctx->d_sched);
+    ctx->d_sched = nullptr;
+    ctx->sched_n = 0;
+    CUDA_TRY(cudaMalloc(&ctx->d_sched, nq * sizeof(int)));
+    ctx->sched_n = nq;
+  }
+  A->state = ctx->d_state;
+  A->sched = ctx->d_sched;
+  A->pieces = ctx->pieces;
+  return PIT_OK;
+}
+
 // Fine batch over output blocks [first, first+count) (global indices).
 int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* halo,
                    const double* rhs, double* out, int first, int count, cudaStream_t st) {
@@ -242,6 +276,12 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
   A.stagger = ctx->stagger;
   A.stagger_mod = ctx->stagger_mod;
   A.sms = ctx->sms;
+  PIT_TRY(attach_pieces(ctx, &A, ctas));
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+  if (!ctx->d_trace) CUDA_TRY(cudaMalloc(&ctx->d_trace, sizeof(long long) * 8 * kMaxPieces * (size_t)ctx->N));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_trace, 0, sizeof(long long) * 8 * kMaxPieces * (size_t)ctx->N, st));
+  A.trace = ctx->d_trace;
+#endif
   CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, false, R.P, A, ctas, st));
   return PIT_OK;
 }
@@ -437,6 +477,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
 #endif
   if (const char* e = std::getenv("PIT_STAGGER")) ctx->stagger = std::atoi(e);
   if (const char* e = std::getenv("PIT_STAGGER_MOD")) ctx->stagger_mod = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("PIT_PIECES")) ctx->pieces = std::max(0, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&ctx->h_status, sizeof(int)) != cudaSuccess ||
@@ -467,6 +508,9 @@ int pit_context_destroy(pit_context* ctx) {
   if (ctx->h_partials) cudaFreeHost(ctx->h_partials);
   for (auto& b : ctx->buf) cudaFree(b);
   for (auto& b : ctx->scratch) cudaFree(b);
+  cudaFree(ctx->d_state);
+  cudaFree(ctx->d_sched);
+  cudaFree(ctx->d_trace);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PIT_OK;
@@ -584,6 +628,7 @@ int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, 
   const int skip = first == 0 ? 1 : 0;  // block 0 is y0, set by the caller
   A.out = out + (size_t)skip * ctx->M;
   A.slab0 = first + skip - 1;
+  PIT_TRY(attach_pieces(ctx, &A, count - skip));
   CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, count - skip, st));
   return PIT_OK;
 }
@@ -686,6 +731,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
     A.out = d.p + ctx->M;
     A.slab0 = 0;
     A.status = ctx->d_status;
+    PIT_TRY(attach_pieces(ctx, &A, ctx->N - 1));
     CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
     PIT_TRY(check_status(ctx, true));
     add_fine(ctx, stats, ms_since(t0));
@@ -729,6 +775,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
   A.mode = kPropagate;
   A.out = d + ctx->M;
   A.status = ctx->d_status;
+  PIT_TRY(attach_pieces(ctx, &A, ctx->N - 1));
   CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
   PIT_TRY(check_status(ctx, true));
   add_fine(ctx, stats, ms_since(t0));
@@ -1126,6 +1173,22 @@ extern "C" int pit_debug_phase_timing(pit_context* ctx, int role, long long* out
   (void)ctx;
   (void)role;
   (void)out32;
+  return set_err(PIT_ERR_INVALID_ARGUMENT, "not an instrumented build");
+#endif
+}
+
+// K1 unit trace of the last fine batch: n rows of {smid, block, t0, t_end,
+// t_loaded, t_computed, 0, 0} (ns).
+extern "C" int pit_debug_trace(pit_context* ctx, long long* out, int n) {
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+  if (n > kMaxPieces * ctx->N) n = kMaxPieces * ctx->N;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(out, ctx->d_trace, sizeof(long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  return PIT_OK;
+#else
+  (void)ctx;
+  (void)out;
+  (void)n;
   return set_err(PIT_ERR_INVALID_ARGUMENT, "not an instrumented build");
 #endif
 }

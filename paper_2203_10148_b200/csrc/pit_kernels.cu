@@ -16,6 +16,9 @@
 
 #include "pit_kernels.cuh"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace pitb {
 
 namespace {
@@ -74,10 +77,13 @@ __device__ __forceinline__ StepLane step_lane(const StepParams& P,
   return L;
 }
 
+// Steps [k0, k1) of one slab's propagation.  The rescale counter restarts
+// from k0 mod R, so cutting a slab into step ranges (piece scheduling) runs
+// exactly the same operation sequence as one uninterrupted pass.
 template <class S, bool SRC>
 __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepParams& P,
                                          const StepLane& L, StepShared<S::NSEG, S::WARPS>& sh,
-                                         const double* s_zc, int tid, int slab) {
+                                         const double* s_zc, int tid, int slab, int k0, int k1) {
   const bool ghosts = P.M < S::NSEG * S::LSEG;
 #ifdef PIT_PHASE_TIMING
   long long ph_acc[16] = {};
@@ -90,9 +96,9 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
     // separable source y += dt*s(t_k) g(x): g read through L1 each step (not
     // held in registers, so wide layouts do not spill)
     const double* ds = P.ds + (size_t)slab * P.steps;
-    double dsk = ds[0];
-    for (int k = 0; k < P.steps; ++k) {
-      const double dsn = (k + 1 < P.steps) ? ds[k + 1] : 0.0;
+    double dsk = ds[k0];
+    for (int k = k0; k < k1; ++k) {
+      const double dsn = (k + 1 < k1) ? ds[k + 1] : 0.0;
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
 #pragma unroll
@@ -108,8 +114,8 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
       dsk = dsn;
     }
   } else {
-    int cnt = 0;
-    for (int k = 0; k < P.steps; ++k) {
+    int cnt = k0 % P.R;
+    for (int k = k0; k < k1; ++k) {
       be_solve<S>(y, P, L, sh, s_zc, tid, ghosts PIT_TIMING_ARGS);
       if (++cnt == P.R) {
         cnt = 0;
@@ -120,7 +126,7 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
       }
       PIT_PHASE(9);
     }
-    if (cnt) {
+    if (k1 == P.steps && cnt) {
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
 #pragma unroll
@@ -133,40 +139,26 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
 #endif
 }
 
-template <class S, bool SRC>
-__global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin))
-    slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
-  double* s_zc = reinterpret_cast<double*>(sh + 1);
-  const int tid = threadIdx.x;
-  const int b = blockIdx.x;
-  const int M = P.M;
-  load_zc<S>(P, s_zc, tid);
-  init_step_shared<S::NSEG, S::WARPS>(P, *sh, tid);
+// Piece state in register order (element (c, j) of thread tid at
+// ((c*SUB + j)*T + tid)): one coalesced 256-byte access per warp and element.
+template <class S>
+__device__ __forceinline__ void load_state(double (&y)[S::NC][S::SUB], const double* st, int tid) {
+#pragma unroll
+  for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+    for (int j = 0; j < S::SUB; ++j) y[c][j] = __ldcg(st + (c * S::SUB + j) * S::T + tid);
+}
+template <class S>
+__device__ __forceinline__ void save_state(const double (&y)[S::NC][S::SUB], double* st, int tid) {
+#pragma unroll
+  for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+    for (int j = 0; j < S::SUB; ++j) __stcg(st + (c * S::SUB + j) * S::T + tid, y[c][j]);
+}
 
-  const double* src;
-  if (b + A.in_shift >= 0)
-    src = A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr;
-  else
-    src = A.halo;
-  double y[S::NC][S::SUB];
-  load_field<S>(y, src, tid, M);
-  const int slab = A.slab0 + b;
-  __syncthreads();
-  const StepLane L = step_lane<S>(P, *sh, tid);
-  if (A.stagger > 0) {
-    // Offset the step phase of co-resident CTAs (block ids differing by a
-    // multiple of the SM count) — tuning knob, off by default.
-    const long long wait = (long long)((b / A.sms) % A.stagger_mod) * A.stagger;
-    const long long t0 = clock64();
-    while (clock64() - t0 < wait) {
-    }
-    __syncthreads();
-  }
-
-  run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab);
-
+template <class S>
+__device__ __forceinline__ void slab_epilogue(const double (&y)[S::NC][S::SUB], const SlabArgs& A,
+                                              int M, int tid, int b, int slab) {
   if (!all_finite<S>(y, tid, M)) atomicMin(A.status, slab);
   const size_t off = (size_t)b * M;
   double* out = A.out + off;
@@ -192,6 +184,141 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
     } else if (A.mode == kResidual) {
       for (int i = tid; i < M; i += S::T) A.out0[i] = A.rhs0[i] - A.L0[i];
     }
+  }
+}
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int sm_id() {
+  int v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// K1.  One CTA per slab (A.state == nullptr), or a persistent grid pulling
+// (piece, slab) units piece-major (see SlabArgs) so that a batch of
+// 1.15 waves does not leave the last wave's SMs one-sixth occupied.
+template <class S, bool SRC>
+__global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin))
+    slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
+  double* s_zc = reinterpret_cast<double*>(sh + 1);
+  __shared__ int s_unit;
+  const int tid = threadIdx.x;
+  const int M = P.M;
+  load_zc<S>(P, s_zc, tid);
+  init_step_shared<S::NSEG, S::WARPS>(P, *sh, tid);
+  auto source_of = [&](int b) -> const double* {
+    if (b + A.in_shift >= 0) return A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr;
+    return A.halo;
+  };
+  double y[S::NC][S::SUB];
+
+  if (A.state == nullptr) {
+    const int b = blockIdx.x;
+    load_field<S>(y, source_of(b), tid, M);
+    const int slab = A.slab0 + b;
+    __syncthreads();
+    const StepLane L = step_lane<S>(P, *sh, tid);
+    if (A.stagger > 0) {
+      // Offset the step phase of co-resident CTAs (block ids differing by a
+      // multiple of the SM count) — tuning knob, off by default.
+      const long long wait = (long long)((b / A.sms) % A.stagger_mod) * A.stagger;
+      const long long t0 = clock64();
+      while (clock64() - t0 < wait) {
+      }
+      __syncthreads();
+    }
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+    const long long tr0 = global_ns();
+#endif
+    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
+    slab_epilogue<S>(y, A, M, tid, b, slab);
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+    if (A.trace && tid == 0) {
+      long long* t = A.trace + 8 * (size_t)b;
+      t[0] = sm_id(), t[1] = b, t[2] = tr0, t[3] = global_ns(), t[4] = tr0, t[5] = t[3];
+    }
+#endif
+    return;
+  }
+
+  __syncthreads();
+  const StepLane L = step_lane<S>(P, *sh, tid);
+  const int units = A.pieces * A.nblk;
+  int* head = A.sched;       // next queue position to pop
+  int* tail = A.sched + 1;   // next push position
+  int* queue = A.sched + 2;  // unit+1 of pushed units (0 = not yet written)
+  for (;;) {
+    if (tid == 0) {
+      // positions < nblk are the first pieces (unit id = position); later
+      // positions are filled in completion order by the CTA finishing the
+      // previous piece of the same slab
+      const int i = atomicAdd(head, 1);
+      int u = units;
+      if (i < A.nblk) {
+        u = i;
+      } else if (i < units) {
+        int v;
+        while ((v = ld_acquire(queue + (i - A.nblk))) == 0) __nanosleep(64);
+        u = v - 1;
+      }
+      s_unit = u;
+    }
+    __syncthreads();
+    const int u = s_unit;
+    __syncthreads();  // s_unit is rewritten at the top of the next unit
+    if (u >= units) break;
+    const int q = u / A.nblk, b = u - q * A.nblk;
+    const int slab = A.slab0 + b;
+    const int k0 = (int)((long long)P.steps * q / A.pieces);
+    const int k1 = (int)((long long)P.steps * (q + 1) / A.pieces);
+    double* st = A.state + (size_t)b * (S::NC * S::SUB * S::T);
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+    const long long tr0 = global_ns();
+#endif
+    if (q == 0) {
+      load_field<S>(y, source_of(b), tid, M);
+    } else {
+      load_state<S>(y, st, tid);
+    }
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+    __syncthreads();
+    const long long tr1 = global_ns();
+#endif
+    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, k0, k1);
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+    __syncthreads();
+    const long long tr2 = global_ns();
+#endif
+    if (q + 1 < A.pieces) {
+      save_state<S>(y, st, tid);
+      // bar.sync orders every thread's state stores before thread 0's
+      // release (cumulativity); the popping CTA acquires before its bar.sync
+      __syncthreads();
+      if (tid == 0) st_release(queue + atomicAdd(tail, 1), u + A.nblk + 1);
+    } else {
+      slab_epilogue<S>(y, A, M, tid, b, slab);
+    }
+#if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
+    if (A.trace && tid == 0) {
+      long long* t = A.trace + 8 * (size_t)u;
+      t[0] = sm_id(), t[1] = blockIdx.x, t[2] = tr0, t[3] = global_ns(), t[4] = tr1, t[5] = tr2;
+    }
+#endif
   }
 }
 
@@ -239,7 +366,7 @@ __global__ void __launch_bounds__(S::T, 1)
 #ifdef PIT_PHASE_TIMING
     const long long sw0 = clock64();
 #endif
-    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab);
+    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
 #ifdef PIT_PHASE_TIMING
     const long long sw1 = clock64();
 #endif
@@ -282,8 +409,29 @@ __global__ void __launch_bounds__(S::T, 1)
   if (!ok) atomicMin(A.status, bad);
 }
 
+// Pieces per slab for a batch of nblk slabs over `slots` resident CTAs.
+// Measured on B200 (tools/pieces_grid.py): between one and two waves, two
+// pieces let the queue refill the slots of the first CTAs to finish (c2:
+// 2.12 -> 1.78 ms); beyond two waves, minimise ceil(waves*q)/q plus a
+// per-piece cost (c4: q = 3, 3.73 -> 3.60 ms).
+inline int choose_pieces(int nblk, int slots) {
+  if (slots <= 0 || nblk <= slots) return 1;
+  if (nblk < 2 * slots) return 2;
+  int best = 1;
+  double best_cost = 1e30;
+  for (int q = 1; q <= 8; ++q) {
+    const long long rounds = ((long long)nblk * q + slots - 1) / slots;
+    const double cost = (double)rounds / q + 0.02 * q;
+    if (cost < best_cost - 1e-12) {
+      best_cost = cost;
+      best = q;
+    }
+  }
+  return best;
+}
+
 template <class S, bool SRC>
-cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaStream_t st) {
+cudaError_t slab_launch(const StepParams& P, const SlabArgs& A0, int ctas, cudaStream_t st) {
   const size_t smem =
       sizeof(StepShared<S::NSEG, S::WARPS>) + sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
   auto k = slab_kernel<S, SRC>;
@@ -291,7 +439,34 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A, int ctas, cudaSt
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<ctas, S::T, smem, st>>>(P, A);
+  SlabArgs A = A0;
+  A.nblk = ctas;
+  int grid = ctas;
+  if (A.state != nullptr) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S::T, smem);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+      return e;
+    const int slots = per_sm * sms;
+    A.pieces = A0.pieces > 0 ? A0.pieces : choose_pieces(ctas, slots);
+    if (A.pieces > kMaxPieces) A.pieces = kMaxPieces;
+    if (A.pieces > P.steps) A.pieces = P.steps;
+    static const bool verbose = std::getenv("PIT_PIECES_VERBOSE") != nullptr;
+    if (verbose)
+      std::fprintf(stderr, "[pit] slab_kernel<%d,%d,%d,%d,%d> ctas=%d per_sm=%d slots=%d pieces=%d\n",
+                   S::MPT, S::NSUB, S::NSEG, S::WARPS, (int)SRC, ctas, per_sm, slots, A.pieces);
+    if (A.pieces <= 1 || slots <= 0) {
+      A.state = nullptr;  // one wave-sequence of plain CTAs
+    } else {
+      const long long units = (long long)A.pieces * ctas;
+      grid = (int)(units < slots ? units : slots);
+      const size_t nq = 2 + (size_t)(A.pieces - 1) * ctas;
+      if ((e = cudaMemsetAsync(A.sched, 0, sizeof(int) * nq, st)) != cudaSuccess) return e;
+    }
+  }
+  k<<<grid, S::T, smem, st>>>(P, A);
   return cudaGetLastError();
 }
 

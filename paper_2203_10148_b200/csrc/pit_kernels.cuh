@@ -26,6 +26,18 @@ struct SlabArgs {
   int stagger;         // cycles of start offset per phase class (0 = off)
   int stagger_mod;     // number of phase classes
   int sms;             // SM count (co-residency stride of block ids)
+  // Piece scheduling (launch_slab fills pieces/nblk): when the batch exceeds
+  // one wave of resident CTAs, each slab's steps are cut into `pieces`
+  // consecutive step ranges and a persistent grid pops (piece, slab) units
+  // from a queue: the first pieces in slab order, then each later piece as
+  // soon as the CTA running its predecessor pushes it.  The state between
+  // pieces goes through state + b*M.
+  // state == nullptr: one CTA per slab, one launch wave (or more).
+  double* state;
+  int* sched;   // {head, tail, queue[(pieces-1)*nblk]}, zeroed by the launcher
+  int pieces;   // 0 = choose from occupancy (launcher), else forced
+  int nblk;     // slabs in the batch (set by the launcher)
+  long long* trace;  // PIT_PHASE_TIMING builds: per unit {smid, block, t_start, t_end} (ns)
 };
 
 // K2: one persistent CTA running the sequential sweep
@@ -38,6 +50,8 @@ struct SweepArgs {
   int slab0;
   int* status;
 };
+
+constexpr int kMaxPieces = 64;
 
 // Launchers; return cudaErrorInvalidConfiguration for an uncompiled layout.
 cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,

@@ -115,6 +115,40 @@ def test_reduced_pitsbicg_bitwise_vs_oracle(name, slabs):
     assert np.array_equal(res.solution, r["lam"])
 
 
+@pytest.mark.parametrize("pieces", [2, 3, 7])
+@pytest.mark.parametrize("name,slabs", [("c2", 9), ("c4", 7)])
+def test_piece_scheduling_bitwise_vs_oracle(name, slabs, pieces, monkeypatch):
+    # K1 cut into step ranges with a persistent unit scheduler (SlabArgs::state)
+    # runs the same operation sequence as one pass per slab
+    monkeypatch.setenv("PIT_PIECES", str(pieces))
+    p = configs.make(name, slabs=slabs)
+    o = OracleProblem(p)
+    rng = np.random.default_rng(13)
+    L = np.ascontiguousarray(rng.uniform(-1, 1, (p.N, p.M)))
+    with api.BlockOperatorContext(p) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))[0]
+        rhs = o.assemble_rhs()
+        assert same(api.assemble_rhs(ctx), rhs)[0]
+        assert same(api.preconditioned_residual(ctx, L, rhs), o.preconditioned_residual(L, rhs))[0]
+        res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+    r = o.solve(1e-10)
+    assert [(x.k, x.residual_norm) for x in res.history.records] == [(a[0], a[1]) for a in r["rows"]]
+    assert np.array_equal(res.solution, r["lam"])
+
+
+def test_piece_scheduling_nonfinite_slab(monkeypatch):
+    monkeypatch.setenv("PIT_PIECES", "4")
+    p = configs.make("c2", slabs=12)
+    L = np.ones((p.N, p.M))
+    L[9, 3] = np.nan
+    L[4, 1] = np.inf
+    with api.BlockOperatorContext(p) as ctx:
+        with pytest.raises(api.SlabError) as e:
+            api.apply_F(ctx, L)
+        assert e.value.slab_index == 4
+        assert np.isfinite(api.apply_F(ctx, np.ones((p.N, p.M)))).all()
+
+
 def test_c3_n16_matches_reference():
     g = gold("c3_n16_reference.npz")
     p = configs.make("c3", slabs=16)
