@@ -62,6 +62,10 @@ enum { PIT_FINE = 0, PIT_COARSE = 1 };
 enum { PIT_SOURCE_NONE = 0, PIT_SOURCE_SEPARABLE = 1 };
 enum { PIT_GUESS_COARSE_SWEEP = 0, PIT_GUESS_ZERO = 1 };
 enum { PIT_CONVERGED = 0, PIT_MAX_ITERATIONS = 1 };
+/* fine propagator scheme: backward Euler (the reference's Propagator,
+ * src/propagator.cpp:50-71) or explicit Euler (config 5; not in the
+ * reference, which has implicit propagators only) */
+enum { PIT_SCHEME_BACKWARD_EULER = 0, PIT_SCHEME_EXPLICIT_EULER = 1 };
 
 /* Problem description: the 1D operator A (dy/dt = -A y + f) as constant
  * tridiagonal bands on M interior nodes of [grid_lo, grid_hi] with Dirichlet
@@ -90,6 +94,21 @@ typedef struct pit_problem_desc {
    * (sub-chunk length = mpt / (nsub*nseg)); all 0 = auto */
   int32_t fine_mpt, fine_nsub, fine_nseg, fine_warps;
   int32_t coarse_mpt, coarse_nsub, coarse_nseg, coarse_warps;
+  /* dimension 2 (config 5): interior = m points per axis on [grid_lo,
+   * grid_hi]^2, blocks of M = m*m values (x fastest); the operator is the
+   * 5-point stencil band_diag (centre) / band_lo (= band_up, each of the four
+   * neighbours), i.e. the reference's 2D assemble_spatial_operator with zero
+   * velocity (src/pde.cpp:66-100).  Fine: fine_scheme must be
+   * PIT_SCHEME_EXPLICIT_EULER; coarse: backward Euler solved by Jacobi-PCG
+   * (solve_cg, src/sparse.cpp:60-114) to coarse_tolerance (0: 1e-12,
+   * kInnerSolveRelTol, pde.hpp:78) within coarse_max_iterations (0: 10*M,
+   * pde.hpp:79).  No sources in 2D. */
+  int32_t fine_scheme;
+  double coarse_tolerance;
+  int64_t coarse_max_iterations;
+  /* K4 layout (tile rows, tile columns, CTAs per cluster, warps per CTA);
+   * all 0 = auto */
+  int32_t tile_rows, tile_cols, tile_cluster, tile_warps;
 } pit_problem_desc;
 
 typedef struct pit_context pit_context;
@@ -155,8 +174,29 @@ int pit_device_count(void);
 int pit_context_create(const pit_problem_desc* desc, pit_context** out);
 int pit_context_destroy(pit_context* ctx);
 int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing);
+/* cumulative inner CG iterations of the 2D coarse sweeps (0 in 1D, where
+ * the coarse step is a direct tridiagonal solve) */
+int pit_coarse_iterations(const pit_context* ctx, int64_t* out);
 /* Coefficients for role PIT_FINE / PIT_COARSE (no device needed). */
 int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out);
+
+/* 2D (config 5) step coefficients, as used by the kernels:
+ *   fine explicit Euler y' = fma(ac, y, an*((yW + yE) + (yN + yS))),
+ *     ac = 1 - dt_f*diag, an = -dt_f*off (long double, rounded once);
+ *   coarse BE matrix I + dt_c*A: centre D = diag*dt_c + 1, neighbour
+ *     O = off*dt_c (ImplicitStepSolver, src/pde.cpp:106-109), minv = 1/D;
+ *   K5 decomposition: cluster CTAs of `threads` threads, `rows` rows each
+ *     (sets the CG reduction order). */
+typedef struct pit_step_coeffs_2d {
+  int32_t m, fine_steps, coarse_steps;
+  double ac, an;
+  double D, O, minv;
+  double rel_tol;
+  int64_t cap;
+  int32_t rows, cluster, threads;
+  int32_t tile_rows, tile_cols, tile_cluster, tile_warps;
+} pit_step_coeffs_2d;
+int pit_step_coefficients_2d(const pit_problem_desc* desc, pit_step_coeffs_2d* out);
 /* zc correction vector (first K0 entries used), length M (no device needed). */
 int pit_step_correction(const pit_problem_desc* desc, int role, double* zc_out);
 /* per-thread weights, length 32*warps each (no device needed): segment-carry

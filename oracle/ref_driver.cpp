@@ -143,6 +143,34 @@ void* pitref_create_1d(int M, double lo, double hi, double diffusion, double rea
   }
 }
 
+// 2D heat on [lo, hi]^2 with m interior points per axis: the reference's
+// own 2D operator (assemble_spatial_operator, zero velocity, pde.cpp:66-100)
+// and its backward-Euler propagators (CG to kInnerSolveRelTol, pde.hpp:78).
+// Blocks are m*m values, x fastest.  Used to pin the 2D coarse CG step.
+void* pitref_create_2d(int m, double lo, double hi, double diffusion, double reaction, int N,
+                       double T, int fine_steps, int coarse_steps, const double* y0) {
+  try {
+    auto r = std::make_unique<RefCtx>();
+    r->M = m * m;
+    r->N = N;
+    const pit::GridPtr g = pit::SpatialGrid::make(2, lo, hi, m + 2);
+    pit::PDECoefficients c;
+    c.diffusion = diffusion;
+    c.reaction = reaction;
+    pit::SpatialOperator op = pit::assemble_spatial_operator(c, g);
+    const pit::TimeSlabPartition part(T, N);
+    pit::Propagator fine(op, part, fine_steps, pit::PropagatorRole::Fine);
+    pit::Propagator coarse(op, part, coarse_steps, pit::PropagatorRole::Coarse);
+    pit::ScalarField init(g, std::vector<double>(y0, y0 + r->M));
+    r->ctx = std::make_unique<pit::BlockOperatorContext>(std::move(fine), std::move(coarse),
+                                                         std::move(init));
+    return r.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
 void pitref_destroy(void* p) { delete static_cast<RefCtx*>(p); }
 
 double pitref_spacing(void* p) {

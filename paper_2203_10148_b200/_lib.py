@@ -28,6 +28,8 @@ PIT_GUESS_COARSE_SWEEP = 0
 PIT_GUESS_ZERO = 1
 PIT_CONVERGED = 0
 PIT_MAX_ITERATIONS = 1
+PIT_SCHEME_BACKWARD_EULER = 0
+PIT_SCHEME_EXPLICIT_EULER = 1
 
 _dp = C.POINTER(C.c_double)
 
@@ -42,7 +44,19 @@ class ProblemDesc(C.Structure):
                 ("source_shape", _dp), ("initial_value", _dp), ("device", C.c_int32),
                 ("fine_mpt", C.c_int32), ("fine_nsub", C.c_int32), ("fine_nseg", C.c_int32),
                 ("fine_warps", C.c_int32), ("coarse_mpt", C.c_int32), ("coarse_nsub", C.c_int32),
-                ("coarse_nseg", C.c_int32), ("coarse_warps", C.c_int32)]
+                ("coarse_nseg", C.c_int32), ("coarse_warps", C.c_int32),
+                ("fine_scheme", C.c_int32), ("coarse_tolerance", C.c_double),
+                ("coarse_max_iterations", C.c_int64), ("tile_rows", C.c_int32),
+                ("tile_cols", C.c_int32), ("tile_cluster", C.c_int32), ("tile_warps", C.c_int32)]
+
+
+class StepCoeffs2DC(C.Structure):
+    _fields_ = [("m", C.c_int32), ("fine_steps", C.c_int32), ("coarse_steps", C.c_int32),
+                ("ac", C.c_double), ("an", C.c_double), ("D", C.c_double), ("O", C.c_double),
+                ("minv", C.c_double), ("rel_tol", C.c_double), ("cap", C.c_int64),
+                ("rows", C.c_int32), ("cluster", C.c_int32), ("threads", C.c_int32),
+                ("tile_rows", C.c_int32), ("tile_cols", C.c_int32), ("tile_cluster", C.c_int32),
+                ("tile_warps", C.c_int32)]
 
 
 class RunStatsC(C.Structure):
@@ -95,6 +109,7 @@ EXPORTS = [
     "pit_fine_source_device",
     "pit_sync_status", "pit_pitsbicg_solve_device",
     "pit_seeded_uniform", "pit_seeded_normal", "pit_measure_fp64_peak",
+    "pit_step_coefficients_2d", "pit_coarse_iterations",
 ]
 
 _lib = None
@@ -147,6 +162,8 @@ def lib():
     L.pit_pitsbicg_solve_device.argtypes = [vp, C.POINTER(SolverConfigC), vp, vp,
                                             C.POINTER(RecordC), C.c_int, C.POINTER(SolveInfoC), vp]
     L.pit_measure_fp64_peak.argtypes = [C.c_int, _dp]
+    L.pit_step_coefficients_2d.argtypes = [C.POINTER(ProblemDesc), C.POINTER(StepCoeffs2DC)]
+    L.pit_coarse_iterations.argtypes = [vp, C.POINTER(C.c_int64)]
     L.pit_seeded_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]
     L.pit_seeded_uniform.restype = None
     L.pit_seeded_normal.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]

@@ -141,6 +141,79 @@ class Problem1D:
         return d, keep
 
 
+@dataclass
+class Problem2D:
+    """A 2D problem (config 5): dy/dt = -A y on the square [lo, hi]^2 with m
+    interior points per axis (h = (hi-lo)/(m+1)), A the isotropic 5-point
+    operator (centre band_diag, each neighbour band_off) — the reference's
+    2D assemble_spatial_operator with zero velocity (src/pde.cpp:66-100).
+    Fine propagator: explicit Euler (fine_steps per slab); coarse: backward
+    Euler (coarse_steps per slab) solved by Jacobi-PCG to coarse_tolerance
+    (the reference's solve_cg control flow, src/sparse.cpp:60-114).  Blocks
+    hold m*m values, x fastest (SpatialGrid::flat_index)."""
+    m: int
+    band_off: float
+    band_diag: float
+    N: int
+    T: float
+    fine_steps: int
+    coarse_steps: int
+    y0: np.ndarray
+    grid_lo: float = 0.0
+    grid_hi: float = 1.0
+    coarse_tolerance: float = 1e-12
+    coarse_max_iterations: int = 0
+    source: Optional[SeparableSource] = None  # always None in 2D
+
+    @property
+    def M(self) -> int:
+        return self.m * self.m
+
+    @property
+    def spacing(self) -> float:
+        return (self.grid_hi - self.grid_lo) / (self.m + 2 - 1)
+
+    def coords(self) -> np.ndarray:
+        h = self.spacing
+        return np.array([self.grid_lo + (k + 1) * h for k in range(self.m)])
+
+    def desc(self, device: int = 0, fine_layout=None, coarse_layout=None):
+        d = _lib.ProblemDesc()
+        d.dimension = 2
+        d.interior = self.m
+        d.grid_lo, d.grid_hi = self.grid_lo, self.grid_hi
+        d.band_lo, d.band_diag, d.band_up = self.band_off, self.band_diag, self.band_off
+        d.slab_count = self.N
+        d.total_time = self.T
+        d.fine_steps, d.coarse_steps = self.fine_steps, self.coarse_steps
+        y0 = np.ascontiguousarray(self.y0, dtype=np.float64).reshape(-1)
+        keep = [y0]
+        d.initial_value = dptr(y0)
+        d.device = device
+        d.fine_scheme = _lib.PIT_SCHEME_EXPLICIT_EULER
+        d.coarse_tolerance = self.coarse_tolerance
+        d.coarse_max_iterations = self.coarse_max_iterations
+        if fine_layout:  # (tile rows, tile cols, CTAs per cluster, warps per CTA)
+            d.tile_rows, d.tile_cols, d.tile_cluster, d.tile_warps = tuple(fine_layout)
+        return d, keep
+
+
+def heat_2d_bands(diffusion: float, h: float):
+    """(neighbour, centre) of the 2D 5-point -mu*Laplacian, as
+    assemble_spatial_operator's 2D branch builds them (src/pde.cpp:66-100:
+    centre 4*mu/h^2 + r, neighbours -mu/h^2; zero velocity, r = 0)."""
+    mu_h2 = diffusion / (h * h)
+    return -mu_h2, 4.0 * mu_h2
+
+
+def step_coefficients_2d(problem: "Problem2D", fine_layout=None):
+    """Host-side 2D coefficient struct (no GPU needed)."""
+    d, keep = problem.desc(0, fine_layout)
+    c = _lib.StepCoeffs2DC()
+    _check(_lib.lib().pit_step_coefficients_2d(C.byref(d), C.byref(c)))
+    return c
+
+
 def _layout4(lay):
     lay = tuple(lay)
     if len(lay) == 2:
@@ -280,7 +353,7 @@ class BlockOperatorContext:
     """pit::BlockOperatorContext (include/pit/block_system.hpp:55-72): the
     partition, both propagators and the initial value, resident on one GPU."""
 
-    def __init__(self, problem: Problem1D, device: int = 0, fine_layout=None,
+    def __init__(self, problem, device: int = 0, fine_layout=None,
                  coarse_layout=None):
         self.problem = problem
         d, keep = problem.desc(device, fine_layout, coarse_layout)
@@ -314,6 +387,12 @@ class BlockOperatorContext:
 
     def block_count(self) -> int:
         return self.N
+
+    def coarse_iterations(self) -> int:
+        """Cumulative inner CG iterations of the 2D coarse sweeps (0 in 1D)."""
+        v = C.c_int64()
+        _check(_lib.lib().pit_coarse_iterations(self._h, C.byref(v)))
+        return v.value
 
     def zero_vector(self) -> np.ndarray:
         return np.zeros((self.N, self.M))

@@ -23,6 +23,7 @@
 #include "coeffs.h"
 #include "pit_b200.h"
 #include "pit_kernels.cuh"
+#include "pit_kernels2d.cuh"
 
 using namespace pitb;
 
@@ -72,6 +73,11 @@ struct pit_context {
   int M = 0, N = 0;
   double h = 0, weight = 0;
   bool has_source = false;
+  // 2D (config 5): m points per axis, M = m*m
+  int dim = 1, m = 0;
+  pit_step_coeffs_2d c2{};
+  Layout2D lay2{};
+  long long* d_cg_iters = nullptr;
   Role role[2];
   double* d_shape = nullptr;
   double* d_y0 = nullptr;
@@ -102,8 +108,28 @@ namespace {
 
 int validate_desc(const pit_problem_desc* d) {
   if (!d) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: null description");
-  if (d->dimension != 1)
-    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: only dimension 1 is supported");
+  if (d->dimension != 1 && d->dimension != 2)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "SpatialGrid: dimension must be 1 or 2");
+  if (d->dimension == 1 && d->fine_scheme != PIT_SCHEME_BACKWARD_EULER)
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_create: 1D fine propagators are backward Euler");
+  if (d->dimension == 2) {
+    if (d->fine_scheme != PIT_SCHEME_EXPLICIT_EULER)
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: 2D fine propagators are explicit Euler "
+                     "(implicit 2D fine steps are not implemented)");
+    if (d->band_lo != d->band_up)
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: 2D operators are the isotropic 5-point stencil "
+                     "(band_lo == band_up)");
+    if (d->source_kind != PIT_SOURCE_NONE)
+      return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: no sources in 2D");
+    if (d->interior > 256)
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: 2D grids up to 256 interior points per axis");
+    if (d->coarse_tolerance < 0.0)
+      return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: negative coarse tolerance");
+  }
   if (d->interior < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "SpatialGrid: points_per_axis must be >= 3");
   if (!(d->grid_hi > d->grid_lo)) return set_err(PIT_ERR_INVALID_ARGUMENT, "SpatialGrid: empty extent");
@@ -122,6 +148,64 @@ int validate_desc(const pit_problem_desc* d) {
 double grid_spacing(const pit_problem_desc* d) {
   // SpatialGrid: spacing = (hi - lo) / (points_per_axis - 1), points = M + 2 (grid.cpp:19)
   return (d->grid_hi - d->grid_lo) / static_cast<double>(d->interior + 2 - 1);
+}
+
+// 2D coefficients (pit_step_coeffs_2d); K4 layout and K5 decomposition.
+int coeffs_2d(const pit_problem_desc* d, pit_step_coeffs_2d* c) {
+  const int m = d->interior;
+  const double slab = d->total_time / d->slab_count;
+  const double dtf = slab / d->fine_steps;  // Propagator::internal_dt
+  const double dtc = slab / d->coarse_steps;
+  const double off = d->band_lo, diag = d->band_diag;
+  *c = pit_step_coeffs_2d{};
+  c->m = m;
+  c->fine_steps = d->fine_steps;
+  c->coarse_steps = d->coarse_steps;
+  c->an = (double)(-(long double)dtf * (long double)off);
+  c->ac = (double)(1.0L - (long double)dtf * (long double)diag);
+  c->O = off * dtc;         // ImplicitStepSolver: val *= dt      (pde.cpp:107)
+  c->D = diag * dtc + 1.0;  //                     diagonal += 1   (pde.cpp:108)
+  c->minv = c->D != 0.0 ? 1.0 / c->D : 1.0;  // jacobi_inverse_diagonal (sparse.cpp:43-50)
+  c->rel_tol = d->coarse_tolerance > 0.0 ? d->coarse_tolerance : 1e-12;
+  c->cap = d->coarse_max_iterations > 0 ? d->coarse_max_iterations : 10LL * m * m;
+  c->rows = kCgRowsMax;
+  c->cluster = (m + c->rows - 1) / c->rows;
+  c->rows = (m + c->cluster - 1) / c->cluster;
+  c->threads = 32 * ((m + 31) / 32);
+  Layout2D L{d->tile_rows, d->tile_cols, d->tile_cluster, d->tile_warps};
+  if (L.tr == 0) L = auto_layout_2d(m);
+  if (L.tr == 0 || !layout2d_supported(L.tr, L.tc, L.cl, L.warps) || 32 * L.tc < m ||
+      L.cl * L.warps * L.tr < m)
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_create: no compiled 2D tile layout covers m=" + std::to_string(m));
+  c->tile_rows = L.tr;
+  c->tile_cols = L.tc;
+  c->tile_cluster = L.cl;
+  c->tile_warps = L.warps;
+  return PIT_OK;
+}
+
+Ex2Params ex2_params(const pit_context* ctx) {
+  Ex2Params P{};
+  P.m = ctx->m;
+  P.steps = ctx->c2.fine_steps;
+  P.ac = ctx->c2.ac;
+  P.an = ctx->c2.an;
+  return P;
+}
+
+Cg2Params cg2_params(const pit_context* ctx) {
+  Cg2Params P{};
+  P.m = ctx->m;
+  P.steps = ctx->c2.coarse_steps;
+  P.rows = ctx->c2.rows;
+  P.cluster = ctx->c2.cluster;
+  P.D = ctx->c2.D;
+  P.O = ctx->c2.O;
+  P.minv = ctx->c2.minv;
+  P.rel_tol = ctx->c2.rel_tol;
+  P.cap = ctx->c2.cap;
+  return P;
 }
 
 int role_coeffs(const pit_problem_desc* d, int role, pit_step_coeffs* c, std::vector<double>* zc,
@@ -200,7 +284,11 @@ int check_status(pit_context* ctx, bool fine_batch) {
     CUDA_TRY(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(int), cudaMemcpyHostToDevice,
                              ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    const std::string what = "implicit step produced non-finite values";
+    const std::string what =
+        ctx->dim == 2 && !fine_batch
+            ? "implicit step solve did not converge (CG true residual above tolerance at the "
+              "iteration cap) or produced non-finite values"
+            : "implicit step produced non-finite values";
     if (fine_batch)
       return set_err(PIT_ERR_SLAB, "slab " + std::to_string(bad) + ": " + what, bad);
     return set_err(PIT_ERR_INNER_SOLVE, what, bad);
@@ -273,6 +361,10 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
     A.out = out;
     A.slab0 = first - 1;
   }
+  if (ctx->dim == 2) {
+    CUDA_TRY(launch_explicit2d(ctx->lay2, ex2_params(ctx), A, ctas, st));
+    return PIT_OK;
+  }
   A.stagger = ctx->stagger;
   A.stagger_mod = ctx->stagger_mod;
   A.sms = ctx->sms;
@@ -286,10 +378,37 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
   return PIT_OK;
 }
 
+// One sequential sweep launch (SweepArgs semantics) for either dimension.
+int launch_sweep_any(pit_context* ctx, int role, bool src, const SweepArgs& A, cudaStream_t st) {
+  if (ctx->dim == 1) {
+    Role& R = ctx->role[role];
+    CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, st));
+    return PIT_OK;
+  }
+  if (role == PIT_COARSE) {
+    CUDA_TRY(launch_cg_sweep2d(cg2_params(ctx), A, ctx->d_cg_iters, st));
+    return PIT_OK;
+  }
+  // 2D fine sweep (sequential_fine_solve, Propagator::propagate): one K4
+  // cluster launch per slab, chained through W
+  if (A.V) return set_err(PIT_ERR_INVALID_ARGUMENT, "internal: fine sweep with an added vector");
+  const size_t M = ctx->M;
+  for (int s = 0; s < A.count; ++s) {
+    SlabArgs S{};
+    S.in = s == 0 ? A.start : A.W + (size_t)(s - 1) * M;
+    S.in_shift = 0;
+    S.out = A.W + (size_t)s * M;
+    S.mode = kPropagate;
+    S.slab0 = A.slab0 + s;
+    S.status = A.status;
+    CUDA_TRY(launch_explicit2d(ctx->lay2, ex2_params(ctx), S, 1, st));
+  }
+  return PIT_OK;
+}
+
 // Sequential sweep over output blocks [first, first+count): W_first-1 = W_prev.
 int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, const double* W_prev,
               double* W, int first, int count, bool add_v, cudaStream_t st) {
-  Role& R = ctx->role[role];
   const size_t M = ctx->M;
   SweepArgs A{};
   A.status = ctx->d_status;
@@ -311,8 +430,7 @@ int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, con
     A.slab0 = first - 1;
   }
   const bool src = with_source && ctx->has_source;
-  CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, st));
-  return PIT_OK;
+  return launch_sweep_any(ctx, role, src, A, st);
 }
 
 // Sum per-block partials (np per block, component k) in slab order.
@@ -357,6 +475,7 @@ int pit_device_count(void) {
 
 int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out) {
   PIT_TRY(validate_desc(desc));
+  if (desc->dimension != 1) return set_err(PIT_ERR_INVALID_ARGUMENT, "not a 1D description");
   std::vector<double> zc, ppos, qpos, zt;
   Layout lay;
   return role_coeffs(desc, role, out, &zc, &lay, &ppos, &qpos, &zt);
@@ -399,17 +518,29 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
   ctx->desc = *desc;
   ctx->desc.source_shape = nullptr;
   ctx->desc.initial_value = nullptr;
-  ctx->M = desc->interior;
+  ctx->dim = desc->dimension;
+  ctx->m = desc->interior;
+  ctx->M = ctx->dim == 2 ? ctx->m * ctx->m : ctx->m;
   ctx->N = desc->slab_count;
   ctx->h = grid_spacing(desc);
-  ctx->weight = ctx->h;  // inner_product weight h^d, d = 1 (grid.cpp:113-114)
+  // inner_product weight h^d (grid.cpp:113-114)
+  ctx->weight = ctx->dim == 2 ? ctx->h * ctx->h : ctx->h;
   ctx->has_source = desc->source_kind == PIT_SOURCE_SEPARABLE;
   ctx->y0.assign(desc->initial_value, desc->initial_value + ctx->M);
   auto fail = [&](int rc) {
     pit_context_destroy(ctx);
     return rc;
   };
-  for (int r = 0; r < 2; ++r) {
+  if (ctx->dim == 2) {
+    int rc = coeffs_2d(desc, &ctx->c2);
+    if (rc) return fail(rc);
+    ctx->lay2 = Layout2D{ctx->c2.tile_rows, ctx->c2.tile_cols, ctx->c2.tile_cluster,
+                         ctx->c2.tile_warps};
+    if (cudaMalloc(&ctx->d_cg_iters, sizeof(long long)) != cudaSuccess ||
+        cudaMemset(ctx->d_cg_iters, 0, sizeof(long long)) != cudaSuccess)
+      return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+  }
+  for (int r = 0; r < (ctx->dim == 1 ? 2 : 0); ++r) {
     std::vector<double> zc, ppos, qpos, zt;
     Layout lay;
     int rc = role_coeffs(desc, r, &ctx->role[r].c, &zc, &lay, &ppos, &qpos, &zt);
@@ -511,9 +642,29 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_state);
   cudaFree(ctx->d_sched);
   cudaFree(ctx->d_trace);
+  cudaFree(ctx->d_cg_iters);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PIT_OK;
+}
+
+int pit_coarse_iterations(const pit_context* ctx, int64_t* out) {
+  if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "null argument");
+  *out = 0;
+  if (ctx->d_cg_iters) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    long long v = 0;
+    CUDA_TRY(cudaMemcpy(&v, ctx->d_cg_iters, sizeof(long long), cudaMemcpyDeviceToHost));
+    *out = v;
+  }
+  return PIT_OK;
+}
+
+int pit_step_coefficients_2d(const pit_problem_desc* desc, pit_step_coeffs_2d* out) {
+  PIT_TRY(validate_desc(desc));
+  if (!out) return set_err(PIT_ERR_INVALID_ARGUMENT, "null output");
+  if (desc->dimension != 2) return set_err(PIT_ERR_INVALID_ARGUMENT, "not a 2D description");
+  return coeffs_2d(desc, out);
 }
 
 int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing) {
@@ -837,7 +988,6 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
   PIT_TRY(to_device(ctx, in, M, &di));
   if (!in) CUDA_TRY(cudaMemsetAsync(di.p, 0, M * sizeof(double), ctx->stream));
   PIT_TRY(to_device(ctx, nullptr, M, &dout));
-  Role& R = ctx->role[role];
   SweepArgs A{};
   A.start = di.p;
   A.W = dout.p;
@@ -849,7 +999,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
     // source_contribution with f == 0 is exactly zero (propagator.cpp:78)
     CUDA_TRY(cudaMemsetAsync(dout.p, 0, M * sizeof(double), ctx->stream));
   } else {
-    CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, ctx->stream));
+    PIT_TRY(launch_sweep_any(ctx, role, src, A, ctx->stream));
     PIT_TRY(check_status(ctx, false));
   }
   return to_host(ctx, dout.p, M, out);

@@ -1,0 +1,596 @@
+// pit_kernels2d.cu — config 5 (2D heat) kernels.  DESIGN.md §3b.
+//
+// K4 explicit2d_kernel: one thread-block cluster per slab holds the m x m
+//   state in registers (TR x TC tile per thread) across all fine steps.
+//   West/east neighbours come from the adjacent lanes (warp shuffles; a warp
+//   spans the full row width, so lanes 0/31 sit on the Dirichlet boundary);
+//   north/south neighbours of a tile's first/last row come from the warp
+//   above/below through shared memory, and across CTAs through distributed
+//   shared memory.  One cluster barrier per step, split arrive/wait: the
+//   tile's interior rows are updated between the arrive of step k-1 and the
+//   wait of step k, hiding the barrier latency.
+// K5 cg_sweep2d_kernel: one persistent cluster runs the sequential coarse
+//   sweep; each slab's backward-Euler step is a Jacobi-PCG solve with the
+//   control flow of the reference's solve_cg (src/sparse.cpp:60-114): exit
+//   on res <= tol, true-residual confirmation, restart, stall and cap.
+//   Reductions: per-thread fma chain over its column strip, warp butterfly,
+//   one slot per warp in every CTA of the cluster (DSMEM stores), a cluster
+//   barrier, then every thread sums the slots in the same fixed order.
+// Every operation order here is mirrored by oracle/pit_oracle2d.c.
+#include "pit_kernels2d.cuh"
+
+#include <cooperative_groups.h>
+
+#include <cmath>
+
+namespace cg = cooperative_groups;
+
+namespace pitb {
+namespace {
+
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+  cl_arrive();
+  cl_wait();
+}
+
+// y' = fma(ac, y, an * ((w + e) + (n + s)))
+__device__ __forceinline__ double ex_point(double ac, double an, double y, double w, double e,
+                                           double n, double s) {
+  return fma(ac, y, an * ((w + e) + (n + s)));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 16 bytes into a peer CTA's shared memory; completion counted on the
+// peer's mbarrier (no fence or barrier on the sending side)
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+          raddr),
+      "d"(a), "d"(b), "r"(rbar)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_async_1(uint32_t raddr, double a, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(
+                   raddr),
+               "d"(a), "r"(rbar)
+               : "memory");
+}
+// TC doubles of a tile row into a peer's row buffer
+template <int TC>
+__device__ __forceinline__ void send_row(uint32_t raddr, const double (&v)[TC], uint32_t rbar) {
+  if constexpr (TC % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < TC; j += 2) st_async_v2(raddr + 8 * j, v[j], v[j + 1], rbar);
+  } else {
+#pragma unroll
+    for (int j = 0; j < TC; ++j) st_async_1(raddr + 8 * j, v[j], rbar);
+  }
+}
+
+template <int TR, int TC, int CL, int WARPS>
+struct Tile2 {
+  static_assert(TR >= 2, "tile needs a first and a last row");
+  static constexpr int T = 32 * WARPS;
+  static constexpr int NC = 32 * TC;       // columns covered by a warp row
+  static constexpr int ROWS = WARPS * TR;  // rows per CTA
+  // top[2][WARPS+1][NC], bot[2][WARPS+1][NC], then 2 mbarriers
+  static constexpr size_t smem = sizeof(double) * 4 * (WARPS + 1) * NC + 2 * sizeof(uint64_t);
+};
+
+// K4.  Per step k (state y^k in registers, halo rows of y^k in buffer k&1):
+//   wait for the halo rows of y^k (warps above/below: __syncthreads; CTAs
+//   above/below: the mbarrier their st.async stores complete), compute the
+//   tile's first and last rows of y^{k+1}, publish them (local stores, and
+//   st.async into the neighbour CTA's buffer (k+1)&1), then the interior rows
+//   while those stores fly.  Buffer (k+1)&1 was last read at step k-1; every
+//   reader finished before its own publish of y^k, which the writer waited
+//   for — no cluster barrier inside the step loop.
+template <int TR, int TC, int CL, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, 1)
+    explicit2d_kernel(const __grid_constant__ Ex2Params P, const __grid_constant__ SlabArgs A) {
+  using S = Tile2<TR, TC, CL, WARPS>;
+  extern __shared__ __align__(16) double sm2[];
+  // top(par, w): first row of warp w's tiles (w == WARPS: CTA below's warp 0)
+  // bot(par, w): last row of warp w-1's tiles (w == 0: CTA above's last warp)
+  double* const top = sm2;
+  double* const bot = sm2 + 2 * (WARPS + 1) * S::NC;
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(sm2 + 4 * (WARPS + 1) * S::NC);
+  auto TOP = [&](int par, int w) { return top + ((size_t)par * (WARPS + 1) + w) * S::NC; };
+  auto BOT = [&](int par, int w) { return bot + ((size_t)par * (WARPS + 1) + w) * S::NC; };
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  const int b = blockIdx.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = P.m;
+  const double ac = P.ac, an = P.an;
+  const int row0 = c * S::ROWS + warp * TR;
+  const int col0 = lane * TC;
+  const bool ghosts = (CL * S::ROWS > m) || (S::NC > m);
+  // halo bytes this CTA receives per step
+  const unsigned rx_bytes = (unsigned)sizeof(double) * S::NC * ((c > 0) + (c < CL - 1));
+
+  for (int i = tid; i < 4 * (WARPS + 1) * S::NC; i += S::T) sm2[i] = 0.0;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+
+  const double* src;
+  if (b + A.in_shift >= 0)
+    src = A.in ? A.in + (size_t)(b + A.in_shift) * m * m : nullptr;
+  else
+    src = A.halo;
+  double y[TR][TC];
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) {
+      const int r = row0 + i, q = col0 + j;
+      y[i][j] = (src && r < m && q < m) ? src[(size_t)r * m + q] : 0.0;
+    }
+  // peer addresses (shared::cluster): CTA c-1's TOP(par, WARPS) and mbarriers,
+  // CTA c+1's BOT(par, 0) and mbarriers; parity 1 is kPar doubles further
+  constexpr uint32_t kParBytes = (uint32_t)(sizeof(double) * (WARPS + 1) * S::NC);
+  const uint32_t up_top = c > 0 ? mapa_u32(smem_u32(TOP(0, WARPS) + col0), c - 1) : 0u;
+  const uint32_t up_bar = c > 0 ? mapa_u32(smem_u32(&mbar[0]), c - 1) : 0u;
+  const uint32_t dn_bot = c < CL - 1 ? mapa_u32(smem_u32(BOT(0, 0) + col0), c + 1) : 0u;
+  const uint32_t dn_bar = c < CL - 1 ? mapa_u32(smem_u32(&mbar[0]), c + 1) : 0u;
+  cl_sync();  // zeroed buffers and initialised mbarriers cluster-wide
+
+  auto publish = [&](int par, bool remote) {
+    double* t0 = TOP(par, warp) + col0;
+    double* b0 = BOT(par, warp + 1) + col0;
+#pragma unroll
+    for (int j = 0; j < TC; ++j) {
+      t0[j] = y[0][j];
+      b0[j] = y[TR - 1][j];
+    }
+    if (!remote) return;
+    if (warp == 0 && c > 0) send_row<TC>(up_top + par * kParBytes, y[0], up_bar + 8 * par);
+    if (warp == WARPS - 1 && c < CL - 1)
+      send_row<TC>(dn_bot + par * kParBytes, y[TR - 1], dn_bar + 8 * par);
+  };
+  if (tid == 0) mbar_arrive_expect_tx(&mbar[0], rx_bytes);
+  publish(0, true);
+
+  for (int k = 0; k < P.steps; ++k) {
+    const int par = k & 1;
+    const bool more = k + 1 < P.steps;  // y^{k+1} halos are consumed
+    if (tid == 0 && more) mbar_arrive_expect_tx(&mbar[par ^ 1], rx_bytes);
+    double Wv[TR], Ev[TR];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) {
+      const double w = __shfl_up_sync(kFull, y[i][TC - 1], 1);
+      const double e = __shfl_down_sync(kFull, y[i][0], 1);
+      Wv[i] = lane == 0 ? 0.0 : w;
+      Ev[i] = lane == 31 ? 0.0 : e;
+    }
+    __syncthreads();  // halo rows of y^k from the warps above/below
+    if ((warp == 0 && c > 0) || (warp == WARPS - 1 && c < CL - 1)) mbar_wait(&mbar[par], (k >> 1) & 1);
+    double o0[TC], o1[TC], oA[TC], oB[TC];  // old rows 0, 1, TR-2, TR-1
+#pragma unroll
+    for (int j = 0; j < TC; ++j) {
+      o0[j] = y[0][j];
+      o1[j] = y[1][j];
+      oA[j] = y[TR - 2][j];
+      oB[j] = y[TR - 1][j];
+    }
+    {
+      const double* nb = BOT(par, warp) + col0;
+      const double* sb = TOP(par, warp + 1) + col0;
+#pragma unroll
+      for (int j = 0; j < TC; ++j)
+        y[0][j] = ex_point(ac, an, o0[j], j > 0 ? o0[j - 1] : Wv[0],
+                           j < TC - 1 ? o0[j + 1] : Ev[0], nb[j], o1[j]);
+#pragma unroll
+      for (int j = 0; j < TC; ++j)
+        y[TR - 1][j] = ex_point(ac, an, oB[j], j > 0 ? oB[j - 1] : Wv[TR - 1],
+                                j < TC - 1 ? oB[j + 1] : Ev[TR - 1], oA[j], sb[j]);
+    }
+    if (ghosts) {
+#pragma unroll
+      for (int j = 0; j < TC; ++j) {
+        if (row0 >= m || col0 + j >= m) y[0][j] = 0.0;
+        if (row0 + TR - 1 >= m || col0 + j >= m) y[TR - 1][j] = 0.0;
+      }
+    }
+    publish(par ^ 1, more);
+    // interior rows 1..TR-2 of y^{k+1} (rows 0 and TR-1 of y^k: o0, oB)
+    {
+      double prev[TC];
+#pragma unroll
+      for (int j = 0; j < TC; ++j) prev[j] = o0[j];
+#pragma unroll
+      for (int i = 1; i < TR - 1; ++i) {
+        double cur[TC];
+#pragma unroll
+        for (int j = 0; j < TC; ++j) cur[j] = y[i][j];
+#pragma unroll
+        for (int j = 0; j < TC; ++j)
+          y[i][j] = ex_point(ac, an, cur[j], j > 0 ? cur[j - 1] : Wv[i],
+                             j < TC - 1 ? cur[j + 1] : Ev[i], prev[j],
+                             i + 1 < TR - 1 ? y[i + 1][j] : oB[j]);
+#pragma unroll
+        for (int j = 0; j < TC; ++j) prev[j] = cur[j];
+      }
+    }
+    if (ghosts) {
+#pragma unroll
+      for (int i = 1; i < TR - 1; ++i)
+#pragma unroll
+        for (int j = 0; j < TC; ++j)
+          if (row0 + i >= m || col0 + j >= m) y[i][j] = 0.0;
+    }
+  }
+  cl_sync();  // no CTA leaves while a peer may still address its buffers
+
+  const int slab = A.slab0 + b;
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) fin = fin && isfinite(y[i][j]);
+  if (!__all_sync(kFull, fin) && lane == 0) atomicMin(A.status, slab);
+  const size_t off = (size_t)b * m * m;
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) {
+      const int r = row0 + i, q = col0 + j;
+      if (r < m && q < m) {
+        const size_t g = off + (size_t)r * m + q;
+        if (A.mode == kApplyF) {
+          A.out[g] = A.Lsub[g] - y[i][j];
+        } else if (A.mode == kResidual) {
+          const double a = A.Lsub[g] - y[i][j];
+          A.out[g] = A.rhs[g] - a;
+        } else {
+          A.out[g] = y[i][j];
+        }
+      }
+    }
+  if (blockIdx.x == 0 && A.out0 != nullptr) {
+    const int n = m * m;
+    if (A.mode == kApplyF) {
+      for (int i = tid; i < n; i += S::T) A.out0[i] = A.L0[i];
+    } else if (A.mode == kResidual) {
+      for (int i = tid; i < n; i += S::T) A.out0[i] = A.rhs0[i] - A.L0[i];
+    }
+  }
+}
+
+template <class K>
+cudaError_t launch_clustered(K kernel, int grid, int block, size_t smem, int cluster,
+                             cudaStream_t st, const void* p0, const void* p1) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return e;
+  if (cluster > 8 &&
+      (e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+          cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[2] = {const_cast<void*>(p0), const_cast<void*>(p1)};
+  return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(kernel), args);
+}
+
+// ---------------------------------------------------------------------------
+// K5
+// ---------------------------------------------------------------------------
+
+constexpr int kSlotCap = 128;  // warps per cluster: 16 CTAs x 8 warps
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(kFull, v, off);
+  return v;
+}
+
+// (S f)_k = fma(D, f, O*((w + e) + (n + s))) from the stencil buffer
+__device__ __forceinline__ double stencil_S(const double* Ps, int pitch, int k, int t, double D,
+                                            double O) {
+  const double* row = Ps + (size_t)(k + 1) * pitch + t + 1;
+  const double w = row[-1], e = row[1], n = row[-pitch], s = row[pitch];
+  return fma(D, row[0], O * ((w + e) + (n + s)));
+}
+
+__global__ void __launch_bounds__(256, 1)
+    cg_sweep2d_kernel(const __grid_constant__ Cg2Params P, const __grid_constant__ SweepArgs A,
+                      long long* iters) {
+  constexpr int RM = kCgRowsMax;
+  extern __shared__ __align__(16) double smc[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  const int C = P.cluster;
+  const int NT = blockDim.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int W = NT >> 5;
+  const int nslot = C * W;
+  const int m = P.m, R = P.rows;
+  const int pitch = NT + 2;
+  double* const Ps = smc;                         // [(RM+2)][pitch], own rows 1..R
+  double* const red = smc + (size_t)(RM + 2) * pitch;  // [4][kSlotCap]
+  const double D = P.D, O = P.O, minv = P.minv;
+
+  for (int i = t; i < (RM + 2) * pitch + 4 * kSlotCap; i += NT) smc[i] = 0.0;
+
+  bool valid[RM];
+#pragma unroll
+  for (int k = 0; k < RM; ++k) valid[k] = t < m && k < R && c * R + k < m;
+  auto gidx = [&](int k) { return (size_t)(c * R + k) * m + t; };
+
+  double* const red_to = cl.map_shared_rank(red, lane < C ? lane : 0);
+  double* const halo_up = c > 0 ? cl.map_shared_rank(Ps + (size_t)(R + 1) * pitch, c - 1) : nullptr;
+  double* const halo_dn = c < C - 1 ? cl.map_shared_rank(Ps, c + 1) : nullptr;
+
+  int pair = 0;
+  // cluster-wide sums of a and b (identical bits in every thread)
+  auto reduce2 = [&](double a, double b, double& ra, double& rb) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane < C) {
+      red_to[(2 * pair) * kSlotCap + c * W + warp] = a;
+      red_to[(2 * pair + 1) * kSlotCap + c * W + warp] = b;
+    }
+    cl_sync();
+    double u = 0.0, v = 0.0;
+    for (int i = lane; i < nslot; i += 32) {
+      u = u + red[(2 * pair) * kSlotCap + i];
+      v = v + red[(2 * pair + 1) * kSlotCap + i];
+    }
+    ra = warp_sum(u);
+    rb = warp_sum(v);
+    pair ^= 1;
+  };
+
+  // field value v at own row k into the stencil buffer (+ neighbours' halos)
+  auto put = [&](int k, double v) {
+    if (k < R) Ps[(size_t)(k + 1) * pitch + t + 1] = v;
+    if (k == 0 && halo_up) halo_up[t + 1] = v;
+    if (k == R - 1 && halo_dn) halo_dn[t + 1] = v;
+  };
+  auto own = [&](int k) { return k < R ? Ps[(size_t)(k + 1) * pitch + t + 1] : 0.0; };
+
+  double x[RM], r[RM], bb[RM], q[RM];
+#pragma unroll
+  for (int k = 0; k < RM; ++k) bb[k] = valid[k] ? A.start[gidx(k)] : 0.0;
+  cl_sync();
+
+  long long total_it = 0;
+  for (int s = 0; s < A.count; ++s) {
+    const int slab = A.slab0 + s;
+    bool ok = true;
+    for (int cs = 0; cs < P.steps && ok; ++cs) {
+    if (cs > 0) {
+#pragma unroll
+      for (int k = 0; k < RM; ++k) bb[k] = x[k];
+    }
+#pragma unroll
+    for (int k = 0; k < RM; ++k) x[k] = 0.0;
+    double nb2, dummy;
+    {
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < RM; ++k) a = fma(bb[k], bb[k], a);
+      reduce2(a, 0.0, nb2, dummy);
+    }
+    const double nb = sqrt(nb2);
+    if (nb != 0.0) {
+      const double tol = P.rel_tol * nb;
+      double rz, rr;
+      {
+        double a = 0.0, b2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < RM; ++k) {
+          r[k] = bb[k];
+          const double z = minv * r[k];  // p = z
+          put(k, z);
+          a = fma(r[k], z, a);
+          b2 = fma(r[k], r[k], b2);
+        }
+        reduce2(a, b2, rz, rr);
+      }
+      double res = sqrt(rr);
+      long long it = 0;
+      bool stalled = false;
+      for (;;) {
+        while (res > tol && it < P.cap && !stalled) {
+          double pq, d0;
+          {
+            double a = 0.0;
+#pragma unroll
+            for (int k = 0; k < RM; ++k) {
+              q[k] = valid[k] ? stencil_S(Ps, pitch, k, t, D, O) : 0.0;
+              a = fma(own(k), q[k], a);
+            }
+            reduce2(a, 0.0, pq, d0);
+          }
+          if (pq == 0.0 || !isfinite(pq)) {
+            stalled = true;
+            break;
+          }
+          const double alpha = rz / pq;
+          double rzn;
+          {
+            double a = 0.0, b2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < RM; ++k) {
+              x[k] = fma(alpha, own(k), x[k]);
+              r[k] = fma(-alpha, q[k], r[k]);
+              const double z = minv * r[k];
+              a = fma(r[k], r[k], a);
+              b2 = fma(r[k], z, b2);
+            }
+            ++it;
+            reduce2(a, b2, rr, rzn);
+          }
+          res = sqrt(rr);
+          if (!isfinite(res) || res <= tol) break;
+          const double beta = rzn / rz;
+#pragma unroll
+          for (int k = 0; k < RM; ++k) put(k, fma(beta, own(k), minv * r[k]));
+          rz = rzn;
+          cl_sync();
+        }
+        // confirm against the exact residual (sparse.cpp:101-104)
+#pragma unroll
+        for (int k = 0; k < RM; ++k) put(k, x[k]);
+        cl_sync();
+        {
+          double a = 0.0, b2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < RM; ++k) {
+            r[k] = valid[k] ? bb[k] - stencil_S(Ps, pitch, k, t, D, O) : 0.0;
+            const double z = minv * r[k];
+            a = fma(r[k], r[k], a);
+            b2 = fma(r[k], z, b2);
+          }
+          reduce2(a, b2, rr, rz);
+        }
+        res = sqrt(rr);
+        if (res <= tol) break;
+        if (it >= P.cap || stalled || !isfinite(res)) {
+          ok = false;
+          break;
+        }
+#pragma unroll
+        for (int k = 0; k < RM; ++k) put(k, minv * r[k]);  // restart: p = z
+        cl_sync();
+      }
+      total_it += it;
+    }
+    }  // coarse steps
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < RM; ++k) fin = fin && isfinite(x[k]);
+    // every thread of the cluster must agree on leaving the sweep
+    double bad_l = (ok && fin) ? 0.0 : 1.0, bad_g, d1;
+    reduce2(bad_l, 0.0, bad_g, d1);
+    if (bad_g != 0.0) {
+      if (c == 0 && t == 0) atomicMin(A.status, slab);
+      break;
+    }
+    const double* V = A.V ? A.V + (size_t)s * m * m : nullptr;
+    double* Wb = A.W + (size_t)s * m * m;
+#pragma unroll
+    for (int k = 0; k < RM; ++k) {
+      if (valid[k]) {
+        const double v = V ? x[k] + V[gidx(k)] : x[k];
+        Wb[gidx(k)] = v;
+        bb[k] = v;
+      }
+    }
+  }
+  if (iters && c == 0 && t == 0) atomicAdd(reinterpret_cast<unsigned long long*>(iters),
+                                           (unsigned long long)total_it);
+  cl_sync();
+}
+
+}  // namespace
+
+bool layout2d_supported(int tr, int tc, int cl, int warps) {
+#define X(TR, TC, CL, WW) \
+  if (tr == TR && tc == TC && cl == CL && warps == WW) return true;
+  PIT_LAYOUTS_2D(X)
+#undef X
+  return false;
+}
+
+Layout2D auto_layout_2d(int m) {
+  static const Layout2D order[] = {{2, 1, 2, 8}, {4, 2, 2, 8}, {4, 4, 4, 8}, {8, 8, 4, 8}};
+  for (const auto& L : order)
+    if (32 * L.tc >= m && L.cl * L.warps * L.tr >= m) return L;
+  return {0, 0, 0, 0};
+}
+
+cudaError_t launch_explicit2d(const Layout2D& L, const Ex2Params& P, const SlabArgs& A, int slabs,
+                              cudaStream_t st) {
+  if (slabs <= 0) return cudaSuccess;
+#define X(TR, TC, CL, WW)                                                                   \
+  if (L.tr == TR && L.tc == TC && L.cl == CL && L.warps == WW) {                            \
+    using S = Tile2<TR, TC, CL, WW>;                                                        \
+    return launch_clustered(explicit2d_kernel<TR, TC, CL, WW>, CL * slabs, S::T, S::smem, CL, \
+                            st, &P, &A);                                                    \
+  }
+  PIT_LAYOUTS_2D(X)
+#undef X
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long* iters,
+                              cudaStream_t st) {
+  if (A.count <= 0) return cudaSuccess;
+  const int nt = 32 * ((P.m + 31) / 32);
+  if (nt > 256 || P.rows > kCgRowsMax || P.cluster * (nt / 32) > kSlotCap || P.cluster > 16)
+    return cudaErrorInvalidConfiguration;
+  const size_t smem = sizeof(double) * ((size_t)(kCgRowsMax + 2) * (nt + 2) + 4 * kSlotCap);
+  auto k = cg_sweep2d_kernel;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return e;
+  if (P.cluster > 8 &&
+      (e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+          cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P.cluster, 1, 1);
+  cfg.blockDim = dim3(nt, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P.cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, P, A, iters);
+}
+
+}  // namespace pitb

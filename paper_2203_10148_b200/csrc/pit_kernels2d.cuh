@@ -1,0 +1,59 @@
+// pit_kernels2d.cuh — 2D (config 5) kernels: K4 explicit-Euler fine slabs
+// and K5 coarse backward-Euler sweep with a cluster-resident Jacobi-PCG.
+// DESIGN.md §3b.  Blocks are m x m values, x fastest (flat index j*m + i,
+// SpatialGrid::flat_index, include/pit/grid.hpp), Dirichlet 0 outside.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pit_kernels.cuh"
+
+namespace pitb {
+
+// K4: one thread-block cluster per slab; explicit Euler
+//   y' = fma(ac, y, an * ((yW + yE) + (yN + yS)))
+// ac = 1 - dt*diag, an = -dt*off (5-point operator, band_lo = band_up = off).
+struct Ex2Params {
+  int m;       // points per axis
+  int steps;   // explicit steps per slab
+  double ac, an;
+};
+
+// K5: one persistent cluster; per slab one BE step (I + dt*A) x = b solved
+// by Jacobi-PCG (src/sparse.cpp:60-114 control flow) with
+//   (S p)_i = fma(D, p_i, O * ((pW + pE) + (pN + pS))),  D = 1 + dt*diag,
+//   O = dt*off (ImplicitStepSolver, src/pde.cpp:103-110), minv = 1/D.
+struct Cg2Params {
+  int m;
+  int steps;       // backward-Euler steps per slab
+  int rows;        // rows per CTA (cluster size C = ceil(m / rows))
+  int cluster;     // C
+  double D, O, minv;
+  double rel_tol;  // kInnerSolveRelTol analogue
+  long long cap;   // iteration cap (10 n, pde.hpp:79)
+};
+
+constexpr int kCgRowsMax = 16;
+
+// K4 layouts: rows per thread tile, columns per thread tile, CTAs per
+// cluster, warps per CTA.  Covers m <= 32*TC columns and CL*WARPS*TR rows.
+#define PIT_LAYOUTS_2D(X) \
+  X(8, 8, 4, 8)           \
+  X(8, 8, 8, 4)           \
+  X(4, 4, 4, 8)           \
+  X(4, 2, 2, 8)           \
+  X(2, 1, 2, 8)
+
+struct Layout2D {
+  int tr, tc, cl, warps;
+};
+// smallest compiled K4 layout covering m (tr == 0: none)
+Layout2D auto_layout_2d(int m);
+bool layout2d_supported(int tr, int tc, int cl, int warps);
+
+cudaError_t launch_explicit2d(const Layout2D& L, const Ex2Params& P, const SlabArgs& A, int slabs,
+                              cudaStream_t st);
+cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long* iters,
+                              cudaStream_t st);
+
+}  // namespace pitb

@@ -12,11 +12,16 @@ from paper_2203_10148_b200 import api
 
 
 class OracleProblem:
-    """orc_1d wrapper: propagators mirror the CUDA step (use_thomas=False)
-    or plain Thomas (True); block algebra in MODE_DEVICE or MODE_REFERENCE."""
+    """orc_1d / orc_2d wrapper: propagators mirror the CUDA kernels
+    (use_thomas=False) or plain Thomas (True, 1D); block algebra in
+    MODE_DEVICE or MODE_REFERENCE."""
 
-    def __init__(self, p: api.Problem1D, mode=O.MODE_DEVICE, use_thomas=False, fine_layout=None,
+    def __init__(self, p, mode=O.MODE_DEVICE, use_thomas=False, fine_layout=None,
                  coarse_layout=None):
+        if isinstance(p, api.Problem2D):
+            self._init_2d(p, mode)
+            return
+        self.dim = 1
         fc, _ = api.step_coefficients(p, 0, fine_layout, coarse_layout)
         cc, _ = api.step_coefficients(p, 1, fine_layout, coarse_layout)
         self.p = p
@@ -36,9 +41,28 @@ class OracleProblem:
         assert self.o, "orc_1d_create failed"
         self.prob = self.lib.orc_1d_problem(self.o)
 
+    def _init_2d(self, p, mode):
+        self.dim = 2
+        self.p = p
+        self.lib = O.orc()
+        self._keep = [np.ascontiguousarray(p.y0, dtype=np.float64).reshape(-1)]
+        c = api.step_coefficients_2d(p)
+        self.o = self.lib.orc_2d_create(p.m, p.band_off, p.band_diag, p.N, p.T, p.fine_steps,
+                                        p.coarse_steps, c.rel_tol, c.cap, O.ptr(self._keep[0]),
+                                        mode)
+        assert self.o, "orc_2d_create failed"
+        self.prob = self.lib.orc_2d_problem(self.o)
+        self.coeffs = self.lib.orc_2d_coeffs(self.o).contents
+
+    def coarse_iterations(self):
+        return self.lib.orc_2d_coarse_iterations(self.o) if self.dim == 2 else 0
+
     def close(self):
         if self.o:
-            self.lib.orc_1d_destroy(self.o)
+            if self.dim == 2:
+                self.lib.orc_2d_destroy(self.o)
+            else:
+                self.lib.orc_1d_destroy(self.o)
             self.o = None
 
     def __del__(self):

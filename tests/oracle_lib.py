@@ -48,6 +48,13 @@ class OrcStepper(C.Structure):
                 ("zt", _dp)]
 
 
+class Orc2Coeffs(C.Structure):
+    _fields_ = [("m", C.c_int), ("fine_steps", C.c_int), ("coarse_steps", C.c_int),
+                ("ac", C.c_double), ("an", C.c_double), ("D", C.c_double), ("O", C.c_double),
+                ("minv", C.c_double), ("rel_tol", C.c_double), ("cap", C.c_longlong),
+                ("rows", C.c_int), ("cluster", C.c_int), ("threads", C.c_int)]
+
+
 def ensure_built() -> None:
     if not os.path.exists(ORACLE_SO) or (os.path.isdir("/root/reference/proj") and not os.path.exists(REF_SO)):
         subprocess.run(["make", "-s", "-C", ORACLE_DIR, "-j8"], check=True)
@@ -109,6 +116,23 @@ def orc():
         lib.orc_vec_axpy.argtypes = [C.c_long, C.c_double, _dp, _dp]
         lib.orc_block_partial.restype = C.c_double
         lib.orc_block_partial.argtypes = [C.c_void_p, _dp, _dp]
+        lib.orc2_coefficients.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                          C.c_int, C.c_int, C.c_double, C.c_longlong,
+                                          C.POINTER(Orc2Coeffs)]
+        lib.orc2_explicit_propagate.argtypes = [C.POINTER(Orc2Coeffs), _dp, _dp]
+        lib.orc2_cg_solve.argtypes = [C.POINTER(Orc2Coeffs), _dp, _dp, C.POINTER(C.c_longlong)]
+        lib.orc2_coarse_propagate.argtypes = [C.POINTER(Orc2Coeffs), _dp, _dp,
+                                              C.POINTER(C.c_longlong)]
+        lib.orc_2d_create.restype = C.c_void_p
+        lib.orc_2d_create.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_double,
+                                      C.c_int, C.c_int, C.c_double, C.c_longlong, _dp, C.c_int]
+        lib.orc_2d_destroy.argtypes = [C.c_void_p]
+        lib.orc_2d_problem.restype = C.c_void_p
+        lib.orc_2d_problem.argtypes = [C.c_void_p]
+        lib.orc_2d_coeffs.restype = C.POINTER(Orc2Coeffs)
+        lib.orc_2d_coeffs.argtypes = [C.c_void_p]
+        lib.orc_2d_coarse_iterations.restype = C.c_longlong
+        lib.orc_2d_coarse_iterations.argtypes = [C.c_void_p]
         _orc = lib
     return _orc
 
@@ -129,6 +153,9 @@ def ref():
                                          C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                          C.c_int, C.c_double, C.c_int, C.c_int, _dp, C.c_int, _dp,
                                          C.c_double, C.c_double, C.c_double]
+        lib.pitref_create_2d.restype = C.c_void_p
+        lib.pitref_create_2d.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                         C.c_int, C.c_double, C.c_int, C.c_int, _dp]
         lib.pitref_destroy.argtypes = [C.c_void_p]
         lib.pitref_spacing.restype = C.c_double
         lib.pitref_spacing.argtypes = [C.c_void_p]
