@@ -190,6 +190,12 @@ int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeff
 typedef struct pit_step_coeffs_2d {
   int32_t m, fine_steps, coarse_steps;
   double ac, an;
+  /* scaled form (an a power of two, kappa = ac/an exact): the kernel carries
+   * z = y / an^j and steps z' = fma(kappa, z, (zW + zE) + (zN + zS)), folding
+   * an^R back every R steps and an^(steps mod R) at the end — the same bits
+   * as the unscaled form wherever no value is subnormal */
+  int32_t scaled, R;
+  double kappa, anR, anLast;
   double D, O, minv;
   double rel_tol;
   int64_t cap;

@@ -36,6 +36,30 @@ void orc2_coefficients(int m, double band_off, double band_diag, double total_ti
   c->coarse_steps = coarse_steps;
   c->an = (double)(-(long double)dtf * (long double)band_off);
   c->ac = (double)(1.0L - (long double)dtf * (long double)band_diag);
+  /* scaled form: an = 2^-sh exactly, kappa = ac/an exact (pit_capi.cu
+   * explicit_scaling) */
+  c->scaled = 0;
+  c->R = 1;
+  c->kappa = 0.0;
+  c->anR = c->anLast = 1.0;
+  {
+    int e = 0;
+    const double mant = frexp(c->an, &e);
+    if (c->an > 0.0 && mant == 0.5 && e - 1 < 0) {
+      const double k = c->ac / c->an;
+      const int sh = 1 - e;
+      int r = 768 / sh;
+      if (isfinite(k) && k * c->an == c->ac && r >= 1) {
+        if (r > fine_steps) r = fine_steps;
+        const int j = fine_steps - r * ((fine_steps - 1) / r);
+        c->scaled = 1;
+        c->R = r;
+        c->kappa = k;
+        c->anR = ldexp(1.0, -sh * r);
+        c->anLast = ldexp(1.0, -sh * j);
+      }
+    }
+  }
   c->O = band_off * dtc;          /* v *= dt           (pde.cpp:107) */
   c->D = band_diag * dtc + 1.0;   /* diagonal += 1.0   (pde.cpp:108) */
   c->minv = c->D != 0.0 ? 1.0 / c->D : 1.0;
@@ -54,6 +78,10 @@ void orc2_explicit_propagate(const orc2_coeffs* c, const double* in, double* out
   double* b = (double*)malloc(n * sizeof(double));
   memcpy(a, in, n * sizeof(double));
   for (int k = 0; k < c->fine_steps; ++k) {
+    /* scaled form: z = y / an^j, folded back by anR before every step
+     * k = R, 2R, ... and by anLast after the last step */
+    if (c->scaled && k > 0 && k % c->R == 0)
+      for (size_t i = 0; i < n; ++i) a[i] = a[i] * c->anR;
     for (int r = 0; r < m; ++r)
       for (int q = 0; q < m; ++q) {
         const double y = a[(size_t)r * m + q];
@@ -61,12 +89,15 @@ void orc2_explicit_propagate(const orc2_coeffs* c, const double* in, double* out
         const double e = q < m - 1 ? a[(size_t)r * m + q + 1] : 0.0;
         const double no = r > 0 ? a[(size_t)(r - 1) * m + q] : 0.0;
         const double so = r < m - 1 ? a[(size_t)(r + 1) * m + q] : 0.0;
-        b[(size_t)r * m + q] = fma(c->ac, y, c->an * ((w + e) + (no + so)));
+        b[(size_t)r * m + q] = c->scaled ? fma(c->kappa, y, (w + e) + (no + so))
+                                         : fma(c->ac, y, c->an * ((w + e) + (no + so)));
       }
     double* t = a;
     a = b;
     b = t;
   }
+  if (c->scaled)
+    for (size_t i = 0; i < n; ++i) a[i] = a[i] * c->anLast;
   memcpy(out, a, n * sizeof(double));
   free(a);
   free(b);

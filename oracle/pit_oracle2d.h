@@ -15,6 +15,8 @@ typedef struct orc2_coeffs {
   int m;              /* points per axis; blocks are m*m, x fastest */
   int fine_steps, coarse_steps;
   double ac, an;      /* explicit Euler: y' = fma(ac, y, an*((w+e)+(n+s))) */
+  int scaled, R;      /* scaled form: z' = fma(kappa, z, (w+e)+(n+s)), z *= anR every R */
+  double kappa, anR, anLast;
   double D, O, minv;  /* BE step matrix I + dt*A: centre, neighbour, 1/D */
   double rel_tol;     /* CG relative tolerance */
   long long cap;      /* CG iteration cap */

@@ -52,7 +52,9 @@ class ProblemDesc(C.Structure):
 
 class StepCoeffs2DC(C.Structure):
     _fields_ = [("m", C.c_int32), ("fine_steps", C.c_int32), ("coarse_steps", C.c_int32),
-                ("ac", C.c_double), ("an", C.c_double), ("D", C.c_double), ("O", C.c_double),
+                ("ac", C.c_double), ("an", C.c_double), ("scaled", C.c_int32), ("R", C.c_int32),
+                ("kappa", C.c_double), ("anR", C.c_double), ("anLast", C.c_double),
+                ("D", C.c_double), ("O", C.c_double),
                 ("minv", C.c_double), ("rel_tol", C.c_double), ("cap", C.c_int64),
                 ("rows", C.c_int32), ("cluster", C.c_int32), ("threads", C.c_int32),
                 ("tile_rows", C.c_int32), ("tile_cols", C.c_int32), ("tile_cluster", C.c_int32),

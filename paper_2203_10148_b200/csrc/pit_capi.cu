@@ -150,6 +150,33 @@ double grid_spacing(const pit_problem_desc* d) {
   return (d->grid_hi - d->grid_lo) / static_cast<double>(d->interior + 2 - 1);
 }
 
+// Scaled explicit form (pit_step_coeffs_2d): an = 2^e exactly and
+// kappa = ac/an exact; rescale period R keeps |z| <= |y| 2^768.
+// oracle/pit_oracle2d.c orc2_coefficients restates this.
+void explicit_scaling(double ac, double an, int steps, int32_t* scaled, int32_t* R, double* kappa,
+                      double* anR, double* anLast) {
+  int e = 0;
+  const double mant = std::frexp(an, &e);  // an = mant * 2^e
+  *scaled = 0;
+  *R = 1;
+  *kappa = 0.0;
+  *anR = 1.0;
+  *anLast = 1.0;
+  if (!(an > 0.0) || mant != 0.5 || e - 1 >= 0) return;
+  const double k = ac / an;
+  if (!std::isfinite(k) || k * an != ac) return;
+  const int sh = 1 - e;  // an = 2^-sh, sh >= 1
+  int r = 768 / sh;
+  if (r < 1) return;
+  if (r > steps) r = steps;
+  const int j = steps - r * ((steps - 1) / r);  // factors carried after the last fold
+  *scaled = 1;
+  *R = r;
+  *kappa = k;
+  *anR = std::ldexp(1.0, -sh * r);
+  *anLast = std::ldexp(1.0, -sh * j);
+}
+
 // 2D coefficients (pit_step_coeffs_2d); K4 layout and K5 decomposition.
 int coeffs_2d(const pit_problem_desc* d, pit_step_coeffs_2d* c) {
   const int m = d->interior;
@@ -163,6 +190,8 @@ int coeffs_2d(const pit_problem_desc* d, pit_step_coeffs_2d* c) {
   c->coarse_steps = d->coarse_steps;
   c->an = (double)(-(long double)dtf * (long double)off);
   c->ac = (double)(1.0L - (long double)dtf * (long double)diag);
+  explicit_scaling(c->ac, c->an, d->fine_steps, &c->scaled, &c->R, &c->kappa, &c->anR,
+                   &c->anLast);
   c->O = off * dtc;         // ImplicitStepSolver: val *= dt      (pde.cpp:107)
   c->D = diag * dtc + 1.0;  //                     diagonal += 1   (pde.cpp:108)
   c->minv = c->D != 0.0 ? 1.0 / c->D : 1.0;  // jacobi_inverse_diagonal (sparse.cpp:43-50)
@@ -191,6 +220,14 @@ Ex2Params ex2_params(const pit_context* ctx) {
   P.steps = ctx->c2.fine_steps;
   P.ac = ctx->c2.ac;
   P.an = ctx->c2.an;
+  P.scaled = ctx->c2.scaled;
+  P.R = ctx->c2.R;
+  P.kappa = ctx->c2.kappa;
+  P.anR = ctx->c2.anR;
+  P.anLast = ctx->c2.anLast;
+  if (const char* e = std::getenv("PIT_UNSCALED")) {
+    if (std::atoi(e)) P.scaled = 0;  // A/B knob: the same bits either way
+  }
   return P;
 }
 

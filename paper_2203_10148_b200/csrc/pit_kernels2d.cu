@@ -62,6 +62,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -105,19 +109,29 @@ struct Tile2 {
   static constexpr int T = 32 * WARPS;
   static constexpr int NC = 32 * TC;       // columns covered by a warp row
   static constexpr int ROWS = WARPS * TR;  // rows per CTA
-  // top[2][WARPS+1][NC], bot[2][WARPS+1][NC], then 2 mbarriers
-  static constexpr size_t smem = sizeof(double) * 4 * (WARPS + 1) * NC + 2 * sizeof(uint64_t);
+  // top[2][WARPS+1][NC], bot[2][WARPS+1][NC], then mbarriers [WARPS][2]
+  static constexpr size_t smem =
+      sizeof(double) * 4 * (WARPS + 1) * NC + 2 * WARPS * sizeof(uint64_t);
 };
 
 // K4.  Per step k (state y^k in registers, halo rows of y^k in buffer k&1):
-//   wait for the halo rows of y^k (warps above/below: __syncthreads; CTAs
-//   above/below: the mbarrier their st.async stores complete), compute the
-//   tile's first and last rows of y^{k+1}, publish them (local stores, and
-//   st.async into the neighbour CTA's buffer (k+1)&1), then the interior rows
-//   while those stores fly.  Buffer (k+1)&1 was last read at step k-1; every
-//   reader finished before its own publish of y^k, which the writer waited
-//   for — no cluster barrier inside the step loop.
-template <int TR, int TC, int CL, int WARPS>
+//   each warp waits on its own mbarrier for the halo rows of y^k (arrivals
+//   of the warps above/below after their shared-memory stores; st.async
+//   byte counts from the neighbour CTA for the cluster-edge warps), computes
+//   its tiles' first and last rows of y^{k+1}, publishes them (shared-memory
+//   stores + arrivals, st.async into the neighbour CTA's buffer (k+1)&1),
+//   then computes the interior rows while those stores fly.  Buffer (k+1)&1
+//   was last read at step k-1 by a reader that published y^k only after that
+//   read, and the writer waited for y^k: no CTA or cluster barrier inside the
+//   step loop, and a warp's step is coupled only to its neighbours'.
+template <bool SCALED>
+__device__ __forceinline__ double ex_update(const Ex2Params& P, double y, double w, double e,
+                                            double n, double s) {
+  if constexpr (SCALED) return fma(P.kappa, y, (w + e) + (n + s));
+  return ex_point(P.ac, P.an, y, w, e, n, s);
+}
+
+template <int TR, int TC, int CL, int WARPS, bool SCALED>
 __global__ void __launch_bounds__(32 * WARPS, 1)
     explicit2d_kernel(const __grid_constant__ Ex2Params P, const __grid_constant__ SlabArgs A) {
   using S = Tile2<TR, TC, CL, WARPS>;
@@ -126,7 +140,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   // bot(par, w): last row of warp w-1's tiles (w == 0: CTA above's last warp)
   double* const top = sm2;
   double* const bot = sm2 + 2 * (WARPS + 1) * S::NC;
-  uint64_t* const mbar = reinterpret_cast<uint64_t*>(sm2 + 4 * (WARPS + 1) * S::NC);
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(sm2 + 4 * (WARPS + 1) * S::NC);  // [w][par]
   auto TOP = [&](int par, int w) { return top + ((size_t)par * (WARPS + 1) + w) * S::NC; };
   auto BOT = [&](int par, int w) { return bot + ((size_t)par * (WARPS + 1) + w) * S::NC; };
   cg::cluster_group cl = cg::this_cluster();
@@ -134,19 +148,22 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   const int b = blockIdx.x / CL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = P.m;
-  const double ac = P.ac, an = P.an;
   const int row0 = c * S::ROWS + warp * TR;
   const int col0 = lane * TC;
   const bool ghosts = (CL * S::ROWS > m) || (S::NC > m);
-  // halo bytes this CTA receives per step
-  const unsigned rx_bytes = (unsigned)sizeof(double) * S::NC * ((c > 0) + (c < CL - 1));
+  // halo bytes this warp receives per step from neighbour CTAs
+  const bool rx_up = warp == 0 && c > 0, rx_dn = warp == WARPS - 1 && c < CL - 1;
+  const unsigned rx_bytes = (unsigned)sizeof(double) * S::NC * (rx_up + rx_dn);
+  uint64_t* const my_bar = &mbar[2 * warp];
 
   for (int i = tid; i < 4 * (WARPS + 1) * S::NC; i += S::T) sm2[i] = 0.0;
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  if (tid < WARPS) {
+    // own arrive.expect_tx + one arrival per neighbouring warp
+    const unsigned cnt = 1 + (tid > 0) + (tid < WARPS - 1);
+    mbar_init(&mbar[2 * tid], cnt);
+    mbar_init(&mbar[2 * tid + 1], cnt);
   }
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 
   const double* src;
   if (b + A.in_shift >= 0)
@@ -161,11 +178,11 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
       const int r = row0 + i, q = col0 + j;
       y[i][j] = (src && r < m && q < m) ? src[(size_t)r * m + q] : 0.0;
     }
-  // peer addresses (shared::cluster): CTA c-1's TOP(par, WARPS) and mbarriers,
-  // CTA c+1's BOT(par, 0) and mbarriers; parity 1 is kPar doubles further
+  // peer addresses (shared::cluster) of the row buffers this warp feeds
+  // (CTA c-1's last warp and CTA c+1's warp 0 consume them)
   constexpr uint32_t kParBytes = (uint32_t)(sizeof(double) * (WARPS + 1) * S::NC);
   const uint32_t up_top = c > 0 ? mapa_u32(smem_u32(TOP(0, WARPS) + col0), c - 1) : 0u;
-  const uint32_t up_bar = c > 0 ? mapa_u32(smem_u32(&mbar[0]), c - 1) : 0u;
+  const uint32_t up_bar = c > 0 ? mapa_u32(smem_u32(&mbar[2 * (WARPS - 1)]), c - 1) : 0u;
   const uint32_t dn_bot = c < CL - 1 ? mapa_u32(smem_u32(BOT(0, 0) + col0), c + 1) : 0u;
   const uint32_t dn_bar = c < CL - 1 ? mapa_u32(smem_u32(&mbar[0]), c + 1) : 0u;
   cl_sync();  // zeroed buffers and initialised mbarriers cluster-wide
@@ -178,61 +195,105 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
       t0[j] = y[0][j];
       b0[j] = y[TR - 1][j];
     }
+    __syncwarp();
+    if (lane == 0) {  // the warps above and below may read them now
+      if (warp > 0) mbar_arrive(&mbar[2 * (warp - 1) + par]);
+      if (warp < WARPS - 1) mbar_arrive(&mbar[2 * (warp + 1) + par]);
+    }
     if (!remote) return;
     if (warp == 0 && c > 0) send_row<TC>(up_top + par * kParBytes, y[0], up_bar + 8 * par);
     if (warp == WARPS - 1 && c < CL - 1)
       send_row<TC>(dn_bot + par * kParBytes, y[TR - 1], dn_bar + 8 * par);
   };
-  if (tid == 0) mbar_arrive_expect_tx(&mbar[0], rx_bytes);
+  // west/east neighbours of row i from the adjacent lanes (a warp spans the
+  // full width: lanes 0 and 31 border the Dirichlet walls)
+  double Wv[TR], Ev[TR];
+  auto shfl_row = [&](int i) {
+    const double w = __shfl_up_sync(kFull, y[i][TC - 1], 1);
+    const double e = __shfl_down_sync(kFull, y[i][0], 1);
+    Wv[i] = lane == 0 ? 0.0 : w;
+    Ev[i] = lane == 31 ? 0.0 : e;
+  };
+  if (lane == 0) mbar_arrive_expect_tx(&my_bar[0], rx_bytes);
   publish(0, true);
 
+  int until_rescale = P.R;
   for (int k = 0; k < P.steps; ++k) {
     const int par = k & 1;
     const bool more = k + 1 < P.steps;  // y^{k+1} halos are consumed
-    if (tid == 0 && more) mbar_arrive_expect_tx(&mbar[par ^ 1], rx_bytes);
-    double Wv[TR], Ev[TR];
+    if (lane == 0 && more) mbar_arrive_expect_tx(&my_bar[par ^ 1], rx_bytes);
+    bool rs = false;
+    if (SCALED) {
+      // fold an^R back before step k when k is a positive multiple of R
+      if (until_rescale == 0) {
+        rs = true;
+        until_rescale = P.R;
 #pragma unroll
-    for (int i = 0; i < TR; ++i) {
-      const double w = __shfl_up_sync(kFull, y[i][TC - 1], 1);
-      const double e = __shfl_down_sync(kFull, y[i][0], 1);
-      Wv[i] = lane == 0 ? 0.0 : w;
-      Ev[i] = lane == 31 ? 0.0 : e;
-    }
-    __syncthreads();  // halo rows of y^k from the warps above/below
-    if ((warp == 0 && c > 0) || (warp == WARPS - 1 && c < CL - 1)) mbar_wait(&mbar[par], (k >> 1) & 1);
-    double o0[TC], o1[TC], oA[TC], oB[TC];  // old rows 0, 1, TR-2, TR-1
+        for (int i = 0; i < TR; ++i)
 #pragma unroll
-    for (int j = 0; j < TC; ++j) {
-      o0[j] = y[0][j];
-      o1[j] = y[1][j];
-      oA[j] = y[TR - 2][j];
-      oB[j] = y[TR - 1][j];
+          for (int j = 0; j < TC; ++j) y[i][j] = y[i][j] * P.anR;
+      }
+      --until_rescale;
     }
+#pragma unroll
+    for (int i = 0; i < TR; ++i) shfl_row(i);
+    mbar_wait(&my_bar[par], (k >> 1) & 1);  // halo rows of y^k
+    // new first/last rows into separate registers: y keeps y^k until the
+    // interior rows are done
+    double n0[TC], nT[TC];
     {
       const double* nb = BOT(par, warp) + col0;
       const double* sb = TOP(par, warp + 1) + col0;
+      double Nv[TC], Sv[TC];
+#pragma unroll
+      for (int j = 0; j < TC; ++j) {
+        Nv[j] = nb[j];
+        Sv[j] = sb[j];
+        if (SCALED && rs) {
+          Nv[j] = Nv[j] * P.anR;
+          Sv[j] = Sv[j] * P.anR;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < TC; ++j)
-        y[0][j] = ex_point(ac, an, o0[j], j > 0 ? o0[j - 1] : Wv[0],
-                           j < TC - 1 ? o0[j + 1] : Ev[0], nb[j], o1[j]);
+        n0[j] = ex_update<SCALED>(P, y[0][j], j > 0 ? y[0][j - 1] : Wv[0],
+                                  j < TC - 1 ? y[0][j + 1] : Ev[0], Nv[j], y[1][j]);
 #pragma unroll
       for (int j = 0; j < TC; ++j)
-        y[TR - 1][j] = ex_point(ac, an, oB[j], j > 0 ? oB[j - 1] : Wv[TR - 1],
-                                j < TC - 1 ? oB[j + 1] : Ev[TR - 1], oA[j], sb[j]);
+        nT[j] = ex_update<SCALED>(P, y[TR - 1][j], j > 0 ? y[TR - 1][j - 1] : Wv[TR - 1],
+                                  j < TC - 1 ? y[TR - 1][j + 1] : Ev[TR - 1], y[TR - 2][j], Sv[j]);
     }
     if (ghosts) {
 #pragma unroll
       for (int j = 0; j < TC; ++j) {
-        if (row0 >= m || col0 + j >= m) y[0][j] = 0.0;
-        if (row0 + TR - 1 >= m || col0 + j >= m) y[TR - 1][j] = 0.0;
+        if (row0 >= m || col0 + j >= m) n0[j] = 0.0;
+        if (row0 + TR - 1 >= m || col0 + j >= m) nT[j] = 0.0;
       }
     }
-    publish(par ^ 1, more);
-    // interior rows 1..TR-2 of y^{k+1} (rows 0 and TR-1 of y^k: o0, oB)
+    {  // publish y^{k+1} first/last rows; their shuffles for step k+1
+      double* t0 = TOP(par ^ 1, warp) + col0;
+      double* b0 = BOT(par ^ 1, warp + 1) + col0;
+#pragma unroll
+      for (int j = 0; j < TC; ++j) {
+        t0[j] = n0[j];
+        b0[j] = nT[j];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (warp > 0) mbar_arrive(&mbar[2 * (warp - 1) + (par ^ 1)]);
+        if (warp < WARPS - 1) mbar_arrive(&mbar[2 * (warp + 1) + (par ^ 1)]);
+      }
+      if (more) {
+        if (warp == 0 && c > 0) send_row<TC>(up_top + (par ^ 1) * kParBytes, n0, up_bar + 8 * (par ^ 1));
+        if (warp == WARPS - 1 && c < CL - 1)
+          send_row<TC>(dn_bot + (par ^ 1) * kParBytes, nT, dn_bar + 8 * (par ^ 1));
+      }
+    }
+    // interior rows 1..TR-2 of y^{k+1}
     {
       double prev[TC];
 #pragma unroll
-      for (int j = 0; j < TC; ++j) prev[j] = o0[j];
+      for (int j = 0; j < TC; ++j) prev[j] = y[0][j];
 #pragma unroll
       for (int i = 1; i < TR - 1; ++i) {
         double cur[TC];
@@ -240,20 +301,28 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
         for (int j = 0; j < TC; ++j) cur[j] = y[i][j];
 #pragma unroll
         for (int j = 0; j < TC; ++j)
-          y[i][j] = ex_point(ac, an, cur[j], j > 0 ? cur[j - 1] : Wv[i],
-                             j < TC - 1 ? cur[j + 1] : Ev[i], prev[j],
-                             i + 1 < TR - 1 ? y[i + 1][j] : oB[j]);
+          y[i][j] = ex_update<SCALED>(P, cur[j], j > 0 ? cur[j - 1] : Wv[i],
+                                      j < TC - 1 ? cur[j + 1] : Ev[i], prev[j], y[i + 1][j]);
+        if (ghosts) {
+#pragma unroll
+          for (int j = 0; j < TC; ++j)
+            if (row0 + i >= m || col0 + j >= m) y[i][j] = 0.0;
+        }
 #pragma unroll
         for (int j = 0; j < TC; ++j) prev[j] = cur[j];
       }
     }
-    if (ghosts) {
 #pragma unroll
-      for (int i = 1; i < TR - 1; ++i)
-#pragma unroll
-        for (int j = 0; j < TC; ++j)
-          if (row0 + i >= m || col0 + j >= m) y[i][j] = 0.0;
+    for (int j = 0; j < TC; ++j) {
+      y[0][j] = n0[j];
+      y[TR - 1][j] = nT[j];
     }
+  }
+  if (SCALED) {
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < TC; ++j) y[i][j] = y[i][j] * P.anLast;
   }
   cl_sync();  // no CTA leaves while a peer may still address its buffers
 
@@ -551,11 +620,13 @@ Layout2D auto_layout_2d(int m) {
 cudaError_t launch_explicit2d(const Layout2D& L, const Ex2Params& P, const SlabArgs& A, int slabs,
                               cudaStream_t st) {
   if (slabs <= 0) return cudaSuccess;
-#define X(TR, TC, CL, WW)                                                                   \
-  if (L.tr == TR && L.tc == TC && L.cl == CL && L.warps == WW) {                            \
-    using S = Tile2<TR, TC, CL, WW>;                                                        \
-    return launch_clustered(explicit2d_kernel<TR, TC, CL, WW>, CL * slabs, S::T, S::smem, CL, \
-                            st, &P, &A);                                                    \
+#define X(TR, TC, CL, WW)                                                                    \
+  if (L.tr == TR && L.tc == TC && L.cl == CL && L.warps == WW) {                             \
+    using S = Tile2<TR, TC, CL, WW>;                                                         \
+    return P.scaled ? launch_clustered(explicit2d_kernel<TR, TC, CL, WW, true>, CL * slabs,  \
+                                       S::T, S::smem, CL, st, &P, &A)                        \
+                    : launch_clustered(explicit2d_kernel<TR, TC, CL, WW, false>, CL * slabs, \
+                                       S::T, S::smem, CL, st, &P, &A);                       \
   }
   PIT_LAYOUTS_2D(X)
 #undef X

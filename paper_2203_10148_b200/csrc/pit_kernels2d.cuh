@@ -17,6 +17,8 @@ struct Ex2Params {
   int m;       // points per axis
   int steps;   // explicit steps per slab
   double ac, an;
+  int scaled, R;  // scaled form (pit_step_coeffs_2d)
+  double kappa, anR, anLast;
 };
 
 // K5: one persistent cluster; per slab one BE step (I + dt*A) x = b solved

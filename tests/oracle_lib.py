@@ -50,7 +50,9 @@ class OrcStepper(C.Structure):
 
 class Orc2Coeffs(C.Structure):
     _fields_ = [("m", C.c_int), ("fine_steps", C.c_int), ("coarse_steps", C.c_int),
-                ("ac", C.c_double), ("an", C.c_double), ("D", C.c_double), ("O", C.c_double),
+                ("ac", C.c_double), ("an", C.c_double), ("scaled", C.c_int), ("R", C.c_int),
+                ("kappa", C.c_double), ("anR", C.c_double), ("anLast", C.c_double),
+                ("D", C.c_double), ("O", C.c_double),
                 ("minv", C.c_double), ("rel_tol", C.c_double), ("cap", C.c_longlong),
                 ("rows", C.c_int), ("cluster", C.c_int), ("threads", C.c_int)]
 

@@ -28,11 +28,13 @@ def coeffs(p):
 def test_2d_coefficients_match_product_bitwise(m, slabs):
     p = configs.make("c5", slabs=slabs, M=m)
     c, pc = coeffs(p)
-    for f in ("ac", "an", "D", "O", "minv", "rel_tol", "cap", "rows", "cluster", "threads"):
+    for f in ("ac", "an", "scaled", "R", "kappa", "anR", "anLast", "D", "O", "minv", "rel_tol",
+              "cap", "rows", "cluster", "threads"):
         assert getattr(c, f) == getattr(pc, f), f
     if m == 256:
         # dt = h^2/8 exactly representable ratios at the BASELINE size
         assert (pc.ac, pc.an, pc.D, pc.O) == (0.5, 0.125, 2049.0, -512.0)
+        assert (pc.scaled, pc.kappa, pc.R) == (1, 4.0, 256)
         assert pc.rel_tol == configs.C5_COARSE_TOL and pc.cap == 10 * 256 * 256
         assert (pc.cluster, pc.rows, pc.threads) == (16, 16, 256)
 
