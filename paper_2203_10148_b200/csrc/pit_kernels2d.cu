@@ -408,6 +408,14 @@ __device__ __forceinline__ double stencil_S(const double* Ps, int pitch, int k, 
   return fma(D, row[0], O * ((w + e) + (n + s)));
 }
 
+// K5 synchronisation: no cluster barrier inside the solve.  Reductions:
+// every warp st.async's its two partials into every CTA's slot array (set
+// `pair`, alternating), counted on that CTA's reduction mbarrier; each CTA
+// waits for C*W*16 bytes, sums the slots in slot order.  A set is rewritten
+// two reductions later, only after every warp of every CTA sent the
+// in-between reduction, i.e. after it read this one.  Field publication for
+// the stencil: own rows to shared memory (+ __syncthreads), first/last row
+// st.async'd into the neighbours' halo rows, counted on their halo mbarrier.
 __global__ void __launch_bounds__(256, 1)
     cg_sweep2d_kernel(const __grid_constant__ Cg2Params P, const __grid_constant__ SweepArgs A,
                       long long* iters) {
@@ -422,157 +430,185 @@ __global__ void __launch_bounds__(256, 1)
   const int nslot = C * W;
   const int m = P.m, R = P.rows;
   const int pitch = NT + 2;
-  double* const Ps = smc;                         // [(RM+2)][pitch], own rows 1..R
-  double* const red = smc + (size_t)(RM + 2) * pitch;  // [4][kSlotCap]
+  double* const Ps = smc;                              // [(RM+2)][pitch], own rows 1..R
+  double* const red = smc + (size_t)(RM + 2) * pitch;  // [2][kSlotCap][2]
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(red + 4 * kSlotCap);  // rbar[2], hbar
   const double D = P.D, O = P.O, minv = P.minv;
+  const unsigned red_bytes = 16u * (unsigned)nslot;
+  const unsigned halo_bytes = 8u * (unsigned)NT * ((c > 0) + (c < C - 1));
 
   for (int i = t; i < (RM + 2) * pitch + 4 * kSlotCap; i += NT) smc[i] = 0.0;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
 
   bool valid[RM];
 #pragma unroll
   for (int k = 0; k < RM; ++k) valid[k] = t < m && k < R && c * R + k < m;
   auto gidx = [&](int k) { return (size_t)(c * R + k) * m + t; };
 
-  double* const red_to = cl.map_shared_rank(red, lane < C ? lane : 0);
-  double* const halo_up = c > 0 ? cl.map_shared_rank(Ps + (size_t)(R + 1) * pitch, c - 1) : nullptr;
-  double* const halo_dn = c < C - 1 ? cl.map_shared_rank(Ps, c + 1) : nullptr;
+  const int tgt = lane < C ? lane : 0;
+  const uint32_t red_to = mapa_u32(smem_u32(red), tgt);
+  const uint32_t rbar_to = mapa_u32(smem_u32(&bars[0]), tgt);
+  const uint32_t up_row = c > 0 ? mapa_u32(smem_u32(Ps + (size_t)(R + 1) * pitch + t + 1), c - 1) : 0u;
+  const uint32_t up_bar = c > 0 ? mapa_u32(smem_u32(&bars[2]), c - 1) : 0u;
+  const uint32_t dn_row = c < C - 1 ? mapa_u32(smem_u32(Ps + t + 1), c + 1) : 0u;
+  const uint32_t dn_bar = c < C - 1 ? mapa_u32(smem_u32(&bars[2]), c + 1) : 0u;
+  cl_sync();  // zeroed buffers, initialised barriers cluster-wide
+  if (t == 0) {
+    mbar_arrive_expect_tx(&bars[0], red_bytes);
+    mbar_arrive_expect_tx(&bars[1], red_bytes);
+    mbar_arrive_expect_tx(&bars[2], halo_bytes);
+  }
 
   int pair = 0;
+  unsigned rph[2] = {0u, 0u}, hph = 0u;
   // cluster-wide sums of a and b (identical bits in every thread)
   auto reduce2 = [&](double a, double b, double& ra, double& rb) {
     a = warp_sum(a);
     b = warp_sum(b);
-    if (lane < C) {
-      red_to[(2 * pair) * kSlotCap + c * W + warp] = a;
-      red_to[(2 * pair + 1) * kSlotCap + c * W + warp] = b;
-    }
-    cl_sync();
+    if (lane < C)
+      st_async_v2(red_to + 16u * (unsigned)((pair * kSlotCap) + c * W + warp), a, b,
+                  rbar_to + 8u * pair);
+    mbar_wait(&bars[pair], rph[pair]);
+    rph[pair] ^= 1u;
+    const double* rs = red + 2 * pair * kSlotCap;
     double u = 0.0, v = 0.0;
     for (int i = lane; i < nslot; i += 32) {
-      u = u + red[(2 * pair) * kSlotCap + i];
-      v = v + red[(2 * pair + 1) * kSlotCap + i];
+      u = u + rs[2 * i];
+      v = v + rs[2 * i + 1];
     }
     ra = warp_sum(u);
     rb = warp_sum(v);
+    if (t == 0) mbar_arrive_expect_tx(&bars[pair], red_bytes);  // its next use
     pair ^= 1;
   };
-
   // field value v at own row k into the stencil buffer (+ neighbours' halos)
   auto put = [&](int k, double v) {
     if (k < R) Ps[(size_t)(k + 1) * pitch + t + 1] = v;
-    if (k == 0 && halo_up) halo_up[t + 1] = v;
-    if (k == R - 1 && halo_dn) halo_dn[t + 1] = v;
+    if (k == 0 && up_row) st_async_1(up_row, v, up_bar);
+    if (k == R - 1 && dn_row) st_async_1(dn_row, v, dn_bar);
+  };
+  // after a full put(): own rows visible CTA-wide, neighbours' rows landed
+  auto published = [&]() {
+    __syncthreads();
+    mbar_wait(&bars[2], hph);
+    hph ^= 1u;
+    if (t == 0) mbar_arrive_expect_tx(&bars[2], halo_bytes);
   };
   auto own = [&](int k) { return k < R ? Ps[(size_t)(k + 1) * pitch + t + 1] : 0.0; };
 
   double x[RM], r[RM], bb[RM], q[RM];
 #pragma unroll
   for (int k = 0; k < RM; ++k) bb[k] = valid[k] ? A.start[gidx(k)] : 0.0;
-  cl_sync();
 
   long long total_it = 0;
   for (int s = 0; s < A.count; ++s) {
     const int slab = A.slab0 + s;
     bool ok = true;
     for (int cs = 0; cs < P.steps && ok; ++cs) {
-    if (cs > 0) {
+      if (cs > 0) {
 #pragma unroll
-      for (int k = 0; k < RM; ++k) bb[k] = x[k];
-    }
-#pragma unroll
-    for (int k = 0; k < RM; ++k) x[k] = 0.0;
-    double nb2, dummy;
-    {
-      double a = 0.0;
-#pragma unroll
-      for (int k = 0; k < RM; ++k) a = fma(bb[k], bb[k], a);
-      reduce2(a, 0.0, nb2, dummy);
-    }
-    const double nb = sqrt(nb2);
-    if (nb != 0.0) {
-      const double tol = P.rel_tol * nb;
-      double rz, rr;
-      {
-        double a = 0.0, b2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < RM; ++k) {
-          r[k] = bb[k];
-          const double z = minv * r[k];  // p = z
-          put(k, z);
-          a = fma(r[k], z, a);
-          b2 = fma(r[k], r[k], b2);
-        }
-        reduce2(a, b2, rz, rr);
+        for (int k = 0; k < RM; ++k) bb[k] = x[k];
       }
-      double res = sqrt(rr);
-      long long it = 0;
-      bool stalled = false;
-      for (;;) {
-        while (res > tol && it < P.cap && !stalled) {
-          double pq, d0;
-          {
-            double a = 0.0;
 #pragma unroll
-            for (int k = 0; k < RM; ++k) {
-              q[k] = valid[k] ? stencil_S(Ps, pitch, k, t, D, O) : 0.0;
-              a = fma(own(k), q[k], a);
-            }
-            reduce2(a, 0.0, pq, d0);
-          }
-          if (pq == 0.0 || !isfinite(pq)) {
-            stalled = true;
-            break;
-          }
-          const double alpha = rz / pq;
-          double rzn;
-          {
-            double a = 0.0, b2 = 0.0;
+      for (int k = 0; k < RM; ++k) x[k] = 0.0;
+      double nb2, dummy;
+      {
+        double a = 0.0;
 #pragma unroll
-            for (int k = 0; k < RM; ++k) {
-              x[k] = fma(alpha, own(k), x[k]);
-              r[k] = fma(-alpha, q[k], r[k]);
-              const double z = minv * r[k];
-              a = fma(r[k], r[k], a);
-              b2 = fma(r[k], z, b2);
-            }
-            ++it;
-            reduce2(a, b2, rr, rzn);
-          }
-          res = sqrt(rr);
-          if (!isfinite(res) || res <= tol) break;
-          const double beta = rzn / rz;
-#pragma unroll
-          for (int k = 0; k < RM; ++k) put(k, fma(beta, own(k), minv * r[k]));
-          rz = rzn;
-          cl_sync();
-        }
-        // confirm against the exact residual (sparse.cpp:101-104)
-#pragma unroll
-        for (int k = 0; k < RM; ++k) put(k, x[k]);
-        cl_sync();
+        for (int k = 0; k < RM; ++k) a = fma(bb[k], bb[k], a);
+        reduce2(a, 0.0, nb2, dummy);
+      }
+      const double nb = sqrt(nb2);
+      if (nb != 0.0) {
+        const double tol = P.rel_tol * nb;
+        double rz, rr;
         {
           double a = 0.0, b2 = 0.0;
 #pragma unroll
           for (int k = 0; k < RM; ++k) {
-            r[k] = valid[k] ? bb[k] - stencil_S(Ps, pitch, k, t, D, O) : 0.0;
-            const double z = minv * r[k];
-            a = fma(r[k], r[k], a);
-            b2 = fma(r[k], z, b2);
+            r[k] = bb[k];
+            const double z = minv * r[k];  // p = z
+            put(k, z);
+            a = fma(r[k], z, a);
+            b2 = fma(r[k], r[k], b2);
           }
-          reduce2(a, b2, rr, rz);
+          published();
+          reduce2(a, b2, rz, rr);
         }
-        res = sqrt(rr);
-        if (res <= tol) break;
-        if (it >= P.cap || stalled || !isfinite(res)) {
-          ok = false;
-          break;
-        }
+        double res = sqrt(rr);
+        long long it = 0;
+        bool stalled = false;
+        for (;;) {
+          while (res > tol && it < P.cap && !stalled) {
+            double pq, d0;
+            {
+              double a = 0.0;
 #pragma unroll
-        for (int k = 0; k < RM; ++k) put(k, minv * r[k]);  // restart: p = z
-        cl_sync();
+              for (int k = 0; k < RM; ++k) {
+                q[k] = valid[k] ? stencil_S(Ps, pitch, k, t, D, O) : 0.0;
+                a = fma(own(k), q[k], a);
+              }
+              reduce2(a, 0.0, pq, d0);
+            }
+            if (pq == 0.0 || !isfinite(pq)) {
+              stalled = true;
+              break;
+            }
+            const double alpha = rz / pq;
+            double rzn;
+            {
+              double a = 0.0, b2 = 0.0;
+#pragma unroll
+              for (int k = 0; k < RM; ++k) {
+                x[k] = fma(alpha, own(k), x[k]);
+                r[k] = fma(-alpha, q[k], r[k]);
+                const double z = minv * r[k];
+                a = fma(r[k], r[k], a);
+                b2 = fma(r[k], z, b2);
+              }
+              ++it;
+              reduce2(a, b2, rr, rzn);
+            }
+            res = sqrt(rr);
+            if (!isfinite(res) || res <= tol) break;
+            const double beta = rzn / rz;
+#pragma unroll
+            for (int k = 0; k < RM; ++k) put(k, fma(beta, own(k), minv * r[k]));
+            published();
+            rz = rzn;
+          }
+          // confirm against the exact residual (sparse.cpp:101-104)
+#pragma unroll
+          for (int k = 0; k < RM; ++k) put(k, x[k]);
+          published();
+          {
+            double a = 0.0, b2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < RM; ++k) {
+              r[k] = valid[k] ? bb[k] - stencil_S(Ps, pitch, k, t, D, O) : 0.0;
+              const double z = minv * r[k];
+              a = fma(r[k], r[k], a);
+              b2 = fma(r[k], z, b2);
+            }
+            reduce2(a, b2, rr, rz);
+          }
+          res = sqrt(rr);
+          if (res <= tol) break;
+          if (it >= P.cap || stalled || !isfinite(res)) {
+            ok = false;
+            break;
+          }
+#pragma unroll
+          for (int k = 0; k < RM; ++k) put(k, minv * r[k]);  // restart: p = z
+          published();
+        }
+        total_it += it;
       }
-      total_it += it;
-    }
     }  // coarse steps
     bool fin = true;
 #pragma unroll
@@ -639,7 +675,8 @@ cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long*
   const int nt = 32 * ((P.m + 31) / 32);
   if (nt > 256 || P.rows > kCgRowsMax || P.cluster * (nt / 32) > kSlotCap || P.cluster > 16)
     return cudaErrorInvalidConfiguration;
-  const size_t smem = sizeof(double) * ((size_t)(kCgRowsMax + 2) * (nt + 2) + 4 * kSlotCap);
+  const size_t smem =
+      sizeof(double) * ((size_t)(kCgRowsMax + 2) * (nt + 2) + 4 * kSlotCap) + 4 * sizeof(uint64_t);
   auto k = cg_sweep2d_kernel;
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
