@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the per-config apply_F and time-to-tolerance lines")
     return ap.parse_args()
 
 
@@ -175,6 +177,85 @@ def run_reference_arm(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def device_apply_rate(name, reps=3):
+    """Best-of-reps device apply_F (inputs resident, dedicated stream) of a
+    full BASELINE config: (gp-steps/s, ms, kernel name)."""
+    import torch
+
+    from paper_2203_10148_b200 import _lib, api, configs
+
+    L = _lib.lib()
+    p = configs.make(name)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream), api.BlockOperatorContext(p) as ctx:
+        x = torch.tensor(np.tile(p.y0, (p.N, 1)), device="cuda")
+        out = torch.empty_like(x)
+        f = lambda: api._check(L.pit_apply_F_device(ctx.handle, x.data_ptr(), None, out.data_ptr(),
+                                                    0, p.N, stream.cuda_stream))
+        f()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            f()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        api._check(L.pit_sync_status(ctx.handle, stream.cuda_stream))
+    gp = configs.gp_steps_per_apply(p)
+    ms = min(ts)
+    return gp / (ms * 1e-3), ms, gp
+
+
+def device_time_to_tolerance(name):
+    """PiTSBiCG (SURVEY §8(d) metric 2) through pit_pitsbicg_solve_device:
+    wall time from solver entry (inputs resident) to ||R|| <= tol, including
+    initial_guess, assemble_rhs and every iteration."""
+    import torch
+
+    from paper_2203_10148_b200 import _lib, api, configs
+
+    L = _lib.lib()
+    p = configs.make(name)
+    tol = configs.tolerance(name)
+    with api.BlockOperatorContext(p) as ctx:
+        lam = torch.empty((p.N, p.M), dtype=torch.float64, device="cuda")
+        cfg = _lib.SolverConfigC(tol, 1e-12, 200, _lib.PIT_GUESS_COARSE_SWEEP)
+        recs = (_lib.RecordC * 202)()
+        info = _lib.SolveInfoC()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        api._check(L.pit_pitsbicg_solve_device(ctx.handle, C.byref(cfg), None, lam.data_ptr(),
+                                               recs, 202, C.byref(info), None))
+        wall = time.perf_counter() - t0
+        n = min(info.record_count, 202)
+        its = ctx.coarse_iterations()
+    last = recs[n - 1] if n else None
+    return {"ms": wall * 1e3, "k": last.k if last else None,
+            "residual": last.residual_norm if last else None, "restarts": info.restarts,
+            "converged": info.status == _lib.PIT_CONVERGED, "tolerance": tol,
+            "fine_applications": int(info.stats.fine_applications),
+            "coarse_applications": int(info.stats.coarse_applications),
+            **({"coarse_cg_iterations": int(its)} if its else {})}
+
+
+def secondary(include_c5_solve=False):
+    out = {"apply_F": {}, "time_to_tolerance": {}}
+    for name in ("c1", "c3", "c4", "c5"):
+        try:
+            rate, ms, gp = device_apply_rate(name)
+            out["apply_F"][name] = {"gp_steps_per_s": rate, "ms": ms, "gp_steps": gp}
+        except Exception as e:  # pragma: no cover
+            out["apply_F"][name] = {"error": str(e)}
+    for name in ("c1", "c2", "c3", "c4") + (("c5",) if include_c5_solve else ()):
+        try:
+            out["time_to_tolerance"][name] = device_time_to_tolerance(name)
+        except Exception as e:  # pragma: no cover
+            out["time_to_tolerance"][name] = {"error": str(e)}
+    return out
+
+
 def run_ours(args, rank, world):
     import torch
 
@@ -340,6 +421,8 @@ def run_ours(args, rank, world):
                      "kernel_ms": kms},
         "clocks": sampler.summary(),
     }
+    if world == 1 and not args.no_secondary:
+        line["secondary"] = secondary()
     if world == 1 and not args.no_cpu_baseline:
         try:
             v, cores, kind, sample = cpu_reference_rate(p)
