@@ -147,6 +147,39 @@ class OracleBackend:
         self.lib.orc_vec_axpy(y.size, a, O.ptr(x), O.ptr(y))
 
 
+class OracleBackend2D(OracleBackend):
+    """2D (config 5) propagators: K4 explicit / K5 CG mirrors."""
+
+    def __init__(self, p, first, count):
+        self.p = p
+        self.o = OracleProblem(p)
+        self.lib = O.orc()
+        self.M = p.M
+        self.first, self.count = first, count
+        self.has_source = False
+        self.shape = None
+        self.c = self.o.coeffs
+
+    def _prop(self, role, with_source, x, slab):
+        out = np.zeros(self.M)
+        xin = np.ascontiguousarray(x)
+        if role == 0:
+            self.lib.orc2_explicit_propagate(C.byref(self.c), O.ptr(xin), O.ptr(out))
+        else:
+            it = C.c_longlong()
+            assert self.lib.orc2_coarse_propagate(C.byref(self.c), O.ptr(xin), O.ptr(out),
+                                                  C.byref(it)) == 1
+        return out
+
+
+def _problem(name, slabs, M, fine_steps):
+    p = configs.make(name, slabs=slabs, M=M)
+    p.fine_steps = fine_steps
+    if name == "c5":
+        p.T = p.N * fine_steps * (p.spacing ** 2 / 8.0)  # keep dt = h^2/8
+    return p
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -161,10 +194,9 @@ def _worker(rank, world, port, case, out_path):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     name, slabs, M, fine_steps = case
-    p = configs.make(name, slabs=slabs, M=M)
-    p.fine_steps = fine_steps
+    p = _problem(name, slabs, M, fine_steps)
     first, count = shard_range(p.N, world, rank)
-    be = OracleBackend(p, first, count)
+    be = (OracleBackend2D if name == "c5" else OracleBackend)(p, first, count)
     ops = ShardedOperators(be, p.N)
     rng = np.random.default_rng(5)
     Lg = rng.uniform(-1, 1, (p.N, p.M))
@@ -182,7 +214,7 @@ def _worker(rank, world, port, case, out_path):
     dist.destroy_process_group()
 
 
-CASES = [("c2", 7, 300, 40), ("c4", 6, 256, 30), ("c3", 5, 200, 50)]
+CASES = [("c2", 7, 300, 40), ("c4", 6, 256, 30), ("c3", 5, 200, 50), ("c5", 5, 12, 48)]
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -200,8 +232,7 @@ def test_sharded_operators_and_solver_bitwise(world, case):
             with open(f"{out}.{r}", "rb") as f:
                 parts.append(pickle.load(f))
     parts.sort(key=lambda x: x["first"])
-    p = configs.make(name, slabs=slabs, M=M)
-    p.fine_steps = fine_steps
+    p = _problem(name, slabs, M, fine_steps)
     o = OracleProblem(p)
     rng = np.random.default_rng(5)
     Lg = rng.uniform(-1, 1, (p.N, p.M))

@@ -130,3 +130,33 @@ def test_full_size_c5_coarse_steps_meet_cg_tolerance():
         slack = 8 * np.finfo(float).eps * (abs(c.D) + 4 * abs(c.O)) * np.linalg.norm(x)
         assert np.linalg.norm(r) <= c.rel_tol * np.linalg.norm(b) + slack, n
     assert its > 0
+
+
+def test_c5_sharded_device_driver_matches_device_solver():
+    """distributed.ShardedOperators over DeviceBackend (world 1) on a 2D
+    problem: K4/K5 through the device entry points, bit-identical to the C++
+    device driver."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_10148_b200.distributed import DeviceBackend, ShardedOperators
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        p = small(32, 6, 256)
+        with api.BlockOperatorContext(p) as ctx:
+            res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+            be = DeviceBackend(ctx, 0, p.N)
+            ops = ShardedOperators(be, p.N)
+            lam, rows, restarts, conv = ops.pitsbicg_solve(tolerance=1e-10)
+            torch.cuda.synchronize()
+        assert np.array_equal(lam.cpu().numpy(), res.solution)
+        assert [(r[0], r[1]) for r in rows] == [(x.k, x.residual_norm) for x in res.history.records]
+    finally:
+        dist.destroy_process_group()
