@@ -15,6 +15,10 @@
 #include <cstdint>
 
 #include "pit_kernels.cuh"
+#include "pit_sync.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -332,37 +336,94 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// K2: one persistent CTA.  V_b prefetched with cp.async into the odd-pitch
-// slot layout (coalesced global reads), W_b drained through the consumed V
-// buffer with coalesced stores.
-template <class S, bool SRC>
+// K2: one persistent CTA running the sequential chain
+//   W_b = Prop(W_{b-1}) (+ V_b).
+// TMA (NSEG == 1, M a multiple of 16, even chunks, 16-byte aligned blocks):
+// thread 0 streams V_{b+1} into buffer (b+1)&1 with 2D tensor loads (128-byte
+// swizzle; completion on an mbarrier) while slab b propagates; after the
+// step every thread adds V_b from and writes W_b into its own rows of buffer
+// b&1 (conflict-free LDS/STS.128 thanks to the swizzle), and thread 0 issues
+// the tensor store of W_b.  A buffer is reloaded only after thread 0's store
+// from it has been read out (bulk wait_group.read).
+// Otherwise: cp.async V into an odd-pitch slot layout and coalesced W stores.
+template <class S>
+__device__ __forceinline__ int swz_off(int p) {  // byte offset of point p in a swizzled slab
+  const int r = p >> 4, q = p & 15;
+  return r * 128 + ((((q >> 1) ^ (r & 7)) << 4) | ((q & 1) << 3));
+}
+
+template <class S, bool SRC, bool TMA>
 __global__ void __launch_bounds__(S::T, 1)
-    sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A) {
-  constexpr int STAGE = S::T * (S::MPT + 1);
+    sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A,
+                 const __grid_constant__ SweepTma X) {
+  constexpr int STAGE_SLOT = S::T * (S::MPT + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
-  double* stage = s_zc + zc_smem_len<S>(P.narrow);  // [2][STAGE]: V double buffer
+  unsigned char* after = reinterpret_cast<unsigned char*>(s_zc + zc_smem_len<S>(P.narrow));
+  // TMA: two 1024-byte aligned slab buffers of M doubles; slot path: two
+  // odd-pitch buffers
+  unsigned char* base = TMA ? reinterpret_cast<unsigned char*>(
+                                  (reinterpret_cast<uintptr_t>(after) + 1023) & ~uintptr_t(1023))
+                            : after;
+  const size_t buf_bytes = TMA ? (size_t)P.M * sizeof(double) : (size_t)STAGE_SLOT * sizeof(double);
+  const int nbuf = TMA ? X.nbuf : 2;
+  uint64_t* vbar = reinterpret_cast<uint64_t*>(base + nbuf * buf_bytes);  // [nbuf]
   const int tid = threadIdx.x;
   const int M = P.M;
   load_zc<S>(P, s_zc, tid);
   init_step_shared<S::NSEG, S::WARPS>(P, *sh, tid);
   double y[S::NC][S::SUB];
   load_field<S>(y, A.start, tid, M);
-  auto prefetch = [&](int b) {
-    double* buf = stage + (b & 1) * STAGE;
-    const double* v = A.V + (size_t)b * M;
-    for (int i = tid; i < M; i += S::T) cp_async8(buf + S::slot_of_point(i), v + i);
-    cp_async_commit();
+  if (TMA && tid == 0) {
+    for (int i = 0; i < nbuf; ++i) mbar_init(&vbar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // slab b uses buffer b % nbuf; V_b is requested D = max(1, nbuf-2) slabs
+  // ahead, into a buffer whose last W store was issued >= 1 slab earlier
+  // (nbuf >= 3)
+  const int D = nbuf > 3 ? nbuf - 2 : 1;
+  auto bidx = [&](int b) { return TMA ? b % nbuf : (b & 1); };
+  // thread 0: wait until at most `pending` of its bulk store groups are
+  // still reading shared memory
+  auto wait_reads = [](int pending) {
+    switch (pending) {
+      case 0: asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); break;
+      case 1: asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); break;
+      case 2: asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory"); break;
+      default: asm volatile("cp.async.bulk.wait_group.read 3;\n" ::: "memory"); break;
+    }
   };
-  if (A.V) prefetch(0);
+  auto bufp = [&](int b) { return base + bidx(b) * buf_bytes; };
+  auto prefetch = [&](int b) {
+    if (TMA) {
+      if (tid == 0) {
+        // the store of W_{b-nbuf}, the previous user of this buffer, has
+        // read it out; W_{b-nbuf+1} .. W_{b-D-1} may still be pending
+        wait_reads(nbuf - D - 1);
+        mbar_arrive_expect_tx(&vbar[bidx(b)], (unsigned)(M * sizeof(double)));
+        for (int r = 0; r < X.rows; r += X.box_rows)
+          tma_load_2d(bufp(b) + r * 128, X.v, 0, b * X.rows + r, &vbar[bidx(b)]);
+      }
+    } else {
+      double* buf = reinterpret_cast<double*>(bufp(b));
+      const double* v = A.V + (size_t)b * M;
+      for (int i = tid; i < M; i += S::T) cp_async8(buf + S::slot_of_point(i), v + i);
+      cp_async_commit();
+    }
+  };
   __syncthreads();
+  if (A.V)
+    for (int b = 0; b < (TMA ? D : 1) && b < A.count; ++b) prefetch(b);
   const StepLane L = step_lane<S>(P, *sh, tid);
   bool ok = true;
   int bad = 0x7fffffff;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
-    if (A.V && b + 1 < A.count) prefetch(b + 1);
+    if (A.V) {
+      const int ahead = TMA ? D : 1;
+      if (b + ahead < A.count) prefetch(b + ahead);
+    }
 #ifdef PIT_PHASE_TIMING
     const long long sw0 = clock64();
 #endif
@@ -374,31 +435,67 @@ __global__ void __launch_bounds__(S::T, 1)
       ok = false;
       bad = slab;
     }
-    double* buf = stage + (b & 1) * STAGE;
-    if (A.V) {
-      if (b + 1 < A.count)
-        cp_async_wait<1>();
-      else
-        cp_async_wait<0>();
-      __syncthreads();
+    if (TMA) {
+      unsigned char* buf = bufp(b);
+      if (A.V) {
+        mbar_wait(&vbar[bidx(b)], (unsigned)((b / nbuf) & 1));  // V_b landed
+#pragma unroll
+        for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+          for (int j = 0; j < S::SUB; j += 2) {
+            const int pnt = S::point(tid, c, j);
+            if (pnt < M) {
+              const double2 v = *reinterpret_cast<const double2*>(buf + swz_off<S>(pnt));
+              y[c][j] = y[c][j] + v.x;
+              y[c][j + 1] = y[c][j + 1] + v.y;
+            }
+          }
+      } else if (b >= nbuf) {
+        if (tid == 0) wait_reads(nbuf - 1);  // W_{b-nbuf} has left this buffer
+        __syncthreads();
+      }
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-        for (int j = 0; j < S::SUB; ++j) {
-          const double v = S::point(tid, c, j) < M ? buf[S::slot(tid, c, j)] : 0.0;
-          y[c][j] = y[c][j] + v;
+        for (int j = 0; j < S::SUB; j += 2) {
+          const int pnt = S::point(tid, c, j);
+          if (pnt < M)
+            *reinterpret_cast<double2*>(buf + swz_off<S>(pnt)) = make_double2(y[c][j], y[c][j + 1]);
         }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        for (int r = 0; r < X.rows; r += X.box_rows)
+          tma_store_2d(X.w, 0, b * X.rows + r, buf + r * 128);
+        bulk_commit();
+      }
+    } else {
+      double* buf = reinterpret_cast<double*>(bufp(b));
+      if (A.V) {
+        if (b + 1 < A.count)
+          cp_async_wait<1>();
+        else
+          cp_async_wait<0>();
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+          for (int j = 0; j < S::SUB; ++j) {
+            const double v = S::point(tid, c, j) < M ? buf[S::slot(tid, c, j)] : 0.0;
+            y[c][j] = y[c][j] + v;
+          }
+      }
+      // drain W_b through slab b's (consumed) V buffer; each thread
+      // overwrites exactly the slots it just read
+#pragma unroll
+      for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+        for (int j = 0; j < S::SUB; ++j) buf[S::slot(tid, c, j)] = y[c][j];
+      __syncthreads();
+      double* W = A.W + (size_t)b * M;
+      for (int i = tid; i < M; i += S::T) W[i] = buf[S::slot_of_point(i)];
+      __syncthreads();  // the buffer is free for the prefetch of slab b+2
     }
-    // drain W_b through slab b's (consumed) V buffer; each thread overwrites
-    // exactly the slots it just read
-#pragma unroll
-    for (int c = 0; c < S::NC; ++c)
-#pragma unroll
-      for (int j = 0; j < S::SUB; ++j) buf[S::slot(tid, c, j)] = y[c][j];
-    __syncthreads();
-    double* W = A.W + (size_t)b * M;
-    for (int i = tid; i < M; i += S::T) W[i] = buf[S::slot_of_point(i)];
-    __syncthreads();  // the buffer is free for the prefetch of slab b+2
 #ifdef PIT_PHASE_TIMING
     if (P.timing && (tid & 31) == 0 && (tid >> 5) < 2) {
       P.timing[(tid >> 5) * 16 + 10] += sw1 - sw0;        // propagation
@@ -406,6 +503,7 @@ __global__ void __launch_bounds__(S::T, 1)
     }
 #endif
   }
+  if (TMA && tid == 0) bulk_wait_all();
   if (!ok) atomicMin(A.status, bad);
 }
 
@@ -470,17 +568,73 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A0, int ctas, cudaS
   return cudaGetLastError();
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency: the library still loads on GPU-less hosts)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// [rows][16] doubles, 128-byte swizzled boxes of box_rows rows
+bool encode_rows(void* out, const double* base, long long rows, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {16, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {16 * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+             const_cast<double*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class S, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
-  const size_t smem = sizeof(StepShared<S::NSEG, S::WARPS>) +
-                      sizeof(double) * ((size_t)zc_smem_len<S>(P.narrow) +
-                                        2 * (size_t)S::T * (S::MPT + 1));
-  auto k = sweep_kernel<S, SRC>;
+  SweepTma X{};
+  // measured (tools/sweep_time.py): the TMA path wins for M >= 4096 (c2
+  // G^-1 2.87 -> 2.28 ms, c4 11.1 -> 8.9 ms) and loses for c3 (M = 2048,
+  // two coarse steps per slab amortise the slot-layout I/O)
+  bool tma = S::NSEG == 1 && S::MPT % 2 == 0 && S::SUB % 2 == 0 && P.M % 16 == 0 &&
+             P.M >= 4096 &&
+             (reinterpret_cast<uintptr_t>(A.W) % 16) == 0 &&
+             (!A.V || (reinterpret_cast<uintptr_t>(A.V) % 16) == 0) &&
+             std::getenv("PIT_NO_TMA") == nullptr;
+  if (tma) {
+    X.rows = P.M / 16;
+    X.box_rows = X.rows;
+    while (X.box_rows > 256) X.box_rows /= 2;
+    tma = X.rows % X.box_rows == 0 && (X.box_rows % 8) == 0 &&
+          encode_rows(X.w, A.W, (long long)A.count * X.rows, X.box_rows) &&
+          (!A.V || encode_rows(X.v, A.V, (long long)A.count * X.rows, X.box_rows));
+  }
+  const size_t buf_bytes =
+      tma ? (size_t)P.M * sizeof(double) : (size_t)S::T * (S::MPT + 1) * sizeof(double);
+  const size_t fixed = sizeof(StepShared<S::NSEG, S::WARPS>) +
+                       sizeof(double) * (size_t)zc_smem_len<S>(P.narrow) + 1024 +
+                       4 * sizeof(uint64_t);
+  X.nbuf = 2;
+  if (tma)
+    for (int n = 4; n >= 3; --n)
+      if (fixed + n * buf_bytes <= 227 * 1024) {
+        X.nbuf = n;
+        break;
+      }
+  const size_t smem = fixed + (size_t)X.nbuf * buf_bytes;
+  auto k = tma ? sweep_kernel<S, SRC, true> : sweep_kernel<S, SRC, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<1, S::T, smem, st>>>(P, A);
+  k<<<1, S::T, smem, st>>>(P, A, X);
   return cudaGetLastError();
 }
 

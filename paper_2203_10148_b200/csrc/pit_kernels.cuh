@@ -53,6 +53,16 @@ struct SweepArgs {
 
 constexpr int kMaxPieces = 64;
 
+// K2 TMA path: V and W viewed as [rows][16] doubles (128-byte rows),
+// 128-byte swizzled boxes of `box_rows` rows (host-encoded tensor maps).
+struct __align__(64) SweepTma {
+  unsigned char v[128];  // CUtensorMap of V (unused when V == nullptr)
+  unsigned char w[128];  // CUtensorMap of W
+  int rows;              // rows per slab = M / 16
+  int box_rows;          // rows per TMA box (divides rows, <= 256)
+  int nbuf;              // slab buffers (3 when shared memory allows, else 2)
+};
+
 // Launchers; return cudaErrorInvalidConfiguration for an uncompiled layout.
 cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st);

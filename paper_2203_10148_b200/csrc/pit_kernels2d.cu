@@ -18,6 +18,7 @@
 //   barrier, then every thread sums the slots in the same fixed order.
 // Every operation order here is mirrored by oracle/pit_oracle2d.c.
 #include "pit_kernels2d.cuh"
+#include "pit_sync.cuh"
 
 #include <cooperative_groups.h>
 
@@ -43,46 +44,6 @@ __device__ __forceinline__ void cl_sync() {
 __device__ __forceinline__ double ex_point(double ac, double an, double y, double w, double e,
                                            double n, double s) {
   return fma(ac, y, an * ((w + e) + (n + s)));
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 16 bytes into a peer CTA's shared memory; completion counted on the
-// peer's mbarrier (no fence or barrier on the sending side)
-__device__ __forceinline__ void st_async_v2(uint32_t raddr, double a, double b, uint32_t rbar) {
-  asm volatile(
-      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
-          raddr),
-      "d"(a), "d"(b), "r"(rbar)
-      : "memory");
 }
 
 __device__ __forceinline__ void st_async_1(uint32_t raddr, double a, uint32_t rbar) {

@@ -36,6 +36,13 @@ namespace pitb {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Barrier among the slab's T compute threads only (named barrier 1): the
+// coarse sweep adds I/O warps that never enter the step.
+template <int T>
+__device__ __forceinline__ void step_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(T) : "memory");
+}
+
 struct StepParams {
   double nl, nu, inv, gneg, invR, invLast;
   double pS, qS;            // nl^SUB, nu^SUB        (sub-chunk carry weights)
@@ -171,7 +178,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
 #pragma unroll
       for (int s = 0; s < NSEG; ++s) sh.fw[s][warp] = I[s];
     }
-    __syncthreads();
+    step_sync<S::T>();
     for (int v = 0; v < warp; ++v)
 #pragma unroll
       for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.p32, Wc[s], sh.fw[s][v]);
@@ -249,7 +256,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
 #pragma unroll
       for (int s = 0; s < NSEG; ++s) sh.bw[s][warp] = I[s];
     }
-    __syncthreads();
+    step_sync<S::T>();
     for (int v = WARPS - 1; v > warp; --v)
 #pragma unroll
       for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.q32, Wc[s], sh.bw[s][v]);
@@ -305,7 +312,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     }
   } else {
     if (tid == 0) sh.b = y[0][0];
-    __syncthreads();
+    step_sync<S::T>();
     const double cc = P.gneg * sh.b;
 #pragma unroll
     for (int c = 0; c < NC; ++c)

@@ -31,6 +31,8 @@ for slabs in (2, 889, 1024):
         out = (C.c_longlong * 32)()
         assert L.pit_debug_phase_timing(ctx.handle, 1, out) == 0
         n = (p.N - 1) * p.coarse_steps
+        print(f"{name} coarse sweep I/O warp: wait W {out[12]/n:.0f} | store W {out[13]/n:.0f} | "
+              f"load V {out[14]/n:.0f} cyc per slab", flush=True)
         for w in (0, 1):
             v = [out[w * 16 + k] / n for k in range(12)]
             print(f"{name} coarse sweep warp{w}: per coarse step | " +
