@@ -244,7 +244,7 @@ def device_time_to_tolerance(name):
             **({"coarse_cg_iterations": int(its)} if its else {})}
 
 
-def secondary(include_c5_solve=False):
+def secondary(include_c5_solve=True):
     out = {"apply_F": {}, "time_to_tolerance": {}}
     for name in ("c1", "c3", "c4", "c5"):
         try:
