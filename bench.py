@@ -161,9 +161,12 @@ def run_reference_arm(args, rank, world):
         if i >= args.warmup:
             rates.append(r)
     v = float(np.median(rates))
+    gp_full = configs.gp_steps_per_apply(p)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "steps": args.steps, "warmup": args.warmup,
+        # one full c2 apply_F at the sampled rate (the sample covers 2*cores+1 slabs)
+        "ms_per_step": gp_full / v * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE c2 inputs, seed 1234)",
         "config": {"workload": f"{CONFIG_NAME}: {configs.DESCRIPTIONS[CONFIG_NAME]}",
