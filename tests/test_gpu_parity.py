@@ -337,3 +337,26 @@ def test_sharded_device_driver_with_source_matches_device_solver():
              for x in res.history.records]
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,slabs,M", [("c1", 4, 100), ("c3", 5, 60), ("c4", 4, 50), ("c5", 3, 10)])
+def test_dense_verification_through_device_operators(name, slabs, M):
+    # run_oracle_checks / `pit verify` (dense_oracle.cpp:110-237) on the GPU
+    # operators, and its negative control
+    from paper_2203_10148_b200 import verify
+
+    p = configs.make(name, slabs=slabs, M=M)
+    with api.BlockOperatorContext(p) as ctx:
+        rep = verify.run_oracle_checks(ctx, trials=2, tolerance=1e-9)
+        bad = verify.run_oracle_checks(ctx, trials=1, tolerance=1e-9, inject_fault=True)
+    assert rep.all_passed(), [(c.name, c.worst_relative_error) for c in rep.checks]
+    assert not any(c.passed for c in bad.checks)
+
+
+def test_dense_verification_size_guard():
+    from paper_2203_10148_b200 import verify
+
+    p = configs.make("c1", slabs=16, M=200)
+    with api.BlockOperatorContext(p) as ctx:
+        with pytest.raises(api.ConfigError):
+            verify.assemble_dense_system(ctx)
