@@ -220,6 +220,9 @@ Ex2Params ex2_params(const pit_context* ctx) {
   P.steps = ctx->c2.fine_steps;
   P.ac = ctx->c2.ac;
   P.an = ctx->c2.an;
+#ifdef PIT_PHASE_TIMING
+  P.timing = ctx->role[PIT_FINE].P.timing;
+#endif
   P.scaled = ctx->c2.scaled;
   P.R = ctx->c2.R;
   P.kappa = ctx->c2.kappa;
@@ -242,6 +245,9 @@ Cg2Params cg2_params(const pit_context* ctx) {
   P.minv = ctx->c2.minv;
   P.rel_tol = ctx->c2.rel_tol;
   P.cap = ctx->c2.cap;
+#ifdef PIT_PHASE_TIMING
+  P.timing = ctx->role[PIT_COARSE].P.timing;
+#endif
   return P;
 }
 
@@ -639,8 +645,8 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
   cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, desc->device);
 #ifdef PIT_PHASE_TIMING
   for (int r = 0; r < 2; ++r) {
-    cudaMalloc(&ctx->role[r].P.timing, 32 * sizeof(long long));
-    cudaMemset(ctx->role[r].P.timing, 0, 32 * sizeof(long long));
+    cudaMalloc(&ctx->role[r].P.timing, 64 * sizeof(long long));
+    cudaMemset(ctx->role[r].P.timing, 0, 64 * sizeof(long long));
   }
 #endif
   if (const char* e = std::getenv("PIT_STAGGER")) ctx->stagger = std::atoi(e);
@@ -1353,7 +1359,7 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
 extern "C" int pit_debug_phase_timing(pit_context* ctx, int role, long long* out32) {
 #ifdef PIT_PHASE_TIMING
   CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(out32, ctx->role[role].P.timing, 32 * sizeof(long long),
+  CUDA_TRY(cudaMemcpy(out32, ctx->role[role].P.timing, 64 * sizeof(long long),
                       cudaMemcpyDeviceToHost));
   return PIT_OK;
 #else

@@ -179,6 +179,20 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   publish(0, true);
 
   int until_rescale = P.R;
+#ifdef PIT_PHASE_TIMING
+  long long tacc[6] = {};
+  long long tt = clock64();
+#define K4_PHASE(i)                     \
+  do {                                  \
+    const long long now_ = clock64();   \
+    tacc[i] += now_ - tt;               \
+    tt = now_;                          \
+  } while (0)
+#else
+#define K4_PHASE(i) \
+  do {              \
+  } while (0)
+#endif
   for (int k = 0; k < P.steps; ++k) {
     const int par = k & 1;
     const bool more = k + 1 < P.steps;  // y^{k+1} halos are consumed
@@ -198,7 +212,9 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
     }
 #pragma unroll
     for (int i = 0; i < TR; ++i) shfl_row(i);
+    K4_PHASE(0);
     mbar_wait(&my_bar[par], (k >> 1) & 1);  // halo rows of y^k
+    K4_PHASE(1);
     // new first/last rows into separate registers: y keeps y^k until the
     // interior rows are done
     double n0[TC], nT[TC];
@@ -231,6 +247,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
         if (row0 + TR - 1 >= m || col0 + j >= m) nT[j] = 0.0;
       }
     }
+    K4_PHASE(2);
     {  // publish y^{k+1} first/last rows; their shuffles for step k+1
       double* t0 = TOP(par ^ 1, warp) + col0;
       double* b0 = BOT(par ^ 1, warp + 1) + col0;
@@ -250,6 +267,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
           send_row<TC>(dn_bot + (par ^ 1) * kParBytes, nT, dn_bar + 8 * (par ^ 1));
       }
     }
+    K4_PHASE(3);
     // interior rows 1..TR-2 of y^{k+1}
     {
       double prev[TC];
@@ -278,7 +296,12 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
       y[0][j] = n0[j];
       y[TR - 1][j] = nT[j];
     }
+    K4_PHASE(4);
   }
+#ifdef PIT_PHASE_TIMING
+  if (P.timing && blockIdx.x == 0 && lane == 0)
+    for (int i = 0; i < 5; ++i) P.timing[warp * 8 + i] = tacc[i];
+#endif
   if (SCALED) {
 #pragma unroll
     for (int i = 0; i < TR; ++i)
@@ -393,7 +416,8 @@ __global__ void __launch_bounds__(256, 1)
   const int pitch = NT + 2;
   double* const Ps = smc;                              // [(RM+2)][pitch], own rows 1..R
   double* const red = smc + (size_t)(RM + 2) * pitch;  // [2][kSlotCap][2]
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(red + 4 * kSlotCap);  // rbar[2], hbar
+  double* const Bs = red + 4 * kSlotCap;               // [RM][NT]: the step's right-hand side
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(Bs + (size_t)RM * NT);  // rbar[2], hbar
   const double D = P.D, O = P.O, minv = P.minv;
   const unsigned red_bytes = 16u * (unsigned)nslot;
   const unsigned halo_bytes = 8u * (unsigned)NT * ((c > 0) + (c < C - 1));
@@ -447,8 +471,12 @@ __global__ void __launch_bounds__(256, 1)
     if (t == 0) mbar_arrive_expect_tx(&bars[pair], red_bytes);  // its next use
     pair ^= 1;
   };
-  // field value v at own row k into the stencil buffer (+ neighbours' halos)
+  // f: the published field (the stencil's operand) in registers; its own
+  // rows also in the stencil buffer (west/east neighbours of other threads)
+  // and its first/last row in the neighbours' halo rows
+  double f[RM];
   auto put = [&](int k, double v) {
+    f[k] = v;
     if (k < R) Ps[(size_t)(k + 1) * pitch + t + 1] = v;
     if (k == 0 && up_row) st_async_1(up_row, v, up_bar);
     if (k == R - 1 && dn_row) st_async_1(dn_row, v, dn_bar);
@@ -460,20 +488,41 @@ __global__ void __launch_bounds__(256, 1)
     hph ^= 1u;
     if (t == 0) mbar_arrive_expect_tx(&bars[2], halo_bytes);
   };
-  auto own = [&](int k) { return k < R ? Ps[(size_t)(k + 1) * pitch + t + 1] : 0.0; };
+  // (S f)_k = fma(D, f, O*((w + e) + (n + s))): north/south from the strip
+  // (halo rows at its ends), west/east from the stencil buffer
+  auto stencil = [&](int k) {
+    const double* row = Ps + (size_t)(k + 1) * pitch + t + 1;
+    const double n = k == 0 ? row[-pitch] : f[k > 0 ? k - 1 : 0];
+    const double s = k == R - 1 ? row[pitch] : f[k + 1 < RM ? k + 1 : RM - 1];
+    return fma(D, f[k], O * ((row[-1] + row[1]) + (n + s)));
+  };
 
-  double x[RM], r[RM], bb[RM], q[RM];
+  double x[RM], r[RM], q[RM];
 #pragma unroll
-  for (int k = 0; k < RM; ++k) bb[k] = valid[k] ? A.start[gidx(k)] : 0.0;
+  for (int k = 0; k < RM; ++k) Bs[k * NT + t] = valid[k] ? A.start[gidx(k)] : 0.0;
 
   long long total_it = 0;
+#ifdef PIT_PHASE_TIMING
+  long long k5acc[8] = {};
+  long long k5t = clock64();
+#define K5_T(i)                            \
+  do {                                     \
+    const long long now_ = clock64();      \
+    if (i > 0) k5acc[i] += now_ - k5t;     \
+    k5t = now_;                            \
+  } while (0)
+#else
+#define K5_T(i) \
+  do {          \
+  } while (0)
+#endif
   for (int s = 0; s < A.count; ++s) {
     const int slab = A.slab0 + s;
     bool ok = true;
     for (int cs = 0; cs < P.steps && ok; ++cs) {
       if (cs > 0) {
 #pragma unroll
-        for (int k = 0; k < RM; ++k) bb[k] = x[k];
+        for (int k = 0; k < RM; ++k) Bs[k * NT + t] = x[k];
       }
 #pragma unroll
       for (int k = 0; k < RM; ++k) x[k] = 0.0;
@@ -481,7 +530,10 @@ __global__ void __launch_bounds__(256, 1)
       {
         double a = 0.0;
 #pragma unroll
-        for (int k = 0; k < RM; ++k) a = fma(bb[k], bb[k], a);
+        for (int k = 0; k < RM; ++k) {
+          const double bk = Bs[k * NT + t];
+          a = fma(bk, bk, a);
+        }
         reduce2(a, 0.0, nb2, dummy);
       }
       const double nb = sqrt(nb2);
@@ -492,7 +544,7 @@ __global__ void __launch_bounds__(256, 1)
           double a = 0.0, b2 = 0.0;
 #pragma unroll
           for (int k = 0; k < RM; ++k) {
-            r[k] = bb[k];
+            r[k] = Bs[k * NT + t];
             const double z = minv * r[k];  // p = z
             put(k, z);
             a = fma(r[k], z, a);
@@ -507,14 +559,17 @@ __global__ void __launch_bounds__(256, 1)
         for (;;) {
           while (res > tol && it < P.cap && !stalled) {
             double pq, d0;
+            K5_T(0);
             {
               double a = 0.0;
 #pragma unroll
               for (int k = 0; k < RM; ++k) {
-                q[k] = valid[k] ? stencil_S(Ps, pitch, k, t, D, O) : 0.0;
-                a = fma(own(k), q[k], a);
+                q[k] = valid[k] ? stencil(k) : 0.0;
+                a = fma(f[k], q[k], a);
               }
+              K5_T(1);
               reduce2(a, 0.0, pq, d0);
+              K5_T(2);
             }
             if (pq == 0.0 || !isfinite(pq)) {
               stalled = true;
@@ -526,22 +581,26 @@ __global__ void __launch_bounds__(256, 1)
               double a = 0.0, b2 = 0.0;
 #pragma unroll
               for (int k = 0; k < RM; ++k) {
-                x[k] = fma(alpha, own(k), x[k]);
+                x[k] = fma(alpha, f[k], x[k]);
                 r[k] = fma(-alpha, q[k], r[k]);
                 const double z = minv * r[k];
                 a = fma(r[k], r[k], a);
                 b2 = fma(r[k], z, b2);
               }
               ++it;
+              K5_T(3);
               reduce2(a, b2, rr, rzn);
+              K5_T(4);
             }
             res = sqrt(rr);
             if (!isfinite(res) || res <= tol) break;
             const double beta = rzn / rz;
 #pragma unroll
-            for (int k = 0; k < RM; ++k) put(k, fma(beta, own(k), minv * r[k]));
+            for (int k = 0; k < RM; ++k) put(k, fma(beta, f[k], minv * r[k]));
+            K5_T(5);
             published();
             rz = rzn;
+            K5_T(6);
           }
           // confirm against the exact residual (sparse.cpp:101-104)
 #pragma unroll
@@ -551,7 +610,7 @@ __global__ void __launch_bounds__(256, 1)
             double a = 0.0, b2 = 0.0;
 #pragma unroll
             for (int k = 0; k < RM; ++k) {
-              r[k] = valid[k] ? bb[k] - stencil_S(Ps, pitch, k, t, D, O) : 0.0;
+              r[k] = valid[k] ? Bs[k * NT + t] - stencil(k) : 0.0;
               const double z = minv * r[k];
               a = fma(r[k], r[k], a);
               b2 = fma(r[k], z, b2);
@@ -585,15 +644,17 @@ __global__ void __launch_bounds__(256, 1)
     double* Wb = A.W + (size_t)s * m * m;
 #pragma unroll
     for (int k = 0; k < RM; ++k) {
-      if (valid[k]) {
-        const double v = V ? x[k] + V[gidx(k)] : x[k];
-        Wb[gidx(k)] = v;
-        bb[k] = v;
-      }
+      const double v = valid[k] ? (V ? x[k] + V[gidx(k)] : x[k]) : 0.0;
+      if (valid[k]) Wb[gidx(k)] = v;
+      Bs[k * NT + t] = v;
     }
   }
   if (iters && c == 0 && t == 0) atomicAdd(reinterpret_cast<unsigned long long*>(iters),
                                            (unsigned long long)total_it);
+#ifdef PIT_PHASE_TIMING
+  if (P.timing && c == 0 && t == 0)
+    for (int i = 0; i < 8; ++i) P.timing[i] = k5acc[i];
+#endif
   cl_sync();
 }
 
@@ -636,8 +697,9 @@ cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long*
   const int nt = 32 * ((P.m + 31) / 32);
   if (nt > 256 || P.rows > kCgRowsMax || P.cluster * (nt / 32) > kSlotCap || P.cluster > 16)
     return cudaErrorInvalidConfiguration;
-  const size_t smem =
-      sizeof(double) * ((size_t)(kCgRowsMax + 2) * (nt + 2) + 4 * kSlotCap) + 4 * sizeof(uint64_t);
+  const size_t smem = sizeof(double) * ((size_t)(kCgRowsMax + 2) * (nt + 2) + 4 * kSlotCap +
+                                        (size_t)kCgRowsMax * nt) +
+                      4 * sizeof(uint64_t);
   auto k = cg_sweep2d_kernel;
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=

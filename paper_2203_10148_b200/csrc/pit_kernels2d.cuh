@@ -19,6 +19,7 @@ struct Ex2Params {
   double ac, an;
   int scaled, R;  // scaled form (pit_step_coeffs_2d)
   double kappa, anR, anLast;
+  long long* timing;  // PIT_PHASE_TIMING builds: [warp][8] cycle totals of cluster 0, CTA 0
 };
 
 // K5: one persistent cluster; per slab one BE step (I + dt*A) x = b solved
@@ -33,6 +34,7 @@ struct Cg2Params {
   double D, O, minv;
   double rel_tol;  // kInnerSolveRelTol analogue
   long long cap;   // iteration cap (10 n, pde.hpp:79)
+  long long* timing;  // PIT_PHASE_TIMING builds: phase cycle totals (CTA 0, thread 0)
 };
 
 constexpr int kCgRowsMax = 16;
