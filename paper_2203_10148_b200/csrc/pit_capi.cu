@@ -89,7 +89,7 @@ struct pit_context {
   cudaStream_t stream = nullptr;
   // solver work buffers (N*M each), allocated on first solve
   double* buf[10] = {};
-  int stagger = 0, stagger_mod = 1, sms = 148;  // slab-kernel phase offset (see SlabArgs)
+  int sms = 148;
   // K1 piece scheduling (SlabArgs::state): 0 = from occupancy, 1 = off, n = forced
   int pieces = 0;
   double* d_state = nullptr;
@@ -408,9 +408,6 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
     CUDA_TRY(launch_explicit2d(ctx->lay2, ex2_params(ctx), A, ctas, st));
     return PIT_OK;
   }
-  A.stagger = ctx->stagger;
-  A.stagger_mod = ctx->stagger_mod;
-  A.sms = ctx->sms;
   PIT_TRY(attach_pieces(ctx, &A, ctas));
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
   if (!ctx->d_trace) CUDA_TRY(cudaMalloc(&ctx->d_trace, sizeof(long long) * 8 * kMaxPieces * (size_t)ctx->N));
@@ -649,8 +646,6 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     cudaMemset(ctx->role[r].P.timing, 0, 64 * sizeof(long long));
   }
 #endif
-  if (const char* e = std::getenv("PIT_STAGGER")) ctx->stagger = std::atoi(e);
-  if (const char* e = std::getenv("PIT_STAGGER_MOD")) ctx->stagger_mod = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("PIT_PIECES")) ctx->pieces = std::max(0, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess ||

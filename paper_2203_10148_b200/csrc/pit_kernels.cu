@@ -237,15 +237,6 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
     const int slab = A.slab0 + b;
     __syncthreads();
     const StepLane L = step_lane<S>(P, *sh, tid);
-    if (A.stagger > 0) {
-      // Offset the step phase of co-resident CTAs (block ids differing by a
-      // multiple of the SM count) — tuning knob, off by default.
-      const long long wait = (long long)((b / A.sms) % A.stagger_mod) * A.stagger;
-      const long long t0 = clock64();
-      while (clock64() - t0 < wait) {
-      }
-      __syncthreads();
-    }
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     const long long tr0 = global_ns();
 #endif

@@ -23,9 +23,6 @@ struct SlabArgs {
   const double* L0;    // block 0 (done by CTA 0 when non-null):
   const double* rhs0;  //   kApplyF:   out0 = L0
   double* out0;        //   kResidual: out0 = rhs0 - L0
-  int stagger;         // cycles of start offset per phase class (0 = off)
-  int stagger_mod;     // number of phase classes
-  int sms;             // SM count (co-residency stride of block ids)
   // Piece scheduling (launch_slab fills pieces/nblk): when the batch exceeds
   // one wave of resident CTAs, each slab's steps are cut into `pieces`
   // consecutive step ranges and a persistent grid pops (piece, slab) units
