@@ -164,6 +164,9 @@ typedef struct pit_step_coeffs {
   int32_t narrow;         /* corner correction in geometric form */
   double pp[5], qq[5], p32, q32;
   double plane[32], qlane[32];
+  /* Kogge-Stone stages per direction: terms whose weight (nl^ch)^d, d > 2^s,
+   * is <= 2^-70 are dropped (the same rule as K0): 5 = exact warp scan */
+  int32_t scan_f, scan_b;
 } pit_step_coeffs;
 
 const char* pit_last_error(void);

@@ -92,7 +92,10 @@ int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int nseg, int warps
     s->pS = (double)nlp[sub];
     s->qS = (double)nup[sub];
     ld pk = nlp[ch], qk = nup[ch];
+    s->scan_f = s->scan_b = 5;
     for (int k = 0; k < 5; ++k) {
+      if (s->scan_f == 5 && fabsl(pk) <= 8.470329472543003e-22L) s->scan_f = k;
+      if (s->scan_b == 5 && fabsl(qk) <= 8.470329472543003e-22L) s->scan_b = k;
       s->pp[k] = (double)pk;
       s->qq[k] = (double)qk;
       pk = pk * pk;
@@ -187,7 +190,7 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     }
     for (int w = 0; w < W; ++w) {
       double* I = Z + 32 * w;
-      for (int st = 0; st < 5; ++st) {
+      for (int st = 0; st < s->scan_f; ++st) {
         int off = 1 << st;
         for (int l = 0; l < 32; ++l) tmp[l] = (l >= off) ? fma(s->pp[st], I[l - off], I[l]) : I[l];
         memcpy(I, tmp, 32 * sizeof(double));
@@ -242,7 +245,7 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     }
     for (int w = 0; w < W; ++w) {
       double* J = Z + 32 * w;
-      for (int st = 0; st < 5; ++st) {
+      for (int st = 0; st < s->scan_b; ++st) {
         int off = 1 << st;
         for (int l = 0; l < 32; ++l)
           tmp[l] = (l < 32 - off) ? fma(s->qq[st], J[l + off], J[l]) : J[l];
@@ -285,7 +288,7 @@ static void chunked_solve(const orc_stepper* s, double* y, double* scratch) {
     if (s->narrow) {
       for (int k = 0; k < 32 && k * ch < s->K0; ++k) {
         const double a = cc * s->zt[k];
-        for (int u = 0; u < nu_; ++u) {
+        for (int u = 0; u < nu_ && u * sub < s->K0; ++u) {
           const double au = a * s->pw[u];
           for (int j = 0; j < sub; ++j) {
             double* v = y + (size_t)k * ch + u * sub + j;

@@ -71,6 +71,8 @@ typedef struct orc_stepper {
   double* ppos;            /* [32*warps] nl^(t*ch), ch = nsub*sub */
   double* qpos;            /* [32*warps] nu^((T-1-t)*ch) */
   double* zt;              /* [32*warps] zc_0 nl^(t*ch) */
+  int scan_f, scan_b;      /* warp-scan stages kept per direction: the first
+                              dropped term has weight (nl^ch)^(2^s) <= 2^-70 */
 } orc_stepper;
 
 int orc_stepper_init(orc_stepper* s, int M, int m, int nsub, int nseg, int warps, int steps,

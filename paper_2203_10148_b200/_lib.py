@@ -96,7 +96,7 @@ class StepCoeffsC(C.Structure):
                 ("nlpow", C.c_double * 32), ("pw", C.c_double * 8), ("narrow", C.c_int32),
                 ("pp", C.c_double * 5), ("qq", C.c_double * 5),
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
-                ("qlane", C.c_double * 32)]
+                ("qlane", C.c_double * 32), ("scan_f", C.c_int32), ("scan_b", C.c_int32)]
 
 
 EXPORTS = [

@@ -117,6 +117,14 @@ int build_step_coeffs(int M, int mpt, int nsub, int nseg, int warps, int steps, 
     c->pS = (double)nlp[sub];
     c->qS = (double)nup[sub];
     ld pk = nlp[ch], qk = nup[ch];
+    c->scan_f = 5;
+    c->scan_b = 5;
+    for (int k = 4; k >= 0; --k) {  // smallest s with (nl^ch)^(2^s) <= 2^-70
+      ld a = nlp[ch], b = nup[ch];
+      for (int r = 0; r < k; ++r) a = a * a, b = b * b;
+      if (fabsl(a) <= 8.470329472543003e-22L) c->scan_f = k;
+      if (fabsl(b) <= 8.470329472543003e-22L) c->scan_b = k;
+    }
     for (int k = 0; k < 5; ++k) {
       c->pp[k] = (double)pk;
       c->qq[k] = (double)qk;

@@ -7,7 +7,9 @@
 // vectors stay in HBM; per iteration only the per-block reduction partials
 // (N doubles per phase) come back to the host, where they are summed in slab
 // order exactly as block_inner_product does (block_system.cpp:76-87).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <chrono>
@@ -101,6 +103,12 @@ struct pit_context {
   double* scratch[3] = {};
   size_t scratch_n[3] = {};
   bool scratch_busy[3] = {};
+  // host-buffer pipelining of pit_apply_F (see pipelined_apply_F)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_pipe = nullptr;
+  unsigned* d_sync = nullptr;  // [1 + kPipeMaxChunks]: in_ready, out_done[]
+  int pipe = -1;               // -1 untested, 0 unavailable/off, 1 ready
+  int pipe_chunks = 0;         // PIT_E2E_CHUNKS (0 = auto)
   size_t nm() const { return (size_t)N * (size_t)M; }
 };
 
@@ -315,6 +323,8 @@ void fill_params(const pit_step_coeffs& c, StepParams* P) {
   P->steps = c.steps;
   P->R = c.R;
   P->K0 = c.K0;
+  P->scan_f = c.scan_f;
+  P->scan_b = c.scan_b;
 }
 
 int check_status(pit_context* ctx, bool fine_batch) {
@@ -368,10 +378,16 @@ int attach_pieces(pit_context* ctx, SlabArgs* A, int ctas) {
 
 // Fine batch over output blocks [first, first+count) (global indices).
 int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* halo,
-                   const double* rhs, double* out, int first, int count, cudaStream_t st) {
+                   const double* rhs, double* out, int first, int count, cudaStream_t st,
+                   const unsigned* in_ready = nullptr, unsigned* out_done = nullptr,
+                   int chunk_blocks = 0) {
   Role& R = ctx->role[PIT_FINE];
   SlabArgs A{};
   A.mode = mode;
+  A.in_ready = in_ready;
+  A.out_done = out_done;
+  A.chunk_blocks = chunk_blocks;
+  A.block_shift = first == 0 ? 1 : 0;
   A.status = ctx->d_status;
   const size_t M = ctx->M;
   int ctas;
@@ -681,6 +697,10 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_sched);
   cudaFree(ctx->d_trace);
   cudaFree(ctx->d_cg_iters);
+  cudaFree(ctx->d_sync);
+  if (ctx->ev_pipe) cudaEventDestroy(ctx->ev_pipe);
+  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PIT_OK;
@@ -889,10 +909,140 @@ void add_coarse(pit_context* ctx, pit_run_stats* s, double ms) {
 
 }  // namespace
 
+namespace {
+
+constexpr int kPipeMaxChunks = 64;
+
+PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Lazily sets up the copy streams, the event and the chunk counters, and
+// probes stream memory operations once (pipe = 0 when anything is missing:
+// pit_apply_F then copies, computes and copies back in sequence).
+int pipe_setup(pit_context* ctx) {
+  if (ctx->pipe >= 0) return PIT_OK;
+  ctx->pipe = 0;
+  if (const char* e = std::getenv("PIT_E2E_CHUNKS")) {
+    ctx->pipe_chunks = std::atoi(e);
+    if (ctx->pipe_chunks < 0) return PIT_OK;  // < 0: pipelining off
+  }
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) !=
+          cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+    return PIT_OK;
+  g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+  if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault, &q) !=
+          cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+    return PIT_OK;
+  g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_pipe, cudaEventDisableTiming));
+  CUDA_TRY(cudaMalloc(&ctx->d_sync, sizeof(unsigned) * (1 + kPipeMaxChunks)));
+  CUDA_TRY(cudaMemsetAsync(ctx->d_sync, 0, sizeof(unsigned) * (1 + kPipeMaxChunks), ctx->stream));
+  // probe: a write and an already-satisfied wait
+  if (g_write32((CUstream)ctx->stream, (CUdeviceptr)ctx->d_sync, 1u, 0) != CUDA_SUCCESS ||
+      g_wait32((CUstream)ctx->stream, (CUdeviceptr)ctx->d_sync, 1u, CU_STREAM_WAIT_VALUE_GEQ) !=
+          CUDA_SUCCESS) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return PIT_OK;
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->pipe = 1;
+  return PIT_OK;
+}
+
+// pit_apply_F over pinned host buffers with the copies overlapped with K1:
+// the input goes up in chunks of whole blocks on the h2d stream (each chunk
+// followed by a stream write in_ready = k+1); K1's CTAs wait for the chunk
+// holding their blocks; each CTA counts its finished output block into
+// out_done[chunk]; the d2h stream waits for a chunk's count and copies it
+// back.  Same kernel, same arithmetic: the output is bit-identical to the
+// sequential path.
+int pipelined_apply_F(pit_context* ctx, const double* L, double* out, double* dL, double* dO) {
+  const int N = ctx->N;
+  const size_t M = ctx->M;
+  int nch = ctx->pipe_chunks > 0 ? ctx->pipe_chunks : 16;
+  nch = std::min(std::min(nch, kPipeMaxChunks), N);
+  const int cb = (N + nch - 1) / nch;  // blocks per chunk
+  nch = (N + cb - 1) / cb;
+  auto unblock = [&]() {  // release every waiter (error paths)
+    for (int k = 0; k <= nch; ++k)
+      g_write32((CUstream)ctx->stream, (CUdeviceptr)(ctx->d_sync + k), 0x7fffffffu, 0);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->h2d);
+    cudaStreamSynchronize(ctx->d2h);
+  };
+  CUDA_TRY(cudaMemsetAsync(ctx->d_sync, 0, sizeof(unsigned) * (1 + nch), ctx->stream));
+  CUDA_TRY(cudaEventRecord(ctx->ev_pipe, ctx->stream));
+  CUDA_TRY(cudaStreamWaitEvent(ctx->h2d, ctx->ev_pipe, 0));
+  CUDA_TRY(cudaStreamWaitEvent(ctx->d2h, ctx->ev_pipe, 0));
+  for (int k = 0; k < nch; ++k) {
+    const size_t b0 = (size_t)k * cb, nb = std::min((size_t)cb, (size_t)N - b0);
+    cudaError_t e = cudaMemcpyAsync(dL + b0 * M, L + b0 * M, nb * M * sizeof(double),
+                                    cudaMemcpyHostToDevice, ctx->h2d);
+    if (e != cudaSuccess || g_write32((CUstream)ctx->h2d, (CUdeviceptr)ctx->d_sync,
+                                      (unsigned)(k + 1), 0) != CUDA_SUCCESS) {
+      unblock();
+      return set_err(PIT_ERR_CUDA, "apply_F: pipelined host-to-device copy failed");
+    }
+  }
+  for (int k = 0; k < nch; ++k) {
+    const size_t b0 = (size_t)k * cb, nb = std::min((size_t)cb, (size_t)N - b0);
+    if (g_wait32((CUstream)ctx->d2h, (CUdeviceptr)(ctx->d_sync + 1 + k), (unsigned)nb,
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+        cudaMemcpyAsync(out + b0 * M, dO + b0 * M, nb * M * sizeof(double),
+                        cudaMemcpyDeviceToHost, ctx->d2h) != cudaSuccess) {
+      unblock();
+      return set_err(PIT_ERR_CUDA, "apply_F: pipelined device-to-host copy failed");
+    }
+  }
+  // One CTA per slab unless PIT_PIECES forces a cut (measured on c2,
+  // tools/e2e_probe.py): CTAs start as their chunk lands and so finish
+  // staggered, which lets the D2H copies overlap the kernel's tail; piece
+  // scheduling packs the kernel tighter (1.78 vs 2.12 ms) but ends every slab
+  // at once and leaves the whole D2H after it (2.81 vs 2.48 ms end to end).
+  const int saved_pieces = ctx->pieces;
+  if (ctx->pieces == 0) ctx->pieces = 1;
+  int rc = run_slab_batch(ctx, kApplyF, dL, nullptr, nullptr, dO, 0, N, ctx->stream, ctx->d_sync,
+                          ctx->d_sync + 1, cb);
+  ctx->pieces = saved_pieces;
+  if (rc) {
+    const std::string msg = g_err;
+    unblock();
+    return set_err(rc, msg);
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
+  return check_status(ctx, true);
+}
+
+}  // namespace
+
 int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats) {
   if (!ctx || !L || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: null argument");
   ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
+  if (ctx->dim == 1 && ctx->N >= 32 && is_pinned(L) && is_pinned(out)) {
+    PIT_TRY(pipe_setup(ctx));
+    if (ctx->pipe == 1) {
+      DevVec dL, dO;
+      PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &dL));
+      PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &dO));
+      PIT_TRY(pipelined_apply_F(ctx, L, out, dL.p, dO.p));
+      add_fine(ctx, stats, ms_since(t0));
+      return PIT_OK;
+    }
+  }
   DevVec dL, dO;
   PIT_TRY(to_device(ctx, L, ctx->nm(), &dL));
   PIT_TRY(to_device(ctx, nullptr, ctx->nm(), &dO));

@@ -211,6 +211,46 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Host-buffer pipelining (SlabArgs::in_ready / out_done): wait until the
+// chunk holding output block g (and so input blocks g-1, g) has landed.
+__device__ __noinline__ void wait_input(const SlabArgs& A, int b, int tid) {
+  if (A.in_ready == nullptr) return;
+  if (tid == 0) {
+    const unsigned need = (unsigned)((b + A.block_shift) / A.chunk_blocks) + 1u;
+    long long t0 = -1;
+    while (ld_acquire_sys(A.in_ready) < need) {
+      // never hang the device on a lost copy: give up after 20 s and report
+      // the slab as failed
+      long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 < 0) t0 = now;
+      if (now - t0 > 20000000000LL) {
+        atomicMin(A.status, A.slab0 + b);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+// ... and publish block g (plus block 0 for CTA 0) once every thread's
+// output stores are globally visible.
+__device__ __noinline__ void signal_output(const SlabArgs& A, int b, int tid) {
+  if (A.out_done == nullptr) return;
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(A.out_done + (b + A.block_shift) / A.chunk_blocks, 1u);
+    if (b == 0 && A.out0 != nullptr) atomicAdd(A.out_done, 1u);
+  }
+}
+
 // K1.  One CTA per slab (A.state == nullptr), or a persistent grid pulling
 // (piece, slab) units piece-major (see SlabArgs) so that a batch of
 // 1.15 waves does not leave the last wave's SMs one-sixth occupied.
@@ -233,6 +273,7 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
 
   if (A.state == nullptr) {
     const int b = blockIdx.x;
+    wait_input(A, b, tid);
     load_field<S>(y, source_of(b), tid, M);
     const int slab = A.slab0 + b;
     __syncthreads();
@@ -242,6 +283,7 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
 #endif
     run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
     slab_epilogue<S>(y, A, M, tid, b, slab);
+    signal_output(A, b, tid);
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     if (A.trace && tid == 0) {
       long long* t = A.trace + 8 * (size_t)b;
@@ -286,6 +328,7 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
     const long long tr0 = global_ns();
 #endif
     if (q == 0) {
+      wait_input(A, b, tid);
       load_field<S>(y, source_of(b), tid, M);
     } else {
       load_state<S>(y, st, tid);
@@ -307,6 +350,7 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
       if (tid == 0) st_release(queue + atomicAdd(tail, 1), u + A.nblk + 1);
     } else {
       slab_epilogue<S>(y, A, M, tid, b, slab);
+      signal_output(A, b, tid);
     }
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     if (A.trace && tid == 0) {
@@ -762,9 +806,24 @@ int ew_grid(size_t n) {
 
 #define PIT_SHAPE(MP, NU, NS, W) Shape<(MP) / ((NU) * (NS)), NU, NS, W>
 
+// Fine layouts specialised on the scan stage count (PIT_SCAN_SPECIAL(X):
+// layout, stages).  Measured: a run-time stage count costs c4 8% against
+// the compile-time loop.
+#define PIT_SCAN_SPECIAL(X)                                                                  \
+  X(64, 4, 1, 1, 0) X(64, 4, 1, 1, 1) X(64, 4, 1, 1, 2) X(64, 4, 1, 1, 3)                   \
+  X(64, 4, 1, 2, 0) X(64, 4, 1, 2, 1) X(64, 4, 1, 2, 2) X(64, 4, 1, 2, 3)                   \
+  X(64, 4, 1, 4, 0) X(64, 4, 1, 4, 1) X(64, 4, 1, 4, 2) X(64, 4, 1, 4, 3)
+
 cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st) {
   if (ctas <= 0) return cudaSuccess;
+  if (!src && P.scan_f == P.scan_b) {
+#define X(MP, NU, NS, W, K)                                                                  \
+  if (mpt == MP && nsub == NU && nseg == NS && warps == W && P.scan_f == K)                  \
+    return slab_launch<Shape<(MP) / ((NU) * (NS)), NU, NS, W, K>, false>(P, A, ctas, st);
+    PIT_SCAN_SPECIAL(X)
+#undef X
+  }
 #define X(MP, NU, NS, W)                                                        \
   if (mpt == MP && nsub == NU && nseg == NS && warps == W)                      \
     return src ? slab_launch<PIT_SHAPE(MP, NU, NS, W), true>(P, A, ctas, st)    \

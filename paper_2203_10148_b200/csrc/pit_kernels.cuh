@@ -35,6 +35,16 @@ struct SlabArgs {
   int pieces;   // 0 = choose from occupancy (launcher), else forced
   int nblk;     // slabs in the batch (set by the launcher)
   long long* trace;  // PIT_PHASE_TIMING builds: per unit {smid, block, t_start, t_end} (ns)
+  // Host-buffer pipelining (pit_apply_F with pinned buffers; nullptr = the
+  // input is resident): the input arrives in chunks of chunk_blocks global
+  // blocks; the copy stream writes in_ready = k+1 after chunk k.  CTA b
+  // (global output block g = b + block_shift) waits for chunk(g) before it
+  // loads, and after its output is stored bumps out_done[chunk(g)] (block 0,
+  // written by CTA 0, counts in chunk 0), on which the D2H stream waits.
+  const unsigned* in_ready;
+  unsigned* out_done;
+  int chunk_blocks;
+  int block_shift;
 };
 
 // K2: one persistent CTA running the sequential sweep

@@ -21,9 +21,15 @@
 //        carry within its segment; segment totals are chained segment to
 //        segment; sub-chunk carries follow; pass 2 reruns every sub-chunk's
 //        sweep from its true carry.
+//        The warp scans keep only the Kogge-Stone stages whose terms can
+//        matter: with chunk multiplier w = nl^ch, a chunk's carry from the
+//        chunk d positions back has weight w^(d-1), so stages stop at the
+//        first s with w^(2^s) <= 2^-70 (scan_f / scan_b; the same threshold
+//        as the corner extent K0).  c2 keeps 2 of 5 stages, c3 none.
 //   y <- y + (gneg*y_0) zc   corner rank-1 (Sherman-Morrison) correction:
 //        narrow form zc_i = zc_0 nl^i on the chunks of segment 0 that start
-//        below K0 (fine propagators), table form otherwise (coarse).
+//        below K0, sub-chunks starting below K0 only (fine propagators),
+//        table form otherwise (coarse).
 // and the diagonal scale inv is deferred: applied as inv^R every R steps
 // (homogeneous propagation) or every step when a source is added.
 // Every multiply-add is an explicit fma(); oracle/pit_oracle.c
@@ -52,6 +58,7 @@ struct StepParams {
   double pp[5], qq[5], p32, q32;  // Kogge-Stone weights: powers of nl^(NSUB*SUB)
   double plane[32], qlane[32];
   int M, steps, R, K0;
+  int scan_f, scan_b;       // Kogge-Stone stages kept (pit_step_coeffs)
   int narrow;               // corner in geometric form on segment 0 only
   const double* zc;     // [K0] correction vector (device), table form
   const double* zt;     // [T] zc_0 * nl^(t*NSUB*SUB), narrow form
@@ -75,9 +82,12 @@ struct StepParams {
   } while (0)
 #endif
 
-template <int SUB_, int NSUB_, int NSEG_, int WARPS_>
+// KS_ < 5: the warp scans keep exactly KS_ Kogge-Stone stages (compile-time
+// specialisation for StepParams::scan_f == scan_b == KS_); KS_ == 5: the
+// stage counts are read from StepParams at run time.
+template <int SUB_, int NSUB_, int NSEG_, int WARPS_, int KS_ = 5>
 struct Shape {
-  static constexpr int SUB = SUB_, NSUB = NSUB_, NSEG = NSEG_, WARPS = WARPS_;
+  static constexpr int SUB = SUB_, NSUB = NSUB_, NSEG = NSEG_, WARPS = WARPS_, KS = KS_;
   static constexpr int T = 32 * WARPS;
   static constexpr int NC = NSUB * NSEG;  // sub-chunks per thread
   static constexpr int CH = NSUB * SUB;   // thread chunk length within a segment
@@ -161,7 +171,8 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
   }
   PIT_PHASE(0);
 #pragma unroll
-  for (int st = 0; st < 5; ++st) {
+  for (int st = 0; st < S::KS; ++st) {
+    if (S::KS == 5 && st >= P.scan_f) break;  // warp-uniform
     const double cw = sh.cf[st][lane];
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_up_sync(kFull, I[s], 1 << st), I[s]);
@@ -239,7 +250,8 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
   }
   PIT_PHASE(4);
 #pragma unroll
-  for (int st = 0; st < 5; ++st) {
+  for (int st = 0; st < S::KS; ++st) {
+    if (S::KS == 5 && st >= P.scan_b) break;  // warp-uniform
     const double cw = sh.cb[st][lane];
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_down_sync(kFull, I[s], 1 << st), I[s]);
@@ -304,6 +316,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
         const double a = cc * P.zt[tid];
 #pragma unroll
         for (int u = 0; u < NSUB; ++u) {
+          if (u * SUB >= P.K0) break;  // warp-uniform: lane 0 has the lowest points
           const double au = a * P.pw[u];
 #pragma unroll
           for (int j = 0; j < SUB; ++j) y[u][j] = fma(au, P.nlpow[j], y[u][j]);

@@ -45,7 +45,7 @@ class OrcStepper(C.Structure):
                 ("p32", C.c_double), ("q32", C.c_double), ("plane", C.c_double * 32),
                 ("qlane", C.c_double * 32), ("R", C.c_int), ("invR", C.c_double),
                 ("invLast", C.c_double), ("zc", _dp), ("ppos", _dp), ("qpos", _dp),
-                ("zt", _dp)]
+                ("zt", _dp), ("scan_f", C.c_int), ("scan_b", C.c_int)]
 
 
 class Orc2Coeffs(C.Structure):

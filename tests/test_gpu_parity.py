@@ -360,3 +360,51 @@ def test_dense_verification_size_guard():
     with api.BlockOperatorContext(p) as ctx:
         with pytest.raises(api.ConfigError):
             verify.assemble_dense_system(ctx)
+
+
+def _pinned(a):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    return t, t.numpy()
+
+
+@pytest.mark.parametrize("chunks", ["0", "1", "3", "64"])
+@pytest.mark.parametrize("name,slabs,pieces", [("c2", 40, "0"), ("c2", 37, "3"), ("c4", 33, "1")])
+def test_pipelined_host_apply_F_bitwise(name, slabs, pieces, chunks, monkeypatch):
+    # pit_apply_F on pinned host buffers overlaps the chunked H2D / D2H copies
+    # with K1 (stream memory operations + in-kernel chunk flags); the result
+    # is the sequential path's, bit for bit, for any chunking and scheduling
+    monkeypatch.setenv("PIT_E2E_CHUNKS", chunks)
+    monkeypatch.setenv("PIT_PIECES", pieces)
+    p = configs.make(name, slabs=slabs)
+    rng = np.random.default_rng(21)
+    L = rng.uniform(-1, 1, (p.N, p.M))
+    tl, Lp = _pinned(L)
+    to, Op = _pinned(np.zeros_like(L))
+    with api.BlockOperatorContext(p) as ctx:
+        ref = api.apply_F(ctx, L)  # pageable: sequential copies
+        for _ in range(3):
+            Op[...] = np.nan
+            api._check(api._lib.lib().pit_apply_F(ctx.handle, api.dptr(Lp), api.dptr(Op), None))
+            assert np.array_equal(Op, ref)
+    assert np.array_equal(ref, OracleProblem(p).apply_F(L))
+
+
+def test_pipelined_host_apply_F_full_c2_and_error():
+    p = configs.make("c2")
+    rng = np.random.default_rng(5)
+    L = rng.uniform(-1, 1, (p.N, p.M))
+    tl, Lp = _pinned(L)
+    to, Op = _pinned(np.zeros_like(L))
+    with api.BlockOperatorContext(p) as ctx:
+        ref = api.apply_F(ctx, L)
+        api._check(api._lib.lib().pit_apply_F(ctx.handle, api.dptr(Lp), api.dptr(Op), None))
+        assert np.array_equal(Op, ref)
+        Lp[700, 11] = np.nan
+        Lp[300, 5] = np.inf
+        with pytest.raises(api.SlabError) as e:
+            api._check(api._lib.lib().pit_apply_F(ctx.handle, api.dptr(Lp), api.dptr(Op), None))
+        assert e.value.slab_index == 300
+        Lp[...] = L
+        api._check(api._lib.lib().pit_apply_F(ctx.handle, api.dptr(Lp), api.dptr(Op), None))
+        assert np.array_equal(Op, ref)

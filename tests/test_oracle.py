@@ -40,7 +40,7 @@ def test_coefficients_bitwise_equal_product(name, role):
         for f in ("delta", "lam", "mu", "dstar", "nl", "nu", "inv", "gneg", "invR", "invLast",
                   "p32", "q32", "pS", "qS", "Pseg", "Qseg"):
             assert getattr(st, f) == getattr(c, f), f
-        for f in ("K0", "R", "narrow"):
+        for f in ("K0", "R", "narrow", "scan_f", "scan_b"):
             assert getattr(st, f) == getattr(c, f), f
         for f in ("pp", "qq", "plane", "qlane"):
             assert list(getattr(st, f)) == list(getattr(c, f)), f
