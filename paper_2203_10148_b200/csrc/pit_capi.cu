@@ -935,6 +935,12 @@ int pipe_setup(pit_context* ctx) {
     ctx->pipe_chunks = std::atoi(e);
     if (ctx->pipe_chunks < 0) return PIT_OK;  // < 0: pipelining off
   }
+  // Under a kernel profiler or sanitizer (ncu / compute-sanitizer inject
+  // through the tree launcher, which exports these) kernels are serialised
+  // against the copy streams, so K1 would wait on chunks that cannot land.
+  for (const char* v : {"NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                        "CUDA_INJECTION64_PATH"})
+    if (std::getenv(v) != nullptr) return PIT_OK;
   void* p = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) !=

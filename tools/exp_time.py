@@ -6,9 +6,10 @@ sys.path.insert(0, ".")
 from paper_2203_10148_b200 import _lib, api, configs  # noqa: E402
 
 L = _lib.lib()
-for name in sys.argv[1:] or ["c2"]:
+for arg in sys.argv[1:] or ["c2"]:
+    name, _, lay = arg.partition(":")
     p = configs.make(name)
-    ctx = api.BlockOperatorContext(p)
+    ctx = api.BlockOperatorContext(p, fine_layout=tuple(int(v) for v in lay.split(",")) if lay else None)
     x = torch.tensor(np.random.default_rng(0).uniform(-1, 1, (p.N, p.M)), device="cuda")
     out = torch.empty_like(x)
     stream = torch.cuda.Stream(); torch.cuda.set_stream(stream); st = stream.cuda_stream
@@ -20,5 +21,5 @@ for name in sys.argv[1:] or ["c2"]:
         e0.record(); f(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     gp = configs.gp_steps_per_apply(p)
     ms = sorted(ts)[3]
-    print(f"{_lib.LIB_PATH.split('/')[-1]} {name}: median {ms:.3f} ms  {gp/ms/1e9:.3f}e12 gp/s  frac {5*gp/ms/1e9/36.7:.3f}", flush=True)
+    print(f"{_lib.LIB_PATH.split('/')[-1]} {arg}: median {ms:.3f} ms  {gp/ms/1e9:.3f}e12 gp/s  frac {5*gp/ms/1e9/36.7:.3f}", flush=True)
     ctx.close()
