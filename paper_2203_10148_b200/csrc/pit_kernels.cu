@@ -836,6 +836,15 @@ cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const 
 cudaError_t launch_sweep(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                          const SweepArgs& A, cudaStream_t st) {
   if (A.count <= 0) return cudaSuccess;
+  // the coarse auto layouts with the full 5-stage scans (slowly decaying
+  // coarse factors) compiled without the run-time stage checks
+  if (!src && P.scan_f == 5 && P.scan_b == 5) {
+#define X(MP, NU, NS, W)                                   \
+  if (mpt == MP && nsub == NU && nseg == NS && warps == W) \
+    return sweep_launch<Shape<(MP) / ((NU) * (NS)), NU, NS, W, 5>, false>(P, A, st);
+    X(8, 1, 1, 8) X(16, 1, 1, 8) X(32, 2, 1, 8)
+#undef X
+  }
 #define X(MP, NU, NS, W)                                                        \
   if (mpt == MP && nsub == NU && nseg == NS && warps == W)                      \
     return src ? sweep_launch<PIT_SHAPE(MP, NU, NS, W), true>(P, A, st)         \

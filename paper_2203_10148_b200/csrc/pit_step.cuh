@@ -82,10 +82,10 @@ struct StepParams {
   } while (0)
 #endif
 
-// KS_ < 5: the warp scans keep exactly KS_ Kogge-Stone stages (compile-time
-// specialisation for StepParams::scan_f == scan_b == KS_); KS_ == 5: the
-// stage counts are read from StepParams at run time.
-template <int SUB_, int NSUB_, int NSEG_, int WARPS_, int KS_ = 5>
+// KS_ in 0..5: the warp scans keep exactly KS_ Kogge-Stone stages
+// (compile-time specialisation for StepParams::scan_f == scan_b == KS_);
+// KS_ < 0: the stage counts are read from StepParams at run time.
+template <int SUB_, int NSUB_, int NSEG_, int WARPS_, int KS_ = -1>
 struct Shape {
   static constexpr int SUB = SUB_, NSUB = NSUB_, NSEG = NSEG_, WARPS = WARPS_, KS = KS_;
   static constexpr int T = 32 * WARPS;
@@ -171,8 +171,8 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
   }
   PIT_PHASE(0);
 #pragma unroll
-  for (int st = 0; st < S::KS; ++st) {
-    if (S::KS == 5 && st >= P.scan_f) break;  // warp-uniform
+  for (int st = 0; st < (S::KS < 0 ? 5 : S::KS); ++st) {
+    if (S::KS < 0 && st >= P.scan_f) break;  // warp-uniform
     const double cw = sh.cf[st][lane];
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_up_sync(kFull, I[s], 1 << st), I[s]);
@@ -250,8 +250,8 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
   }
   PIT_PHASE(4);
 #pragma unroll
-  for (int st = 0; st < S::KS; ++st) {
-    if (S::KS == 5 && st >= P.scan_b) break;  // warp-uniform
+  for (int st = 0; st < (S::KS < 0 ? 5 : S::KS); ++st) {
+    if (S::KS < 0 && st >= P.scan_b) break;  // warp-uniform
     const double cw = sh.cb[st][lane];
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_down_sync(kFull, I[s], 1 << st), I[s]);
