@@ -109,6 +109,20 @@ typedef struct pit_problem_desc {
   /* K4 layout (tile rows, tile columns, CTAs per cluster, warps per CTA);
    * all 0 = auto */
   int32_t tile_rows, tile_cols, tile_cluster, tile_warps;
+  /* dimension 2 with fine_scheme == PIT_SCHEME_BACKWARD_EULER: the
+   * reference's desk/paper presets (src/presets.cpp, runner.cpp:75-88).  Both
+   * propagators step backward Euler on the general 5-point operator
+   * `stencil` (host, [5][M]: the south, west, centre, east, north entries of
+   * A per interior node as assemble_spatial_operator emits them,
+   * src/pde.cpp:66-100, 0 where a row has no such entry; NULL = the
+   * isotropic band_diag / band_lo stencil) and solve every step with
+   * Jacobi-PCG, or Jacobi-BiCGStab when `nonsymmetric` (ImplicitStepSolver,
+   * src/pde.cpp:112-130), to fine/coarse_tolerance (0: 1e-12) within
+   * fine/coarse_max_iterations (0: 10*M).  m <= 50. */
+  const double* stencil;
+  int32_t nonsymmetric;
+  double fine_tolerance;
+  int64_t fine_max_iterations;
 } pit_problem_desc;
 
 typedef struct pit_context pit_context;

@@ -844,3 +844,8 @@ void orc_vec_update_p(long n, double omega, double beta, const double* d, const 
 void orc_vec_axpy(long n, double a, const double* x, double* y) {
   for (long i = 0; i < n; ++i) y[i] = fma(a, x[i], y[i]);
 }
+
+int orc_problem_propagate(const orc_problem* p, int role, int with_source, const double* in,
+                          int slab, double* out) {
+  return p->prop(p->user, role, with_source, in, slab, out);
+}

@@ -146,6 +146,9 @@ int orc_parareal(const orc_problem* p, double tol, double eps0, int max_iter, in
 orc_problem* orc_problem_new(int M, int N, double weight, int has_source, int mode,
                              const double* y0, orc_prop_fn prop, void* user);
 void orc_problem_delete(orc_problem* p);
+/* one propagation through the problem's callback (tests) */
+int orc_problem_propagate(const orc_problem* p, int role, int with_source, const double* in,
+                          int slab, double* out);
 
 /* Elementwise BiCGStab phases in the device op order (tests of sharded drivers). */
 void orc_vec_update_s(long n, double alpha, const double* r, const double* d, double* s);

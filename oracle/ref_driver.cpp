@@ -20,7 +20,9 @@
 #include "pit/errors.hpp"
 #include "pit/executor.hpp"
 #include "pit/pde.hpp"
+#include "pit/presets.hpp"
 #include "pit/propagator.hpp"
+#include "pit/runner.hpp"
 #include "pit/solvers.hpp"
 
 namespace {
@@ -169,6 +171,34 @@ void* pitref_create_2d(int m, double lo, double hi, double diffusion, double rea
     fail(e);
     return nullptr;
   }
+}
+
+// The reference's own experiment contexts: build_context(make_preset(case,
+// scale), N) (runner.cpp:75-88, presets.cpp:48-77); case 0 diffusion,
+// 1 diffusion_reaction, 2 advection_diffusion_reaction; scale 0 desk, 1 paper.
+void* pitref_create_preset(int case_id, int scale, int N) {
+  try {
+    const pit::CaseName cn = case_id == 0   ? pit::CaseName::Diffusion
+                             : case_id == 1 ? pit::CaseName::DiffusionReaction
+                                            : pit::CaseName::AdvectionDiffusionReaction;
+    const pit::ExperimentPreset preset =
+        pit::make_preset(cn, scale == 1 ? pit::Scale::Paper : pit::Scale::Desk);
+    auto r = std::make_unique<RefCtx>();
+    r->ctx = std::make_unique<pit::BlockOperatorContext>(pit::build_context(preset, N));
+    r->M = static_cast<int>(r->ctx->initial_value().values().size());
+    r->N = N;
+    return r.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+int pitref_initial_value(void* p, double* out) {
+  auto* r = static_cast<RefCtx*>(p);
+  auto v = r->ctx->initial_value().values();
+  std::memcpy(out, v.data(), sizeof(double) * v.size());
+  return 0;
 }
 
 void pitref_destroy(void* p) { delete static_cast<RefCtx*>(p); }

@@ -47,7 +47,9 @@ class ProblemDesc(C.Structure):
                 ("coarse_nseg", C.c_int32), ("coarse_warps", C.c_int32),
                 ("fine_scheme", C.c_int32), ("coarse_tolerance", C.c_double),
                 ("coarse_max_iterations", C.c_int64), ("tile_rows", C.c_int32),
-                ("tile_cols", C.c_int32), ("tile_cluster", C.c_int32), ("tile_warps", C.c_int32)]
+                ("tile_cols", C.c_int32), ("tile_cluster", C.c_int32), ("tile_warps", C.c_int32),
+                ("stencil", _dp), ("nonsymmetric", C.c_int32), ("fine_tolerance", C.c_double),
+                ("fine_max_iterations", C.c_int64)]
 
 
 class StepCoeffs2DC(C.Structure):

@@ -198,6 +198,70 @@ class Problem2D:
         return d, keep
 
 
+@dataclass
+class Problem2DImplicit:
+    """A 2D problem with backward-Euler fine and coarse propagators on the
+    reference's general 5-point operator: the desk/paper presets
+    (src/presets.cpp:47-77, assembled by runner.cpp:75-88; see presets.py).
+    `stencil` is [5, m*m]: the south, west, centre, east, north entries of A
+    per interior node exactly as assemble_spatial_operator emits them
+    (src/pde.cpp:66-100), 0 where the row has no such entry.  Every step is
+    solved by Jacobi-PCG (symmetric operator) or Jacobi-BiCGStab
+    (`nonsymmetric`, e.g. the rotation velocity) to the reference's 1e-12
+    within 10 n iterations (ImplicitStepSolver, src/pde.cpp:112-130).  m <= 50."""
+    m: int
+    stencil: np.ndarray
+    nonsymmetric: bool
+    N: int
+    T: float
+    fine_steps: int
+    coarse_steps: int
+    y0: np.ndarray
+    grid_lo: float = -0.5
+    grid_hi: float = 0.5
+    fine_tolerance: float = 1e-12
+    coarse_tolerance: float = 1e-12
+    fine_max_iterations: int = 0
+    coarse_max_iterations: int = 0
+    source: Optional[SeparableSource] = None  # the presets have f = 0
+
+    @property
+    def M(self) -> int:
+        return self.m * self.m
+
+    @property
+    def spacing(self) -> float:
+        return (self.grid_hi - self.grid_lo) / (self.m + 2 - 1)
+
+    def coords(self) -> np.ndarray:
+        h = self.spacing
+        return np.array([self.grid_lo + (k + 1) * h for k in range(self.m)])
+
+    def desc(self, device: int = 0, fine_layout=None, coarse_layout=None):
+        d = _lib.ProblemDesc()
+        d.dimension = 2
+        d.interior = self.m
+        d.grid_lo, d.grid_hi = self.grid_lo, self.grid_hi
+        st = np.ascontiguousarray(self.stencil, dtype=np.float64).reshape(-1)
+        if st.size != 5 * self.M:
+            raise ValueError("stencil must be [5, m*m]")
+        d.band_lo, d.band_diag, d.band_up = 0.0, 0.0, 0.0
+        d.slab_count = self.N
+        d.total_time = self.T
+        d.fine_steps, d.coarse_steps = self.fine_steps, self.coarse_steps
+        y0 = np.ascontiguousarray(self.y0, dtype=np.float64).reshape(-1)
+        keep = [y0, st]
+        d.initial_value = dptr(y0)
+        d.stencil = dptr(st)
+        d.nonsymmetric = 1 if self.nonsymmetric else 0
+        d.device = device
+        d.fine_scheme = _lib.PIT_SCHEME_BACKWARD_EULER
+        d.fine_tolerance, d.coarse_tolerance = self.fine_tolerance, self.coarse_tolerance
+        d.fine_max_iterations = self.fine_max_iterations
+        d.coarse_max_iterations = self.coarse_max_iterations
+        return d, keep
+
+
 def heat_2d_bands(diffusion: float, h: float):
     """(neighbour, centre) of the 2D 5-point -mu*Laplacian, as
     assemble_spatial_operator's 2D branch builds them (src/pde.cpp:66-100:

@@ -81,6 +81,10 @@ struct pit_context {
   Layout2D lay2{};
   long long* d_cg_iters = nullptr;
   Role role[2];
+  // 2D backward Euler (K6): per role I + dt*A stencil and Jacobi inverse
+  bool be2 = false;
+  Be2Params bp[2]{};
+  double* d_be2[2] = {};  // [6][M]: coef[5][M], minv[M]
   double* d_shape = nullptr;
   double* d_y0 = nullptr;
   std::vector<double> y0;
@@ -121,11 +125,21 @@ int validate_desc(const pit_problem_desc* d) {
   if (d->dimension == 1 && d->fine_scheme != PIT_SCHEME_BACKWARD_EULER)
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "pit_context_create: 1D fine propagators are backward Euler");
-  if (d->dimension == 2) {
+  if (d->dimension == 2 && d->fine_scheme == PIT_SCHEME_BACKWARD_EULER) {
+    if (!be2d_supported(d->interior))
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: implicit 2D propagators need m <= 50 points per axis");
+    if (!d->stencil && d->band_lo != d->band_up)
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: 2D band operators are isotropic (band_lo == band_up)");
+    if (d->source_kind != PIT_SOURCE_NONE)
+      return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: no sources in 2D");
+    if (d->coarse_tolerance < 0.0 || d->fine_tolerance < 0.0)
+      return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: negative inner tolerance");
+  } else if (d->dimension == 2) {
     if (d->fine_scheme != PIT_SCHEME_EXPLICIT_EULER)
       return set_err(PIT_ERR_INVALID_ARGUMENT,
-                     "pit_context_create: 2D fine propagators are explicit Euler "
-                     "(implicit 2D fine steps are not implemented)");
+                     "pit_context_create: unknown 2D fine scheme");
     if (d->band_lo != d->band_up)
       return set_err(PIT_ERR_INVALID_ARGUMENT,
                      "pit_context_create: 2D operators are the isotropic 5-point stencil "
@@ -420,6 +434,10 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
     A.out = out;
     A.slab0 = first - 1;
   }
+  if (ctx->be2) {
+    CUDA_TRY(launch_be2d_batch(ctx->bp[PIT_FINE], A, ctas, st));
+    return PIT_OK;
+  }
   if (ctx->dim == 2) {
     CUDA_TRY(launch_explicit2d(ctx->lay2, ex2_params(ctx), A, ctas, st));
     return PIT_OK;
@@ -439,6 +457,10 @@ int launch_sweep_any(pit_context* ctx, int role, bool src, const SweepArgs& A, c
   if (ctx->dim == 1) {
     Role& R = ctx->role[role];
     CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, st));
+    return PIT_OK;
+  }
+  if (ctx->be2) {
+    CUDA_TRY(launch_be2d_sweep(ctx->bp[role], A, st));
     return PIT_OK;
   }
   if (role == PIT_COARSE) {
@@ -587,7 +609,57 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     pit_context_destroy(ctx);
     return rc;
   };
-  if (ctx->dim == 2) {
+  ctx->be2 = ctx->dim == 2 && desc->fine_scheme == PIT_SCHEME_BACKWARD_EULER;
+  if (ctx->be2) {
+    // ImplicitStepSolver (pde.cpp:103-110): every entry times dt, then the
+    // diagonal + 1; jacobi_inverse_diagonal (sparse.cpp:43-50)
+    const int M = ctx->M;
+    std::vector<double> st(5 * (size_t)M, 0.0);
+    if (desc->stencil) {
+      st.assign(desc->stencil, desc->stencil + 5 * (size_t)M);
+    } else {
+      const int m = ctx->m;
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) {
+          const size_t r = (size_t)j * m + i;
+          st[r] = j > 0 ? desc->band_lo : 0.0;
+          st[M + r] = i > 0 ? desc->band_lo : 0.0;
+          st[2 * (size_t)M + r] = desc->band_diag;
+          st[3 * (size_t)M + r] = i < m - 1 ? desc->band_lo : 0.0;
+          st[4 * (size_t)M + r] = j < m - 1 ? desc->band_lo : 0.0;
+        }
+    }
+    for (int r = 0; r < 2; ++r) {
+      const int steps = r == PIT_FINE ? desc->fine_steps : desc->coarse_steps;
+      const double dt = (desc->total_time / desc->slab_count) / steps;
+      std::vector<double> h(6 * (size_t)M);
+      for (size_t k = 0; k < 5 * (size_t)M; ++k) h[k] = st[k] * dt;
+      for (int i = 0; i < M; ++i) {
+        double& c = h[2 * (size_t)M + i];
+        c = c + 1.0;
+        h[5 * (size_t)M + i] = c != 0.0 ? 1.0 / c : 1.0;
+      }
+      if (cudaMalloc(&ctx->d_be2[r], sizeof(double) * h.size()) != cudaSuccess ||
+          cudaMemcpy(ctx->d_be2[r], h.data(), sizeof(double) * h.size(),
+                     cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+      Be2Params& P = ctx->bp[r];
+      P.m = ctx->m;
+      P.M = M;
+      P.steps = steps;
+      P.coef = ctx->d_be2[r];
+      P.minv = ctx->d_be2[r] + 5 * (size_t)M;
+      const double tol = r == PIT_FINE ? desc->fine_tolerance : desc->coarse_tolerance;
+      const long long cap = r == PIT_FINE ? desc->fine_max_iterations : desc->coarse_max_iterations;
+      P.rel_tol = tol > 0.0 ? tol : 1e-12;          // kInnerSolveRelTol (pde.hpp:78)
+      P.cap = cap > 0 ? (int)std::min<long long>(cap, INT_MAX) : 10 * M;  // pde.hpp:79
+      P.symmetric = desc->nonsymmetric ? 0 : 1;
+    }
+    if (cudaMalloc(&ctx->d_cg_iters, sizeof(long long)) != cudaSuccess ||
+        cudaMemset(ctx->d_cg_iters, 0, sizeof(long long)) != cudaSuccess)
+      return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
+    ctx->bp[PIT_COARSE].iters = ctx->d_cg_iters;
+  } else if (ctx->dim == 2) {
     int rc = coeffs_2d(desc, &ctx->c2);
     if (rc) return fail(rc);
     ctx->lay2 = Layout2D{ctx->c2.tile_rows, ctx->c2.tile_cols, ctx->c2.tile_cluster,
@@ -697,6 +769,8 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_sched);
   cudaFree(ctx->d_trace);
   cudaFree(ctx->d_cg_iters);
+  cudaFree(ctx->d_be2[0]);
+  cudaFree(ctx->d_be2[1]);
   cudaFree(ctx->d_sync);
   if (ctx->ev_pipe) cudaEventDestroy(ctx->ev_pipe);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);

@@ -57,6 +57,27 @@ bool layout2d_supported(int tr, int tc, int cl, int warps);
 
 cudaError_t launch_explicit2d(const Layout2D& L, const Ex2Params& P, const SlabArgs& A, int slabs,
                               cudaStream_t st);
+
+// K6 (pit_kernels2d_be.cu): 2D backward Euler on the reference's general
+// 5-point operator (assemble_spatial_operator with velocity, pde.cpp:66-100),
+// each step solved by Jacobi-PCG (symmetric) or Jacobi-BiCGStab with the
+// reference's control flow (sparse.cpp:60-206).
+struct Be2Params {
+  int m, M;              // points per axis, m*m
+  int steps;             // backward-Euler steps per slab
+  const double* coef;    // [5][M] device: south, west, centre, east, north of I + dt*A (0 = absent)
+  const double* minv;    // [M] device: Jacobi inverse diagonal (jacobi_inverse_diagonal)
+  double rel_tol;        // kInnerSolveRelTol (pde.hpp:78)
+  int cap;               // kInnerSolveCapFactor * n (pde.hpp:79)
+  int symmetric;         // 1: solve_cg, 0: solve_bicgstab (ImplicitStepSolver::solve)
+  long long* iters;      // sweeps: cumulative inner iterations (optional)
+};
+constexpr int kBe2Threads = 512;
+constexpr int kBe2MaxPPT = 5;  // points per thread: m*m <= 2560
+size_t be2d_smem_bytes(int m);
+bool be2d_supported(int m);
+cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st);
+cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st);
 cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long* iters,
                               cudaStream_t st);
 

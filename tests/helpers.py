@@ -21,6 +21,9 @@ class OracleProblem:
         if isinstance(p, api.Problem2D):
             self._init_2d(p, mode)
             return
+        if isinstance(p, api.Problem2DImplicit):
+            self._init_be2d(p, mode)
+            return
         self.dim = 1
         fc, _ = api.step_coefficients(p, 0, fine_layout, coarse_layout)
         cc, _ = api.step_coefficients(p, 1, fine_layout, coarse_layout)
@@ -54,12 +57,30 @@ class OracleProblem:
         self.prob = self.lib.orc_2d_problem(self.o)
         self.coeffs = self.lib.orc_2d_coeffs(self.o).contents
 
+    def _init_be2d(self, p, mode):
+        self.dim = 3  # 2D backward Euler (K6 mirror)
+        self.p = p
+        self.lib = O.orc()
+        st = np.ascontiguousarray(p.stencil, dtype=np.float64).reshape(-1)
+        self._keep = [np.ascontiguousarray(p.y0, dtype=np.float64).reshape(-1), st]
+        self.o = self.lib.orc_be2d_create(p.m, p.grid_lo, p.grid_hi, O.ptr(st),
+                                          1 if p.nonsymmetric else 0, p.N, p.T, p.fine_steps,
+                                          p.coarse_steps, p.fine_tolerance, p.fine_max_iterations,
+                                          p.coarse_tolerance, p.coarse_max_iterations,
+                                          O.ptr(self._keep[0]), mode)
+        assert self.o, "orc_be2d_create failed"
+        self.prob = self.lib.orc_be2d_problem(self.o)
+
     def coarse_iterations(self):
+        if self.dim == 3:
+            return self.lib.orc_be2d_coarse_iterations(self.o)
         return self.lib.orc_2d_coarse_iterations(self.o) if self.dim == 2 else 0
 
     def close(self):
         if self.o:
-            if self.dim == 2:
+            if self.dim == 3:
+                self.lib.orc_be2d_destroy(self.o)
+            elif self.dim == 2:
                 self.lib.orc_2d_destroy(self.o)
             else:
                 self.lib.orc_1d_destroy(self.o)
@@ -102,6 +123,12 @@ class OracleProblem:
         assert self.lib.orc_preconditioned_residual(
             self.prob, O.ptr(np.ascontiguousarray(lam)), O.ptr(np.ascontiguousarray(rhs)),
             O.ptr(out), None) == 0
+        return out
+
+    def propagate(self, role, x, slab, with_source=False):
+        out = np.zeros(self.p.M)
+        assert self.lib.orc_problem_propagate(self.prob, role, 1 if with_source else 0,
+                                              O.ptr(np.ascontiguousarray(x)), slab, O.ptr(out)) == 0
         return out
 
     def block_dot(self, a, b):

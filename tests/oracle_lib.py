@@ -135,6 +135,18 @@ def orc():
         lib.orc_2d_coeffs.argtypes = [C.c_void_p]
         lib.orc_2d_coarse_iterations.restype = C.c_longlong
         lib.orc_2d_coarse_iterations.argtypes = [C.c_void_p]
+        lib.orc_problem_propagate.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp]
+        lib.orc_be2_stencil.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                        C.c_int, _dp]
+        lib.orc_be2d_create.restype = C.c_void_p
+        lib.orc_be2d_create.argtypes = [C.c_int, C.c_double, C.c_double, _dp, C.c_int, C.c_int,
+                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_longlong,
+                                        C.c_double, C.c_longlong, _dp, C.c_int]
+        lib.orc_be2d_destroy.argtypes = [C.c_void_p]
+        lib.orc_be2d_problem.restype = C.c_void_p
+        lib.orc_be2d_problem.argtypes = [C.c_void_p]
+        lib.orc_be2d_coarse_iterations.restype = C.c_longlong
+        lib.orc_be2d_coarse_iterations.argtypes = [C.c_void_p]
         _orc = lib
     return _orc
 
@@ -158,6 +170,9 @@ def ref():
         lib.pitref_create_2d.restype = C.c_void_p
         lib.pitref_create_2d.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                          C.c_int, C.c_double, C.c_int, C.c_int, _dp]
+        lib.pitref_create_preset.restype = C.c_void_p
+        lib.pitref_create_preset.argtypes = [C.c_int, C.c_int, C.c_int]
+        lib.pitref_initial_value.argtypes = [C.c_void_p, _dp]
         lib.pitref_destroy.argtypes = [C.c_void_p]
         lib.pitref_spacing.restype = C.c_double
         lib.pitref_spacing.argtypes = [C.c_void_p]

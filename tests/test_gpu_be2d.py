@@ -1,0 +1,88 @@
+"""GPU: K6 (2D backward Euler on the reference's general 5-point operator,
+the desk/paper presets) bit for bit against its CPU mirror
+(oracle/pit_oracle2d_be.c), which tests/test_oracle2d_be.py pins to the
+reference's own Propagator and pitsbicg_solve."""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from helpers import OracleProblem
+from paper_2203_10148_b200 import api, presets
+
+pytestmark = pytest.mark.gpu
+
+
+def same(a, b):
+    return np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", presets.CASES)
+def test_desk_operators_bitwise_vs_oracle(case):
+    p = presets.build_problem(presets.make_preset(case, "desk"), 8)
+    o = OracleProblem(p)
+    rng = np.random.default_rng(3)
+    L = rng.uniform(-1, 1, (p.N, p.M))
+    with api.BlockOperatorContext(p) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))
+        assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))
+        assert same(api.assemble_rhs(ctx), o.assemble_rhs())
+        assert same(api.initial_guess(ctx, api.InitialGuessPolicy.CoarseSweep), o.initial_guess())
+        assert same(api.sequential_fine_solve(ctx), o.sequential_fine())
+        rhs = o.assemble_rhs()
+        assert same(api.preconditioned_residual(ctx, L, rhs), o.preconditioned_residual(L, rhs))
+        assert ctx.coarse_iterations() == o.coarse_iterations()
+
+
+@pytest.mark.parametrize("which", ["pitsbicg", "parareal"])
+@pytest.mark.parametrize("case", presets.CASES)
+def test_desk_solvers_bitwise_vs_oracle(case, which):
+    p = presets.build_problem(presets.make_preset(case, "desk"), 8)
+    o = OracleProblem(p)
+    with api.BlockOperatorContext(p) as ctx:
+        fn = api.pitsbicg_solve if which == "pitsbicg" else api.parareal_solve
+        res = fn(ctx, api.SolverConfig(tolerance=1e-8))
+    r = o.solve(1e-8, which=which)
+    assert [(x.k, x.residual_norm, x.fine_applications, x.coarse_applications)
+            for x in res.history.records] == r["rows"]
+    assert res.history.restarts == r["restarts"]
+    assert np.array_equal(res.solution, r["lam"])
+
+
+@pytest.mark.parametrize("case", ["diffusion", "advection_diffusion_reaction"])
+def test_paper_scale_apply_F_bitwise(case):
+    # m = 49: five points per thread, 208 KB of shared memory per CTA
+    p = presets.build_problem(presets.make_preset(case, "paper"), 4)
+    p = dataclasses.replace(p, fine_steps=40, T=p.T * 40 / p.fine_steps)  # keep dt, fewer steps
+    o = OracleProblem(p)
+    L = np.random.default_rng(5).uniform(-1, 1, (p.N, p.M))
+    with api.BlockOperatorContext(p) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))
+        assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))
+
+
+def test_inner_solve_cap_raises_reference_errors():
+    p = presets.build_problem(presets.make_preset("advection_diffusion_reaction", "desk"), 4)
+    L = np.random.default_rng(1).uniform(-1, 1, (p.N, p.M))
+    with api.BlockOperatorContext(dataclasses.replace(p, fine_max_iterations=1)) as ctx:
+        with pytest.raises(api.SlabError) as e:
+            api.apply_F(ctx, L)
+        assert e.value.slab_index == 0
+    with api.BlockOperatorContext(dataclasses.replace(p, coarse_max_iterations=1)) as ctx:
+        with pytest.raises(api.InnerSolveError):
+            api.apply_G_inverse(ctx, L)
+        # the context survives (executor.cpp:142-152 analogue)
+        assert np.isfinite(api.apply_F(ctx, L)).all()
+
+
+def test_desk_all_slab_counts_converge():
+    # the preset's slab counts {4, ..., 64} through the device solver
+    for n in presets.make_preset("diffusion").slab_counts:
+        p = presets.build_problem(presets.make_preset("diffusion"), n)
+        with api.BlockOperatorContext(p) as ctx:
+            res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-8))
+            seq = api.sequential_fine_solve(ctx)
+        assert res.history.status == api.SolveStatus.Converged
+        assert np.max(np.abs(res.solution - seq)) < 1e-6 * np.max(np.abs(seq))
