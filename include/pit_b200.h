@@ -136,13 +136,17 @@ typedef struct pit_run_stats {
   double coarse_sequential_ms;
 } pit_run_stats;
 
-/* One convergence-history row (include/pit/solvers.hpp:17-24). */
+/* One convergence-history row (include/pit/solvers.hpp:17-24).
+ * error_vs_reference = block_norm_n_inf(lambda - reference) when a reference
+ * is set (pit_set_reference; SolveOptions::reference), has_error = 1. */
 typedef struct pit_record {
   int32_t k;
   double residual_norm;
   int64_t fine_applications;
   int64_t coarse_applications;
   double wall_ms;
+  double error_vs_reference;
+  int32_t has_error;
 } pit_record;
 
 /* Solver configuration (include/pit/solvers.hpp:36-44). */
@@ -241,6 +245,11 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
                   double* out);
 int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, double* out);
 int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out);
+
+/* SolveOptions::reference (solvers.hpp:50-52): a host block vector [N*M]
+ * kept on the device; every history row of the following solves carries
+ * block_norm_n_inf(lambda - reference).  NULL clears it. */
+int pit_set_reference(pit_context* ctx, const double* reference);
 
 /* Full solve.  lambda_out [N*M]; lambda_init optional override [N*M];
  * first_residual_out optional [N*M]; records optional [max_records]. */

@@ -184,9 +184,16 @@ class Backend {
     std::vector<pit_record> rows(static_cast<size_t>(config.max_iterations) + 2);
     pit_solve_info info{};
     auto fn = pitsbicg ? pit_pitsbicg_solve : pit_parareal_solve;
-    check(fn(h_.get(), &c, init.empty() ? nullptr : init.data(), lam.data(),
-             first.empty() ? nullptr : first.data(), rows.data(), static_cast<int>(rows.size()),
-             &info));
+    // SolveOptions::reference: every row carries block_norm_n_inf(lambda - reference)
+    if (options.reference) {
+      const std::vector<double> ref = flat(*options.reference, "reference");
+      check(pit_set_reference(h_.get(), ref.data()));
+    }
+    const int rc = fn(h_.get(), &c, init.empty() ? nullptr : init.data(), lam.data(),
+                      first.empty() ? nullptr : first.data(), rows.data(),
+                      static_cast<int>(rows.size()), &info);
+    if (options.reference) pit_set_reference(h_.get(), nullptr);
+    check(rc);
     SolveResult r{unflat(lam), {}};
     for (int i = 0; i < info.record_count; ++i) {
       IterationRecord rec;
@@ -195,6 +202,7 @@ class Backend {
       rec.fine_applications = static_cast<long>(rows[i].fine_applications);
       rec.coarse_applications = static_cast<long>(rows[i].coarse_applications);
       rec.wall_ms = rows[i].wall_ms;
+      if (rows[i].has_error) rec.error_vs_reference = rows[i].error_vs_reference;
       r.history.records.push_back(rec);
     }
     r.history.status =

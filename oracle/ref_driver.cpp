@@ -13,6 +13,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -191,6 +192,30 @@ void* pitref_create_preset(int case_id, int scale, int N) {
   } catch (const std::exception& e) {
     fail(e);
     return nullptr;
+  }
+}
+
+// pit::run_experiment (runner.cpp:108-147) on a preset with the given slab
+// counts; writes <out_dir>/<case>.csv.  solver: 0 parareal, 1 pitsbicg, 2 both.
+int pitref_run_experiment(int case_id, int scale, const int* slabs, int nslabs, int solver,
+                          double tol, const char* out_dir) {
+  try {
+    const pit::CaseName cn = case_id == 0   ? pit::CaseName::Diffusion
+                             : case_id == 1 ? pit::CaseName::DiffusionReaction
+                                            : pit::CaseName::AdvectionDiffusionReaction;
+    pit::RunSpec spec;
+    spec.preset = pit::make_preset(cn, scale == 1 ? pit::Scale::Paper : pit::Scale::Desk);
+    spec.preset.slab_counts.assign(slabs, slabs + nslabs);
+    spec.solver = solver == 0 ? pit::SolverChoice::Parareal
+                  : solver == 1 ? pit::SolverChoice::PiTSBiCG
+                                : pit::SolverChoice::Both;
+    spec.solver_config.tolerance = tol;
+    spec.out_dir = out_dir;
+    std::ostringstream log;
+    pit::run_experiment(spec, log);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
   }
 }
 

@@ -72,7 +72,8 @@ class RunStatsC(C.Structure):
 class RecordC(C.Structure):
     _fields_ = [("k", C.c_int32), ("residual_norm", C.c_double),
                 ("fine_applications", C.c_int64), ("coarse_applications", C.c_int64),
-                ("wall_ms", C.c_double)]
+                ("wall_ms", C.c_double), ("error_vs_reference", C.c_double),
+                ("has_error", C.c_int32)]
 
 
 class SolverConfigC(C.Structure):
@@ -113,7 +114,7 @@ EXPORTS = [
     "pit_fine_source_device",
     "pit_sync_status", "pit_pitsbicg_solve_device",
     "pit_seeded_uniform", "pit_seeded_normal", "pit_measure_fp64_peak",
-    "pit_step_coefficients_2d", "pit_coarse_iterations",
+    "pit_step_coefficients_2d", "pit_coarse_iterations", "pit_set_reference",
 ]
 
 _lib = None
@@ -133,6 +134,7 @@ def lib():
     L.pit_version.restype = C.c_char_p
     L.pit_context_create.argtypes = [C.POINTER(ProblemDesc), C.POINTER(vp)]
     L.pit_context_destroy.argtypes = [vp]
+    L.pit_set_reference.argtypes = [vp, _dp]
     L.pit_context_shape.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]
     L.pit_step_coefficients.argtypes = [C.POINTER(ProblemDesc), C.c_int, C.POINTER(StepCoeffsC)]
     L.pit_step_correction.argtypes = [C.POINTER(ProblemDesc), C.c_int, _dp]

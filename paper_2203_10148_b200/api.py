@@ -619,13 +619,22 @@ def _solve(which: int, ctx: BlockOperatorContext, config: SolverConfig,
     info = _lib.SolveInfoC()
     cfg = config._c()
     fn = _lib.lib().pit_pitsbicg_solve if which == 0 else _lib.lib().pit_parareal_solve
-    _check(fn(ctx.handle, C.byref(cfg), dptr(init), dptr(lam), dptr(first), recs, cap,
-              C.byref(info)))
+    ref = None
+    if options.reference is not None:
+        ref = ctx._vec(options.reference, "reference")
+        _check(_lib.lib().pit_set_reference(ctx.handle, dptr(ref)))
+    try:
+        _check(fn(ctx.handle, C.byref(cfg), dptr(init), dptr(lam), dptr(first), recs, cap,
+                  C.byref(info)))
+    finally:
+        if ref is not None:
+            _lib.lib().pit_set_reference(ctx.handle, None)
     hist = ConvergenceHistory()
     for i in range(info.record_count):
         r = recs[i]
         hist.records.append(IterationRecord(r.k, r.residual_norm, r.fine_applications,
-                                            r.coarse_applications, r.wall_ms))
+                                            r.coarse_applications, r.wall_ms,
+                                            r.error_vs_reference if r.has_error else None))
     hist.status = SolveStatus.Converged if info.status == _lib.PIT_CONVERGED \
         else SolveStatus.MaxIterations
     hist.restarts = info.restarts
@@ -633,10 +642,6 @@ def _solve(which: int, ctx: BlockOperatorContext, config: SolverConfig,
     hist.min_restart_margin = info.min_restart_margin
     if first is not None:
         options.first_residual_out[...] = first
-    if options.reference is not None and hist.records:
-        ref = ctx._vec(options.reference, "reference")
-        hist.records[-1].error_vs_reference = float(
-            max(np.sqrt(ctx.spacing * np.sum((lam - ref) ** 2, axis=1))))
     return SolveResult(lam, hist)
 
 

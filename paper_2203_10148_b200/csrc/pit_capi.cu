@@ -107,6 +107,9 @@ struct pit_context {
   double* scratch[3] = {};
   size_t scratch_n[3] = {};
   bool scratch_busy[3] = {};
+  // SolveOptions::reference: per-row error_vs_reference (Recorder)
+  double* d_ref = nullptr;
+  double* d_ref_diff = nullptr;
   // host-buffer pipelining of pit_apply_F (see pipelined_apply_F)
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_pipe = nullptr;
@@ -772,6 +775,8 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_be2[0]);
   cudaFree(ctx->d_be2[1]);
   cudaFree(ctx->d_sync);
+  cudaFree(ctx->d_ref);
+  cudaFree(ctx->d_ref_diff);
   if (ctx->ev_pipe) cudaEventDestroy(ctx->ev_pipe);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -1305,18 +1310,42 @@ int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out) {
 
 namespace {
 
+// block_norm_n_inf(lambda - reference) (solvers.cpp:131), on the device:
+// diff = fma(-1, ref, lambda) = lambda - ref exactly rounded.
+double error_vs_reference(pit_context* ctx, const double* lam) {
+  const size_t nm = ctx->nm();
+  if (cudaMemcpyAsync(ctx->d_ref_diff, lam, nm * sizeof(double), cudaMemcpyDeviceToDevice,
+                      ctx->stream) != cudaSuccess ||
+      launch_axpy(nm, -1.0, ctx->d_ref, ctx->d_ref_diff, ctx->stream) != cudaSuccess)
+    return NAN;
+  const double* A[1] = {ctx->d_ref_diff};
+  if (launch_dots(ctx->M, ctx->N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream) !=
+          cudaSuccess ||
+      fetch_partials(ctx, ctx->N))
+    return NAN;
+  return max_sqrt_partials(ctx->h_partials, ctx->N, 1, 0);
+}
+
 struct Recorder {
   pit_record* rows;
   int cap;
   int n = 0;
   pit_run_stats* stats;
   Clock::time_point t0;
+  pit_context* ctx = nullptr;   // with a reference set: error_vs_reference of *lam
+  const double* lam = nullptr;
   void operator()(int k, double res) {
     if (n < cap && rows) {
       rows[n].k = k;
       rows[n].residual_norm = res;
       rows[n].fine_applications = stats->fine_applications;
       rows[n].coarse_applications = stats->coarse_applications;
+      rows[n].has_error = 0;
+      rows[n].error_vs_reference = 0.0;
+      if (ctx && ctx->d_ref && lam) {
+        rows[n].error_vs_reference = error_vs_reference(ctx, lam);
+        rows[n].has_error = 1;
+      }
       rows[n].wall_ms = ms_since(t0);
     }
     ++n;
@@ -1375,7 +1404,7 @@ int pitsbicg_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
   pit_solve_info inf{};
   inf.min_restart_margin = INFINITY;
   pit_run_stats& st = inf.stats;
-  Recorder rec{rows, cap, 0, &st, Clock::now()};
+  Recorder rec{rows, cap, 0, &st, Clock::now(), ctx, lam};
   auto finish = [&](int status) {
     inf.status = status;
     inf.total_records = rec.n;
@@ -1497,7 +1526,7 @@ int parareal_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
   pit_solve_info inf{};
   inf.min_restart_margin = INFINITY;
   pit_run_stats& st = inf.stats;
-  Recorder rec{rows, cap, 0, &st, Clock::now()};
+  Recorder rec{rows, cap, 0, &st, Clock::now(), ctx, lam};
   if (!have_init) PIT_TRY(initial_guess_dev(ctx, cfg->initial_guess, lam, &st));
   PIT_TRY(assemble_rhs_dev(ctx, rhs, &st));
   int status = PIT_MAX_ITERATIONS;
@@ -1549,6 +1578,24 @@ int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const 
 }
 
 }  // namespace
+
+int pit_set_reference(pit_context* ctx, const double* reference) {
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (!reference) {
+    cudaFree(ctx->d_ref);
+    cudaFree(ctx->d_ref_diff);
+    ctx->d_ref = ctx->d_ref_diff = nullptr;
+    return PIT_OK;
+  }
+  if (!ctx->d_ref) {
+    CUDA_TRY(cudaMalloc(&ctx->d_ref, ctx->nm() * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&ctx->d_ref_diff, ctx->nm() * sizeof(double)));
+  }
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_ref, reference, ctx->nm() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PIT_OK;
+}
 
 int pit_pitsbicg_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
                        double* lambda_out, double* first_residual_out, pit_record* records,

@@ -173,6 +173,8 @@ def ref():
         lib.pitref_create_preset.restype = C.c_void_p
         lib.pitref_create_preset.argtypes = [C.c_int, C.c_int, C.c_int]
         lib.pitref_initial_value.argtypes = [C.c_void_p, _dp]
+        lib.pitref_run_experiment.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int,
+                                              C.c_int, C.c_double, C.c_char_p]
         lib.pitref_destroy.argtypes = [C.c_void_p]
         lib.pitref_spacing.restype = C.c_double
         lib.pitref_spacing.argtypes = [C.c_void_p]

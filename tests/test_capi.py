@@ -41,8 +41,27 @@ def test_struct_sizes_match_header_layout():
     # pit_problem_desc etc. are passed by pointer; a layout drift would corrupt
     # every call, so pin the sizes computed by ctypes.
     assert C.sizeof(_lib.SolverConfigC) == 24
-    assert C.sizeof(_lib.RecordC) == 40
+    assert C.sizeof(_lib.RecordC) == 56
     assert C.sizeof(_lib.RunStatsC) == 40
+    # and against the C compiler's view of include/pit_b200.h
+    import os
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = ('#include <stdio.h>\n#include <stddef.h>\n#include "pit_b200.h"\n'
+           'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(pit_problem_desc), '
+           'sizeof(pit_record), sizeof(pit_solve_info), sizeof(pit_step_coeffs), '
+           'sizeof(pit_step_coeffs_2d), offsetof(pit_problem_desc, fine_max_iterations));'
+           'return 0;}\n')
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "s.c"), os.path.join(d, "s")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-I", os.path.join(root, "include"), c, "-o", exe], check=True)
+        got = [int(v) for v in subprocess.run([exe], capture_output=True, text=True,
+                                              check=True).stdout.split()]
+    assert got == [C.sizeof(_lib.ProblemDesc), C.sizeof(_lib.RecordC), C.sizeof(_lib.SolveInfoC),
+                   C.sizeof(_lib.StepCoeffsC), C.sizeof(_lib.StepCoeffs2DC),
+                   _lib.ProblemDesc.fine_max_iterations.offset]
 
 
 def test_no_gpu_fails_loudly():
