@@ -113,29 +113,72 @@ def run_oracle_checks(ctx: BlockOperatorContext, trials: int = 3, tolerance: flo
     return OracleCheckReport([f_check, g_check, ident])
 
 
+def preset_problem(case: str, dimension: int = 2, grid_points: int = 5, slabs: int = 3):
+    """cli.cpp do_verify's context (cli.cpp:58-75): the case's coefficients on
+    make_unit(dimension, grid_points), T = 0.1 over `slabs` slabs, fine dt =
+    slab/8, one coarse step, the Gaussian initial value."""
+    from . import api, presets
+
+    pr = presets.make_preset(case, "desk")
+    if dimension == 1 and pr.rotation:
+        raise ValueError("the rotation velocity field needs a 2D grid; pick another case")
+    m = grid_points - 2
+    lo, hi = -0.5, 0.5
+    T = 0.1
+    if dimension == 2:
+        return api.Problem2DImplicit(
+            m=m, stencil=presets.stencil_2d(m, lo, hi, pr.mu, pr.r, pr.rotation),
+            nonsymmetric=pr.rotation, N=slabs, T=T, fine_steps=8, coarse_steps=1,
+            y0=presets.gaussian_2d(m, lo, hi, pr.gaussian_sigma), grid_lo=lo, grid_hi=hi)
+    h = (hi - lo) / (m + 1)
+    lo_b, di_b, up_b = api.diffusion_reaction_bands(pr.mu, pr.r, h)
+    x = np.array([lo + (k + 1) * h for k in range(m)])
+    y0 = np.exp(-(x * x) / (2.0 * pr.gaussian_sigma ** 2))
+    return api.Problem1D(M=m, band_lo=lo_b, band_diag=di_b, band_up=up_b, N=slabs, T=T,
+                         fine_steps=8, coarse_steps=1, y0=y0, grid_lo=lo, grid_hi=hi)
+
+
 def main(argv=None) -> int:
-    """`python -m paper_2203_10148_b200.verify c1 [--slabs N] [--grid-points M]
-    [--trials T] [--tolerance X] [--inject-fault]` — the `pit verify`
-    analogue over the BASELINE configs (sizes reduced to the dense limit)."""
+    """`python -m paper_2203_10148_b200.verify [--case diffusion] [--dim 2]
+    [--grid-points 5] [--slabs 3] [--trials 20] [--tolerance 1e-10]
+    [--inject-fault]` — `pit verify` (cli.cpp:58-89) over the device
+    operators; or `verify c1..c5 [--slabs N] [--grid-points M]` for the
+    BASELINE configs reduced to the dense limit."""
     import argparse
 
     from . import configs
 
     ap = argparse.ArgumentParser(description="dense cross-check of the device operators")
-    ap.add_argument("case", choices=sorted(configs.SHAPES))
-    ap.add_argument("--slabs", type=int, default=4)
+    ap.add_argument("config", nargs="?", choices=sorted(configs.SHAPES), default=None)
+    ap.add_argument("--case", default="diffusion")
+    ap.add_argument("--dim", type=int, default=2)
+    ap.add_argument("--slabs", type=int, default=None)
     ap.add_argument("--grid-points", type=int, default=None)
-    ap.add_argument("--trials", type=int, default=3)
+    ap.add_argument("--trials", type=int, default=None)
     ap.add_argument("--tolerance", type=float, default=1e-10)
     ap.add_argument("--inject-fault", action="store_true")
     a = ap.parse_args(argv)
-    m = a.grid_points or (12 if a.case == "c5" else max(2, DENSE_ORACLE_LIMIT // a.slabs))
-    p = configs.make(a.case, slabs=a.slabs, M=m)
+    if a.config:
+        slabs = a.slabs or 4
+        trials = a.trials or 3
+        m = a.grid_points or (12 if a.config == "c5" else max(2, DENSE_ORACLE_LIMIT // slabs))
+        p = configs.make(a.config, slabs=slabs, M=m)
+        label = f"{a.config}, {p.N} slabs x {p.M} nodes"
+    else:
+        trials = a.trials or 20
+        try:
+            p = preset_problem(a.case, a.dim, a.grid_points or 5, a.slabs or 3)
+        except ValueError as e:
+            print(f"error: {e}")
+            return 2
+        label = f"{a.case}, {a.dim}D, {a.grid_points or 5} points/axis, N={p.N}"
     with BlockOperatorContext(p) as ctx:
-        rep = run_oracle_checks(ctx, a.trials, a.tolerance, a.inject_fault)
-    print(f"oracle checks on {a.case}, {p.N} slabs x {p.M} nodes, {a.trials} trials")
+        rep = run_oracle_checks(ctx, trials, a.tolerance, a.inject_fault)
+    print(f"oracle checks on {label}, {trials} trials, tolerance {a.tolerance}")
     for c in rep.checks:
-        print(f"  {c.name:44s} {c.worst_relative_error:.3e}  {'PASS' if c.passed else 'FAIL'}")
+        print(f"  [{'pass' if c.passed else 'FAIL'}] {c.name:40s} worst relative error "
+              f"{c.worst_relative_error:.3e}")
+    print("all checks passed" if rep.all_passed() else "CHECKS FAILED")
     return 0 if rep.all_passed() else 1
 
 

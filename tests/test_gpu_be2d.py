@@ -86,3 +86,26 @@ def test_desk_all_slab_counts_converge():
             seq = api.sequential_fine_solve(ctx)
         assert res.history.status == api.SolveStatus.Converged
         assert np.max(np.abs(res.solution - seq)) < 1e-6 * np.max(np.abs(seq))
+
+
+@pytest.mark.parametrize("case,dim", [("diffusion", 2), ("diffusion_reaction", 2),
+                                      ("advection_diffusion_reaction", 2), ("diffusion", 1),
+                                      ("diffusion_reaction", 1)])
+def test_pit_verify_presets_through_device_operators(case, dim):
+    # `pit verify` (cli.cpp:58-89: grid 5 points/axis, 3 slabs, 20 trials,
+    # 1e-10) on the device operators, and its inject-fault negative control
+    from paper_2203_10148_b200 import verify
+
+    p = verify.preset_problem(case, dim, 5, 3)
+    with api.BlockOperatorContext(p) as ctx:
+        rep = verify.run_oracle_checks(ctx, trials=20, tolerance=1e-10)
+        bad = verify.run_oracle_checks(ctx, trials=1, tolerance=1e-10, inject_fault=True)
+    assert rep.all_passed(), [(c.name, c.worst_relative_error) for c in rep.checks]
+    assert not any(c.passed for c in bad.checks)
+    assert verify.main(["--case", case, "--dim", str(dim)]) == 0
+
+
+def test_pit_verify_rejects_rotation_in_1d():
+    from paper_2203_10148_b200 import verify
+
+    assert verify.main(["--case", "advection_diffusion_reaction", "--dim", "1"]) == 2
