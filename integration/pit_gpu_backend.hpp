@@ -9,11 +9,16 @@
 //   pit::SolveResult r = gpu.pitsbicg_solve(cfg, exec, opts); // == pit::pitsbicg_solve
 //
 // Requirements checked at construction (else std::invalid_argument):
-//   * 1D grid; SpatialOperator a constant-band tridiagonal CSR (what
+//   * 1D grid: SpatialOperator a constant-band tridiagonal CSR (what
 //     assemble_spatial_operator builds for 1D, pde.cpp:55-64, or a hand-built
 //     constant-coefficient operator such as central-difference advection);
+//   * 2D grid (the desk/paper presets, runner.cpp:75-88): any 5-point CSR
+//     (assemble_spatial_operator's 2D rows, pde.cpp:66-100, any velocity),
+//     m <= 50 points per axis; both propagators backward Euler with the
+//     reference's inner solvers (CG if op().symmetric(), else BiCGStab);
 //   * a source, if any, separable f(t,x) = amp*sin(omega*t+phase)*g(x),
-//     described by a SeparableSource (the std::function itself is opaque).
+//     described by a SeparableSource (the std::function itself is opaque;
+//     1D only).
 #pragma once
 
 #include <chrono>
@@ -54,8 +59,10 @@ class Backend {
                    int device = 0)
       : ctx_(ctx) {
     const SpatialGrid& g = ctx.fine().op().grid();
-    if (g.dimension() != 1)
-      throw std::invalid_argument("pit::gpu::Backend: only 1D grids are supported");
+    if (g.dimension() == 2) {
+      init_2d(ctx, g, device);
+      return;
+    }
     const CsrMatrix& A = ctx.fine().op().matrix();
     double band[3] = {0.0, 0.0, 0.0};  // lo, diag, up
     bool seen[3] = {false, false, false};
@@ -101,6 +108,44 @@ class Backend {
     check(pit_context_create(&d, &c));
     h_.reset(c);
     M_ = d.interior;
+    N_ = d.slab_count;
+  }
+
+  // 2D: the per-row south/west/centre/east/north entries of A (0 when the
+  // CSR row has none) and the operator's symmetry flag go to the device.
+  void init_2d(const BlockOperatorContext& ctx, const SpatialGrid& g, int device) {
+    if (ctx.fine().has_source())
+      throw std::invalid_argument("pit::gpu::Backend: no sources on 2D grids");
+    const SpatialOperator& op = ctx.fine().op();
+    const CsrMatrix& A = op.matrix();
+    const int m = g.interior_per_axis(), M = m * m;
+    std::vector<double> st(5 * static_cast<size_t>(M), 0.0);
+    for (int i = 0; i < A.n; ++i)
+      for (int k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k) {
+        const int d = A.col[k] - i;
+        const int slot = d == -m ? 0 : d == -1 ? 1 : d == 0 ? 2 : d == 1 ? 3 : d == m ? 4 : -1;
+        if (slot < 0) throw std::invalid_argument("pit::gpu::Backend: operator is not 5-point");
+        st[static_cast<size_t>(slot) * M + i] = A.val[k];
+      }
+    pit_problem_desc d{};
+    d.dimension = 2;
+    d.interior = m;
+    d.grid_lo = g.lo();
+    d.grid_hi = g.hi();
+    d.slab_count = ctx.block_count();
+    d.total_time = ctx.partition().total_time();
+    d.fine_steps = ctx.fine().steps_per_slab();
+    d.coarse_steps = ctx.coarse().steps_per_slab();
+    const auto y0 = ctx.initial_value().values();
+    d.initial_value = y0.data();
+    d.device = device;
+    d.fine_scheme = PIT_SCHEME_BACKWARD_EULER;
+    d.stencil = st.data();
+    d.nonsymmetric = op.symmetric() ? 0 : 1;
+    pit_context* c = nullptr;
+    check(pit_context_create(&d, &c));
+    h_.reset(c);
+    M_ = M;
     N_ = d.slab_count;
   }
 

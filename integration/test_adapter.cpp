@@ -7,7 +7,9 @@
 
 #include "pit/block_system.hpp"
 #include "pit/pde.hpp"
+#include "pit/presets.hpp"
 #include "pit/propagator.hpp"
+#include "pit/runner.hpp"
 #include "pit/solvers.hpp"
 #include "pit_gpu_backend.hpp"
 
@@ -24,6 +26,23 @@ static double rel(const BlockVector& a, const BlockVector& b) {
     worst = std::fmax(worst, std::sqrt(d) / (s > 0 ? std::sqrt(s) : 1.0));
   }
   return worst;
+}
+
+// max_n ||a_n - b_n|| / max_n ||b_n|| (blocks decay by orders of magnitude
+// over the desk horizon, so per-block relative errors of tiny blocks say
+// nothing about the solve)
+static double relmax(const BlockVector& a, const BlockVector& b) {
+  double d = 0.0, s = 0.0;
+  for (int n = 0; n < a.block_count(); ++n) {
+    double dn = 0, sn = 0;
+    for (size_t i = 0; i < a[n].size(); ++i) {
+      dn += (a[n][i] - b[n][i]) * (a[n][i] - b[n][i]);
+      sn += b[n][i] * b[n][i];
+    }
+    d = std::fmax(d, std::sqrt(dn));
+    s = std::fmax(s, std::sqrt(sn));
+  }
+  return d / (s > 0 ? s : 1.0);
 }
 
 int main() {
@@ -59,6 +78,36 @@ int main() {
   const bool ok = eF < 1e-10 && eG < 1e-10 && eS < 1e-10 && kc == kg &&
                   rc.history.restarts == rg.history.restarts &&
                   st_cpu.fine_applications == st_gpu.fine_applications;
-  std::printf("%s\n", ok ? "ADAPTER OK" : "ADAPTER FAIL");
-  return ok ? 0 : 1;
+  // the reference's own desk presets (build_context, runner.cpp:75-88),
+  // 2D backward Euler with CG / BiCGStab inner solves, N = 8
+  bool ok2 = true;
+  for (const CaseName cn : {CaseName::Diffusion, CaseName::DiffusionReaction,
+                            CaseName::AdvectionDiffusionReaction}) {
+    const BlockOperatorContext c2 = build_context(make_preset(cn, Scale::Desk), 8);
+    gpu::Backend g2(c2);
+    BlockVector X = c2.zero_vector();
+    for (int n = 0; n < c2.block_count(); ++n)
+      for (size_t i = 0; i < X[n].size(); ++i) X[n][i] = std::cos(0.37 * n + 0.011 * i);
+    const double f2 = rel(g2.apply_F(X, exec), apply_F(c2, X, exec));
+    const double g2e = rel(g2.apply_G_inverse(X), apply_G_inverse(c2, X));
+    SolverConfig c8;  // default tolerance 1e-8, as run_experiment
+    const BlockVector ref = sequential_fine_solve(c2);
+    SolveOptions o;
+    o.reference = &ref;
+    const SolveResult r1 = pitsbicg_solve(c2, c8, exec, o);
+    const SolveResult r2 = g2.pitsbicg_solve(c8, exec, o);
+    const double s2 = relmax(r2.solution, r1.solution);
+    const auto &a = r1.history.records.back(), &b = r2.history.records.back();
+    const bool e_ok = b.error_vs_reference.has_value() &&
+                      std::fabs(*b.error_vs_reference - *a.error_vs_reference) <=
+                          1e-4 * *a.error_vs_reference + 1e-11;
+    std::printf("%s desk N=8: apply_F rel %.3e, G^-1 rel %.3e, pitsbicg k %d/%d, lambda relmax %.3e, "
+                "error_vs_reference %.6e/%.6e\n",
+                to_string(cn).c_str(), f2, g2e, a.k, b.k, s2, *a.error_vs_reference,
+                b.error_vs_reference ? *b.error_vs_reference : -1.0);
+    ok2 = ok2 && f2 < 1e-9 && g2e < 1e-9 && a.k == b.k && s2 < 1e-8 && e_ok &&
+          r1.history.restarts == r2.history.restarts;
+  }
+  std::printf("%s\n", ok && ok2 ? "ADAPTER OK" : "ADAPTER FAIL");
+  return ok && ok2 ? 0 : 1;
 }
