@@ -247,8 +247,68 @@ def device_time_to_tolerance(name):
             **({"coarse_cg_iterations": int(its)} if its else {})}
 
 
+PRESET_LINES = (("diffusion", "desk", 16), ("advection_diffusion_reaction", "desk", 16),
+                ("advection_diffusion_reaction", "paper", 64))
+
+
+def preset_time_to_tolerance(case, scale, n, with_reference=False):
+    """The reference's own experiments (presets.cpp; K6):
+    device PiTSBiCG to the runner's default 1e-8 (warm solve, inputs
+    resident), beside the reference's pitsbicg_solve on the host cores
+    (oracle/_ref, SlabExecutor(nproc)) when that library is present."""
+    import torch
+
+    from paper_2203_10148_b200 import _lib, api, presets
+
+    L = _lib.lib()
+    p = presets.build_problem(presets.make_preset(case, scale), n)
+    with api.BlockOperatorContext(p) as ctx:
+        lam = torch.empty((p.N, p.M), dtype=torch.float64, device="cuda")
+        cfg = _lib.SolverConfigC(1e-8, 1e-12, 200, _lib.PIT_GUESS_COARSE_SWEEP)
+        recs = (_lib.RecordC * 202)()
+        info = _lib.SolveInfoC()
+        for _ in range(2):  # time the second (work vectors allocated by the first)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            api._check(L.pit_pitsbicg_solve_device(ctx.handle, C.byref(cfg), None,
+                                                   lam.data_ptr(), recs, 202, C.byref(info), None))
+            wall = time.perf_counter() - t0
+    n_rec = min(info.record_count, 202)
+    out = {"N": n, "m": p.m, "ms": wall * 1e3, "k": recs[n_rec - 1].k,
+           "restarts": info.restarts, "converged": info.status == _lib.PIT_CONVERGED}
+    ref_so = os.path.join(ROOT, "oracle", "_ref", "libpitref.so")
+    if with_reference and os.path.exists(ref_so):
+        R = C.CDLL(ref_so)
+        R.pitref_create_preset.restype = C.c_void_p
+        R.pitref_create_preset.argtypes = [C.c_int, C.c_int, C.c_int]
+        R.pitref_destroy.argtypes = [C.c_void_p]
+        h = R.pitref_create_preset(presets.CASES.index(case), 0 if scale == "desk" else 1, n)
+        cap = 64
+        k = (C.c_int * cap)()
+        res = (C.c_double * cap)()
+        fa = (C.c_long * cap)()
+        ca = (C.c_long * cap)()
+        nrec, rs, conv = C.c_int(), C.c_int(), C.c_int()
+        lam_h = np.zeros((p.N, p.M))
+        cores = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        R.pitref_pitsbicg(C.c_void_p(h), C.c_double(1e-8), C.c_double(1e-12), 200, 0, cores, None,
+                          lam_h.ctypes.data_as(C.POINTER(C.c_double)), None, k, res, fa, ca, cap,
+                          C.byref(nrec), C.byref(rs), C.byref(conv))
+        out["reference_cpu"] = {"ms": (time.perf_counter() - t0) * 1e3, "cores": cores,
+                                "k": k[max(0, min(nrec.value, cap) - 1)]}
+        R.pitref_destroy(C.c_void_p(h))
+    return out
+
+
 def secondary(include_c5_solve=True):
-    out = {"apply_F": {}, "time_to_tolerance": {}}
+    out = {"apply_F": {}, "time_to_tolerance": {}, "presets_time_to_tolerance": {}}
+    for case, scale, n in PRESET_LINES:
+        try:
+            out["presets_time_to_tolerance"][f"{scale}/{case}"] = preset_time_to_tolerance(
+                case, scale, n)
+        except Exception as e:  # pragma: no cover
+            out["presets_time_to_tolerance"][f"{scale}/{case}"] = {"error": str(e)}
     for name in ("c1", "c3", "c4", "c5"):
         try:
             rate, ms, gp = device_apply_rate(name)
@@ -435,6 +495,14 @@ def run_ours(args, rank, world):
             v, cores, kind, sample = cpu_reference_rate(p)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                                     "sample": sample}
+            if not args.no_secondary:
+                # the reference's own pitsbicg_solve on the presets of
+                # secondary.presets_time_to_tolerance, same host cores
+                pre = {}
+                for case, scale, n in PRESET_LINES:
+                    r = preset_time_to_tolerance(case, scale, n, with_reference=True)
+                    pre[f"{scale}/{case}"] = r.get("reference_cpu")
+                line["cpu_baseline"]["presets_time_to_tolerance"] = pre
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                                     "sample": f"unavailable: {e}"}
