@@ -172,7 +172,29 @@ class OracleBackend2D(OracleBackend):
         return out
 
 
+class OracleBackendBE2D(OracleBackend):
+    """2D backward-Euler presets (K6 mirror)."""
+
+    def __init__(self, p, first, count):
+        self.p = p
+        self.o = OracleProblem(p)
+        self.lib = O.orc()
+        self.M = p.M
+        self.first, self.count = first, count
+        self.has_source = False
+        self.shape = None
+
+    def _prop(self, role, with_source, x, slab):
+        return self.o.propagate(role, x, slab)
+
+
 def _problem(name, slabs, M, fine_steps):
+    if name.startswith("preset:"):
+        import dataclasses
+
+        from paper_2203_10148_b200 import presets
+        p = presets.build_problem(presets.make_preset(name.split(":")[1]), slabs)
+        return dataclasses.replace(p, fine_steps=fine_steps, T=p.T * fine_steps / p.fine_steps)
     p = configs.make(name, slabs=slabs, M=M)
     p.fine_steps = fine_steps
     if name == "c5":
@@ -196,7 +218,8 @@ def _worker(rank, world, port, case, out_path):
     name, slabs, M, fine_steps = case
     p = _problem(name, slabs, M, fine_steps)
     first, count = shard_range(p.N, world, rank)
-    be = (OracleBackend2D if name == "c5" else OracleBackend)(p, first, count)
+    be = (OracleBackendBE2D if name.startswith("preset:") else
+          OracleBackend2D if name == "c5" else OracleBackend)(p, first, count)
     ops = ShardedOperators(be, p.N)
     rng = np.random.default_rng(5)
     Lg = rng.uniform(-1, 1, (p.N, p.M))
@@ -214,7 +237,8 @@ def _worker(rank, world, port, case, out_path):
     dist.destroy_process_group()
 
 
-CASES = [("c2", 7, 300, 40), ("c4", 6, 256, 30), ("c3", 5, 200, 50), ("c5", 5, 12, 48)]
+CASES = [("c2", 7, 300, 40), ("c4", 6, 256, 30), ("c3", 5, 200, 50), ("c5", 5, 12, 48),
+         ("preset:advection_diffusion_reaction", 5, None, 10)]
 
 
 @pytest.mark.parametrize("world", [2, 3])

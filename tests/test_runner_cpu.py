@@ -1,0 +1,46 @@
+"""CPU: the runner's output format (runner.cpp:17-55, 90-106) and argument
+handling, without a device."""
+from __future__ import annotations
+
+import io
+
+import pytest
+
+from paper_2203_10148_b200 import api, presets, runner
+
+
+def _hist():
+    h = api.ConvergenceHistory()
+    h.records = [api.IterationRecord(0, 0.5, 3, 6, 1.25, 0.125),
+                 api.IterationRecord(1, 1.0 / 3.0, 9, 12, 2.5, None)]
+    h.status = api.SolveStatus.Converged
+    h.restarts = 1
+    h.stats.fine_applications, h.stats.coarse_applications = 9, 12
+    return h
+
+
+def test_csv_rows_and_log_line():
+    out = io.StringIO()
+    runner.append_csv_rows(out, "diffusion", "pitsbicg", 4, _hist())
+    assert out.getvalue().splitlines() == [
+        "diffusion,pitsbicg,4,0,0.5,3,6,0.125,1.25",
+        "diffusion,pitsbicg,4,1,0.33333333333333331,9,12,,2.5"]
+    log = io.StringIO()
+    runner.log_result(log, "diffusion", "pitsbicg", 4, _hist(), "B200")
+    assert log.getvalue() == ("diffusion N=4 pitsbicg: converged at k=1, residual 0.333, fine 9, "
+                              "coarse 12, restarts 1, 2.5 ms (B200)\n")
+    assert runner.HEADER == ("case,solver,N,k,residual_N_inf,fine_applications,"
+                             "coarse_applications,error_vs_reference,wall_ms\n")
+
+
+def test_slab_list_and_presets():
+    assert runner.parse_slab_list("4, 8,16") == [4, 8, 16]
+    with pytest.raises(ValueError):
+        runner.parse_slab_list("4,x")
+    p = presets.make_preset("advection_diffusion_reaction", "paper")
+    assert (p.grid_points, p.total_time, p.mu, p.r, p.rotation) == (51, 6.4, 0.1, 0.5, True)
+    with pytest.raises(ValueError, match="unknown case"):
+        presets.make_preset("nope")
+    with pytest.raises(ValueError, match="not a multiple"):
+        presets.fine_steps(1.6, 3, 1e-3)
+    assert presets.fine_steps(1.6, 64, 1e-3) == 25
