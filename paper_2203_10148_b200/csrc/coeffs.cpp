@@ -25,8 +25,7 @@ const L kLayouts[] = {
     {8, 1, 1, 4},   {8, 1, 1, 8},   {8, 1, 1, 16}, {8, 1, 1, 32}, {16, 1, 1, 4}, {16, 1, 1, 8},
     {16, 1, 1, 16}, {16, 1, 1, 32}, {32, 2, 1, 4}, {32, 2, 1, 8}, {32, 1, 2, 4}, {32, 2, 2, 4},
     {64, 2, 2, 1},  {64, 2, 2, 2},  {64, 2, 2, 4}, {64, 4, 1, 2}, {64, 1, 4, 2}, {64, 4, 1, 1},
-    {64, 4, 1, 4},  {64, 1, 2, 2},  {32, 2, 2, 8}, {64, 2, 2, 8}, {16, 2, 1, 16}, {16, 2, 2, 8}, {64, 4, 1, 8},
-    {32, 2, 1, 2}};
+    {64, 4, 1, 4},  {64, 1, 2, 2},  {32, 2, 2, 8}, {64, 2, 2, 8}, {16, 2, 1, 16}, {16, 2, 2, 8}, {64, 4, 1, 8}};
 }  // namespace
 
 bool layout_supported(int mpt, int nsub, int nseg, int warps) {

@@ -802,7 +802,7 @@ int ew_grid(size_t n) {
   X(16, 1, 1, 16) X(16, 1, 1, 32) X(32, 2, 1, 4) X(32, 2, 1, 8) X(32, 1, 2, 4) X(32, 2, 2, 4) \
   X(64, 2, 2, 1) X(64, 2, 2, 2) X(64, 2, 2, 4) X(64, 4, 1, 2) X(64, 1, 4, 2) X(64, 4, 1, 1)  \
   X(64, 4, 1, 4) X(64, 1, 2, 2) X(32, 2, 2, 8) X(64, 2, 2, 8) X(16, 2, 1, 16) X(16, 2, 2, 8)   \
-  X(64, 4, 1, 8) X(32, 2, 1, 2)
+  X(64, 4, 1, 8)
 
 #define PIT_SHAPE(MP, NU, NS, W) Shape<(MP) / ((NU) * (NS)), NU, NS, W>
 
@@ -812,8 +812,7 @@ int ew_grid(size_t n) {
 #define PIT_SCAN_SPECIAL(X)                                                                  \
   X(64, 4, 1, 1, 0) X(64, 4, 1, 1, 1) X(64, 4, 1, 1, 2) X(64, 4, 1, 1, 3)                   \
   X(64, 4, 1, 2, 0) X(64, 4, 1, 2, 1) X(64, 4, 1, 2, 2) X(64, 4, 1, 2, 3)                   \
-  X(64, 4, 1, 4, 0) X(64, 4, 1, 4, 1) X(64, 4, 1, 4, 2) X(64, 4, 1, 4, 3)                   \
-  X(32, 2, 1, 2, 0) X(32, 2, 1, 2, 1) X(32, 2, 1, 2, 2) X(32, 2, 1, 2, 3)
+  X(64, 4, 1, 4, 0) X(64, 4, 1, 4, 1) X(64, 4, 1, 4, 2) X(64, 4, 1, 4, 3)
 
 cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                         const SlabArgs& A, int ctas, cudaStream_t st) {
