@@ -232,6 +232,11 @@ int pit_step_positions(const pit_problem_desc* desc, int role, double* ppos_out,
                        double* zt_out);
 
 /* ---- host-pointer entry points (copy in, compute, copy out) ---------- */
+/* pit_apply_F with page-locked L and out (cudaHostAlloc / cudaHostRegister /
+ * torch pin_memory) overlaps the copies with the fine batch: the input goes
+ * up in chunks of blocks, K1's slabs start as their chunk lands and their
+ * output chunks go back as they complete (same kernel, same bits).  Pageable
+ * buffers take the sequential copy-compute-copy path. */
 int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats);
 int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats);
 int pit_apply_G_inverse(pit_context* ctx, const double* V, double* out, pit_run_stats* stats);
