@@ -11,7 +11,7 @@ solve (log_result, runner.cpp:31-55; the executor's worker count and
 fine-phase efficiency are replaced by the device name).
 
     python -m paper_2203_10148_b200.runner run --case diffusion --solver both \\
-        --slabs 4,8 --scale desk --out out
+        --slabs 4,8 --scale desk --out out [--config overrides.txt]
 """
 from __future__ import annotations
 
@@ -101,8 +101,12 @@ def run_experiment(spec: RunSpec, log: TextIO = sys.stdout) -> str:
     return path
 
 
+class ConfigError(ValueError):
+    """pit::ConfigError (CLI exit code 2)."""
+
+
 def parse_slab_list(text: str) -> List[int]:
-    """parse_slab_list (config.cpp): comma-separated slab counts >= 2."""
+    """parse_slab_list (config.cpp:46-66): comma-separated slab counts >= 2."""
     out = []
     for tok in text.split(","):
         tok = tok.strip()
@@ -111,11 +115,82 @@ def parse_slab_list(text: str) -> List[int]:
         try:
             v = int(tok)
         except ValueError:
-            raise ValueError(f"bad slab count '{tok}'") from None
+            v = 0
+        if v < 2:
+            raise ConfigError(f"slab counts must be integers >= 2, got '{tok}'")
         out.append(v)
     if not out:
-        raise ValueError("empty slab list")
+        raise ConfigError(f"slab list '{text}' is empty")
     return out
+
+
+_KEYS = {"case": str, "mu": float, "r": float, "velocity": str, "grid_points": int, "T": float,
+         "dt_fine": float, "slabs": str, "epsilon": float, "epsilon0": float, "max_iters": int,
+         "workers": int}
+
+
+def parse_config_text(text: str) -> dict:
+    """parse_config_text (config.cpp:68-118): `key = value` lines, `#`
+    comments; unknown keys and malformed values are ConfigErrors."""
+    out = {}
+    for line_no, raw in enumerate(text.splitlines(), 1):
+        entry = raw.split("#", 1)[0].strip()
+        if not entry:
+            continue
+        if "=" not in entry:
+            raise ConfigError(f"config line {line_no}: expected key = value")
+        key, value = (x.strip() for x in entry.split("=", 1))
+        if not key or not value:
+            raise ConfigError(f"config line {line_no}: expected key = value")
+        if key not in _KEYS:
+            raise ConfigError(f"config line {line_no}: unknown key '{key}'")
+        kind = _KEYS[key]
+        if key == "case":
+            if value not in presets.CASES:
+                raise ConfigError(f"unknown case '{value}' (expected diffusion, "
+                                  "diffusion_reaction, or advection_diffusion_reaction)")
+            out[key] = value
+        elif key == "velocity":
+            if value not in ("zero", "rotation"):
+                raise ConfigError(f"config line {line_no}: unknown velocity '{value}'")
+            out[key] = value == "rotation"
+        elif key == "slabs":
+            out[key] = parse_slab_list(value)
+        else:
+            try:
+                out[key] = kind(value)
+            except ValueError:
+                what = "an integer" if kind is int else "a number"
+                raise ConfigError(f"config line {line_no}: expected {what}, got '{value}'") from None
+    return out
+
+
+def apply_overrides(ov: dict, preset: presets.ExperimentPreset, solver: api.SolverConfig) -> None:
+    """apply_overrides (config.cpp:128-151); `workers` has no device meaning."""
+    if "case" in ov:
+        base = presets.make_preset(ov["case"], "desk")
+        preset.case_name, preset.rotation, preset.mu, preset.r = (base.case_name, base.rotation,
+                                                                  base.mu, base.r)
+    if "mu" in ov:
+        preset.mu = ov["mu"]
+    if "r" in ov:
+        preset.r = ov["r"]
+    if "velocity" in ov:
+        preset.rotation = ov["velocity"]
+    if "grid_points" in ov:
+        preset.grid_points = ov["grid_points"]
+    if "T" in ov:
+        preset.total_time = ov["T"]
+    if "dt_fine" in ov:
+        preset.dt_fine = ov["dt_fine"]
+    if "slabs" in ov:
+        preset.slab_counts = ov["slabs"]
+    if "epsilon" in ov:
+        solver.tolerance = ov["epsilon"]
+    if "epsilon0" in ov:
+        solver.restart_tolerance = ov["epsilon0"]
+    if "max_iters" in ov:
+        solver.max_iterations = ov["max_iters"]
 
 
 def main(argv: Optional[List[str]] = None) -> int:
@@ -129,6 +204,7 @@ def main(argv: Optional[List[str]] = None) -> int:
     run.add_argument("--slabs", default="", help="comma-separated slab counts (default preset sweep)")
     run.add_argument("--scale", default="desk", help="paper | desk")
     run.add_argument("--out", default="out", help="output directory")
+    run.add_argument("--config", default="", help="key = value file overriding the flags")
     run.add_argument("--tolerance", type=float, default=None, help="solver tolerance")
     run.add_argument("--max-iterations", type=int, default=None)
     run.add_argument("--device", type=int, default=0)
@@ -138,6 +214,12 @@ def main(argv: Optional[List[str]] = None) -> int:
         if args.slabs:
             preset.slab_counts = parse_slab_list(args.slabs)
         cfg = api.SolverConfig()
+        if args.config:
+            try:
+                text = open(args.config).read()
+            except OSError:
+                raise ConfigError(f"cannot read config file '{args.config}'") from None
+            apply_overrides(parse_config_text(text), preset, cfg)
         if args.tolerance is not None:
             cfg.tolerance = args.tolerance
         if args.max_iterations is not None:

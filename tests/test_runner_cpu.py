@@ -44,3 +44,27 @@ def test_slab_list_and_presets():
     with pytest.raises(ValueError, match="not a multiple"):
         presets.fine_steps(1.6, 3, 1e-3)
     assert presets.fine_steps(1.6, 64, 1e-3) == 25
+
+
+def test_config_overrides():
+    # parse_config_text / apply_overrides (config.cpp:68-151)
+    ov = runner.parse_config_text("""
+        # comment
+        case = advection_diffusion_reaction
+        mu = 0.2          # trailing comment
+        slabs = 4, 8
+        epsilon = 1e-9
+        max_iters = 50
+        workers = 3
+    """)
+    p = presets.make_preset("diffusion", "paper")
+    cfg = api.SolverConfig()
+    runner.apply_overrides(ov, p, cfg)
+    assert (p.case_name, p.rotation, p.mu, p.r, p.grid_points) == \
+        ("advection_diffusion_reaction", True, 0.2, 0.5, 51)
+    assert p.slab_counts == [4, 8] and cfg.tolerance == 1e-9 and cfg.max_iterations == 50
+    for bad, msg in (("mu 1", "expected key = value"), ("nope = 1", "unknown key"),
+                     ("grid_points = x", "expected an integer"), ("slabs = 1,4", ">= 2"),
+                     ("velocity = swirl", "unknown velocity")):
+        with pytest.raises(runner.ConfigError, match=msg):
+            runner.parse_config_text(bad)
