@@ -123,3 +123,54 @@ def test_criterion8_solvers_start_from_identical_first_residual():
         api.parareal_solve(ctx, api.SolverConfig(), options=api.SolveOptions(first_residual_out=a))
         api.pitsbicg_solve(ctx, api.SolverConfig(), options=api.SolveOptions(first_residual_out=b))
     assert np.array_equal(a, b)
+
+
+# ---- the reference's doctest cases that pin this path ----------------------
+
+def _identity_problems(n):
+    """dy/dt = 0 (A = 0): 1D bands 0 and the 2D 5-point K6 path with a zero
+    stencil (test_block_system.cpp:82-103, test_solvers.cpp:167-197)."""
+    rng = np.random.default_rng(11)
+    p1 = api.Problem1D(M=40, band_lo=0.0, band_diag=0.0, band_up=0.0, N=n, T=1.0, fine_steps=4,
+                       coarse_steps=2, y0=rng.uniform(-1, 1, 40))
+    m = 5
+    p2 = api.Problem2DImplicit(m=m, stencil=np.zeros((5, m * m)), nonsymmetric=False, N=n, T=1.0,
+                               fine_steps=4, coarse_steps=2, y0=rng.uniform(-1, 1, m * m))
+    return p1, p2
+
+
+def test_identity_dynamics_F_telescopes_and_G_inverse_accumulates():
+    for p in _identity_problems(4):
+        x = np.random.default_rng(200).uniform(-1, 1, (p.N, p.M))
+        with api.BlockOperatorContext(p) as ctx:
+            fx, gx = api.apply_F(ctx, x), api.apply_G_inverse(ctx, x)
+        assert np.array_equal(fx[0], x[0])
+        for n in range(1, p.N):
+            assert np.array_equal(fx[n], x[n] - x[n - 1])
+        acc = x[0].copy()
+        assert np.array_equal(gx[0], acc)
+        for n in range(1, p.N):
+            acc = acc + x[n]
+            assert np.array_equal(gx[n], acc)
+
+
+def test_half_step_exit_on_identity_dynamics():
+    n = 6
+    for p in _identity_problems(n):
+        with api.BlockOperatorContext(p) as ctx:
+            res = api.pitsbicg_solve(ctx, api.SolverConfig(
+                initial_guess=api.InitialGuessPolicy.Zero))
+        rows = res.history.records
+        assert res.history.status == api.SolveStatus.Converged and len(rows) == 2
+        assert (rows[0].k, rows[0].fine_applications, rows[0].coarse_applications) == (0, n - 1, n - 1)
+        assert rows[1].k == 1 and rows[1].residual_norm == 0.0
+        assert rows[1].fine_applications == rows[1].coarse_applications == 2 * (n - 1)
+        for b in range(n):
+            assert np.array_equal(res.solution[b], p.y0)
+
+
+def test_restart_engages_on_desk_diffusion():
+    with desk("diffusion", 8) as ctx:
+        res = api.pitsbicg_solve(ctx, api.SolverConfig())
+    assert res.history.status == api.SolveStatus.Converged
+    assert res.history.restarts >= 1 and res.history.records[-1].residual_norm <= 1e-8
