@@ -37,12 +37,12 @@ bool layout_supported(int mpt, int nsub, int nseg, int warps) {
 Layout auto_layout(int M, int role) {
   // fine: 64 contiguous points per thread as 4 sub-chunks of 16 (four
   // interleaved chains, one warp scan per direction); coarse (one persistent
-  // CTA, latency bound): 8 warps, few points each.  Measured on B200,
+  // CTA, latency bound): 8 warps (16 at M = 8192), few points each.  Measured on B200,
   // profiles/README.md.
   static const L fine[] = {{4, 1, 1, 1},  {4, 1, 1, 2},  {4, 1, 1, 4},  {8, 1, 1, 4},
                            {64, 4, 1, 1}, {64, 4, 1, 2}, {64, 4, 1, 4}, {64, 4, 1, 8}};
-  static const L coarse[] = {{4, 1, 1, 1},  {4, 1, 1, 2},  {4, 1, 1, 4},  {4, 1, 1, 8},
-                             {8, 1, 1, 8},  {16, 1, 1, 8}, {32, 2, 1, 8}, {16, 1, 1, 32}};
+  static const L coarse[] = {{4, 1, 1, 1},  {4, 1, 1, 2},   {4, 1, 1, 4},  {4, 1, 1, 8},
+                             {8, 1, 1, 8},  {16, 1, 1, 8},  {16, 1, 1, 16}, {16, 1, 1, 32}};
   const L* list = role == PIT_FINE ? fine : coarse;
   for (int i = 0; i < 8; ++i)
     if (32 * list[i].warps * list[i].mpt >= M)

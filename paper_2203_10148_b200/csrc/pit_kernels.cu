@@ -842,7 +842,7 @@ cudaError_t launch_sweep(int mpt, int nsub, int nseg, int warps, bool src, const
 #define X(MP, NU, NS, W)                                   \
   if (mpt == MP && nsub == NU && nseg == NS && warps == W) \
     return sweep_launch<Shape<(MP) / ((NU) * (NS)), NU, NS, W, 5>, false>(P, A, st);
-    X(8, 1, 1, 8) X(16, 1, 1, 8) X(32, 2, 1, 8)
+    X(8, 1, 1, 8) X(16, 1, 1, 8) X(16, 1, 1, 16)
 #undef X
   }
 #define X(MP, NU, NS, W)                                                        \
