@@ -29,13 +29,24 @@ namespace {
 
 constexpr int kT = kBe2Threads, kNW = kBe2Threads / 32;
 
+// Per-thread context: owned points (padded indices), stencil rows (in
+// registers up to 3 points per thread, else read from shared memory),
+// reduction slots and the three operand buffers the stencil reads.
 template <int PPT>
 struct Be2Ctx {
+  static constexpr bool kRegCoef = PPT <= 3;
   int m, M, pitch;
   int ip[PPT];        // padded index of owned point k (or -1)
-  double cs[PPT], cw[PPT], cc[PPT], ce[PPT], cn[PPT], mi[PPT];
+  int gi[PPT];        // interior index of owned point k
+  double cr[6][kRegCoef ? PPT : 1];  // S, W, C, E, N, minv (kRegCoef)
+  const double* cf;   // [6][M] shared memory (!kRegCoef)
   double* red;        // [2][2][kNW]
   int par;            // reduction slot set
+  double *opx, *opp, *ops;  // padded operand buffers (x, p or p^, s^)
+  __device__ __forceinline__ double coef(int j, int k) const {
+    if constexpr (kRegCoef) return cr[j][k];
+    return cf[(size_t)j * M + gi[k]];
+  }
 };
 
 template <int PPT>
@@ -62,83 +73,87 @@ __device__ __forceinline__ double2 block_sum2(Be2Ctx<PPT>& c, double a, double b
   return make_double2(sa, sb);
 }
 
-// <a,b> (and <c,d>) over the interior: per-thread fma chains in point order
+// Solver vectors of the owned points, in registers.
 template <int PPT>
-__device__ __forceinline__ double dot1(Be2Ctx<PPT>& c, const double* a, const double* b) {
+using Vec = double[PPT];
+
+// <a,b> (and <e,f>): per-thread fma chains in point order
+template <int PPT>
+__device__ __forceinline__ double dot1(Be2Ctx<PPT>& c, const Vec<PPT>& a, const Vec<PPT>& b) {
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) s = fma(a[c.ip[k]], b[c.ip[k]], s);
+    if (c.ip[k] >= 0) s = fma(a[k], b[k], s);
   return block_sum2(c, s, 0.0).x;
 }
 template <int PPT>
-__device__ __forceinline__ double2 dot2(Be2Ctx<PPT>& c, const double* a, const double* b,
-                                        const double* e, const double* f) {
+__device__ __forceinline__ double2 dot2(Be2Ctx<PPT>& c, const Vec<PPT>& a, const Vec<PPT>& b,
+                                        const Vec<PPT>& e, const Vec<PPT>& f) {
   double s = 0.0, t = 0.0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
     if (c.ip[k] >= 0) {
-      s = fma(a[c.ip[k]], b[c.ip[k]], s);
-      t = fma(e[c.ip[k]], f[c.ip[k]], t);
+      s = fma(a[k], b[k], s);
+      t = fma(e[k], f[k], t);
     }
   return block_sum2(c, s, t);
 }
 
-// (A x)_i in CSR column order south, west, centre, east, north
-// (assemble_spatial_operator's row order); x must be visible (barrier).
+// (A op)_i in CSR column order south, west, centre, east, north
+// (assemble_spatial_operator's row order); op complete (barrier).
 template <int PPT>
-__device__ __forceinline__ double stencil(const Be2Ctx<PPT>& c, int k, const double* x) {
+__device__ __forceinline__ double stencil(const Be2Ctx<PPT>& c, int k, const double* op) {
   const int i = c.ip[k];
   double s = 0.0;
-  s = fma(c.cs[k], x[i - c.pitch], s);
-  s = fma(c.cw[k], x[i - 1], s);
-  s = fma(c.cc[k], x[i], s);
-  s = fma(c.ce[k], x[i + 1], s);
-  s = fma(c.cn[k], x[i + c.pitch], s);
+  s = fma(c.coef(0, k), op[i - c.pitch], s);
+  s = fma(c.coef(1, k), op[i - 1], s);
+  s = fma(c.coef(2, k), op[i], s);
+  s = fma(c.coef(3, k), op[i + 1], s);
+  s = fma(c.coef(4, k), op[i + c.pitch], s);
   return s;
+}
+
+template <int PPT>
+__device__ __forceinline__ void publish(const Be2Ctx<PPT>& c, double* op, const Vec<PPT>& v) {
+#pragma unroll
+  for (int k = 0; k < PPT; ++k)
+    if (c.ip[k] >= 0) op[c.ip[k]] = v[k];
 }
 
 // r = b - A x (true_residual, sparse.cpp:53-58); returns ||r||
 template <int PPT>
-__device__ __forceinline__ double true_residual(Be2Ctx<PPT>& c, const double* b, const double* x,
-                                                double* r) {
+__device__ __forceinline__ double true_residual(Be2Ctx<PPT>& c, const Vec<PPT>& b,
+                                                const Vec<PPT>& x, Vec<PPT>& r) {
+  publish(c, c.opx, x);
   __syncthreads();  // x complete
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
     if (c.ip[k] >= 0) {
-      const int i = c.ip[k];
-      r[i] = b[i] - stencil(c, k, x);
-      s = fma(r[i], r[i], s);
+      r[k] = b[k] - stencil(c, k, c.opx);
+      s = fma(r[k], r[k], s);
     }
   return sqrt(block_sum2(c, s, 0.0).x);
 }
 
-// Vectors of one solve (padded, in shared memory).
-struct Be2Vec {
-  double *x, *b, *r, *rt, *p, *ph, *v, *s, *sh, *t;
-};
-
-// Jacobi-PCG, control flow of solve_cg (sparse.cpp:60-114).  Uses x, b, r,
-// and p (padded operand), v (z), t (q).  Returns true when converged.
+// Jacobi-PCG, control flow of solve_cg (sparse.cpp:60-114).
 template <int PPT>
-__device__ bool cg_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, int cap, int* iters) {
-  double *x = V.x, *b = V.b, *r = V.r, *p = V.p, *z = V.v, *q = V.t;
+__device__ bool cg_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double rel_tol, int cap,
+                         int* iters) {
+  Vec<PPT> r, z, p, q;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) x[c.ip[k]] = 0.0;
+  for (int k = 0; k < PPT; ++k) x[k] = r[k] = z[k] = p[k] = q[k] = 0.0;
   const double norm_b = sqrt(dot1(c, b, b));
   *iters = 0;
   if (norm_b == 0.0) return true;
   const double tol = rel_tol * norm_b;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) {
-      const int i = c.ip[k];
-      r[i] = b[i];
-      z[i] = c.mi[k] * r[i];
-      p[i] = z[i];
-    }
+  for (int k = 0; k < PPT; ++k) {
+    r[k] = b[k];
+    z[k] = c.coef(5, k) * r[k];
+    p[k] = z[k];
+  }
+  publish(c, c.opp, p);
   double2 d = dot2(c, r, z, r, r);
   double rz = d.x, res = sqrt(d.y);
   int it = 0;
@@ -150,9 +165,8 @@ __device__ bool cg_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, int ca
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
         if (c.ip[k] >= 0) {
-          const int i = c.ip[k];
-          q[i] = stencil(c, k, p);
-          pq = fma(p[i], q[i], pq);
+          q[k] = stencil(c, k, c.opp);
+          pq = fma(p[k], q[k], pq);
         }
       pq = block_sum2(c, pq, 0.0).x;
       if (pq == 0.0 || !isfinite(pq)) {
@@ -161,24 +175,19 @@ __device__ bool cg_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, int ca
       }
       const double alpha = rz / pq;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) {
-          const int i = c.ip[k];
-          x[i] = fma(alpha, p[i], x[i]);
-          r[i] = fma(-alpha, q[i], r[i]);
-          z[i] = c.mi[k] * r[i];
-        }
+      for (int k = 0; k < PPT; ++k) {
+        x[k] = fma(alpha, p[k], x[k]);
+        r[k] = fma(-alpha, q[k], r[k]);
+        z[k] = c.coef(5, k) * r[k];
+      }
       ++it;
       d = dot2(c, r, r, r, z);
       res = sqrt(d.x);
       if (!isfinite(res) || res <= tol) break;
       const double beta = d.y / rz;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) {
-          const int i = c.ip[k];
-          p[i] = fma(beta, p[i], z[i]);
-        }
+      for (int k = 0; k < PPT; ++k) p[k] = fma(beta, p[k], z[k]);
+      publish(c, c.opp, p);  // read by the next stencil after its barrier
       rz = d.y;
     }
     // confirm against the exact residual (sparse.cpp:97-110)
@@ -187,25 +196,25 @@ __device__ bool cg_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, int ca
     if (res <= tol) return true;
     if (it >= cap || stalled || !isfinite(res)) return false;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) {
-        const int i = c.ip[k];
-        z[i] = c.mi[k] * r[i];
-        p[i] = z[i];
-      }
+    for (int k = 0; k < PPT; ++k) {
+      z[k] = c.coef(5, k) * r[k];
+      p[k] = z[k];
+    }
+    publish(c, c.opp, p);
     rz = dot1(c, r, z);
   }
 }
 
 // Jacobi-BiCGStab, control flow of solve_bicgstab (sparse.cpp:116-206).
 template <int PPT>
-__device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, int cap,
-                               int* iters) {
-  double *x = V.x, *b = V.b, *r = V.r, *rt = V.rt, *p = V.p, *ph = V.ph, *v = V.v, *s = V.s,
-         *sh = V.sh, *t = V.t;
+__device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double rel_tol,
+                               int cap, int* iters) {
+  // p^ and s^ live only in their operand buffers (own values read back)
+  Vec<PPT> r, rt, p, v, s, t;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) x[c.ip[k]] = 0.0;
+  for (int k = 0; k < PPT; ++k) x[k] = r[k] = rt[k] = p[k] = v[k] = s[k] = t[k] = 0.0;
+  double* const ph = c.opp;
+  double* const sh = c.ops;
   const double norm_b = sqrt(dot1(c, b, b));
   *iters = 0;
   if (norm_b == 0.0) return true;
@@ -213,11 +222,6 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
   double rho_prev = 1.0, alpha = 1.0, omega = 1.0, res = 0.0;
   int it = 0;
   bool restart = true, first = true;
-  auto set_rt = [&]() {
-#pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) rt[c.ip[k]] = r[c.ip[k]];
-  };
   while (it < cap) {
     if (restart) {
       res = true_residual(c, b, x, r);
@@ -229,7 +233,8 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
         *iters = it;
         return false;
       }
-      set_rt();
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) rt[k] = r[k];
       first = true;
       restart = false;
       rho_prev = 1.0;
@@ -244,29 +249,23 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
     }
     if (first) {
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) p[c.ip[k]] = r[c.ip[k]];
+      for (int k = 0; k < PPT; ++k) p[k] = r[k];
       first = false;
     } else {
       const double beta = (rho / rho_prev) * (alpha / omega);
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) {
-          const int i = c.ip[k];
-          p[i] = fma(beta, fma(-omega, v[i], p[i]), r[i]);
-        }
+      for (int k = 0; k < PPT; ++k) p[k] = fma(beta, fma(-omega, v[k], p[k]), r[k]);
     }
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) ph[c.ip[k]] = c.mi[k] * p[c.ip[k]];
+      if (c.ip[k] >= 0) ph[c.ip[k]] = c.coef(5, k) * p[k];
     __syncthreads();  // ph complete
     double rv = 0.0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
       if (c.ip[k] >= 0) {
-        const int i = c.ip[k];
-        v[i] = stencil(c, k, ph);
-        rv = fma(rt[i], v[i], rv);
+        v[k] = stencil(c, k, c.opp);
+        rv = fma(rt[k], v[k], rv);
       }
     rv = block_sum2(c, rv, 0.0).x;
     if (rv == 0.0 || !isfinite(rv)) {
@@ -279,15 +278,14 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
       if (c.ip[k] >= 0) {
-        const int i = c.ip[k];
-        s[i] = fma(-alpha, v[i], r[i]);
-        ss = fma(s[i], s[i], ss);
+        s[k] = fma(-alpha, v[k], r[k]);
+        ss = fma(s[k], s[k], ss);
       }
     if (sqrt(block_sum2(c, ss, 0.0).x) <= tol) {
       // half-iteration exit; keep going from the exact residual if spurious
 #pragma unroll
       for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) x[c.ip[k]] = fma(alpha, ph[c.ip[k]], x[c.ip[k]]);
+        if (c.ip[k] >= 0) x[k] = fma(alpha, ph[c.ip[k]], x[k]);
       ++it;
       res = true_residual(c, b, x, r);
       if (res <= tol) {
@@ -298,7 +296,8 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
         *iters = it;
         return false;
       }
-      set_rt();
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) rt[k] = r[k];
       first = true;
       rho_prev = 1.0;
       alpha = 1.0;
@@ -307,16 +306,15 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
     }
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) sh[c.ip[k]] = c.mi[k] * s[c.ip[k]];
+      if (c.ip[k] >= 0) sh[c.ip[k]] = c.coef(5, k) * s[k];
     __syncthreads();  // sh complete
     double tt = 0.0, ts = 0.0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
       if (c.ip[k] >= 0) {
-        const int i = c.ip[k];
-        t[i] = stencil(c, k, sh);
-        tt = fma(t[i], t[i], tt);
-        ts = fma(t[i], s[i], ts);
+        t[k] = stencil(c, k, c.ops);
+        tt = fma(t[k], t[k], tt);
+        ts = fma(t[k], s[k], ts);
       }
     const double2 d = block_sum2(c, tt, ts);
     omega = d.x == 0.0 ? 0.0 : d.y / d.x;
@@ -324,10 +322,9 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
       if (c.ip[k] >= 0) {
-        const int i = c.ip[k];
-        x[i] = fma(omega, sh[i], fma(alpha, ph[i], x[i]));
-        r[i] = fma(-omega, t[i], s[i]);
-        rr = fma(r[i], r[i], rr);
+        x[k] = fma(omega, sh[c.ip[k]], fma(alpha, ph[c.ip[k]], x[k]));
+        r[k] = fma(-omega, t[k], s[k]);
+        rr = fma(r[k], r[k], rr);
       }
     ++it;
     res = sqrt(block_sum2(c, rr, 0.0).x);
@@ -350,67 +347,74 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Be2Vec& V, double rel_tol, 
   return res <= tol;
 }
 
-// `steps` backward-Euler steps of the state in V.b (padded), result in V.b.
-// Returns false at the first step whose solve fails or is non-finite
-// (InnerSolveError, pde.cpp:119-128).
+// `steps` backward-Euler steps of the state y (registers).  Returns false at
+// the first step whose solve fails or is non-finite (InnerSolveError,
+// pde.cpp:119-128).
 template <int PPT>
-__device__ bool propagate(Be2Ctx<PPT>& c, Be2Vec& V, const Be2Params& P, long long* iters) {
+__device__ bool propagate(Be2Ctx<PPT>& c, Vec<PPT>& y, const Be2Params& P, long long* iters) {
+  Vec<PPT> x;
   for (int step = 0; step < P.steps; ++step) {
     int it = 0;
-    const bool ok = P.symmetric ? cg_solve(c, V, P.rel_tol, P.cap, &it)
-                                : bicgstab_solve(c, V, P.rel_tol, P.cap, &it);
+    const bool ok = P.symmetric ? cg_solve(c, y, x, P.rel_tol, P.cap, &it)
+                                : bicgstab_solve(c, y, x, P.rel_tol, P.cap, &it);
     if (iters && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(iters),
                                              (unsigned long long)it);
     bool bad = !ok;
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0 && !isfinite(V.x[c.ip[k]])) bad = true;
+      if (c.ip[k] >= 0 && !isfinite(x[k])) bad = true;
     if (__syncthreads_or(bad)) return false;
-    double* nb = V.x;  // the solution is the next right-hand side
-    V.x = V.b;
-    V.b = nb;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) y[k] = x[k];  // the solution is the next right-hand side
   }
   return true;
 }
 
 template <int PPT>
-__device__ void setup(Be2Ctx<PPT>& c, Be2Vec& V, const Be2Params& P, unsigned char* smem) {
+__device__ void setup(Be2Ctx<PPT>& c, const Be2Params& P, unsigned char* smem) {
   c.m = P.m;
   c.M = P.M;
   c.pitch = P.m + 2;
   const int np = c.pitch * c.pitch;
   double* base = reinterpret_cast<double*>(smem);
-  double* vec[10];
-  for (int v = 0; v < 10; ++v) vec[v] = base + (size_t)v * np;
-  V = Be2Vec{vec[0], vec[1], vec[2], vec[3], vec[4], vec[5], vec[6], vec[7], vec[8], vec[9]};
-  c.red = base + (size_t)10 * np;
+  c.opx = base;
+  c.opp = base + np;
+  c.ops = base + 2 * (size_t)np;
+  c.red = base + 3 * (size_t)np;
+  double* cf = c.red + 4 * kNW;
   c.par = 0;
-  for (int i = threadIdx.x; i < 10 * np; i += kT) base[i] = 0.0;  // ghost rings stay 0
+  for (int i = threadIdx.x; i < 3 * np; i += kT) base[i] = 0.0;  // ghost rings stay 0
+  if constexpr (!Be2Ctx<PPT>::kRegCoef) {
+    for (int i = threadIdx.x; i < 5 * P.M; i += kT) cf[i] = P.coef[i];
+    for (int i = threadIdx.x; i < P.M; i += kT) cf[5 * P.M + i] = P.minv[i];
+    c.cf = cf;
+  } else {
+    c.cf = nullptr;
+  }
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int i = threadIdx.x + k * kT;
+    c.gi[k] = i < P.M ? i : 0;
     if (i < P.M) {
       const int ix = i % P.m, iy = i / P.m;
       c.ip[k] = (iy + 1) * c.pitch + ix + 1;
-      c.cs[k] = P.coef[i];
-      c.cw[k] = P.coef[P.M + i];
-      c.cc[k] = P.coef[2 * P.M + i];
-      c.ce[k] = P.coef[3 * P.M + i];
-      c.cn[k] = P.coef[4 * P.M + i];
-      c.mi[k] = P.minv[i];
     } else {
       c.ip[k] = -1;
-      c.cs[k] = c.cw[k] = c.cc[k] = c.ce[k] = c.cn[k] = c.mi[k] = 0.0;
+    }
+    if constexpr (Be2Ctx<PPT>::kRegCoef) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) c.cr[j][k] = i < P.M ? P.coef[(size_t)j * P.M + i] : 0.0;
+      c.cr[5][k] = i < P.M ? P.minv[i] : 0.0;
     }
   }
   __syncthreads();
 }
 
 template <int PPT>
-__device__ __forceinline__ void load_block(const Be2Ctx<PPT>& c, double* dst, const double* src) {
+__device__ __forceinline__ void load_block(const Be2Ctx<PPT>& c, Vec<PPT>& dst, const double* src) {
 #pragma unroll
   for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) dst[c.ip[k]] = src ? src[threadIdx.x + k * kT] : 0.0;
+    dst[k] = (src && c.ip[k] >= 0) ? src[threadIdx.x + k * kT] : 0.0;
 }
 
 // Fine batch (SlabArgs semantics of K1): CTA b propagates its input block and
@@ -420,28 +424,27 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
     be2d_batch_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SlabArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Be2Ctx<PPT> c;
-  Be2Vec V;
-  setup<PPT>(c, V, P, smem_raw);
+  setup<PPT>(c, P, smem_raw);
   const int b = blockIdx.x, slab = A.slab0 + b;
   const int M = P.M;
   const double* src = b + A.in_shift >= 0 ? (A.in ? A.in + (size_t)(b + A.in_shift) * M : nullptr)
                                           : A.halo;
-  load_block(c, V.b, src);
-  const bool ok = propagate(c, V, P, nullptr);
+  Vec<PPT> y;
+  load_block(c, y, src);
+  const bool ok = propagate(c, y, P, nullptr);
   if (!ok && threadIdx.x == 0) atomicMin(A.status, slab);
   const size_t off = (size_t)b * M;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int i = threadIdx.x + k * kT;
     if (i < M) {
-      const double y = V.b[c.ip[k]];
       if (A.mode == kApplyF) {
-        A.out[off + i] = A.Lsub[off + i] - y;
+        A.out[off + i] = A.Lsub[off + i] - y[k];
       } else if (A.mode == kResidual) {
-        const double a = A.Lsub[off + i] - y;
+        const double a = A.Lsub[off + i] - y[k];
         A.out[off + i] = A.rhs[off + i] - a;
       } else {
-        A.out[off + i] = y;
+        A.out[off + i] = y[k];
       }
     }
   }
@@ -461,12 +464,12 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
     be2d_sweep_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SweepArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Be2Ctx<PPT> c;
-  Be2Vec V;
-  setup<PPT>(c, V, P, smem_raw);
+  setup<PPT>(c, P, smem_raw);
   const int M = P.M;
-  load_block(c, V.b, A.start);
+  Vec<PPT> y;
+  load_block(c, y, A.start);
   for (int b = 0; b < A.count; ++b) {
-    if (!propagate(c, V, P, P.iters)) {
+    if (!propagate(c, y, P, P.iters)) {
       if (threadIdx.x == 0) atomicMin(A.status, A.slab0 + b);
       return;
     }
@@ -475,26 +478,21 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
     for (int k = 0; k < PPT; ++k) {
       const int i = threadIdx.x + k * kT;
       if (i < M) {
-        double y = V.b[c.ip[k]];
-        if (A.V) {
-          y = y + A.V[(size_t)b * M + i];  // W_n = G(W_{n-1}) + V_n (block_system.cpp:187-188)
-          V.b[c.ip[k]] = y;
-        }
-        W[i] = y;
+        if (A.V) y[k] = y[k] + A.V[(size_t)b * M + i];  // W_n = G(W_{n-1}) + V_n (block_system.cpp:187-188)
+        W[i] = y[k];
       }
     }
   }
 }
 
-template <class K>
-cudaError_t launch_be2(K k, int grid, size_t smem, const Be2Params& P, const void* args,
-                       cudaStream_t st);
-
 }  // namespace
 
 size_t be2d_smem_bytes(int m) {
-  const size_t np = (size_t)(m + 2) * (m + 2);
-  return sizeof(double) * (10 * np + 4 * kNW);
+  // three padded operand buffers, reduction slots, and (more than 3 points
+  // per thread) the stencil rows and Jacobi inverse
+  const size_t np = (size_t)(m + 2) * (m + 2), M = (size_t)m * m;
+  const bool reg_coef = (M + kBe2Threads - 1) / kBe2Threads <= 3;
+  return sizeof(double) * (3 * np + 4 * kNW + (reg_coef ? 0 : 6 * M));
 }
 
 bool be2d_supported(int m) {
