@@ -12,11 +12,13 @@
 // restarts, half-step exit and true-residual confirmation, the 10n cap.
 //
 // One CTA of kBe2Threads threads per slab (fine batch), or one CTA sweeping
-// the slabs in order (coarse sweep, sequential fine solve).  All solver
-// vectors live in shared memory in a zero-padded (m+2)^2 layout, so the
-// stencil reads its neighbours without bounds tests; thread t owns interior
-// points t, t+T, ... (PPT of them), whose stencil rows and Jacobi inverse
-// stay in registers.  Reductions: per-thread fma chain over its points in
+// the slabs in order (coarse sweep, sequential fine solve).  Thread t owns
+// interior points t, t+T, ... (PPT of them) and keeps their solver vectors
+// in registers; only the stencil's operands (x, p or p^, s^) go through
+// zero-padded (m+2)^2 shared-memory buffers, so the stencil reads its
+// neighbours without bounds tests.  Stencil rows and the Jacobi inverse stay
+// in registers up to 3 points per thread, in shared memory beyond.
+// Reductions: per-thread fma chain over its points in
 // order, xor butterfly, warp totals summed in order by every thread (one
 // block barrier).  oracle/pit_oracle2d_be.c performs the identical
 // operation sequence.
