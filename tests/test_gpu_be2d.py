@@ -109,3 +109,24 @@ def test_pit_verify_rejects_rotation_in_1d():
     from paper_2203_10148_b200 import verify
 
     assert verify.main(["--case", "advection_diffusion_reaction", "--dim", "1"]) == 2
+
+
+@pytest.mark.parametrize("m", [1, 3, 22, 23, 39, 45, 50])
+@pytest.mark.parametrize("nonsym", [False, True])
+def test_k6_all_thread_layouts_bitwise(m, nonsym):
+    # every points-per-thread instantiation (1..5; stencil rows in registers
+    # up to 3, in shared memory beyond) on a random 5-point operator (the
+    # rotation preset's structure: diagonally dominant, upwind-like
+    # off-diagonals), fine batch and coarse sweep against the oracle
+    rng = np.random.default_rng(m * 7 + nonsym)
+    st = presets.stencil_2d(m, -0.5, 0.5, 0.2, 0.5, nonsym)
+    if nonsym:  # symmetric operators keep CG's assumptions
+        st[[0, 1, 3, 4]] *= rng.uniform(0.8, 1.2, (4, m * m))
+    p = api.Problem2DImplicit(m=m, stencil=st, nonsymmetric=nonsym, N=3, T=0.03, fine_steps=3,
+                              coarse_steps=1, y0=rng.uniform(-1, 1, m * m))
+    o = OracleProblem(p)
+    L = rng.uniform(-1, 1, (p.N, p.M))
+    with api.BlockOperatorContext(p) as ctx:
+        assert same(api.apply_F(ctx, L), o.apply_F(L))
+        assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))
+        assert ctx.coarse_iterations() == o.coarse_iterations()
