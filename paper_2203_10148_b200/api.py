@@ -483,12 +483,16 @@ def _stats_in(stats, sc):
 
 
 def apply_F(ctx: BlockOperatorContext, L: np.ndarray, exec=None,
-            stats: Optional[RunStats] = None) -> np.ndarray:
+            stats: Optional[RunStats] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
     """(F L)_0 = L_0, (F L)_n = L_n - FineHom(L_{n-1})  (block_system.cpp:115-147).
     `exec` (a SlabExecutor) is accepted for signature compatibility; the
-    slab fan-out is the kernel grid."""
+    slab fan-out is the kernel grid.  With page-locked `L` and `out` (e.g.
+    torch pin_memory) the copies overlap the kernel (pit_apply_F)."""
     L = ctx._vec(L, "apply_F")
-    out = np.empty_like(L)
+    if out is None:
+        out = np.empty_like(L)
+    elif out.shape != L.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("apply_F: out must be a C-contiguous float64 array of L's shape")
     sc = _stats_out(stats)
     _check(_lib.lib().pit_apply_F(ctx.handle, dptr(L), dptr(out), C.byref(sc) if sc else None))
     _stats_in(stats, sc)

@@ -400,6 +400,8 @@ def test_pipelined_host_apply_F_full_c2_and_error():
         ref = api.apply_F(ctx, L)
         api._check(api._lib.lib().pit_apply_F(ctx.handle, api.dptr(Lp), api.dptr(Op), None))
         assert np.array_equal(Op, ref)
+        Op[...] = 0.0
+        assert api.apply_F(ctx, Lp, out=Op) is Op and np.array_equal(Op, ref)  # the Python API
         Lp[700, 11] = np.nan
         Lp[300, 5] = np.inf
         with pytest.raises(api.SlabError) as e:
