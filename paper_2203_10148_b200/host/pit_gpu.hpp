@@ -11,8 +11,11 @@
 // Block vectors are contiguous block-major std::vector<double> (N*M).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -76,6 +79,7 @@ struct IterationRecord {
   long fine_applications = 0;
   long coarse_applications = 0;
   double wall_ms = 0.0;
+  std::optional<double> error_vs_reference;  // with SolveOptions::reference
 };
 
 struct ConvergenceHistory {
@@ -99,6 +103,7 @@ struct SolverConfig {  // pit::SolverConfig (solvers.hpp:36-44)
 
 struct SolveOptions {
   const BlockVector* initial_guess_override = nullptr;
+  const BlockVector* reference = nullptr;  // every row: ||lambda - reference||_{N,inf}
   BlockVector* first_residual_out = nullptr;
 };
 
@@ -124,8 +129,49 @@ struct Problem1D {
   int device = 0;
 };
 
+// The reference's 2D experiments (presets.cpp, runner.cpp:75-88): m x m
+// interior nodes, both propagators backward Euler on a 5-point operator given
+// per node as its south, west, centre, east, north CSR entries (0 = absent),
+// inner solves Jacobi-PCG or (nonsymmetric) Jacobi-BiCGStab.  See
+// make_preset / build_problem below.
+struct Problem2D {
+  int m = 0;
+  double grid_lo = -0.5, grid_hi = 0.5;
+  std::vector<double> stencil;  // [5][m*m]
+  bool nonsymmetric = false;
+  int N = 2;
+  double T = 1.0;
+  int fine_steps = 1, coarse_steps = 1;
+  std::vector<double> y0;
+  double fine_tolerance = 0.0, coarse_tolerance = 0.0;  // 0: 1e-12
+  int device = 0;
+};
+
 class BlockOperatorContext {  // pit::BlockOperatorContext (block_system.hpp:55-72)
  public:
+  explicit BlockOperatorContext(const Problem2D& p) : M_(p.m * p.m), N_(p.N) {
+    if (static_cast<int>(p.y0.size()) != M_ || static_cast<int>(p.stencil.size()) != 5 * M_)
+      throw std::invalid_argument("ScalarField: value count does not match grid");
+    pit_problem_desc d{};
+    d.dimension = 2;
+    d.interior = p.m;
+    d.grid_lo = p.grid_lo;
+    d.grid_hi = p.grid_hi;
+    d.slab_count = p.N;
+    d.total_time = p.T;
+    d.fine_steps = p.fine_steps;
+    d.coarse_steps = p.coarse_steps;
+    d.initial_value = p.y0.data();
+    d.device = p.device;
+    d.fine_scheme = PIT_SCHEME_BACKWARD_EULER;
+    d.stencil = p.stencil.data();
+    d.nonsymmetric = p.nonsymmetric ? 1 : 0;
+    d.fine_tolerance = p.fine_tolerance;
+    d.coarse_tolerance = p.coarse_tolerance;
+    pit_context* c = nullptr;
+    check(pit_context_create(&d, &c));
+    ctx_.reset(c);
+  }
   explicit BlockOperatorContext(const Problem1D& p) : M_(p.M), N_(p.N) {
     pit_problem_desc d{};
     d.dimension = 1;
@@ -256,14 +302,23 @@ inline SolveResult solve(bool pitsbicg, const BlockOperatorContext& ctx,
   pit_solve_info info{};
   BlockVector first;
   if (options.first_residual_out) first = ctx.zero_vector();
+  if (options.reference) {
+    ctx.require_shape(*options.reference, "reference");
+    check(pit_set_reference(ctx.handle(), options.reference->data()));
+  }
   auto fn = pitsbicg ? pit_pitsbicg_solve : pit_parareal_solve;
-  check(fn(ctx.handle(), &c, init ? init->data() : nullptr, r.solution.data(),
-           options.first_residual_out ? first.data() : nullptr, rows.data(),
-           static_cast<int>(rows.size()), &info));
-  for (int i = 0; i < info.record_count; ++i)
-    r.history.records.push_back({rows[i].k, rows[i].residual_norm,
-                                 static_cast<long>(rows[i].fine_applications),
-                                 static_cast<long>(rows[i].coarse_applications), rows[i].wall_ms});
+  const int rc = fn(ctx.handle(), &c, init ? init->data() : nullptr, r.solution.data(),
+                    options.first_residual_out ? first.data() : nullptr, rows.data(),
+                    static_cast<int>(rows.size()), &info);
+  if (options.reference) pit_set_reference(ctx.handle(), nullptr);
+  check(rc);
+  for (int i = 0; i < info.record_count; ++i) {
+    IterationRecord rec{rows[i].k, rows[i].residual_norm,
+                        static_cast<long>(rows[i].fine_applications),
+                        static_cast<long>(rows[i].coarse_applications), rows[i].wall_ms, {}};
+    if (rows[i].has_error) rec.error_vs_reference = rows[i].error_vs_reference;
+    r.history.records.push_back(rec);
+  }
   r.history.status =
       info.status == PIT_CONVERGED ? SolveStatus::Converged : SolveStatus::MaxIterations;
   r.history.restarts = info.restarts;
@@ -283,6 +338,80 @@ inline SolveResult pitsbicg_solve(const BlockOperatorContext& ctx, const SolverC
 inline SolveResult parareal_solve(const BlockOperatorContext& ctx, const SolverConfig& config,
                                   const SolveOptions& options = {}) {
   return detail::solve(false, ctx, config, options);
+}
+
+// ---- the reference's presets (presets.cpp:48-77, runner.cpp:75-88) ------
+
+enum class CaseName { Diffusion, DiffusionReaction, AdvectionDiffusionReaction };
+enum class Scale { Paper, Desk };
+
+struct ExperimentPreset {  // pit::ExperimentPreset (presets.hpp:25-40)
+  CaseName case_name = CaseName::Diffusion;
+  bool rotation = false;
+  double mu = 1.0, r = 0.0;
+  int grid_points = 33;
+  double total_time = 1.6, dt_fine = 1e-3;
+  std::vector<int> slab_counts{4, 8, 16, 32, 64};
+  double gaussian_sigma = 0.1;
+};
+
+inline ExperimentPreset make_preset(CaseName name, Scale scale) {
+  ExperimentPreset p;
+  p.case_name = name;
+  if (name == CaseName::DiffusionReaction) p.r = 1.5;
+  if (name == CaseName::AdvectionDiffusionReaction) {
+    p.rotation = true;
+    p.mu = 0.1;
+    p.r = 0.5;
+  }
+  if (scale == Scale::Paper) {
+    p.grid_points = 51;
+    p.total_time = 6.4;
+  }
+  return p;
+}
+
+// build_context as a device problem: assemble_spatial_operator's 2D rows
+// (pde.cpp:66-100), make_fine_propagator's step count (propagator.cpp:88-98),
+// one coarse step, gaussian_initial_condition (grid.cpp:120-141).
+inline Problem2D build_problem(const ExperimentPreset& pr, int slab_count) {
+  if (slab_count < 2) throw std::invalid_argument("TimeSlabPartition: need at least 2 slabs");
+  Problem2D p;
+  p.m = pr.grid_points - 2;
+  const int m = p.m, n = m * m;
+  const double lo = p.grid_lo, h = (p.grid_hi - lo) / (pr.grid_points - 1);
+  const double mu_h2 = pr.mu / (h * h);
+  p.stencil.assign(5 * static_cast<size_t>(n), 0.0);
+  p.y0.resize(n);
+  const double inv = 1.0 / (2.0 * pr.gaussian_sigma * pr.gaussian_sigma);
+  for (int j = 0; j < m; ++j) {
+    const double y = lo + (j + 1) * h;
+    for (int i = 0; i < m; ++i) {
+      const double x = lo + (i + 1) * h;
+      const double ux = pr.rotation ? -y : 0.0, uy = pr.rotation ? x : 0.0;
+      const double centre = 4.0 * mu_h2 + pr.r + (std::fabs(ux) + std::fabs(uy)) / h;
+      double w = -mu_h2, e = -mu_h2, s = -mu_h2, nn = -mu_h2;
+      if (ux > 0.0) w -= ux / h; else if (ux < 0.0) e += ux / h;
+      if (uy > 0.0) s -= uy / h; else if (uy < 0.0) nn += uy / h;
+      const size_t row = static_cast<size_t>(j) * m + i;
+      p.stencil[row] = (s != 0.0 && j > 0) ? s : 0.0;
+      p.stencil[n + row] = (w != 0.0 && i > 0) ? w : 0.0;
+      p.stencil[2 * static_cast<size_t>(n) + row] = centre;
+      p.stencil[3 * static_cast<size_t>(n) + row] = (e != 0.0 && i < m - 1) ? e : 0.0;
+      p.stencil[4 * static_cast<size_t>(n) + row] = (nn != 0.0 && j < m - 1) ? nn : 0.0;
+      p.y0[row] = std::exp(-(x * x + y * y) * inv);
+    }
+  }
+  p.nonsymmetric = pr.rotation;
+  p.N = slab_count;
+  p.T = pr.total_time;
+  const double ratio = (pr.total_time / slab_count) / pr.dt_fine;
+  const int steps = std::max(1, static_cast<int>(std::lround(ratio)));
+  if (std::fabs(ratio - steps) > 1e-9 * steps)
+    throw std::invalid_argument("make_fine_propagator: slab length is not a multiple of dt");
+  p.fine_steps = steps;
+  p.coarse_steps = 1;
+  return p;
 }
 
 }  // namespace pit_gpu

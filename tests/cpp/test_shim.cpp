@@ -42,6 +42,20 @@ int main() {
     ok = false;
   } catch (const pit_gpu::ConfigError&) {
   }
+  // the reference's desk rotation preset (K6, BiCGStab inner solves) with a
+  // reference solution: converges, every row carries error_vs_reference
+  const auto pr = pit_gpu::make_preset(pit_gpu::CaseName::AdvectionDiffusionReaction,
+                                       pit_gpu::Scale::Desk);
+  pit_gpu::BlockOperatorContext c2(pit_gpu::build_problem(pr, 8));
+  const pit_gpu::BlockVector ref = pit_gpu::sequential_fine_solve(c2);
+  pit_gpu::SolveOptions opts;
+  opts.reference = &ref;
+  const auto r2 = pit_gpu::pitsbicg_solve(c2, pit_gpu::SolverConfig{}, opts);
+  const auto& l2 = r2.history.records.back();
+  std::printf("desk rotation N=8: k=%d residual=%.3e error=%.3e\n", l2.k, l2.residual_norm,
+              l2.error_vs_reference ? *l2.error_vs_reference : -1.0);
+  ok = ok && r2.history.status == pit_gpu::SolveStatus::Converged && l2.residual_norm <= 1e-8 &&
+       l2.error_vs_reference && *l2.error_vs_reference < 1e-7;
   std::printf("%s\n", ok ? "SHIM OK" : "SHIM FAIL");
   return ok ? 0 : 1;
 }
