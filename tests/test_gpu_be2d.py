@@ -130,3 +130,33 @@ def test_k6_all_thread_layouts_bitwise(m, nonsym):
         assert same(api.apply_F(ctx, L), o.apply_F(L))
         assert same(api.apply_G_inverse(ctx, L), o.apply_G_inverse(L))
         assert ctx.coarse_iterations() == o.coarse_iterations()
+
+
+@pytest.mark.parametrize("case", presets.CASES)
+def test_device_matches_reference_fixtures(case):
+    # the reference's own outputs on its desk presets (committed fixtures, no
+    # reference tree needed on the box): operators and PiTSBiCG
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "presets_desk_reference.npz"))
+
+    def relmax(a, b):
+        return np.max(np.linalg.norm(a - b, axis=1)) / np.max(np.linalg.norm(b, axis=1))
+
+    p = presets.build_problem(presets.make_preset(case), 4)
+    with api.BlockOperatorContext(p) as ctx:
+        assert relmax(api.sequential_fine_solve(ctx), g[f"{case}_seq4"]) < 1e-10
+        assert relmax(api.apply_F(ctx, g[f"{case}_probe4"]), g[f"{case}_F4"]) < 1e-10
+        assert relmax(api.apply_G_inverse(ctx, g[f"{case}_probe4"]), g[f"{case}_G4"]) < 1e-10
+        r4 = api.pitsbicg_solve(ctx, api.SolverConfig())
+    assert relmax(r4.solution, g[f"{case}_lam4"]) < 1e-9
+    q = presets.build_problem(presets.make_preset(case), 8)
+    with api.BlockOperatorContext(q) as ctx:
+        r8 = api.pitsbicg_solve(ctx, api.SolverConfig())
+    for r, key in ((r4, "4"), (r8, "8")):
+        rows = g[f"{case}_rows{key}"]
+        assert [(x.k, x.fine_applications, x.coarse_applications) for x in r.history.records] == \
+            [(int(a), int(b), int(c)) for a, b, c in rows[:, [0, 2, 3]]]
+        assert np.allclose([x.residual_norm for x in r.history.records], rows[:, 1], rtol=1e-6,
+                           atol=1e-13)
+        assert r.history.restarts == int(g[f"{case}_restarts{key}"])

@@ -101,3 +101,36 @@ def test_oracle_pitsbicg_matches_reference(cid, case):
         assert abs(a[1] - b[1]) <= 1e-6 * abs(b[1]) + 1e-13
     scale = np.max(np.abs(ref["lam"]))
     assert np.max(np.abs(r["lam"] - ref["lam"])) <= 1e-9 * scale
+
+
+# ---- against the committed reference fixtures (tests/golden/make_golden_presets.py)
+
+def _gold():
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                "presets_desk_reference.npz"))
+
+
+def _relmax(a, b):
+    return np.max(np.linalg.norm(a - b, axis=1)) / np.max(np.linalg.norm(b, axis=1))
+
+
+@pytest.mark.parametrize("case", presets.CASES)
+def test_oracle_matches_reference_fixtures(case):
+    g = _gold()
+    p = presets.build_problem(presets.make_preset(case), 4)
+    assert np.array_equal(p.y0, g[f"{case}_y0"])
+    o = OracleProblem(p)
+    assert _relmax(o.sequential_fine(), g[f"{case}_seq4"]) < 1e-10
+    assert _relmax(o.apply_F(g[f"{case}_probe4"]), g[f"{case}_F4"]) < 1e-10
+    assert _relmax(o.apply_G_inverse(g[f"{case}_probe4"]), g[f"{case}_G4"]) < 1e-10
+    for n, key in ((4, "4"), (8, "8")):
+        q = presets.build_problem(presets.make_preset(case), n)
+        r = OracleProblem(q).solve(1e-8)
+        rows = g[f"{case}_rows{key}"]
+        assert [int(x[0]) for x in r["rows"]] == [int(x) for x in rows[:, 0]]
+        assert [(x[2], x[3]) for x in r["rows"]] == [(int(a), int(b)) for a, b in rows[:, 2:4]]
+        assert np.allclose([x[1] for x in r["rows"]], rows[:, 1], rtol=1e-6, atol=1e-13)
+        assert r["restarts"] == int(g[f"{case}_restarts{key}"])
+        if n == 4:
+            assert _relmax(r["lam"], g[f"{case}_lam4"]) < 1e-9
