@@ -22,6 +22,7 @@
  *   pit_block_inner_product / pit_block_norm_n_inf
  *                          <- pit::block_inner_product / block_norm_n_inf
  *                                                       include/pit/block_system.hpp:37-40
+ *   pit_set_reference      <- pit::SolveOptions::reference  include/pit/solvers.hpp:50-52
  *   pit_context_create     <- pit::BlockOperatorContext ctor (block_system.hpp:55-72)
  *                             + Propagator ctors (propagator.hpp:31-36) + SpatialOperator
  *
