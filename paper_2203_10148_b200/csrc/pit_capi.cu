@@ -1082,16 +1082,6 @@ int pipelined_apply_F(pit_context* ctx, const double* L, double* out, double* dL
       return set_err(PIT_ERR_CUDA, "apply_F: pipelined host-to-device copy failed");
     }
   }
-  for (int k = 0; k < nch; ++k) {
-    const size_t b0 = (size_t)k * cb, nb = std::min((size_t)cb, (size_t)N - b0);
-    if (g_wait32((CUstream)ctx->d2h, (CUdeviceptr)(ctx->d_sync + 1 + k), (unsigned)nb,
-                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
-        cudaMemcpyAsync(out + b0 * M, dO + b0 * M, nb * M * sizeof(double),
-                        cudaMemcpyDeviceToHost, ctx->d2h) != cudaSuccess) {
-      unblock();
-      return set_err(PIT_ERR_CUDA, "apply_F: pipelined device-to-host copy failed");
-    }
-  }
   // One CTA per slab unless PIT_PIECES forces a cut (measured on c2,
   // tools/e2e_probe.py): CTAs start as their chunk lands and so finish
   // staggered, which lets the D2H copies overlap the kernel's tail; piece
@@ -1099,6 +1089,9 @@ int pipelined_apply_F(pit_context* ctx, const double* L, double* out, double* dL
   // at once and leaves the whole D2H after it (2.81 vs 2.48 ms end to end).
   const int saved_pieces = ctx->pieces;
   if (ctx->pieces == 0) ctx->pieces = 1;
+  // K1 is launched before the D2H stream's waits are enqueued: with lazy
+  // module loading a first launch may wait for outstanding work, and the
+  // waits depend on this very kernel.
   int rc = run_slab_batch(ctx, kApplyF, dL, nullptr, nullptr, dO, 0, N, ctx->stream, ctx->d_sync,
                           ctx->d_sync + 1, cb);
   ctx->pieces = saved_pieces;
@@ -1106,6 +1099,17 @@ int pipelined_apply_F(pit_context* ctx, const double* L, double* out, double* dL
     const std::string msg = g_err;
     unblock();
     return set_err(rc, msg);
+  }
+  for (int k = 0; k < nch; ++k) {
+    const size_t b0 = (size_t)k * cb, nb = std::min((size_t)cb, (size_t)N - b0);
+    if (g_wait32((CUstream)ctx->d2h, (CUdeviceptr)(ctx->d_sync + 1 + k), (unsigned)nb,
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+        cudaMemcpyAsync(out + b0 * M, dO + b0 * M, nb * M * sizeof(double),
+                        cudaMemcpyDeviceToHost, ctx->d2h) != cudaSuccess) {
+      cudaStreamSynchronize(ctx->stream);  // K1 needs only the H2D side
+      cudaStreamSynchronize(ctx->d2h);
+      return set_err(PIT_ERR_CUDA, "apply_F: pipelined device-to-host copy failed");
+    }
   }
   CUDA_TRY(cudaStreamSynchronize(ctx->d2h));
   return check_status(ctx, true);

@@ -410,3 +410,22 @@ def test_pipelined_host_apply_F_full_c2_and_error():
         Lp[...] = L
         api._check(api._lib.lib().pit_apply_F(ctx.handle, api.dptr(Lp), api.dptr(Op), None))
         assert np.array_equal(Op, ref)
+
+
+def test_pipelined_host_apply_F_as_first_launch():
+    # a fresh process whose first K1 launch is the overlapped pinned path
+    # (lazy module loading must not wait on the D2H stream's waits, which
+    # depend on that very kernel)
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, '.'); import numpy as np, torch; "
+            "from paper_2203_10148_b200 import api, configs; "
+            "p = configs.make('c2', slabs=48); "
+            "L = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, (p.N, p.M))).pin_memory().numpy(); "
+            "O = torch.zeros((p.N, p.M), dtype=torch.float64).pin_memory().numpy(); "
+            "ctx = api.BlockOperatorContext(p); api.apply_F(ctx, L, out=O); "
+            "print('ok', bool(np.isfinite(O).all()))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=180)
+    assert r.returncode == 0 and "ok True" in r.stdout, r.stdout + r.stderr
