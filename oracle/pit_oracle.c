@@ -432,19 +432,26 @@ static void vaxpy(const orc_problem* p, double* y, double a, const double* x) {
 
 int orc_apply_F(const orc_problem* p, const double* L, double* out, orc_history* h) {
   const int M = p->M, N = p->N;
-  double* y = (double*)malloc((size_t)M * sizeof(double));
   memcpy(out, L, (size_t)M * sizeof(double));
+  int rc = 0, bad = N;
+  /* slabs are independent (block_system.cpp:123-132); the lowest failing
+   * slab's code wins, as SlabExecutor reports it (executor.cpp:142-152) */
+#pragma omp parallel for schedule(dynamic, 1) if (p->parallel)
   for (int n = 1; n < N; ++n) {
-    int rc = p->prop(p->user, ORC_FINE, 0, L + (size_t)(n - 1) * M, n - 1, y);
-    if (rc) {
-      free(y);
-      return rc;
+    double* o = out + (size_t)n * M;
+    int r = p->prop(p->user, ORC_FINE, 0, L + (size_t)(n - 1) * M, n - 1, o);
+    if (r) {
+#pragma omp critical(orc_slab_error)
+      if (n < bad) {
+        bad = n;
+        rc = r;
+      }
+      continue;
     }
     const double* Ln = L + (size_t)n * M;
-    double* o = out + (size_t)n * M;
-    for (int i = 0; i < M; ++i) o[i] = Ln[i] - y[i];
+    for (int i = 0; i < M; ++i) o[i] = Ln[i] - o[i];
   }
-  free(y);
+  if (rc) return rc;
   if (h) h->fine_applications += N - 1;
   return 0;
 }
@@ -455,14 +462,20 @@ int orc_assemble_rhs(const orc_problem* p, double* rhs, orc_history* h) {
   memcpy(rhs, p->y0, (size_t)M * sizeof(double));
   if (!p->has_source) return 0;
   double* zero = (double*)calloc((size_t)M, sizeof(double));
+  int rc = 0, bad = N;
+#pragma omp parallel for schedule(dynamic, 1) if (p->parallel)
   for (int n = 1; n < N; ++n) {
-    int rc = p->prop(p->user, ORC_FINE, 1, zero, n - 1, rhs + (size_t)n * M);
-    if (rc) {
-      free(zero);
-      return rc;
+    int r = p->prop(p->user, ORC_FINE, 1, zero, n - 1, rhs + (size_t)n * M);
+    if (r) {
+#pragma omp critical(orc_slab_error)
+      if (n < bad) {
+        bad = n;
+        rc = r;
+      }
     }
   }
   free(zero);
+  if (rc) return rc;
   if (h) h->fine_applications += N - 1;
   return 0;
 }
@@ -778,6 +791,7 @@ orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double 
   o->prob.y0 = o->y0;
   o->prob.prop = orc_1d_prop;
   o->prob.user = o;
+  o->prob.parallel = 1;
   return o;
 }
 

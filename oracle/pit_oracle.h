@@ -103,6 +103,12 @@ typedef struct orc_problem {
   const double* y0; /* [M] */
   orc_prop_fn prop;
   void* user;
+  /* 1: the fine propagator is re-entrant, so the independent slabs of
+   * apply_F / assemble_rhs run on OpenMP threads (the per-slab arithmetic is
+   * unchanged, so results are bitwise independent of the thread count);
+   * 0 (callback problems, e.g. the reference's Propagator through Python):
+   * slabs run in order on the calling thread */
+  int parallel;
 } orc_problem;
 
 typedef struct orc_record {

@@ -279,6 +279,7 @@ orc_2d* orc_2d_create(int m, double band_off, double band_diag, int N, double to
   memcpy(o->y0, y0, n * sizeof(double));
   const double h = 1.0 / (m + 1);
   o->prob = orc_problem_new((int)n, N, h * h, 0, mode, o->y0, prop2d, o);
+  o->prob->parallel = 1;
   return o;
 }
 

@@ -371,6 +371,7 @@ orc_be2d* orc_be2d_create(int m, double lo, double hi, const double* stencil, in
   memcpy(o->y0, y0, n * sizeof(double));
   const double h = (hi - lo) / (double)(m + 1);
   o->prob = orc_problem_new((int)n, N, h * h, 0, mode, o->y0, prop_be2, o);
+  o->prob->parallel = 1;
   return o;
 }
 

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <random>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -355,6 +356,23 @@ int pitref_parareal(void* p, double tol, double eps0, int max_iter, int zero_gue
   return run_solver(1, p, tol, eps0, max_iter, zero_guess, workers, lambda_init, lambda_out,
                     first_residual_out, rec_k, rec_res, rec_fine, rec_coarse, max_rec, nrec,
                     restarts, converged);
+}
+
+// Seeded inputs with the generator family of the reference's own tests
+// (tests/oracles.cpp:108-122): std::mt19937_64 + libstdc++ distributions,
+// drawn in order — the same bits as pit_seeded_* in the product library, so
+// the bench's reference arm builds BASELINE inputs without loading it.
+void pitref_seeded_normal(unsigned long long seed, long n, double mean, double stddev,
+                          double* out) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> dist(mean, stddev);
+  for (long i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+void pitref_seeded_uniform(unsigned long long seed, long n, double a, double b, double* out) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dist(a, b);
+  for (long i = 0; i < n; ++i) out[i] = dist(rng);
 }
 
 }  // extern "C"

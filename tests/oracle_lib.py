@@ -190,5 +190,7 @@ def ref():
                                            C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_int,
                                            C.POINTER(C.c_int), C.POINTER(C.c_int),
                                            C.POINTER(C.c_int)]
+        lib.pitref_seeded_normal.argtypes = [C.c_ulonglong, C.c_long, C.c_double, C.c_double, _dp]
+        lib.pitref_seeded_uniform.argtypes = [C.c_ulonglong, C.c_long, C.c_double, C.c_double, _dp]
         _ref = lib
     return _ref

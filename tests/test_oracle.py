@@ -265,3 +265,26 @@ def test_device_mode_dot_is_fixed_tree():
     assert abs(o.block_dot(a, b) - ref) < 1e-12 * abs(ref) + 1e-14
     assert o.block_norm(a) == pytest.approx(max(np.sqrt(p.spacing * np.sum(a * a, axis=1))),
                                             rel=1e-14)
+
+
+def test_c3_full_size_pitsbicg_matches_reference():
+    # the full BASELINE c3 (N = 512) against the reference binary's own solve
+    # (tests/golden/c3_full_reference.npz, make_golden_c3_full.py): same k,
+    # restarts and counters; lambda within the reference's inner-solve floor
+    # (its BiCGStab steps stop at 1e-12; 6.7e-10 at full N)
+    g = gold("c3_full_reference.npz")
+    p = configs.make("c3")
+    o = OracleProblem(p)
+    r = o.solve(1e-10)
+    lam_n = o.propagate(0, r["lam"][-1], p.N - 1, True)
+    o.close()
+    hist = g["pitsbicg_hist"]
+    assert [row[0] for row in r["rows"]] == [int(k) for k in hist[:, 0]] == [0, 1, 2, 3]
+    assert [(row[2], row[3]) for row in r["rows"]] == [(int(a), int(b)) for a, b in hist[:, 2:4]]
+    assert r["restarts"] == int(g["pitsbicg_restarts"]) == 0
+    assert abs(r["rows"][-1][1] - hist[-1, 1]) < 1e-4 * hist[-1, 1]
+    assert rel_block(r["lam"][g["blocks"]], g["lambda_blocks"]) < 7e-10
+    norms = np.linalg.norm(r["lam"], axis=1)
+    assert np.max(np.abs(norms - g["lambda_block_norms"]) / g["lambda_block_norms"]) < 7e-10
+    # lambda_N adds one more fine slab of the reference's drift (7.01e-10)
+    assert np.linalg.norm(lam_n - g["lambda_N"]) / np.linalg.norm(g["lambda_N"]) < 7.5e-10
