@@ -44,6 +44,7 @@
 #ifndef PIT_B200_H
 #define PIT_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -190,6 +191,13 @@ typedef struct pit_step_coeffs {
 
 const char* pit_last_error(void);
 int pit_last_error_slab(void);
+/* The payload of the last PIT_ERR_INNER_SOLVE on this thread
+ * (pit::InnerSolveError::achieved_relative_residual / iterations,
+ * include/pit/errors.hpp:15-21, thrown at src/pde.cpp:119-128): the inner
+ * Krylov solve's relative true residual and iteration count of the failing
+ * step (2D propagators; the 1D direct solve reports NaN and 0).  Returns
+ * PIT_ERR_INVALID_ARGUMENT when the last error carried no payload. */
+int pit_last_error_detail(double* achieved_relative_residual, int64_t* iterations);
 const char* pit_version(void);
 int pit_device_count(void);
 
@@ -199,6 +207,15 @@ int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing);
 /* cumulative inner CG iterations of the 2D coarse sweeps (0 in 1D, where
  * the coarse step is a direct tridiagonal solve) */
 int pit_coarse_iterations(const pit_context* ctx, int64_t* out);
+/* Fine slabs resident at once on the context's GPU (K1 occupancy x SMs):
+ * the device's worker count for pit::timing_report (src/executor.cpp:156-171),
+ * whose parallel_efficiency = fine_busy_ms / (slots * fine_parallel_ms). */
+int pit_context_slots(const pit_context* ctx, int* slots);
+/* Page-locked host buffers (cudaMallocHost): host block vectors here take
+ * pit_apply_F's overlapped copy path (staging for C++ bindings whose own
+ * storage is pageable, e.g. the reference's BlockVector). */
+int pit_host_alloc(size_t bytes, void** out);
+int pit_host_free(void* p);
 /* Coefficients for role PIT_FINE / PIT_COARSE (no device needed). */
 int pit_step_coefficients(const pit_problem_desc* desc, int role, pit_step_coeffs* out);
 
@@ -251,6 +268,15 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
                   double* out);
 int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, double* out);
 int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out);
+
+/* SolveOptions::iterate_observer (include/pit/solvers.hpp:54, called at
+ * src/solvers.cpp:101,136): after each history row of the following solves
+ * the observer receives the row and the iterate it describes as a host array
+ * lambda[N*M] (valid for the duration of the call).  NULL clears it.  While
+ * an observer is set every row costs one device-to-host copy of lambda. */
+typedef void (*pit_iterate_observer)(const pit_record* row, const double* lambda, int N, int M,
+                                     void* user);
+int pit_set_iterate_observer(pit_context* ctx, pit_iterate_observer fn, void* user);
 
 /* SolveOptions::reference (solvers.hpp:50-52): a host block vector [N*M]
  * kept on the device; every history row of the following solves carries

@@ -21,12 +21,15 @@
 //     1D only).
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "pit/block_system.hpp"
@@ -46,7 +49,14 @@ inline void check(int rc) {
   const std::string msg = pit_last_error();
   switch (rc) {
     case PIT_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
-    case PIT_ERR_INNER_SOLVE: throw pit::InnerSolveError(msg, 0.0, 0);
+    case PIT_ERR_INNER_SOLVE: {
+      // the achieved relative residual and iteration count of the failing
+      // inner solve (errors.hpp:15-21)
+      double rel = std::nan("");
+      int64_t its = 0;
+      pit_last_error_detail(&rel, &its);
+      throw pit::InnerSolveError(msg, rel, static_cast<int>(its));
+    }
     case PIT_ERR_SLAB: throw pit::SlabError(pit_last_error_slab(), msg);
     case PIT_ERR_CONFIG: throw pit::ConfigError(msg);
     default: throw pit::Error(msg);
@@ -59,6 +69,19 @@ class Backend {
                    int device = 0)
       : ctx_(ctx) {
     const SpatialGrid& g = ctx.fine().op().grid();
+    // one spatial operator feeds both device propagators: the reference's
+    // context only checks grid, partition and source agreement
+    // (block_system.cpp:90-113), so reject a coarse operator that differs
+    {
+      const SpatialOperator& f = ctx.fine().op();
+      const SpatialOperator& c = ctx.coarse().op();
+      const CsrMatrix& a = f.matrix();
+      const CsrMatrix& b = c.matrix();
+      if (a.n != b.n || a.row_ptr != b.row_ptr || a.col != b.col || a.val != b.val ||
+          f.symmetric() != c.symmetric())
+        throw std::invalid_argument(
+            "pit::gpu::Backend: the fine and coarse propagators must share one spatial operator");
+    }
     if (g.dimension() == 2) {
       init_2d(ctx, g, device);
       return;
@@ -149,14 +172,29 @@ class Backend {
     N_ = d.slab_count;
   }
 
+  // pit::apply_F.  The BlockVector's blocks are gathered (host threads) into
+  // a page-locked staging buffer, so pit_apply_F takes its overlapped path:
+  // chunked H2D copies, K1's slabs starting as their chunk lands, chunked
+  // D2H copies of finished output blocks; the result is scattered back.
   BlockVector apply_F(const BlockVector& L, SlabExecutor& /*exec*/,
                       RunStats* stats = nullptr) const {
-    auto x = flat(L, "apply_F");
-    std::vector<double> out(x.size());
+    check_blocks(L, "apply_F");
+    stage();
+    gather(L, stage_in_);
     pit_run_stats s{};
-    check(pit_apply_F(h_.get(), x.data(), out.data(), &s));
+    check(pit_apply_F(h_.get(), stage_in_, stage_out_, &s));
     add(stats, s);
-    return unflat(out);
+    BlockVector v = ctx_.zero_vector();
+    scatter(stage_out_, v);
+    return v;
+  }
+
+  // Fine slabs resident at once on the GPU: the worker count to pass to
+  // pit::timing_report (executor.cpp:156-171) for a device run.
+  int worker_count() const {
+    int slots = 0;
+    check(pit_context_slots(h_.get(), &slots));
+    return slots;
   }
 
   BlockVector apply_G_inverse(const BlockVector& V, RunStats* stats = nullptr) const {
@@ -189,6 +227,52 @@ class Backend {
   struct Del {
     void operator()(pit_context* c) const { pit_context_destroy(c); }
   };
+  struct HostDel {
+    void operator()(double* p) const { pit_host_free(p); }
+  };
+
+  void check_blocks(const BlockVector& v, const char* what) const {
+    if (v.block_count() != N_)
+      throw std::invalid_argument(std::string(what) + ": block count does not match the partition");
+    for (int n = 0; n < N_; ++n) require_same_grid(v[n], ctx_.initial_value());
+  }
+  void stage() const {
+    if (stage_in_) return;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(N_) * M_;
+    void *a = nullptr, *b = nullptr;
+    check(pit_host_alloc(bytes, &a));
+    in_keep_.reset(static_cast<double*>(a));
+    check(pit_host_alloc(bytes, &b));
+    out_keep_.reset(static_cast<double*>(b));
+    stage_in_ = in_keep_.get();
+    stage_out_ = out_keep_.get();
+  }
+  // block copies split over host threads (a single thread's memcpy is far
+  // below the host's memory bandwidth)
+  template <class F>
+  void parallel_blocks(F&& f) const {
+    const int nt = std::max(1, std::min<int>(8, static_cast<int>(std::thread::hardware_concurrency())));
+    if (nt == 1 || static_cast<size_t>(N_) * M_ < (1u << 18)) {
+      for (int n = 0; n < N_; ++n) f(n);
+      return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        for (int n = t * N_ / nt; n < (t + 1) * N_ / nt; ++n) f(n);
+      });
+    for (auto& x : th) x.join();
+  }
+  void gather(const BlockVector& v, double* dst) const {
+    parallel_blocks([&](int n) {
+      std::memcpy(dst + static_cast<size_t>(n) * M_, v[n].values().data(), sizeof(double) * M_);
+    });
+  }
+  void scatter(const double* src, BlockVector& v) const {
+    parallel_blocks([&](int n) {
+      std::memcpy(v[n].values().data(), src + static_cast<size_t>(n) * M_, sizeof(double) * M_);
+    });
+  }
 
   std::vector<double> flat(const BlockVector& v, const char* what) const {
     if (v.block_count() != N_)
@@ -229,6 +313,23 @@ class Backend {
     std::vector<pit_record> rows(static_cast<size_t>(config.max_iterations) + 2);
     pit_solve_info info{};
     auto fn = pitsbicg ? pit_pitsbicg_solve : pit_parareal_solve;
+    // SolveOptions::iterate_observer (solvers.hpp:54): each row with the
+    // iterate it describes, rebuilt as a BlockVector
+    struct Obs {
+      const Backend* self;
+      const std::function<void(const IterationRecord&, const BlockVector&)>* fn;
+    } obs{this, &options.iterate_observer};
+    if (options.iterate_observer) {
+      check(pit_set_iterate_observer(
+          h_.get(),
+          [](const pit_record* row, const double* lam, int, int, void* user) {
+            auto* o = static_cast<Obs*>(user);
+            BlockVector v = o->self->ctx_.zero_vector();
+            o->self->scatter(lam, v);
+            (*o->fn)(to_record(*row), v);
+          },
+          &obs));
+    }
     // SolveOptions::reference: every row carries block_norm_n_inf(lambda - reference)
     if (options.reference) {
       const std::vector<double> ref = flat(*options.reference, "reference");
@@ -238,18 +339,10 @@ class Backend {
                       first.empty() ? nullptr : first.data(), rows.data(),
                       static_cast<int>(rows.size()), &info);
     if (options.reference) pit_set_reference(h_.get(), nullptr);
+    if (options.iterate_observer) pit_set_iterate_observer(h_.get(), nullptr, nullptr);
     check(rc);
     SolveResult r{unflat(lam), {}};
-    for (int i = 0; i < info.record_count; ++i) {
-      IterationRecord rec;
-      rec.k = rows[i].k;
-      rec.residual_norm = rows[i].residual_norm;
-      rec.fine_applications = static_cast<long>(rows[i].fine_applications);
-      rec.coarse_applications = static_cast<long>(rows[i].coarse_applications);
-      rec.wall_ms = rows[i].wall_ms;
-      if (rows[i].has_error) rec.error_vs_reference = rows[i].error_vs_reference;
-      r.history.records.push_back(rec);
-    }
+    for (int i = 0; i < info.record_count; ++i) r.history.records.push_back(to_record(rows[i]));
     r.history.status =
         info.status == PIT_CONVERGED ? SolveStatus::Converged : SolveStatus::MaxIterations;
     r.history.restarts = info.restarts;
@@ -258,9 +351,24 @@ class Backend {
     return r;
   }
 
+  static IterationRecord to_record(const pit_record& row) {
+    IterationRecord rec;
+    rec.k = row.k;
+    rec.residual_norm = row.residual_norm;
+    rec.fine_applications = static_cast<long>(row.fine_applications);
+    rec.coarse_applications = static_cast<long>(row.coarse_applications);
+    rec.wall_ms = row.wall_ms;
+    if (row.has_error) rec.error_vs_reference = row.error_vs_reference;
+    return rec;
+  }
+
   const BlockOperatorContext& ctx_;
   std::unique_ptr<pit_context, Del> h_;
   int M_ = 0, N_ = 0;
+  // page-locked staging of apply_F (allocated on first use)
+  mutable std::unique_ptr<double, HostDel> in_keep_, out_keep_;
+  mutable double* stage_in_ = nullptr;
+  mutable double* stage_out_ = nullptr;
 };
 
 }  // namespace pit::gpu

@@ -4,6 +4,9 @@
 // oracle/Makefile (needs the reference headers; runs on the GPU box).
 #include <cmath>
 #include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "pit/block_system.hpp"
 #include "pit/pde.hpp"
@@ -108,6 +111,99 @@ int main() {
     ok2 = ok2 && f2 < 1e-9 && g2e < 1e-9 && a.k == b.k && s2 < 1e-8 && e_ok &&
           r1.history.restarts == r2.history.restarts;
   }
-  std::printf("%s\n", ok && ok2 ? "ADAPTER OK" : "ADAPTER FAIL");
-  return ok && ok2 ? 0 : 1;
+  // iterate_observer (solvers.hpp:54): the same rows, each with its iterate
+  bool ok3 = true;
+  {
+    std::vector<std::pair<IterationRecord, BlockVector>> seen_cpu, seen_gpu;
+    SolveOptions oc, og;
+    oc.iterate_observer = [&](const IterationRecord& r, const BlockVector& v) {
+      seen_cpu.emplace_back(r, v);
+    };
+    og.iterate_observer = [&](const IterationRecord& r, const BlockVector& v) {
+      seen_gpu.emplace_back(r, v);
+    };
+    const SolveResult a = pitsbicg_solve(ctx, cfg, exec, oc);
+    const SolveResult b = gpu.pitsbicg_solve(cfg, exec, og);
+    ok3 = seen_cpu.size() == seen_gpu.size() && seen_gpu.size() == b.history.records.size() &&
+          !seen_gpu.empty() && rel(seen_gpu.back().second, b.solution) == 0.0;
+    for (size_t i = 0; ok3 && i < seen_cpu.size(); ++i)
+      ok3 = seen_cpu[i].first.k == seen_gpu[i].first.k &&
+            seen_cpu[i].first.fine_applications == seen_gpu[i].first.fine_applications &&
+            rel(seen_gpu[i].second, seen_cpu[i].second) < 1e-9;
+    std::printf("iterate_observer: %zu rows cpu, %zu rows gpu: %s\n", seen_cpu.size(),
+                seen_gpu.size(), ok3 ? "same" : "DIFFERENT");
+  }
+  // InnerSolveError payload (errors.hpp:15-21): a NaN right-hand side through
+  // the desk preset's coarse sweep, on both paths
+  bool ok4 = false;
+  {
+    const BlockOperatorContext c2 = build_context(make_preset(CaseName::Diffusion, Scale::Desk), 4);
+    gpu::Backend g2(c2);
+    BlockVector X = c2.zero_vector();
+    for (int n = 0; n < c2.block_count(); ++n)
+      for (size_t i = 0; i < X[n].size(); ++i) X[n][i] = std::cos(0.1 * n + 0.02 * i);
+    X[1][5] = std::nan("");
+    double rc_rel = 0, rg_rel = 0;
+    int rc_it = -1, rg_it = -2;
+    std::string wc, wg;
+    try {
+      apply_G_inverse(c2, X);
+    } catch (const InnerSolveError& e) {
+      rc_rel = e.achieved_relative_residual, rc_it = e.iterations, wc = e.what();
+    }
+    try {
+      g2.apply_G_inverse(X);
+    } catch (const InnerSolveError& e) {
+      rg_rel = e.achieved_relative_residual, rg_it = e.iterations, wg = e.what();
+    }
+    auto unsign = [](std::string w) {  // the sign of a NaN is not part of the contract
+      for (size_t k; (k = w.find("-nan")) != std::string::npos;) w.erase(k, 1);
+      return w;
+    };
+    ok4 = !wc.empty() && rc_it == rg_it && std::isnan(rc_rel) == std::isnan(rg_rel) &&
+          unsign(wc) == unsign(wg);
+    std::printf("InnerSolveError cpu {%g, %d, \"%s\"} gpu {%g, %d, \"%s\"}\n", rc_rel, rc_it,
+                wc.c_str(), rg_rel, rg_it, wg.c_str());
+  }
+  // a coarse propagator on another operator is rejected at construction
+  bool ok5 = false;
+  {
+    PDECoefficients c3;
+    c3.diffusion = 2.0;
+    const SpatialOperator op2 = assemble_spatial_operator(c3, g);
+    BlockOperatorContext bad(Propagator(op, part, 100, PropagatorRole::Fine),
+                             Propagator(op2, part, 1, PropagatorRole::Coarse), ScalarField(g, y0));
+    try {
+      gpu::Backend gb(bad);
+    } catch (const std::invalid_argument&) {
+      ok5 = true;
+    }
+    std::printf("different coarse operator rejected: %s\n", ok5 ? "yes" : "NO");
+  }
+  // pinned staging: N >= 32 takes pit_apply_F's overlapped copy path
+  bool ok6 = false;
+  {
+    const int M2 = 256, N2 = 40;
+    const GridPtr g2 = SpatialGrid::make(1, 0.0, 1.0, M2 + 2);
+    const SpatialOperator op3 = assemble_spatial_operator(c, g2);
+    const TimeSlabPartition part2(N2 / 1024.0, N2);
+    std::vector<double> z0(M2);
+    for (int i = 0; i < M2; ++i) z0[i] = std::sin(3 * M_PI * g2->interior_coord(i));
+    BlockOperatorContext c4(Propagator(op3, part2, 50, PropagatorRole::Fine),
+                            Propagator(op3, part2, 1, PropagatorRole::Coarse), ScalarField(g2, z0));
+    gpu::Backend g4(c4);
+    BlockVector X = c4.zero_vector();
+    for (int n = 0; n < N2; ++n)
+      for (int i = 0; i < M2; ++i) X[n][i] = std::cos(0.3 * n + 0.05 * i);
+    RunStats sg;
+    double e = 0;
+    for (int rep = 0; rep < 3; ++rep) e = std::fmax(e, rel(g4.apply_F(X, exec, &sg), apply_F(c4, X, exec)));
+    ok6 = e < 1e-10 && g4.worker_count() > 0 && sg.fine_busy_ms > 0.0 &&
+          sg.fine_applications == 3L * (N2 - 1);
+    std::printf("pinned-staging apply_F rel %.3e, device slots %d, fine busy %.3f ms / wall %.3f ms\n",
+                e, g4.worker_count(), sg.fine_busy_ms, sg.fine_parallel_ms);
+  }
+  const bool all = ok && ok2 && ok3 && ok4 && ok5 && ok6;
+  std::printf("%s\n", all ? "ADAPTER OK" : "ADAPTER FAIL");
+  return all ? 0 : 1;
 }

@@ -115,7 +115,13 @@ EXPORTS = [
     "pit_sync_status", "pit_pitsbicg_solve_device",
     "pit_seeded_uniform", "pit_seeded_normal", "pit_measure_fp64_peak",
     "pit_step_coefficients_2d", "pit_coarse_iterations", "pit_set_reference",
+    "pit_last_error_detail", "pit_set_iterate_observer", "pit_context_slots", "pit_host_alloc",
+    "pit_host_free",
 ]
+
+# void (*)(const pit_record*, const double* lambda, int N, int M, void* user)
+ITERATE_OBSERVER = C.CFUNCTYPE(None, C.POINTER(RecordC), C.POINTER(C.c_double), C.c_int, C.c_int,
+                               C.c_void_p)
 
 _lib = None
 
@@ -168,6 +174,11 @@ def lib():
     L.pit_pitsbicg_solve_device.argtypes = [vp, C.POINTER(SolverConfigC), vp, vp,
                                             C.POINTER(RecordC), C.c_int, C.POINTER(SolveInfoC), vp]
     L.pit_measure_fp64_peak.argtypes = [C.c_int, _dp]
+    L.pit_last_error_detail.argtypes = [_dp, C.POINTER(C.c_int64)]
+    L.pit_set_iterate_observer.argtypes = [vp, ITERATE_OBSERVER, vp]
+    L.pit_context_slots.argtypes = [vp, C.POINTER(C.c_int)]
+    L.pit_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+    L.pit_host_free.argtypes = [vp]
     L.pit_step_coefficients_2d.argtypes = [C.POINTER(ProblemDesc), C.POINTER(StepCoeffs2DC)]
     L.pit_coarse_iterations.argtypes = [vp, C.POINTER(C.c_int64)]
     L.pit_seeded_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]

@@ -31,7 +31,15 @@ class PitError(RuntimeError):
 
 
 class InnerSolveError(PitError):
-    """pit::InnerSolveError (errors.hpp:15-21)."""
+    """pit::InnerSolveError (errors.hpp:15-21): carries the inner solve's
+    achieved relative residual and iteration count (thrown at
+    src/pde.cpp:119-128; NaN and 0 for the 1D direct solve)."""
+
+    def __init__(self, what: str, achieved_relative_residual: float = float("nan"),
+                 iterations: int = 0):
+        super().__init__(what)
+        self.achieved_relative_residual = achieved_relative_residual
+        self.iterations = iterations
 
 
 class SlabError(PitError):
@@ -58,7 +66,9 @@ def _check(rc: int) -> None:
     if rc == _lib.PIT_ERR_INVALID_ARGUMENT:
         raise ValueError(msg)
     if rc == _lib.PIT_ERR_INNER_SOLVE:
-        raise InnerSolveError(msg)
+        rel, its = C.c_double(float("nan")), C.c_int64(0)
+        L.pit_last_error_detail(C.byref(rel), C.byref(its))
+        raise InnerSolveError(msg, rel.value, its.value)
     if rc == _lib.PIT_ERR_SLAB:
         raise SlabError(L.pit_last_error_slab(), msg)
     if rc == _lib.PIT_ERR_CONFIG:
@@ -400,7 +410,9 @@ class SolveOptions:
     initial_guess_override: Optional[np.ndarray] = None
     reference: Optional[np.ndarray] = None
     first_residual_out: Optional[np.ndarray] = None  # filled in place, shape (N, M)
-    iterate_observer: Optional[Callable] = None       # not supported on the device path
+    # called after every history row with (IterationRecord, lambda (N, M)),
+    # as SolveOptions::iterate_observer (solvers.hpp:54); lambda is a copy
+    iterate_observer: Optional[Callable] = None
 
 
 @dataclass
@@ -609,8 +621,6 @@ def _solve(which: int, ctx: BlockOperatorContext, config: SolverConfig,
            options: Optional[SolveOptions]) -> SolveResult:
     config.validate()
     options = options or SolveOptions()
-    if options.iterate_observer is not None:
-        raise ValueError("iterate_observer is not supported by the device-resident solver")
     init = None
     if options.initial_guess_override is not None:
         init = ctx._vec(options.initial_guess_override, "initial guess")
@@ -627,12 +637,26 @@ def _solve(which: int, ctx: BlockOperatorContext, config: SolverConfig,
     if options.reference is not None:
         ref = ctx._vec(options.reference, "reference")
         _check(_lib.lib().pit_set_reference(ctx.handle, dptr(ref)))
+    cb = None
+    if options.iterate_observer is not None:
+        user_fn = options.iterate_observer
+
+        def _observe(row, lam_p, n, m, _user):
+            r = row.contents
+            rec = IterationRecord(r.k, r.residual_norm, r.fine_applications, r.coarse_applications,
+                                  r.wall_ms, r.error_vs_reference if r.has_error else None)
+            user_fn(rec, np.ctypeslib.as_array(lam_p, shape=(n, m)).copy())
+
+        cb = _lib.ITERATE_OBSERVER(_observe)
+        _check(_lib.lib().pit_set_iterate_observer(ctx.handle, cb, None))
     try:
         _check(fn(ctx.handle, C.byref(cfg), dptr(init), dptr(lam), dptr(first), recs, cap,
                   C.byref(info)))
     finally:
         if ref is not None:
             _lib.lib().pit_set_reference(ctx.handle, None)
+        if cb is not None:
+            _lib.lib().pit_set_iterate_observer(ctx.handle, _lib.ITERATE_OBSERVER(), None)
     hist = ConvergenceHistory()
     for i in range(info.record_count):
         r = recs[i]

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -33,10 +34,15 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_err_slab = -1;
+// InnerSolveError payload of the last failure (include/pit/errors.hpp:15-21)
+thread_local bool g_err_detail = false;
+thread_local double g_err_relres = 0.0;
+thread_local int64_t g_err_iters = 0;
 
 int set_err(int code, const std::string& msg, int slab = -1) {
   g_err = msg;
   g_err_slab = slab;
+  g_err_detail = false;
   return code;
 }
 
@@ -53,6 +59,29 @@ int set_err(int code, const std::string& msg, int slab = -1) {
     int rc_ = (expr);      \
     if (rc_) return rc_;   \
   } while (0)
+
+// Binds the context's device for the duration of an entry point and restores
+// the caller's current device on exit (a process may drive several contexts
+// on different GPUs, and the caller — e.g. torch — may switch devices
+// between calls).  dev < 0: no-op.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (dev < 0) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) {
+      cudaGetLastError();
+      cur = -1;
+    }
+    if (cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+#define PIT_DEVICE_SCOPE(ctx) DeviceScope device_scope_((ctx) ? (ctx)->desc.device : -1)
 
 using Clock = std::chrono::steady_clock;
 double ms_since(Clock::time_point t0) {
@@ -88,8 +117,14 @@ struct pit_context {
   double* d_shape = nullptr;
   double* d_y0 = nullptr;
   std::vector<double> y0;
-  int* d_status = nullptr;
-  int* h_status = nullptr;       // pinned
+  DevStatus* d_status = nullptr;
+  DevStatus* h_status = nullptr;  // pinned mirror
+  unsigned long long busy_mark = 0;  // busy_ns already charged to RunStats
+  // SolveOptions::iterate_observer (solvers.hpp:54): called after every
+  // history row with the iterate the row describes (host copy)
+  pit_iterate_observer observer = nullptr;
+  void* observer_user = nullptr;
+  double* h_observed = nullptr;  // pinned N*M, allocated when an observer is set
   double* h_partials = nullptr;  // pinned, 3*N
   double* d_partials = nullptr;  // 3*N
   cudaStream_t stream = nullptr;
@@ -345,25 +380,52 @@ void fill_params(const pit_step_coeffs& c, StepParams* P) {
 }
 
 int check_status(pit_context* ctx, bool fine_batch) {
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int), cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
                            ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const int bad = *ctx->h_status;
+  const int bad = ctx->h_status->slab;
   if (bad != INT_MAX) {
-    *ctx->h_status = INT_MAX;
-    CUDA_TRY(cudaMemcpyAsync(ctx->d_status, ctx->h_status, sizeof(int), cudaMemcpyHostToDevice,
-                             ctx->stream));
+    const double relres = ctx->h_status->fail[0], iters = ctx->h_status->fail[1];
+    const int kind = (int)ctx->h_status->fail[2];
+    // reset the failure fields (not busy_ns)
+    DevStatus* h = ctx->h_status;
+    h->slab = INT_MAX;
+    h->fail[0] = h->fail[1] = 0.0;
+    h->fail[2] = -1.0;
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_status, ctx->h_status, offsetof(DevStatus, busy_ns),
+                             cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    const std::string what =
-        ctx->dim == 2 && !fine_batch
-            ? "implicit step solve did not converge (CG true residual above tolerance at the "
-              "iteration cap) or produced non-finite values"
-            : "implicit step produced non-finite values";
-    if (fine_batch)
+    if (fine_batch) {
+      const std::string what = ctx->dim == 2 && ctx->be2
+                                   ? "implicit step solve did not converge or produced non-finite "
+                                     "values"
+                                   : "implicit step produced non-finite values";
       return set_err(PIT_ERR_SLAB, "slab " + std::to_string(bad) + ": " + what, bad);
-    return set_err(PIT_ERR_INNER_SOLVE, what, bad);
+    }
+    // InnerSolveError with the reference's message and payload
+    // (src/pde.cpp:119-128)
+    std::string what;
+    if (kind == kFailNotConverged)
+      what = "implicit step solve did not converge (relative residual " + std::to_string(relres) +
+             " after " + std::to_string((long long)iters) + " iterations)";
+    else
+      what = "implicit step produced non-finite values";
+    const int rc = set_err(PIT_ERR_INNER_SOLVE, what, bad);
+    g_err_detail = kind == kFailNotConverged || kind == kFailNonFinite;
+    g_err_relres = relres;
+    g_err_iters = (int64_t)iters;
+    return rc;
   }
   return PIT_OK;
+}
+
+void bind_status(pit_context* ctx, SlabArgs* A) {
+  A->status = &ctx->d_status->slab;
+  A->busy_ns = &ctx->d_status->busy_ns;
+}
+void bind_status(pit_context* ctx, SweepArgs* A) {
+  A->status = &ctx->d_status->slab;
+  A->fail_info = ctx->d_status->fail;
 }
 
 // State and scheduler buffers for K1 piece scheduling (grow-only; the
@@ -405,7 +467,7 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
   A.out_done = out_done;
   A.chunk_blocks = chunk_blocks;
   A.block_shift = first == 0 ? 1 : 0;
-  A.status = ctx->d_status;
+  bind_status(ctx, &A);
   const size_t M = ctx->M;
   int ctas;
   if (first == 0) {
@@ -492,7 +554,7 @@ int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, con
               double* W, int first, int count, bool add_v, cudaStream_t st) {
   const size_t M = ctx->M;
   SweepArgs A{};
-  A.status = ctx->d_status;
+  bind_status(ctx, &A);
   if (first == 0) {
     // block 0: W_0 = V_0 (G^-1) — the caller seeds block 0 otherwise
     if (add_v && V != W)
@@ -594,7 +656,12 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     return set_err(PIT_ERR_CUDA, "no CUDA device: the PiT kernels require a B200 (sm_100a)");
   if (desc->device < 0 || desc->device >= ndev)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: bad device ordinal");
-  CUDA_TRY(cudaSetDevice(desc->device));
+  DeviceScope device_scope_(desc->device);  // the caller's device is restored on return
+  {
+    int cur = -1;
+    CUDA_TRY(cudaGetDevice(&cur));
+    if (cur != desc->device) return set_err(PIT_ERR_CUDA, "pit_context_create: cannot bind device");
+  }
   auto ctx = new pit_context();
   ctx->desc = *desc;
   ctx->desc.source_shape = nullptr;
@@ -739,14 +806,17 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
 #endif
   if (const char* e = std::getenv("PIT_PIECES")) ctx->pieces = std::max(0, std::atoi(e));
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&ctx->d_status, sizeof(int)) != cudaSuccess ||
-      cudaMallocHost(&ctx->h_status, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_status, sizeof(DevStatus)) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_status, sizeof(DevStatus)) != cudaSuccess ||
       cudaMalloc(&ctx->d_partials, sizeof(double) * 3 * (size_t)ctx->N) != cudaSuccess ||
       cudaMallocHost(&ctx->h_partials, sizeof(double) * 3 * (size_t)ctx->N) != cudaSuccess)
     return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
   {
-    const int im = INT_MAX;  // "no failing slab"
-    if (cudaMemcpy(ctx->d_status, &im, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+    DevStatus init{};
+    init.slab = INT_MAX;  // "no failing slab"
+    init.fail[2] = -1.0;
+    *ctx->h_status = init;
+    if (cudaMemcpy(ctx->d_status, &init, sizeof(DevStatus), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(set_err(PIT_ERR_CUDA, "pit_context_create: status init failed"));
   }
   *out = ctx;
@@ -754,6 +824,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
 }
 
 int pit_context_destroy(pit_context* ctx) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx) return PIT_OK;
   for (auto& R : ctx->role) {
     cudaFree(R.d_zc);
@@ -765,6 +836,7 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_status);
   cudaFree(ctx->d_partials);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->h_observed) cudaFreeHost(ctx->h_observed);
   if (ctx->h_partials) cudaFreeHost(ctx->h_partials);
   for (auto& b : ctx->buf) cudaFree(b);
   for (auto& b : ctx->scratch) cudaFree(b);
@@ -786,6 +858,7 @@ int pit_context_destroy(pit_context* ctx) {
 }
 
 int pit_coarse_iterations(const pit_context* ctx, int64_t* out) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "null argument");
   *out = 0;
   if (ctx->d_cg_iters) {
@@ -805,6 +878,7 @@ int pit_step_coefficients_2d(const pit_problem_desc* desc, pit_step_coeffs_2d* o
 }
 
 int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
   if (M) *M = ctx->M;
   if (N) *N = ctx->N;
@@ -816,6 +890,7 @@ int pit_context_shape(const pit_context* ctx, int* M, int* N, double* spacing) {
 
 int pit_apply_F_device(pit_context* ctx, const double* L, const double* halo, double* out,
                        int first, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !L || !out || first < 0 || count < 1 || first + count > ctx->N)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: block count does not match the partition");
   return run_slab_batch(ctx, kApplyF, L, halo, nullptr, out, first, count,
@@ -824,6 +899,7 @@ int pit_apply_F_device(pit_context* ctx, const double* L, const double* halo, do
 
 int pit_residual_device(pit_context* ctx, const double* lambda, const double* halo,
                         const double* rhs, double* out, int first, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !lambda || !rhs || !out || first < 0 || count < 1 || first + count > ctx->N)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "residual: block count does not match the partition");
   return run_slab_batch(ctx, kResidual, lambda, halo, rhs, out, first, count,
@@ -832,6 +908,7 @@ int pit_residual_device(pit_context* ctx, const double* lambda, const double* ha
 
 int pit_coarse_sweep_device(pit_context* ctx, const double* V, const double* W_prev, double* W,
                             int first, int count, int with_source, int add_v, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !W || first < 0 || count < 1 || first + count > ctx->N || (add_v && !V))
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "apply_G_inverse: block count does not match the partition");
@@ -841,6 +918,7 @@ int pit_coarse_sweep_device(pit_context* ctx, const double* V, const double* W_p
 
 int pit_block_partials_device(pit_context* ctx, const double* a, const double* b, double* partials,
                               int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !a || !b || !partials || count < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "block partials: bad arguments");
   const double* A[1] = {a};
@@ -853,6 +931,7 @@ int pit_block_partials_device(pit_context* ctx, const double* a, const double* b
 int pit_block_partials2_device(pit_context* ctx, const double* a0, const double* b0,
                                const double* a1, const double* b1, double* partials, int count,
                                void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !a0 || !b0 || !a1 || !b1 || !partials || count < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "block partials: bad arguments");
   const double* A[2] = {a0, a1};
@@ -864,6 +943,7 @@ int pit_block_partials2_device(pit_context* ctx, const double* a0, const double*
 
 int pit_update_s_device(pit_context* ctx, double alpha, const double* r, const double* d, double* s,
                         double* partials, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !r || !d || !s || !partials || count < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "update_s: bad arguments");
   CUDA_TRY(launch_update_s(ctx->M, count, ctx->weight, alpha, r, d, s, partials,
@@ -874,6 +954,7 @@ int pit_update_s_device(pit_context* ctx, double alpha, const double* r, const d
 int pit_update_lr_device(pit_context* ctx, double alpha, double omega, const double* p,
                          const double* s, const double* t, const double* rs, double* lam, double* r,
                          double* partials, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !p || !s || !t || !rs || !lam || !r || !partials || count < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "update_lr: bad arguments");
   CUDA_TRY(launch_update_lr(ctx->M, count, ctx->weight, alpha, omega, p, s, t, rs, lam, r,
@@ -883,6 +964,7 @@ int pit_update_lr_device(pit_context* ctx, double alpha, double omega, const dou
 
 int pit_update_p_device(pit_context* ctx, double omega, double beta, const double* d,
                         const double* r, double* p, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !d || !r || !p || count < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "update_p: bad arguments");
   CUDA_TRY(launch_update_p((size_t)count * ctx->M, omega, beta, d, r, p,
@@ -892,18 +974,21 @@ int pit_update_p_device(pit_context* ctx, double omega, double beta, const doubl
 
 int pit_axpy_device(pit_context* ctx, double a, const double* x, double* y, int count,
                     void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !x || !y || count < 1) return set_err(PIT_ERR_INVALID_ARGUMENT, "axpy: bad arguments");
   CUDA_TRY(launch_axpy((size_t)count * ctx->M, a, x, y, stream ? (cudaStream_t)stream : ctx->stream));
   return PIT_OK;
 }
 
 int pit_add_device(pit_context* ctx, const double* x, double* y, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !x || !y || count < 1) return set_err(PIT_ERR_INVALID_ARGUMENT, "add: bad arguments");
   CUDA_TRY(launch_add((size_t)count * ctx->M, x, y, stream ? (cudaStream_t)stream : ctx->stream));
   return PIT_OK;
 }
 
 int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !out || first < 0 || count < 1 || first + count > ctx->N)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "assemble_rhs: block count does not match the partition");
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
@@ -912,7 +997,7 @@ int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, 
   Role& R = ctx->role[PIT_FINE];
   SlabArgs A{};
   A.mode = kPropagate;
-  A.status = ctx->d_status;
+  bind_status(ctx, &A);
   const int skip = first == 0 ? 1 : 0;  // block 0 is y0, set by the caller
   A.out = out + (size_t)skip * ctx->M;
   A.slab0 = first + skip - 1;
@@ -922,9 +1007,12 @@ int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, 
 }
 
 int pit_sync_status(pit_context* ctx, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
   if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
-  return check_status(ctx, true);
+  const int rc = check_status(ctx, true);
+  ctx->busy_mark = ctx->h_status->busy_ns;  // device-entry batches carry no RunStats
+  return rc;
 }
 
 // ---- host-pointer entry points -------------------------------------------
@@ -974,11 +1062,18 @@ int to_host(pit_context* ctx, const double* d, size_t n, double* h) {
   return PIT_OK;
 }
 
+// RunStats bookkeeping (executor.hpp:24-30): fine_busy_ms sums the per-slab
+// durations the fine kernels measured (DevStatus::busy_ns, read back by the
+// check_status that follows every fine batch), as the executor sums its
+// per-task times (executor.cpp:124-128).
 void add_fine(pit_context* ctx, pit_run_stats* s, double ms) {
+  const unsigned long long now = ctx->h_status->busy_ns;
+  const double busy = (double)(now - ctx->busy_mark) * 1e-6;
+  ctx->busy_mark = now;
   if (!s) return;
   s->fine_applications += ctx->N - 1;
   s->fine_parallel_ms += ms;
-  s->fine_busy_ms += ms;
+  s->fine_busy_ms += busy;
 }
 void add_coarse(pit_context* ctx, pit_run_stats* s, double ms) {
   if (!s) return;
@@ -1118,6 +1213,7 @@ int pipelined_apply_F(pit_context* ctx, const double* L, double* out, double* dL
 }  // namespace
 
 int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* stats) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !L || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: null argument");
   ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
@@ -1143,6 +1239,7 @@ int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* s
 }
 
 int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !rhs) return set_err(PIT_ERR_INVALID_ARGUMENT, "assemble_rhs: null argument");
   ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
@@ -1158,7 +1255,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
     A.in = nullptr;
     A.out = d.p + ctx->M;
     A.slab0 = 0;
-    A.status = ctx->d_status;
+    bind_status(ctx, &A);
     PIT_TRY(attach_pieces(ctx, &A, ctx->N - 1));
     CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
     PIT_TRY(check_status(ctx, true));
@@ -1168,6 +1265,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
 }
 
 int pit_apply_G_inverse(pit_context* ctx, const double* V, double* out, pit_run_stats* stats) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !V || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_G_inverse: null argument");
   ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
@@ -1202,7 +1300,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
   SlabArgs A{};
   A.mode = kPropagate;
   A.out = d + ctx->M;
-  A.status = ctx->d_status;
+  bind_status(ctx, &A);
   PIT_TRY(attach_pieces(ctx, &A, ctx->N - 1));
   CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
   PIT_TRY(check_status(ctx, true));
@@ -1212,6 +1310,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
 }  // namespace
 
 int pit_initial_guess(pit_context* ctx, int policy, double* out, pit_run_stats* stats) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "initial_guess: null argument");
   ScratchScope scope_{ctx};
   DevVec d;
@@ -1222,6 +1321,7 @@ int pit_initial_guess(pit_context* ctx, int policy, double* out, pit_run_stats* 
 
 int pit_preconditioned_residual(pit_context* ctx, const double* lambda, const double* rhs,
                                 double* out, pit_run_stats* stats) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !lambda || !rhs || !out)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "preconditioned_residual: null argument");
   ScratchScope scope_{ctx};
@@ -1241,6 +1341,7 @@ int pit_preconditioned_residual(pit_context* ctx, const double* lambda, const do
 }
 
 int pit_sequential_fine_solve(pit_context* ctx, double* out) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "sequential_fine_solve: null argument");
   ScratchScope scope_{ctx};
   DevVec d;
@@ -1255,6 +1356,7 @@ int pit_sequential_fine_solve(pit_context* ctx, double* out) {
 
 int pit_propagate(pit_context* ctx, int role, int with_source, const double* in, int slab,
                   double* out) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !out || (role != PIT_FINE && role != PIT_COARSE))
     return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: bad argument");
   ScratchScope scope_{ctx};
@@ -1270,7 +1372,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
   A.W = dout.p;
   A.count = 1;
   A.slab0 = slab;
-  A.status = ctx->d_status;
+  bind_status(ctx, &A);
   const bool src = with_source && ctx->has_source;
   if (!in && !src) {
     // source_contribution with f == 0 is exactly zero (propagator.cpp:78)
@@ -1283,6 +1385,7 @@ int pit_propagate(pit_context* ctx, int role, int with_source, const double* in,
 }
 
 int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, double* out) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !a || !b || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "block_inner_product: null");
   ScratchScope scope_{ctx};
   DevVec da, db;
@@ -1297,6 +1400,7 @@ int pit_block_inner_product(pit_context* ctx, const double* a, const double* b, 
 }
 
 int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !a || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "block_norm_n_inf: null");
   ScratchScope scope_{ctx};
   DevVec da;
@@ -1338,21 +1442,31 @@ struct Recorder {
   Clock::time_point t0;
   pit_context* ctx = nullptr;   // with a reference set: error_vs_reference of *lam
   const double* lam = nullptr;
+  int rc = PIT_OK;              // first failure of an observer's copy
   void operator()(int k, double res) {
-    if (n < cap && rows) {
-      rows[n].k = k;
-      rows[n].residual_norm = res;
-      rows[n].fine_applications = stats->fine_applications;
-      rows[n].coarse_applications = stats->coarse_applications;
-      rows[n].has_error = 0;
-      rows[n].error_vs_reference = 0.0;
-      if (ctx && ctx->d_ref && lam) {
-        rows[n].error_vs_reference = error_vs_reference(ctx, lam);
-        rows[n].has_error = 1;
-      }
-      rows[n].wall_ms = ms_since(t0);
+    pit_record row{};
+    row.k = k;
+    row.residual_norm = res;
+    row.fine_applications = stats->fine_applications;
+    row.coarse_applications = stats->coarse_applications;
+    if (ctx && ctx->d_ref && lam) {
+      row.error_vs_reference = error_vs_reference(ctx, lam);
+      row.has_error = 1;
     }
+    row.wall_ms = ms_since(t0);
+    if (n < cap && rows) rows[n] = row;
     ++n;
+    // SolveOptions::iterate_observer: after the row is recorded, with the
+    // iterate it describes (solvers.cpp:101, 136)
+    if (ctx && ctx->observer && lam) {
+      if (cudaMemcpyAsync(ctx->h_observed, lam, ctx->nm() * sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+          cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+        if (!rc) rc = set_err(PIT_ERR_CUDA, "iterate_observer: device-to-host copy failed");
+        return;
+      }
+      ctx->observer(&row, ctx->h_observed, ctx->N, ctx->M, ctx->observer_user);
+    }
   }
 };
 
@@ -1409,7 +1523,8 @@ int pitsbicg_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
   inf.min_restart_margin = INFINITY;
   pit_run_stats& st = inf.stats;
   Recorder rec{rows, cap, 0, &st, Clock::now(), ctx, lam};
-  auto finish = [&](int status) {
+  auto finish = [&](int status) -> int {
+    if (rec.rc) return rec.rc;
     inf.status = status;
     inf.total_records = rec.n;
     inf.record_count = std::min(rec.n, cap);
@@ -1554,6 +1669,7 @@ int parareal_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
     CUDA_TRY(launch_add(ctx->nm(), corr, lam, ctx->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (rec.rc) return rec.rc;
   inf.status = status;
   inf.total_records = rec.n;
   inf.record_count = std::min(rec.n, cap);
@@ -1583,7 +1699,51 @@ int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const 
 
 }  // namespace
 
+int pit_context_slots(const pit_context* ctx, int* slots) {
+  PIT_DEVICE_SCOPE(ctx);
+  if (!ctx || !slots) return set_err(PIT_ERR_INVALID_ARGUMENT, "null argument");
+  if (ctx->dim == 1) {
+    const Role& R = ctx->role[PIT_FINE];
+    CUDA_TRY(slab_slots(R.mpt, R.nsub, R.nseg, R.warps, false, R.P, slots));
+  } else if (ctx->be2) {
+    *slots = ctx->sms;  // K6: one 512-thread CTA per SM
+  } else {
+    *slots = ctx->sms / std::max(1, ctx->lay2.cl);  // K4: one cluster per slab, 1 CTA per SM
+  }
+  return PIT_OK;
+}
+
+int pit_host_alloc(size_t bytes, void** out) {
+  if (!out) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_host_alloc: null output");
+  *out = nullptr;
+  CUDA_TRY(cudaMallocHost(out, bytes));
+  return PIT_OK;
+}
+
+int pit_host_free(void* p) {
+  if (p) CUDA_TRY(cudaFreeHost(p));
+  return PIT_OK;
+}
+
+int pit_last_error_detail(double* achieved_relative_residual, int64_t* iterations) {
+  if (!g_err_detail) return PIT_ERR_INVALID_ARGUMENT;
+  if (achieved_relative_residual) *achieved_relative_residual = g_err_relres;
+  if (iterations) *iterations = g_err_iters;
+  return PIT_OK;
+}
+
+int pit_set_iterate_observer(pit_context* ctx, pit_iterate_observer fn, void* user) {
+  PIT_DEVICE_SCOPE(ctx);
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (fn && !ctx->h_observed)
+    CUDA_TRY(cudaMallocHost(&ctx->h_observed, ctx->nm() * sizeof(double)));
+  ctx->observer = fn;
+  ctx->observer_user = user;
+  return PIT_OK;
+}
+
 int pit_set_reference(pit_context* ctx, const double* reference) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
   if (!reference) {
     cudaFree(ctx->d_ref);
@@ -1604,6 +1764,7 @@ int pit_set_reference(pit_context* ctx, const double* reference) {
 int pit_pitsbicg_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
                        double* lambda_out, double* first_residual_out, pit_record* records,
                        int max_records, pit_solve_info* info) {
+  PIT_DEVICE_SCOPE(ctx);
   return solve_host(0, ctx, cfg, lambda_init, lambda_out, first_residual_out, records,
                     max_records, info);
 }
@@ -1611,6 +1772,7 @@ int pit_pitsbicg_solve(pit_context* ctx, const pit_solver_config* cfg, const dou
 int pit_parareal_solve(pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
                        double* lambda_out, double* first_residual_out, pit_record* records,
                        int max_records, pit_solve_info* info) {
+  PIT_DEVICE_SCOPE(ctx);
   return solve_host(1, ctx, cfg, lambda_init, lambda_out, first_residual_out, records,
                     max_records, info);
 }
@@ -1619,6 +1781,7 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                               const double* lambda_init_dev, double* lambda_dev,
                               pit_record* records, int max_records, pit_solve_info* info,
                               void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !lambda_dev) return set_err(PIT_ERR_INVALID_ARGUMENT, "solve: null argument");
   PIT_TRY(validate_cfg(cfg));
   if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
@@ -1633,6 +1796,7 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
 
 // instrumented builds only: per-phase cycle totals of CTA 0 (warps 0, 1)
 extern "C" int pit_debug_phase_timing(pit_context* ctx, int role, long long* out32) {
+  PIT_DEVICE_SCOPE(ctx);
 #ifdef PIT_PHASE_TIMING
   CUDA_TRY(cudaDeviceSynchronize());
   CUDA_TRY(cudaMemcpy(out32, ctx->role[role].P.timing, 64 * sizeof(long long),
@@ -1649,6 +1813,7 @@ extern "C" int pit_debug_phase_timing(pit_context* ctx, int role, long long* out
 // K1 unit trace of the last fine batch: n rows of {smid, block, t0, t_end,
 // t_loaded, t_computed, 0, 0} (ns).
 extern "C" int pit_debug_trace(pit_context* ctx, long long* out, int n) {
+  PIT_DEVICE_SCOPE(ctx);
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
   if (n > kMaxPieces * ctx->N) n = kMaxPieces * ctx->N;
   CUDA_TRY(cudaDeviceSynchronize());
@@ -1664,7 +1829,7 @@ extern "C" int pit_debug_trace(pit_context* ctx, long long* out, int n) {
 
 int pit_measure_fp64_peak(int device, double* tflops) {
   if (!tflops) return set_err(PIT_ERR_INVALID_ARGUMENT, "null output");
-  CUDA_TRY(cudaSetDevice(device));
+  DeviceScope device_scope_(device);
   CUDA_TRY(measure_fp64_peak(tflops));
   return PIT_OK;
 }

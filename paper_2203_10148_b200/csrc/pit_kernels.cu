@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
   if (A.state == nullptr) {
     const int b = blockIdx.x;
     wait_input(A, b, tid);
+    const long long tb0 = global_ns();
     load_field<S>(y, source_of(b), tid, M);
     const int slab = A.slab0 + b;
     __syncthreads();
@@ -284,6 +285,8 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
     run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
     slab_epilogue<S>(y, A, M, tid, b, slab);
     signal_output(A, b, tid);
+    if (A.busy_ns != nullptr && tid == 0)
+      atomicAdd(A.busy_ns, (unsigned long long)(global_ns() - tb0));
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     if (A.trace && tid == 0) {
       long long* t = A.trace + 8 * (size_t)b;
@@ -327,8 +330,9 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     const long long tr0 = global_ns();
 #endif
+    if (q == 0) wait_input(A, b, tid);
+    const long long tb0 = global_ns();
     if (q == 0) {
-      wait_input(A, b, tid);
       load_field<S>(y, source_of(b), tid, M);
     } else {
       load_state<S>(y, st, tid);
@@ -352,6 +356,8 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
       slab_epilogue<S>(y, A, M, tid, b, slab);
       signal_output(A, b, tid);
     }
+    if (A.busy_ns != nullptr && tid == 0)
+      atomicAdd(A.busy_ns, (unsigned long long)(global_ns() - tb0));
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     if (A.trace && tid == 0) {
       long long* t = A.trace + 8 * (size_t)u;
@@ -539,7 +545,14 @@ __global__ void __launch_bounds__(S::T, 1)
 #endif
   }
   if (TMA && tid == 0) bulk_wait_all();
-  if (!ok) atomicMin(A.status, bad);
+  if (!ok) {
+    atomicMin(A.status, bad);
+    if (A.fail_info != nullptr) {  // direct solve: no Krylov iterations
+      A.fail_info[0] = __longlong_as_double(0x7ff8000000000000LL);
+      A.fail_info[1] = 0.0;
+      A.fail_info[2] = kFailNonFinite;
+    }
+  }
 }
 
 // Pieces per slab for a batch of nblk slabs over `slots` resident CTAs.
@@ -601,6 +614,28 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A0, int ctas, cudaS
   }
   k<<<grid, S::T, smem, st>>>(P, A);
   return cudaGetLastError();
+}
+
+// Resident slab CTAs of one K1 wave (occupancy x SMs): the device's
+// "worker count" for the executor's timing report (executor.cpp:156-171).
+template <class S, bool SRC>
+cudaError_t slab_slots_t(const StepParams& P, int* slots) {
+  const size_t smem =
+      sizeof(StepShared<S::NSEG, S::WARPS>) + sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
+  auto k = slab_kernel<S, SRC>;
+  cudaError_t e;
+  if (smem > 48 * 1024 &&
+      (e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+          cudaSuccess)
+    return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, S::T, smem)) != cudaSuccess)
+    return e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+    return e;
+  *slots = per_sm * sms;
+  return cudaSuccess;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
@@ -828,6 +863,17 @@ cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const 
   if (mpt == MP && nsub == NU && nseg == NS && warps == W)                      \
     return src ? slab_launch<PIT_SHAPE(MP, NU, NS, W), true>(P, A, ctas, st)    \
                : slab_launch<PIT_SHAPE(MP, NU, NS, W), false>(P, A, ctas, st);
+  PIT_LAYOUTS(X)
+#undef X
+  return cudaErrorInvalidConfiguration;
+}
+
+cudaError_t slab_slots(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
+                       int* slots) {
+#define X(MP, NU, NS, W)                                                   \
+  if (mpt == MP && nsub == NU && nseg == NS && warps == W)                 \
+    return src ? slab_slots_t<PIT_SHAPE(MP, NU, NS, W), true>(P, slots)    \
+               : slab_slots_t<PIT_SHAPE(MP, NU, NS, W), false>(P, slots);
   PIT_LAYOUTS(X)
 #undef X
   return cudaErrorInvalidConfiguration;

@@ -9,6 +9,24 @@ namespace pitb {
 
 enum SlabMode { kApplyF = 0, kResidual = 1, kPropagate = 2 };
 
+// Per-context device status (pinned host mirror), read back in one copy
+// after each operator:
+//   slab     lowest failing slab (INT_MAX = none): SlabError / InnerSolveError
+//   fail[3]  sequential-sweep failure payload of InnerSolveError
+//            (include/pit/errors.hpp:15-21): achieved relative residual,
+//            inner iterations, kind (0 = the Krylov solve missed its
+//            tolerance at the cap or stalled, 1 = non-finite values)
+//   busy_ns  summed per-slab durations of the fine batches (cumulative): the
+//            device analogue of the executor's per-task busy time
+//            (executor.cpp:124-128), feeding RunStats::fine_busy_ms
+struct DevStatus {
+  int slab;
+  int pad;
+  double fail[3];
+  unsigned long long busy_ns;
+};
+constexpr int kFailNotConverged = 0, kFailNonFinite = 1;
+
 // K1: one CTA per slab, all slabs of the batch in parallel.
 struct SlabArgs {
   const double* in;    // CTA b reads field in + (b + in_shift)*M (nullptr: zero field)
@@ -45,6 +63,7 @@ struct SlabArgs {
   unsigned* out_done;
   int chunk_blocks;
   int block_shift;
+  unsigned long long* busy_ns;  // DevStatus::busy_ns (nullptr: not measured)
 };
 
 // K2: one persistent CTA running the sequential sweep
@@ -56,6 +75,7 @@ struct SweepArgs {
   int count;
   int slab0;
   int* status;
+  double* fail_info;  // DevStatus::fail, written with the failing slab
 };
 
 constexpr int kMaxPieces = 64;
@@ -75,6 +95,9 @@ cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const 
                         const SlabArgs& A, int ctas, cudaStream_t st);
 cudaError_t launch_sweep(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
                          const SweepArgs& A, cudaStream_t st);
+// resident K1 CTAs per wave for the layout (occupancy x SMs)
+cudaError_t slab_slots(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
+                       int* slots);
 
 // K3: block-vector algebra, one CTA (kVecThreads) per block, fixed reduction
 // order (oracle/pit_oracle.c orc_block_partial, ORC_MODE_DEVICE).

@@ -116,6 +116,8 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
   const bool rx_up = warp == 0 && c > 0, rx_dn = warp == WARPS - 1 && c < CL - 1;
   const unsigned rx_bytes = (unsigned)sizeof(double) * S::NC * (rx_up + rx_dn);
   uint64_t* const my_bar = &mbar[2 * warp];
+  long long tb0 = 0;  // busy time of the slab (DevStatus::busy_ns)
+  if (c == 0 && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb0));
 
   for (int i = tid; i < 4 * (WARPS + 1) * S::NC; i += S::T) sm2[i] = 0.0;
   if (tid < WARPS) {
@@ -343,6 +345,11 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
       for (int i = tid; i < n; i += S::T) A.out0[i] = A.rhs0[i] - A.L0[i];
     }
   }
+  if (A.busy_ns != nullptr && c == 0 && tid == 0) {
+    long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    atomicAdd(A.busy_ns, (unsigned long long)(t1 - tb0));
+  }
 }
 
 template <class K>
@@ -519,6 +526,7 @@ __global__ void __launch_bounds__(256, 1)
   for (int s = 0; s < A.count; ++s) {
     const int slab = A.slab0 + s;
     bool ok = true;
+    double fail_rel = 0.0, fail_it = 0.0;  // InnerSolveError payload (errors.hpp:15-21)
     for (int cs = 0; cs < P.steps && ok; ++cs) {
       if (cs > 0) {
 #pragma unroll
@@ -621,6 +629,8 @@ __global__ void __launch_bounds__(256, 1)
           if (res <= tol) break;
           if (it >= P.cap || stalled || !isfinite(res)) {
             ok = false;
+            fail_rel = res / nb;
+            fail_it = (double)it;
             break;
           }
 #pragma unroll
@@ -637,7 +647,14 @@ __global__ void __launch_bounds__(256, 1)
     double bad_l = (ok && fin) ? 0.0 : 1.0, bad_g, d1;
     reduce2(bad_l, 0.0, bad_g, d1);
     if (bad_g != 0.0) {
-      if (c == 0 && t == 0) atomicMin(A.status, slab);
+      if (c == 0 && t == 0) {
+        atomicMin(A.status, slab);
+        if (A.fail_info != nullptr) {
+          A.fail_info[0] = fail_rel;
+          A.fail_info[1] = fail_it;
+          A.fail_info[2] = ok ? kFailNonFinite : kFailNotConverged;
+        }
+      }
       break;
     }
     const double* V = A.V ? A.V + (size_t)s * m * m : nullptr;

@@ -141,12 +141,13 @@ __device__ __forceinline__ double true_residual(Be2Ctx<PPT>& c, const Vec<PPT>& 
 // Jacobi-PCG, control flow of solve_cg (sparse.cpp:60-114).
 template <int PPT>
 __device__ bool cg_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double rel_tol, int cap,
-                         int* iters) {
+                         int* iters, double* relres) {
   Vec<PPT> r, z, p, q;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) x[k] = r[k] = z[k] = p[k] = q[k] = 0.0;
   const double norm_b = sqrt(dot1(c, b, b));
   *iters = 0;
+  *relres = 0.0;
   if (norm_b == 0.0) return true;
   const double tol = rel_tol * norm_b;
 #pragma unroll
@@ -195,6 +196,7 @@ __device__ bool cg_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double 
     // confirm against the exact residual (sparse.cpp:97-110)
     res = true_residual(c, b, x, r);
     *iters = it;
+    *relres = res / norm_b;
     if (res <= tol) return true;
     if (it >= cap || stalled || !isfinite(res)) return false;
 #pragma unroll
@@ -210,7 +212,7 @@ __device__ bool cg_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double 
 // Jacobi-BiCGStab, control flow of solve_bicgstab (sparse.cpp:116-206).
 template <int PPT>
 __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double rel_tol,
-                               int cap, int* iters) {
+                               int cap, int* iters, double* relres) {
   // p^ and s^ live only in their operand buffers (own values read back)
   Vec<PPT> r, rt, p, v, s, t;
 #pragma unroll
@@ -219,6 +221,7 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
   double* const sh = c.ops;
   const double norm_b = sqrt(dot1(c, b, b));
   *iters = 0;
+  *relres = 0.0;
   if (norm_b == 0.0) return true;
   const double tol = rel_tol * norm_b;
   double rho_prev = 1.0, alpha = 1.0, omega = 1.0, res = 0.0;
@@ -233,6 +236,7 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
       }
       if (!isfinite(res)) {
         *iters = it;
+        *relres = res / norm_b;
         return false;
       }
 #pragma unroll
@@ -296,6 +300,7 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
       }
       if (!isfinite(res)) {
         *iters = it;
+        *relres = res / norm_b;
         return false;
       }
 #pragma unroll
@@ -346,6 +351,7 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
   }
   res = true_residual(c, b, x, r);
   *iters = it;
+  *relres = res / norm_b;
   return res <= tol;
 }
 
@@ -353,19 +359,28 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
 // the first step whose solve fails or is non-finite (InnerSolveError,
 // pde.cpp:119-128).
 template <int PPT>
-__device__ bool propagate(Be2Ctx<PPT>& c, Vec<PPT>& y, const Be2Params& P, long long* iters) {
+__device__ bool propagate(Be2Ctx<PPT>& c, Vec<PPT>& y, const Be2Params& P, long long* iters,
+                          double* fail_info = nullptr) {
   Vec<PPT> x;
   for (int step = 0; step < P.steps; ++step) {
     int it = 0;
-    const bool ok = P.symmetric ? cg_solve(c, y, x, P.rel_tol, P.cap, &it)
-                                : bicgstab_solve(c, y, x, P.rel_tol, P.cap, &it);
+    double relres = 0.0;
+    const bool ok = P.symmetric ? cg_solve(c, y, x, P.rel_tol, P.cap, &it, &relres)
+                                : bicgstab_solve(c, y, x, P.rel_tol, P.cap, &it, &relres);
     if (iters && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(iters),
                                              (unsigned long long)it);
     bool bad = !ok;
 #pragma unroll
     for (int k = 0; k < PPT; ++k)
       if (c.ip[k] >= 0 && !isfinite(x[k])) bad = true;
-    if (__syncthreads_or(bad)) return false;
+    if (__syncthreads_or(bad)) {
+      if (fail_info != nullptr && threadIdx.x == 0) {  // InnerSolveError payload
+        fail_info[0] = relres;
+        fail_info[1] = (double)it;
+        fail_info[2] = ok ? kFailNonFinite : kFailNotConverged;
+      }
+      return false;
+    }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) y[k] = x[k];  // the solution is the next right-hand side
   }
@@ -425,6 +440,8 @@ template <int PPT>
 __global__ void __launch_bounds__(kBe2Threads, 1)
     be2d_batch_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SlabArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  long long tb0 = 0;  // busy time of the slab (DevStatus::busy_ns)
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb0));
   Be2Ctx<PPT> c;
   setup<PPT>(c, P, smem_raw);
   const int b = blockIdx.x, slab = A.slab0 + b;
@@ -458,6 +475,11 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
         A.out0[i] = A.rhs0[i] - A.L0[i];
     }
   }
+  if (A.busy_ns != nullptr && threadIdx.x == 0) {
+    long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    atomicAdd(A.busy_ns, (unsigned long long)(t1 - tb0));
+  }
 }
 
 // Sequential sweep (SweepArgs semantics of K2): W_b = Prop(W_{b-1}) (+ V_b).
@@ -471,7 +493,7 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
   Vec<PPT> y;
   load_block(c, y, A.start);
   for (int b = 0; b < A.count; ++b) {
-    if (!propagate(c, y, P, P.iters)) {
+    if (!propagate(c, y, P, P.iters, A.fail_info)) {
       if (threadIdx.x == 0) atomicMin(A.status, A.slab0 + b);
       return;
     }
