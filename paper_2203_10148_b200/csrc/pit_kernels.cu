@@ -555,6 +555,131 @@ __global__ void __launch_bounds__(S::T, 1)
   }
 }
 
+// K2 with a dedicated I/O warp (TMA layouts: NSEG == 1, M a multiple of 16,
+// 16-byte aligned blocks).  The T compute threads never meet a CTA-wide
+// barrier in the slab loop: their only synchronisation is the step's named
+// barrier (step_sync) and two mbarriers per slab buffer, so no compute warp
+// waits for the TMA issue or for another warp's I/O.
+//   vfull[i]  the I/O thread's arrival (with the V_b bytes when V is added):
+//             buffer i holds V_b and its previous W store has drained;
+//   wfull[i]  T arrivals: every compute thread has written its rows of W_b
+//             (fence.proxy.async first), so the I/O thread may store it.
+// The I/O thread (warp WARPS, lane 0): loads V_0 .. V_{nbuf-1}; then per
+// slab s: wait wfull, TMA-store W_s, wait for the store to have read the
+// buffer, load V_{s+nbuf} into it.  Same arithmetic as sweep_kernel, so the
+// same bits.
+template <class S, bool SRC>
+__global__ void __launch_bounds__(S::T + 32, 1)
+    sweep_io_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A,
+                    const __grid_constant__ SweepTma X) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
+  double* s_zc = reinterpret_cast<double*>(sh + 1);
+  unsigned char* after = reinterpret_cast<unsigned char*>(s_zc + zc_smem_len<S>(P.narrow));
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(after) + 1023) & ~uintptr_t(1023));
+  const size_t buf_bytes = (size_t)P.M * sizeof(double);
+  const int nbuf = X.nbuf;
+  uint64_t* vfull = reinterpret_cast<uint64_t*>(base + nbuf * buf_bytes);  // [nbuf]
+  uint64_t* wfull = vfull + nbuf;                                           // [nbuf]
+  const int tid = threadIdx.x;
+  const int M = P.M;
+  const bool io = tid >= S::T;
+  if (!io) {
+    load_zc<S>(P, s_zc, tid);
+    init_step_shared<S::NSEG, S::WARPS>(P, *sh, tid);
+  } else if (tid == S::T) {
+    for (int i = 0; i < nbuf; ++i) {
+      mbar_init(&vfull[i], 1);
+      mbar_init(&wfull[i], S::T);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();  // the only CTA-wide barrier
+  auto bufp = [&](int b) { return base + (b % nbuf) * buf_bytes; };
+
+  if (io) {
+    if (tid != S::T) return;
+    const unsigned bytes = (unsigned)(M * sizeof(double));
+    auto fill = [&](int b) {  // buffer b % nbuf is free: V_b in (or just released)
+      uint64_t* bar = &vfull[b % nbuf];
+      if (A.V) {
+        mbar_arrive_expect_tx(bar, bytes);
+        for (int r = 0; r < X.rows; r += X.box_rows)
+          tma_load_2d(bufp(b) + r * 128, X.v, 0, b * X.rows + r, bar);
+      } else {
+        mbar_arrive(bar);
+      }
+    };
+    for (int b = 0; b < nbuf && b < A.count; ++b) fill(b);
+    for (int s = 0; s < A.count; ++s) {
+      mbar_wait(&wfull[s % nbuf], (unsigned)((s / nbuf) & 1));
+      for (int r = 0; r < X.rows; r += X.box_rows)
+        tma_store_2d(X.w, 0, s * X.rows + r, bufp(s) + r * 128);
+      bulk_commit();
+      if (s + nbuf < A.count) {
+        bulk_wait_read();  // the store has read the buffer out
+        fill(s + nbuf);
+      }
+    }
+    bulk_wait_all();
+    return;
+  }
+
+  double y[S::NC][S::SUB];
+  load_field<S>(y, A.start, tid, M);
+  const StepLane L = step_lane<S>(P, *sh, tid);
+  bool ok = true;
+  int bad = 0x7fffffff;
+  for (int b = 0; b < A.count; ++b) {
+    const int slab = A.slab0 + b;
+#ifdef PIT_PHASE_TIMING
+    const long long sw0 = clock64();
+#endif
+    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
+#ifdef PIT_PHASE_TIMING
+    const long long sw1 = clock64();
+#endif
+    if (ok && !all_finite<S>(y, tid, M)) {
+      ok = false;
+      bad = slab;
+    }
+    unsigned char* buf = bufp(b);
+    mbar_wait(&vfull[b % nbuf], (unsigned)((b / nbuf) & 1));  // V_b landed / buffer free
+#pragma unroll
+    for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+      for (int j = 0; j < S::SUB; j += 2) {
+        const int pnt = S::point(tid, c, j);
+        if (pnt < M) {
+          double2* q = reinterpret_cast<double2*>(buf + swz_off<S>(pnt));
+          if (A.V) {
+            const double2 v = *q;
+            y[c][j] = y[c][j] + v.x;
+            y[c][j + 1] = y[c][j + 1] + v.y;
+          }
+          *q = make_double2(y[c][j], y[c][j + 1]);
+        }
+      }
+    fence_proxy_async_smem();
+    mbar_arrive(&wfull[b % nbuf]);
+#ifdef PIT_PHASE_TIMING
+    if (P.timing && (tid & 31) == 0 && (tid >> 5) < 2) {
+      P.timing[(tid >> 5) * 16 + 10] += sw1 - sw0;        // propagation
+      P.timing[(tid >> 5) * 16 + 11] += clock64() - sw1;  // V add + W store
+    }
+#endif
+  }
+  if (!ok) {
+    atomicMin(A.status, bad);
+    if (A.fail_info != nullptr) {  // direct solve: no Krylov iterations
+      A.fail_info[0] = __longlong_as_double(0x7ff8000000000000LL);
+      A.fail_info[1] = 0.0;
+      A.fail_info[2] = kFailNonFinite;
+    }
+  }
+}
+
 // Pieces per slab for a batch of nblk slabs over `slots` resident CTAs.
 // Measured on B200 (tools/pieces_grid.py): between one and two waves, two
 // pieces let the queue refill the slots of the first CTAs to finish (c2:
@@ -667,6 +792,16 @@ bool encode_rows(void* out, const double* base, long long rows, int box_rows) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// smallest M that streams V/W through TMA (measured, tools/sweep_time.py;
+// PIT_SWEEP_TMA_MIN overrides for A/B runs)
+inline int tma_min_points() {
+  static const int v = [] {
+    const char* e = std::getenv("PIT_SWEEP_TMA_MIN");
+    return e ? std::atoi(e) : 1024;
+  }();
+  return v;
+}
+
 template <class S, bool SRC>
 cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t st) {
   SweepTma X{};
@@ -674,7 +809,7 @@ cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t s
   // G^-1 2.87 -> 2.28 ms, c4 11.1 -> 8.9 ms) and loses for c3 (M = 2048,
   // two coarse steps per slab amortise the slot-layout I/O)
   bool tma = S::NSEG == 1 && S::MPT % 2 == 0 && S::SUB % 2 == 0 && P.M % 16 == 0 &&
-             P.M >= 4096 &&
+             P.M >= tma_min_points() &&
              (reinterpret_cast<uintptr_t>(A.W) % 16) == 0 &&
              (!A.V || (reinterpret_cast<uintptr_t>(A.V) % 16) == 0) &&
              std::getenv("PIT_NO_TMA") == nullptr;
@@ -690,7 +825,7 @@ cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t s
       tma ? (size_t)P.M * sizeof(double) : (size_t)S::T * (S::MPT + 1) * sizeof(double);
   const size_t fixed = sizeof(StepShared<S::NSEG, S::WARPS>) +
                        sizeof(double) * (size_t)zc_smem_len<S>(P.narrow) + 1024 +
-                       4 * sizeof(uint64_t);
+                       8 * sizeof(uint64_t);
   X.nbuf = 2;
   if (tma)
     for (int n = 4; n >= 3; --n)
@@ -699,12 +834,15 @@ cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t s
         break;
       }
   const size_t smem = fixed + (size_t)X.nbuf * buf_bytes;
-  auto k = tma ? sweep_kernel<S, SRC, true> : sweep_kernel<S, SRC, false>;
+  static const bool legacy = std::getenv("PIT_SWEEP_LEGACY") != nullptr;  // A/B knob
+  auto k = tma ? (legacy ? sweep_kernel<S, SRC, true> : sweep_io_kernel<S, SRC>)
+               : sweep_kernel<S, SRC, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<1, S::T, smem, st>>>(P, A, X);
+  const int threads = tma && !legacy ? S::T + 32 : S::T;
+  k<<<1, threads, smem, st>>>(P, A, X);
   return cudaGetLastError();
 }
 

@@ -64,6 +64,9 @@ class ShardedOperators:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        if self.world > n_blocks:
+            raise ValueError(f"ShardedOperators: {self.world} ranks for {n_blocks} blocks "
+                             "(every rank must own at least one block)")
         first, count = shard_range(n_blocks, self.world, self.rank)
         self.shard = Shard(first, count, self.rank, self.world)
         self.backend = backend

@@ -106,19 +106,23 @@ class ConfigError(ValueError):
 
 
 def parse_slab_list(text: str) -> List[int]:
-    """parse_slab_list (config.cpp:46-66): comma-separated slab counts >= 2."""
+    """parse_slab_list (config.cpp:50-66): comma-separated slab counts >= 2.
+    Tokens are split like std::getline(',') (a trailing comma ends the list,
+    an empty entry inside it is an error) and parsed like strtol: an optional
+    sign and decimal digits, nothing else."""
+    import re
+
     out = []
-    for tok in text.split(","):
-        tok = tok.strip()
+    parts = text.split(",")
+    if parts and parts[-1] == "":
+        parts = parts[:-1]  # getline yields no token after a trailing comma
+    for item in parts:
+        tok = item.strip()
         if not tok:
-            continue
-        try:
-            v = int(tok)
-        except ValueError:
-            v = 0
-        if v < 2:
+            raise ConfigError(f"empty entry in slab list '{text}'")
+        if not re.fullmatch(r"[+-]?[0-9]+", tok) or int(tok) < 2:
             raise ConfigError(f"slab counts must be integers >= 2, got '{tok}'")
-        out.append(v)
+        out.append(int(tok))
     if not out:
         raise ConfigError(f"slab list '{text}' is empty")
     return out

@@ -1,0 +1,94 @@
+"""The C ABI's reference-facing extras on the GPU: the InnerSolveError
+payload (include/pit/errors.hpp:15-21), SolveOptions::iterate_observer
+(solvers.hpp:54), the executor's busy-time bookkeeping (RunStats::
+fine_busy_ms, executor.cpp:124-128) and the device worker count."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from helpers import OracleProblem
+from paper_2203_10148_b200 import _lib, api, configs, presets
+
+pytestmark = pytest.mark.gpu
+
+
+def test_inner_solve_error_payload_cap():
+    # K5 (2D coarse CG) stopped by a 5-iteration cap: the reference's message
+    # and payload ("did not converge (relative residual R after I iterations)")
+    p = configs.make("c5", slabs=3, M=32)
+    p.coarse_max_iterations = 5
+    x = np.random.default_rng(0).normal(size=(p.N, p.M))
+    with api.BlockOperatorContext(p) as ctx:
+        with pytest.raises(api.InnerSolveError) as e:
+            api.apply_G_inverse(ctx, x)
+        assert e.value.iterations == 5
+        assert e.value.achieved_relative_residual > 1e-12
+        assert f"after 5 iterations" in str(e.value)
+        assert "relative residual" in str(e.value)
+        # the context survives and the next call is clean
+        p.coarse_max_iterations = 0
+    with api.BlockOperatorContext(p) as ctx:
+        assert np.isfinite(api.apply_G_inverse(ctx, x)).all()
+
+
+def test_inner_solve_error_payload_matches_reference_nan():
+    # K6 (the reference's desk preset): a NaN right-hand side stops the
+    # coarse CG at iteration 0 with a NaN residual, as pit::solve_cg does
+    import oracle_lib as O
+
+    q = presets.build_problem(presets.make_preset("diffusion"), 4)
+    x = np.cos(0.1 * np.arange(q.N)[:, None] + 0.02 * np.arange(q.M)[None, :])
+    x[1, 5] = np.nan
+    with api.BlockOperatorContext(q) as ctx:
+        with pytest.raises(api.InnerSolveError) as e:
+            api.apply_G_inverse(ctx, x)
+    assert e.value.iterations == 0 and math.isnan(e.value.achieved_relative_residual)
+    assert "did not converge" in str(e.value)
+    if O.ref_available():
+        R = O.ref()
+        h = R.pitref_create_preset(presets.CASES.index("diffusion"), 0, 4)
+        out = np.zeros_like(x)
+        assert R.pitref_apply_G_inverse(h, O.ptr(np.ascontiguousarray(x)), O.ptr(out)) != 0
+        msg = R.pitref_last_error().decode()
+        R.pitref_destroy(h)
+        assert msg.replace("-nan", "nan") == str(e.value).replace("-nan", "nan")
+
+
+def test_iterate_observer_rows_and_iterates():
+    p = configs.make("c1")
+    seen = []
+    with api.BlockOperatorContext(p) as ctx:
+        res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10),
+                                 options=api.SolveOptions(
+                                     iterate_observer=lambda r, lam: seen.append((r, lam))))
+        guess = api.initial_guess(ctx, api.InitialGuessPolicy.CoarseSweep)
+        # the observer is cleared after the solve
+        api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+    assert len(seen) == len(res.history.records) == 6
+    assert [r.k for r, _ in seen] == [r.k for r in res.history.records]
+    assert np.array_equal(seen[0][1], guess)          # row 0 describes the initial guess
+    assert np.array_equal(seen[-1][1], res.solution)  # the last row the solution
+    o = OracleProblem(p)
+    assert np.array_equal(res.solution, o.solve(1e-10)["lam"])
+
+
+def test_run_stats_busy_time_and_worker_count():
+    import ctypes as C
+
+    p = configs.make("c2", slabs=200)
+    L = np.tile(p.y0, (p.N, 1))
+    with api.BlockOperatorContext(p) as ctx:
+        st = api.RunStats()
+        api.apply_F(ctx, L, stats=st)
+        api.apply_F(ctx, L, stats=st)
+        slots = C.c_int()
+        api._check(_lib.lib().pit_context_slots(ctx.handle, C.byref(slots)))
+    assert st.fine_applications == 2 * (p.N - 1)
+    assert slots.value >= 148
+    # 199 slabs on >= 148 slots: busy time is close to slabs x one slab's time
+    # and below slots x wall time (parallel_efficiency <= 1)
+    assert 0.0 < st.fine_busy_ms <= slots.value * st.fine_parallel_ms
+    assert st.fine_busy_ms > 50 * st.fine_parallel_ms

@@ -37,6 +37,12 @@ def test_slab_list_and_presets():
     assert runner.parse_slab_list("4, 8,16") == [4, 8, 16]
     with pytest.raises(ValueError):
         runner.parse_slab_list("4,x")
+    # the reference's parse_slab_list (config.cpp:50-66): getline on ',' and strtol
+    assert runner.parse_slab_list("4,8,") == [4, 8]
+    assert runner.parse_slab_list("+4") == [4]
+    for bad in ("4,,8", ",4", "1_6", "4.0", "1", "", " "):
+        with pytest.raises(runner.ConfigError):
+            runner.parse_slab_list(bad)
     p = presets.make_preset("advection_diffusion_reaction", "paper")
     assert (p.grid_points, p.total_time, p.mu, p.r, p.rotation) == (51, 6.4, 0.1, 0.5, True)
     with pytest.raises(ValueError, match="unknown case"):
