@@ -334,6 +334,53 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                               pit_record* records, int max_records, pit_solve_info* info,
                               void* stream);
 
+/* ---- slab-sharded multi-GPU (one rank per GPU) -------- */
+/* Replaces the reference's slab fan-out (block_system.cpp:123-132,
+ * executor.cpp:105-154) across GPUs.  Every rank creates a context for the
+ * whole problem (N = all slabs) on its own GPU, and attaches a communicator;
+ * it then owns the contiguous slab range (first, count) = the first N % world
+ * ranks get ceil(N/world) blocks, the others floor(N/world).  Traffic: one
+ * halo block per rank pair per fine batch, the coarse chain's W block per
+ * rank pair per sweep, and an all-gather of per-block reduction partials,
+ * summed in global slab order on every rank, so histories are bit-identical
+ * to one GPU's for any world size.
+ * Transports: NCCL (rank 0 makes the id with pit_comm_nccl_unique_id, the
+ * caller distributes it) or host callbacks (blocking, on host buffers). */
+typedef struct pit_comm pit_comm;
+typedef struct pit_comm_ops {
+  int (*send)(const double* buf, size_t n, int peer, void* user);
+  int (*recv)(double* buf, size_t n, int peer, void* user);
+  int (*allgather)(const double* in, size_t n, double* out /* [world*n] */, void* user);
+  void* user;
+} pit_comm_ops;
+int pit_comm_nccl_unique_id(unsigned char* id /* [128] */);
+int pit_comm_create_nccl(const unsigned char* id /* [128] */, int rank, int world, int device,
+                         pit_comm** out);
+int pit_comm_create_host(const pit_comm_ops* ops, int rank, int world, pit_comm** out);
+int pit_comm_destroy(pit_comm* comm);
+/* NULL detaches (the context is single-GPU again); the comm must outlive its
+ * use by the context */
+int pit_context_attach_comm(pit_context* ctx, pit_comm* comm);
+int pit_context_shard(const pit_context* ctx, int* first, int* count);
+/* Sharded operators and solvers on the rank's local blocks (device arrays of
+ * count*M doubles, block `first` at offset 0).  apply_F overlaps the halo
+ * exchange with the interior slabs: the rank's first block waits for the
+ * halo, every other block starts at once. */
+int pit_sharded_apply_F_device(pit_context* ctx, const double* L_local, double* out_local,
+                               void* stream);
+/* Collective pit_sync_status: every rank returns the error of the lowest
+ * failing slab of any rank (a SlabError for a fine batch, InnerSolveError
+ * with its payload for a sweep). */
+int pit_sharded_sync_status(pit_context* ctx, void* stream);
+int pit_sharded_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
+                                      const double* lambda_init_local, double* lambda_local,
+                                      pit_record* records, int max_records, pit_solve_info* info,
+                                      void* stream);
+int pit_sharded_parareal_solve_device(pit_context* ctx, const pit_solver_config* cfg,
+                                      const double* lambda_init_local, double* lambda_local,
+                                      pit_record* records, int max_records, pit_solve_info* info,
+                                      void* stream);
+
 /* Measured FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA):
  * the roofline denominator for the FP64-pipe-bound fine propagator. */
 int pit_measure_fp64_peak(int device, double* tflops);

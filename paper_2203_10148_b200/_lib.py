@@ -116,8 +116,22 @@ EXPORTS = [
     "pit_seeded_uniform", "pit_seeded_normal", "pit_measure_fp64_peak",
     "pit_step_coefficients_2d", "pit_coarse_iterations", "pit_set_reference",
     "pit_last_error_detail", "pit_set_iterate_observer", "pit_context_slots", "pit_host_alloc",
-    "pit_host_free",
+    "pit_host_free", "pit_comm_nccl_unique_id", "pit_comm_create_nccl", "pit_comm_create_host",
+    "pit_comm_destroy", "pit_context_attach_comm", "pit_context_shard",
+    "pit_sharded_apply_F_device", "pit_sharded_pitsbicg_solve_device",
+    "pit_sharded_parareal_solve_device", "pit_sharded_sync_status",
 ]
+
+# pit_comm_ops callbacks (host transport)
+COMM_SEND = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_int, C.c_void_p)
+COMM_RECV = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_int, C.c_void_p)
+COMM_ALLGATHER = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_double),
+                             C.c_void_p)
+
+
+class CommOpsC(C.Structure):
+    _fields_ = [("send", COMM_SEND), ("recv", COMM_RECV), ("allgather", COMM_ALLGATHER),
+                ("user", C.c_void_p)]
 
 # void (*)(const pit_record*, const double* lambda, int N, int M, void* user)
 ITERATE_OBSERVER = C.CFUNCTYPE(None, C.POINTER(RecordC), C.POINTER(C.c_double), C.c_int, C.c_int,
@@ -179,6 +193,17 @@ def lib():
     L.pit_context_slots.argtypes = [vp, C.POINTER(C.c_int)]
     L.pit_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
     L.pit_host_free.argtypes = [vp]
+    L.pit_comm_nccl_unique_id.argtypes = [C.c_char_p]
+    L.pit_comm_create_nccl.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.pit_comm_create_host.argtypes = [C.POINTER(CommOpsC), C.c_int, C.c_int, C.POINTER(vp)]
+    L.pit_comm_destroy.argtypes = [vp]
+    L.pit_context_attach_comm.argtypes = [vp, vp]
+    L.pit_context_shard.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.pit_sharded_apply_F_device.argtypes = [vp, vp, vp, vp]
+    L.pit_sharded_sync_status.argtypes = [vp, vp]
+    for name in ("pit_sharded_pitsbicg_solve_device", "pit_sharded_parareal_solve_device"):
+        getattr(L, name).argtypes = [vp, C.POINTER(SolverConfigC), vp, vp, C.POINTER(RecordC),
+                                     C.c_int, C.POINTER(SolveInfoC), vp]
     L.pit_step_coefficients_2d.argtypes = [C.POINTER(ProblemDesc), C.POINTER(StepCoeffs2DC)]
     L.pit_coarse_iterations.argtypes = [vp, C.POINTER(C.c_int64)]
     L.pit_seeded_uniform.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]

@@ -25,6 +25,7 @@
 
 #include "coeffs.h"
 #include "pit_b200.h"
+#include "pit_comm.h"
 #include "pit_kernels.cuh"
 #include "pit_kernels2d.cuh"
 
@@ -119,6 +120,16 @@ struct pit_context {
   std::vector<double> y0;
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned mirror
+  // slab-sharded multi-GPU (pit_context_attach_comm): owned blocks, the halo
+  // / chain block, the partials all-gather buffers, a high-priority stream
+  // for the halo exchange and the boundary slab
+  pit_comm* comm = nullptr;
+  int shard_first = 0, shard_count = 0;
+  double* d_halo = nullptr;
+  double* d_gather = nullptr;
+  double* h_gather = nullptr;  // pinned
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_comm[2] = {};
   unsigned long long busy_mark = 0;  // busy_ns already charged to RunStats
   // SolveOptions::iterate_observer (solvers.hpp:54): called after every
   // history row with the iterate the row describes (host copy)
@@ -128,8 +139,9 @@ struct pit_context {
   double* h_partials = nullptr;  // pinned, 3*N
   double* d_partials = nullptr;  // 3*N
   cudaStream_t stream = nullptr;
-  // solver work buffers (N*M each), allocated on first solve
+  // solver work buffers (the rank's blocks each), allocated on first solve
   double* buf[10] = {};
+  size_t buf_n = 0;
   int sms = 148;
   // K1 piece scheduling (SlabArgs::state): 0 = from occupancy, 1 = off, n = forced
   int pieces = 0;
@@ -383,13 +395,14 @@ int check_status(pit_context* ctx, bool fine_batch) {
   CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
                            ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  const int bad = ctx->h_status->slab;
+  const int bad = fine_batch ? ctx->h_status->slab : ctx->h_status->sweep_slab;
   if (bad != INT_MAX) {
     const double relres = ctx->h_status->fail[0], iters = ctx->h_status->fail[1];
     const int kind = (int)ctx->h_status->fail[2];
     // reset the failure fields (not busy_ns)
     DevStatus* h = ctx->h_status;
     h->slab = INT_MAX;
+    h->sweep_slab = INT_MAX;
     h->fail[0] = h->fail[1] = 0.0;
     h->fail[2] = -1.0;
     CUDA_TRY(cudaMemcpyAsync(ctx->d_status, ctx->h_status, offsetof(DevStatus, busy_ns),
@@ -424,7 +437,7 @@ void bind_status(pit_context* ctx, SlabArgs* A) {
   A->busy_ns = &ctx->d_status->busy_ns;
 }
 void bind_status(pit_context* ctx, SweepArgs* A) {
-  A->status = &ctx->d_status->slab;
+  A->status = &ctx->d_status->sweep_slab;
   A->fail_info = ctx->d_status->fail;
 }
 
@@ -595,9 +608,15 @@ int fetch_partials(pit_context* ctx, int count) {
   return PIT_OK;
 }
 
-int ensure_buffers(pit_context* ctx) {
-  if (ctx->buf[0]) return PIT_OK;
-  for (auto& b : ctx->buf) CUDA_TRY(cudaMalloc(&b, ctx->nm() * sizeof(double)));
+int ensure_buffers(pit_context* ctx, size_t n) {
+  if (ctx->buf[0] && ctx->buf_n >= n) return PIT_OK;
+  for (auto& b : ctx->buf) {
+    cudaFree(b);
+    b = nullptr;
+  }
+  ctx->buf_n = 0;
+  for (auto& b : ctx->buf) CUDA_TRY(cudaMalloc(&b, n * sizeof(double)));
+  ctx->buf_n = n;
   return PIT_OK;
 }
 
@@ -670,6 +689,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
   ctx->m = desc->interior;
   ctx->M = ctx->dim == 2 ? ctx->m * ctx->m : ctx->m;
   ctx->N = desc->slab_count;
+  ctx->shard_count = ctx->N;
   ctx->h = grid_spacing(desc);
   // inner_product weight h^d (grid.cpp:113-114)
   ctx->weight = ctx->dim == 2 ? ctx->h * ctx->h : ctx->h;
@@ -814,6 +834,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
   {
     DevStatus init{};
     init.slab = INT_MAX;  // "no failing slab"
+    init.sweep_slab = INT_MAX;
     init.fail[2] = -1.0;
     *ctx->h_status = init;
     if (cudaMemcpy(ctx->d_status, &init, sizeof(DevStatus), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -849,6 +870,12 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_sync);
   cudaFree(ctx->d_ref);
   cudaFree(ctx->d_ref_diff);
+  cudaFree(ctx->d_halo);
+  cudaFree(ctx->d_gather);
+  if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  for (auto& e : ctx->ev_comm)
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_pipe) cudaEventDestroy(ctx->ev_pipe);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -1010,7 +1037,8 @@ int pit_sync_status(pit_context* ctx, void* stream) {
   PIT_DEVICE_SCOPE(ctx);
   if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
   if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
-  const int rc = check_status(ctx, true);
+  int rc = check_status(ctx, true);
+  if (!rc) rc = check_status(ctx, false);
   ctx->busy_mark = ctx->h_status->busy_ns;  // device-entry batches carry no RunStats
   return rc;
 }
@@ -1418,19 +1446,236 @@ int pit_block_norm_n_inf(pit_context* ctx, const double* a, double* out) {
 
 namespace {
 
+// ---------------------------------------------------------------------------
+// The solvers on a rank's blocks.  One GPU: the rank owns every block and no
+// communicator is attached.  Sharded (pit_context_attach_comm): the rank owns
+// blocks [first, first+count) and the halo, the coarse chain and the
+// reductions go through the communicator; the arithmetic of
+// every block is the same kernel's, and the partials are summed in global
+// slab order, so every world size gives the one-GPU bits.
+// ---------------------------------------------------------------------------
+
+// fine.source_contribution of blocks [first, first+count) (block 0, y0, is
+// the caller's): the K1 source propagation from the zero field
+int fine_source(pit_context* ctx, double* out, int first, int count, cudaStream_t st) {
+  const int skip = first == 0 ? 1 : 0;
+  if (count - skip <= 0) return PIT_OK;
+  Role& R = ctx->role[PIT_FINE];
+  SlabArgs A{};
+  A.mode = kPropagate;
+  bind_status(ctx, &A);
+  A.out = out + (size_t)skip * ctx->M;
+  A.slab0 = first + skip - 1;
+  PIT_TRY(attach_pieces(ctx, &A, count - skip));
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, count - skip, st));
+  return PIT_OK;
+}
+
+struct Run {
+  pit_context* ctx;
+  pit_comm* comm;  // nullptr: one GPU
+  int first, count;
+  cudaStream_t st;
+  size_t nl() const { return (size_t)count * ctx->M; }
+  bool has_prev() const { return comm && comm->rank > 0; }
+  bool has_next() const { return comm && comm->rank + 1 < comm->world; }
+};
+
+Run make_run(pit_context* ctx, bool sharded) {
+  if (sharded && ctx->comm) return Run{ctx, ctx->comm, ctx->shard_first, ctx->shard_count, ctx->stream};
+  return Run{ctx, nullptr, 0, ctx->N, ctx->stream};
+}
+
+int comm_err(int rc, const char* what) {
+  return set_err(rc ? rc : PIT_ERR_CUDA, what ? what : "communication failed");
+}
+#define COMM_TRY(expr)                       \
+  do {                                       \
+    const char* what_ = nullptr;             \
+    int rc_ = (expr);                        \
+    if (rc_) return comm_err(rc_, what_);    \
+  } while (0)
+
+// Status checks: one GPU after every phase (as the reference throws at the
+// failing call); sharded at the next reduction, where every rank learns the
+// lowest failing slab of all ranks and raises the same error (a rank that
+// stopped early would leave its peers waiting in the chain).
+int run_check(Run& R, bool fine_batch) {
+  if (R.comm) return PIT_OK;
+  return check_status(R.ctx, fine_batch);
+}
+
+// fine batch (apply_F or the preconditioned residual's rhs - F lam) over the
+// rank's blocks; sharded: the blocks after the first start at once, the
+// first waits for the halo block first-1 from rank-1 (on the comm stream)
+int run_fine(Run& R, int mode, const double* x, const double* rhs, double* out,
+             pit_run_stats* stats) {
+  pit_context* ctx = R.ctx;
+  const size_t M = ctx->M;
+  const auto t0 = Clock::now();
+  if (!R.has_prev() && !R.has_next()) {
+    PIT_TRY(run_slab_batch(ctx, mode, x, nullptr, rhs, out, 0, R.count, R.st));
+  } else {
+    cudaStream_t cs = ctx->comm_stream;
+    CUDA_TRY(cudaEventRecord(ctx->ev_comm[0], R.st));  // x ready
+    if (R.first == 0) {
+      PIT_TRY(run_slab_batch(ctx, mode, x, nullptr, rhs, out, 0, R.count, R.st));
+      CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev_comm[0], 0));
+      COMM_TRY(pitcomm::send(R.comm, x + (R.count - 1) * M, M, R.comm->rank + 1, cs, &what_));
+    } else {
+      if (R.count > 1)
+        PIT_TRY(run_slab_batch(ctx, mode, x + M, x, rhs ? rhs + M : nullptr, out + M, R.first + 1,
+                               R.count - 1, R.st));
+      CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev_comm[0], 0));
+      COMM_TRY(pitcomm::shift(R.comm, x + (R.count - 1) * M, ctx->d_halo, M, cs, &what_));
+      PIT_TRY(run_slab_batch(ctx, mode, x, ctx->d_halo, rhs, out, R.first, 1, cs));
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev_comm[1], cs));
+    CUDA_TRY(cudaStreamWaitEvent(R.st, ctx->ev_comm[1], 0));
+  }
+  PIT_TRY(run_check(R, true));
+  add_fine(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+
+// the sequential chain W_n = G(W_{n-1}) (+ V_n) over the rank's blocks;
+// sharded: W_{first-1} comes from rank-1, W_{last} goes to rank+1
+int run_chain(Run& R, int role, bool with_source, const double* V, double* W, bool add_v,
+              pit_run_stats* stats) {
+  pit_context* ctx = R.ctx;
+  const size_t M = ctx->M;
+  const auto t0 = Clock::now();
+  if (R.first == 0) {
+    PIT_TRY(run_sweep(ctx, role, with_source, V, nullptr, W, 0, R.count, add_v, R.st));
+  } else {
+    COMM_TRY(pitcomm::recv(R.comm, ctx->d_halo, M, R.comm->rank - 1, R.st, &what_));
+    PIT_TRY(run_sweep(ctx, role, with_source, V, ctx->d_halo, W, R.first, R.count, add_v, R.st));
+  }
+  if (R.has_next())
+    COMM_TRY(pitcomm::send(R.comm, W + (R.count - 1) * M, M, R.comm->rank + 1, R.st, &what_));
+  PIT_TRY(run_check(R, false));
+  if (role == PIT_COARSE) add_coarse(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+
+// ctx->h_partials[N*np] (global slab order) from the rank's local partials
+// in ctx->d_partials[count*np]
+int run_reduce(Run& R, int np) {
+  pit_context* ctx = R.ctx;
+  if (!R.comm) return fetch_partials(ctx, R.count * np);
+  const int world = R.comm->world, N = ctx->N;
+  const int maxc = (N + world - 1) / world;
+  const size_t per = (size_t)maxc * 3 + 4;  // partials, then DevStatus' slab fields + fail[3]
+  double* send = ctx->d_gather;
+  double* recv = ctx->d_gather + per;
+  CUDA_TRY(cudaMemcpyAsync(send, ctx->d_partials, sizeof(double) * (size_t)R.count * np,
+                           cudaMemcpyDeviceToDevice, R.st));
+  CUDA_TRY(cudaMemcpyAsync(send + (size_t)maxc * 3, ctx->d_status, offsetof(DevStatus, busy_ns),
+                           cudaMemcpyDeviceToDevice, R.st));
+  COMM_TRY(pitcomm::allgather(R.comm, send, per, recv, R.st, &what_));
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_gather, recv, sizeof(double) * per * world,
+                           cudaMemcpyDeviceToHost, R.st));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
+  int bad_fine = INT_MAX, bad_sweep = INT_MAX, sweep_rank = -1;
+  for (int r = 0; r < world; ++r) {
+    const int base = N / world, extra = N % world;
+    const int fr = r * base + std::min(r, extra), cr = base + (r < extra ? 1 : 0);
+    const double* g = ctx->h_gather + (size_t)r * per;
+    std::memcpy(ctx->h_partials + (size_t)fr * np, g, sizeof(double) * (size_t)cr * np);
+    DevStatus s{};
+    std::memcpy(&s, g + (size_t)maxc * 3, offsetof(DevStatus, busy_ns));
+    bad_fine = std::min(bad_fine, s.slab);
+    if (s.sweep_slab < bad_sweep) {
+      bad_sweep = s.sweep_slab;
+      sweep_rank = r;
+    }
+  }
+  if (bad_fine == INT_MAX && bad_sweep == INT_MAX) return PIT_OK;
+  // every rank raises the same error; the local status is cleared as
+  // check_status would
+  const bool local_failed = ctx->h_status->slab != INT_MAX || ctx->h_status->sweep_slab != INT_MAX;
+  (void)local_failed;
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                           R.st));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
+  DevStatus* h = ctx->h_status;
+  h->slab = h->sweep_slab = INT_MAX;
+  h->fail[0] = h->fail[1] = 0.0;
+  h->fail[2] = -1.0;
+  CUDA_TRY(cudaMemcpyAsync(ctx->d_status, ctx->h_status, offsetof(DevStatus, busy_ns),
+                           cudaMemcpyHostToDevice, R.st));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
+  if (bad_sweep != INT_MAX) {
+    DevStatus s{};
+    std::memcpy(&s, ctx->h_gather + (size_t)sweep_rank * per + (size_t)maxc * 3,
+                offsetof(DevStatus, busy_ns));
+    const int kind = (int)s.fail[2];
+    const std::string what =
+        kind == kFailNotConverged
+            ? "implicit step solve did not converge (relative residual " +
+                  std::to_string(s.fail[0]) + " after " + std::to_string((long long)s.fail[1]) +
+                  " iterations)"
+            : "implicit step produced non-finite values";
+    const int rc = set_err(PIT_ERR_INNER_SOLVE, what, bad_sweep);
+    g_err_detail = kind == kFailNotConverged || kind == kFailNonFinite;
+    g_err_relres = s.fail[0];
+    g_err_iters = (int64_t)s.fail[1];
+    return rc;
+  }
+  return set_err(PIT_ERR_SLAB,
+                 "slab " + std::to_string(bad_fine) + ": implicit step produced non-finite values",
+                 bad_fine);
+}
+
+// per-block h<a_k, b_k> of the rank's blocks, reduced: ctx->h_partials
+int run_dots(Run& R, int np, const double* const* a, const double* const* b) {
+  CUDA_TRY(launch_dots(R.ctx->M, R.count, R.ctx->weight, np, a, b, R.ctx->d_partials, R.st));
+  return run_reduce(R, np);
+}
+
+int run_copy(Run& R, double* dst, const double* src) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, R.nl() * sizeof(double), cudaMemcpyDeviceToDevice, R.st));
+  return PIT_OK;
+}
+
+// initial_guess (solvers.cpp:49-64) over the rank's blocks
+int run_initial_guess(Run& R, int policy, double* d, pit_run_stats* stats) {
+  pit_context* ctx = R.ctx;
+  CUDA_TRY(cudaMemsetAsync(d, 0, R.nl() * sizeof(double), R.st));
+  if (policy == PIT_GUESS_ZERO) return PIT_OK;
+  if (R.first == 0)
+    CUDA_TRY(cudaMemcpyAsync(d, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
+                             R.st));
+  return run_chain(R, PIT_COARSE, true, nullptr, d, false, stats);
+}
+
+// assemble_rhs (block_system.cpp:149-172) over the rank's blocks
+int run_rhs(Run& R, double* d, pit_run_stats* stats) {
+  pit_context* ctx = R.ctx;
+  const auto t0 = Clock::now();
+  CUDA_TRY(cudaMemsetAsync(d, 0, R.nl() * sizeof(double), R.st));
+  if (R.first == 0)
+    CUDA_TRY(cudaMemcpyAsync(d, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
+                             R.st));
+  if (!ctx->has_source) return PIT_OK;
+  PIT_TRY(fine_source(ctx, d, R.first, R.count, R.st));
+  PIT_TRY(run_check(R, true));
+  add_fine(ctx, stats, ms_since(t0));
+  return PIT_OK;
+}
+
 // block_norm_n_inf(lambda - reference) (solvers.cpp:131), on the device:
 // diff = fma(-1, ref, lambda) = lambda - ref exactly rounded.
-double error_vs_reference(pit_context* ctx, const double* lam) {
-  const size_t nm = ctx->nm();
-  if (cudaMemcpyAsync(ctx->d_ref_diff, lam, nm * sizeof(double), cudaMemcpyDeviceToDevice,
-                      ctx->stream) != cudaSuccess ||
-      launch_axpy(nm, -1.0, ctx->d_ref, ctx->d_ref_diff, ctx->stream) != cudaSuccess)
+double error_vs_reference(Run& R, const double* lam) {
+  pit_context* ctx = R.ctx;
+  const size_t nl = R.nl();
+  if (cudaMemcpyAsync(ctx->d_ref_diff, lam, nl * sizeof(double), cudaMemcpyDeviceToDevice,
+                      R.st) != cudaSuccess ||
+      launch_axpy(nl, -1.0, ctx->d_ref + (size_t)R.first * ctx->M, ctx->d_ref_diff, R.st) !=
+          cudaSuccess)
     return NAN;
   const double* A[1] = {ctx->d_ref_diff};
-  if (launch_dots(ctx->M, ctx->N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream) !=
-          cudaSuccess ||
-      fetch_partials(ctx, ctx->N))
-    return NAN;
+  if (run_dots(R, 1, A, A)) return NAN;
   return max_sqrt_partials(ctx->h_partials, ctx->N, 1, 0);
 }
 
@@ -1440,32 +1685,33 @@ struct Recorder {
   int n = 0;
   pit_run_stats* stats;
   Clock::time_point t0;
-  pit_context* ctx = nullptr;   // with a reference set: error_vs_reference of *lam
+  Run* run = nullptr;           // with a reference set: error_vs_reference of *lam
   const double* lam = nullptr;
   int rc = PIT_OK;              // first failure of an observer's copy
   void operator()(int k, double res) {
+    pit_context* ctx = run->ctx;
     pit_record row{};
     row.k = k;
     row.residual_norm = res;
     row.fine_applications = stats->fine_applications;
     row.coarse_applications = stats->coarse_applications;
-    if (ctx && ctx->d_ref && lam) {
-      row.error_vs_reference = error_vs_reference(ctx, lam);
+    if (ctx->d_ref && lam) {
+      row.error_vs_reference = error_vs_reference(*run, lam);
       row.has_error = 1;
     }
     row.wall_ms = ms_since(t0);
     if (n < cap && rows) rows[n] = row;
     ++n;
     // SolveOptions::iterate_observer: after the row is recorded, with the
-    // iterate it describes (solvers.cpp:101, 136)
-    if (ctx && ctx->observer && lam) {
-      if (cudaMemcpyAsync(ctx->h_observed, lam, ctx->nm() * sizeof(double),
-                          cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
-          cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    // iterate it describes (solvers.cpp:101, 136); sharded: the rank's blocks
+    if (ctx->observer && lam) {
+      if (cudaMemcpyAsync(ctx->h_observed, lam, run->nl() * sizeof(double),
+                          cudaMemcpyDeviceToHost, run->st) != cudaSuccess ||
+          cudaStreamSynchronize(run->st) != cudaSuccess) {
         if (!rc) rc = set_err(PIT_ERR_CUDA, "iterate_observer: device-to-host copy failed");
         return;
       }
-      ctx->observer(&row, ctx->h_observed, ctx->N, ctx->M, ctx->observer_user);
+      ctx->observer(&row, ctx->h_observed, run->count, ctx->M, ctx->observer_user);
     }
   }
 };
@@ -1480,49 +1726,32 @@ int validate_cfg(const pit_solver_config* cfg) {
 }
 
 // G^-1 F x  ->  out   (F into tmp, then the in-place sweep)
-int apply_GF(pit_context* ctx, const double* x, double* tmp, double* out, pit_run_stats* st) {
-  auto t0 = Clock::now();
-  PIT_TRY(run_slab_batch(ctx, kApplyF, x, nullptr, nullptr, tmp, 0, ctx->N, ctx->stream));
-  PIT_TRY(check_status(ctx, true));
-  add_fine(ctx, st, ms_since(t0));
-  t0 = Clock::now();
-  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, tmp, nullptr, out, 0, ctx->N, true, ctx->stream));
-  PIT_TRY(check_status(ctx, false));
-  add_coarse(ctx, st, ms_since(t0));
-  return PIT_OK;
+int apply_GF(Run& R, const double* x, double* tmp, double* out, pit_run_stats* st) {
+  PIT_TRY(run_fine(R, kApplyF, x, nullptr, tmp, st));
+  return run_chain(R, PIT_COARSE, false, tmp, out, true, st);
 }
 
-int precond_residual_dev(pit_context* ctx, const double* lam, const double* rhs, double* out,
-                         pit_run_stats* st) {
-  auto t0 = Clock::now();
-  PIT_TRY(run_slab_batch(ctx, kResidual, lam, nullptr, rhs, out, 0, ctx->N, ctx->stream));
-  PIT_TRY(check_status(ctx, true));
-  add_fine(ctx, st, ms_since(t0));
-  t0 = Clock::now();
-  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, out, nullptr, out, 0, ctx->N, true, ctx->stream));
-  PIT_TRY(check_status(ctx, false));
-  add_coarse(ctx, st, ms_since(t0));
-  return PIT_OK;
+// preconditioned_residual (solvers.cpp:66-71): G^-1 (rhs - F lam)
+int precond_residual(Run& R, const double* lam, const double* rhs, double* out,
+                     pit_run_stats* st) {
+  PIT_TRY(run_fine(R, kResidual, lam, rhs, out, st));
+  return run_chain(R, PIT_COARSE, false, out, out, true, st);
 }
 
-int copy_dev(pit_context* ctx, double* dst, const double* src) {
-  CUDA_TRY(cudaMemcpyAsync(dst, src, ctx->nm() * sizeof(double), cudaMemcpyDeviceToDevice,
-                           ctx->stream));
-  return PIT_OK;
-}
-
-// pitsbicg_solve, src/solvers.cpp:116-220.  lam (device) holds the iterate.
-int pitsbicg_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init, double* lam,
+// pitsbicg_solve, src/solvers.cpp:116-220.  lam (device) holds the rank's
+// blocks of the iterate.
+int pitsbicg_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* lam,
                  double* first_residual_dev, pit_record* rows, int cap, pit_solve_info* info) {
-  PIT_TRY(ensure_buffers(ctx));
-  const int N = ctx->N, M = ctx->M;
-  const size_t nm = ctx->nm();
+  pit_context* ctx = R.ctx;
+  PIT_TRY(ensure_buffers(ctx, R.nl()));
+  const int N = ctx->N, M = ctx->M, nb = R.count;
+  const size_t nl = R.nl();
   double *rhs = ctx->buf[1], *r = ctx->buf[2], *rs = ctx->buf[3], *p = ctx->buf[4],
          *d = ctx->buf[5], *s = ctx->buf[6], *t = ctx->buf[7], *f = ctx->buf[8];
   pit_solve_info inf{};
   inf.min_restart_margin = INFINITY;
   pit_run_stats& st = inf.stats;
-  Recorder rec{rows, cap, 0, &st, Clock::now(), ctx, lam};
+  Recorder rec{rows, cap, 0, &st, Clock::now(), &R, lam};
   auto finish = [&](int status) -> int {
     if (rec.rc) return rec.rc;
     inf.status = status;
@@ -1531,90 +1760,78 @@ int pitsbicg_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
     if (info) *info = inf;
     return PIT_OK;
   };
-  if (!have_init) PIT_TRY(initial_guess_dev(ctx, cfg->initial_guess, lam, &st));
-  PIT_TRY(assemble_rhs_dev(ctx, rhs, &st));
-  PIT_TRY(precond_residual_dev(ctx, lam, rhs, r, &st));
-  if (first_residual_dev) PIT_TRY(copy_dev(ctx, first_residual_dev, r));
+  if (!have_init) PIT_TRY(run_initial_guess(R, cfg->initial_guess, lam, &st));
+  PIT_TRY(run_rhs(R, rhs, &st));
+  PIT_TRY(precond_residual(R, lam, rhs, r, &st));
+  if (first_residual_dev) PIT_TRY(run_copy(R, first_residual_dev, r));
   // ||r|| and <r,r> (= rho of iteration 1, r~ = r) from one partials pass
   {
     const double* A[1] = {r};
-    CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
-    PIT_TRY(fetch_partials(ctx, N));
+    PIT_TRY(run_dots(R, 1, A, A));
   }
   double r_norm = max_sqrt_partials(ctx->h_partials, N, 1, 0);
   double rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);  // <r, r~> with r~ = r
   rec(0, r_norm);
   if (r_norm <= cfg->tolerance) return finish(PIT_CONVERGED);
-  PIT_TRY(copy_dev(ctx, rs, r));
-  PIT_TRY(copy_dev(ctx, p, r));
+  PIT_TRY(run_copy(R, rs, r));
+  PIT_TRY(run_copy(R, p, r));
 
   for (int k = 1; k <= cfg->max_iterations; ++k) {
     auto restart = [&]() -> int {
-      PIT_TRY(copy_dev(ctx, rs, r));
-      PIT_TRY(copy_dev(ctx, p, r));
+      PIT_TRY(run_copy(R, rs, r));
+      PIT_TRY(run_copy(R, p, r));
       ++inf.restarts;
       rec(k, r_norm);
+      // r~ = r: <r, r~> becomes <r, r>
+      const double* A[1] = {r};
+      PIT_TRY(run_dots(R, 1, A, A));
+      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
       return PIT_OK;
     };
     // rho = <r, r~>: the value computed when r (or r~) last changed
     const double rho = rr_shadow;
-    PIT_TRY(apply_GF(ctx, p, f, d, &st));
+    PIT_TRY(apply_GF(R, p, f, d, &st));
     {
       const double* A[1] = {d};
       const double* B[1] = {rs};
-      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, B, ctx->d_partials, ctx->stream));
-      PIT_TRY(fetch_partials(ctx, N));
+      PIT_TRY(run_dots(R, 1, A, B));
     }
     const double d_dot = sum_partials(ctx->h_partials, N, 1, 0);
     if (std::abs(d_dot) < 1e-300) {
       PIT_TRY(restart());
-      // r~ = r: <r, r~> becomes <r, r>
-      const double* A[1] = {r};
-      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
-      PIT_TRY(fetch_partials(ctx, N));
-      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
       continue;
     }
     const double alpha = rho / d_dot;
-    CUDA_TRY(launch_update_s(M, N, ctx->weight, alpha, r, d, s, ctx->d_partials, ctx->stream));
-    PIT_TRY(fetch_partials(ctx, N));
+    CUDA_TRY(launch_update_s(M, nb, ctx->weight, alpha, r, d, s, ctx->d_partials, R.st));
+    PIT_TRY(run_reduce(R, 1));
     const double s_norm = max_sqrt_partials(ctx->h_partials, N, 1, 0);
     if (s_norm <= cfg->tolerance) {
-      CUDA_TRY(launch_axpy(nm, alpha, p, lam, ctx->stream));
+      CUDA_TRY(launch_axpy(nl, alpha, p, lam, R.st));
       std::swap(ctx->buf[2], ctx->buf[6]);  // r = move(s)
       rec(k, s_norm);
-      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      CUDA_TRY(cudaStreamSynchronize(R.st));
       return finish(PIT_CONVERGED);
     }
-    PIT_TRY(apply_GF(ctx, s, f, t, &st));
+    PIT_TRY(apply_GF(R, s, f, t, &st));
     {
       const double* A[2] = {t, t};
       const double* B[2] = {t, s};
-      CUDA_TRY(launch_dots(M, N, ctx->weight, 2, A, B, ctx->d_partials, ctx->stream));
-      PIT_TRY(fetch_partials(ctx, 2 * N));
+      PIT_TRY(run_dots(R, 2, A, B));
     }
     const double tt = sum_partials(ctx->h_partials, N, 2, 0);
     if (tt < 1e-300) {
       PIT_TRY(restart());
-      const double* A[1] = {r};
-      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
-      PIT_TRY(fetch_partials(ctx, N));
-      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
       continue;
     }
     const double omega = sum_partials(ctx->h_partials, N, 2, 1) / tt;
     if (std::abs(omega) < 1e-300) {
       PIT_TRY(restart());
-      const double* A[1] = {r};
-      CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
-      PIT_TRY(fetch_partials(ctx, N));
-      rr_shadow = sum_partials(ctx->h_partials, N, 1, 0);
       continue;
     }
     // lambda += alpha p; lambda += omega s; s -= omega t; r = move(s)
-    CUDA_TRY(launch_update_lr(M, N, ctx->weight, alpha, omega, p, s, t, rs, lam, r,
-                              ctx->d_partials, ctx->stream));
-    PIT_TRY(fetch_partials(ctx, 2 * N));
+    CUDA_TRY(launch_update_lr(M, nb, ctx->weight, alpha, omega, p, s, t, rs, lam, r,
+                              ctx->d_partials, R.st));
+    PIT_TRY(run_reduce(R, 2));
     r_norm = max_sqrt_partials(ctx->h_partials, N, 2, 0);
     const double rr = sum_partials(ctx->h_partials, N, 2, 0);
     const double r_dot = sum_partials(ctx->h_partials, N, 2, 1);
@@ -1622,40 +1839,40 @@ int pitsbicg_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
     if (r_norm <= cfg->tolerance) return finish(PIT_CONVERGED);
     inf.min_restart_margin = std::min(inf.min_restart_margin, std::abs(r_dot) / cfg->restart_tolerance);
     if (std::abs(r_dot) <= cfg->restart_tolerance) {
-      PIT_TRY(copy_dev(ctx, rs, r));
-      PIT_TRY(copy_dev(ctx, p, r));
+      PIT_TRY(run_copy(R, rs, r));
+      PIT_TRY(run_copy(R, p, r));
       ++inf.restarts;
       rr_shadow = rr;
     } else {
       const double beta = (alpha / omega) * (r_dot / rho);
-      CUDA_TRY(launch_update_p(nm, omega, beta, d, r, p, ctx->stream));
+      CUDA_TRY(launch_update_p(nl, omega, beta, d, r, p, R.st));
       rr_shadow = r_dot;
     }
   }
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
   return finish(PIT_MAX_ITERATIONS);
 }
 
 // parareal_solve, src/solvers.cpp:73-114.
-int parareal_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init, double* lam,
+int parareal_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* lam,
                  double* first_residual_dev, pit_record* rows, int cap, pit_solve_info* info) {
-  PIT_TRY(ensure_buffers(ctx));
-  const int N = ctx->N, M = ctx->M;
+  pit_context* ctx = R.ctx;
+  PIT_TRY(ensure_buffers(ctx, R.nl()));
+  const int N = ctx->N;
   double *rhs = ctx->buf[1], *corr = ctx->buf[2];
   pit_solve_info inf{};
   inf.min_restart_margin = INFINITY;
   pit_run_stats& st = inf.stats;
-  Recorder rec{rows, cap, 0, &st, Clock::now(), ctx, lam};
-  if (!have_init) PIT_TRY(initial_guess_dev(ctx, cfg->initial_guess, lam, &st));
-  PIT_TRY(assemble_rhs_dev(ctx, rhs, &st));
+  Recorder rec{rows, cap, 0, &st, Clock::now(), &R, lam};
+  if (!have_init) PIT_TRY(run_initial_guess(R, cfg->initial_guess, lam, &st));
+  PIT_TRY(run_rhs(R, rhs, &st));
   int status = PIT_MAX_ITERATIONS;
   for (int k = 0;; ++k) {
     const pit_run_stats before = st;
-    PIT_TRY(precond_residual_dev(ctx, lam, rhs, corr, &st));
-    if (k == 0 && first_residual_dev) PIT_TRY(copy_dev(ctx, first_residual_dev, corr));
+    PIT_TRY(precond_residual(R, lam, rhs, corr, &st));
+    if (k == 0 && first_residual_dev) PIT_TRY(run_copy(R, first_residual_dev, corr));
     const double* A[1] = {corr};
-    CUDA_TRY(launch_dots(M, N, ctx->weight, 1, A, A, ctx->d_partials, ctx->stream));
-    PIT_TRY(fetch_partials(ctx, N));
+    PIT_TRY(run_dots(R, 1, A, A));
     const double res = max_sqrt_partials(ctx->h_partials, N, 1, 0);
     const pit_run_stats after = st;
     st = before;  // the row charges the work spent reaching the current iterate
@@ -1666,9 +1883,9 @@ int parareal_dev(pit_context* ctx, const pit_solver_config* cfg, bool have_init,
       break;
     }
     if (k == cfg->max_iterations) break;
-    CUDA_TRY(launch_add(ctx->nm(), corr, lam, ctx->stream));
+    CUDA_TRY(launch_add(R.nl(), corr, lam, R.st));
   }
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
   if (rec.rc) return rec.rc;
   inf.status = status;
   inf.total_records = rec.n;
@@ -1682,18 +1899,43 @@ int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const 
                int max_records, pit_solve_info* info) {
   if (!ctx || !lambda_out) return set_err(PIT_ERR_INVALID_ARGUMENT, "solve: null argument");
   PIT_TRY(validate_cfg(cfg));
-  PIT_TRY(ensure_buffers(ctx));
+  Run R = make_run(ctx, false);
+  PIT_TRY(ensure_buffers(ctx, R.nl()));
   double* lam = ctx->buf[0];
   double* first = first_residual_out ? ctx->buf[9] : nullptr;
   if (lambda_init)
     CUDA_TRY(cudaMemcpyAsync(lam, lambda_init, ctx->nm() * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
   if (which == 0)
-    PIT_TRY(pitsbicg_dev(ctx, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
+    PIT_TRY(pitsbicg_dev(R, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
   else
-    PIT_TRY(parareal_dev(ctx, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
+    PIT_TRY(parareal_dev(R, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
   PIT_TRY(to_host(ctx, ctx->buf[0], ctx->nm(), lambda_out));
   if (first_residual_out) PIT_TRY(to_host(ctx, first, ctx->nm(), first_residual_out));
+  return PIT_OK;
+}
+
+// the *_solve_device entry points: lambda (and the optional initial guess)
+// are the caller's device arrays of the rank's blocks
+int solve_device(int which, bool sharded, pit_context* ctx, const pit_solver_config* cfg,
+                 const double* lambda_init_dev, double* lambda_dev, pit_record* records,
+                 int max_records, pit_solve_info* info, void* stream) {
+  if (!ctx || !lambda_dev) return set_err(PIT_ERR_INVALID_ARGUMENT, "solve: null argument");
+  if (sharded && !ctx->comm)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "sharded solve: no communicator attached");
+  PIT_TRY(validate_cfg(cfg));
+  Run R = make_run(ctx, sharded);
+  if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  if (lambda_init_dev && lambda_init_dev != lambda_dev)
+    CUDA_TRY(cudaMemcpyAsync(lambda_dev, lambda_init_dev, R.nl() * sizeof(double),
+                             cudaMemcpyDeviceToDevice, R.st));
+  if (which == 0)
+    PIT_TRY(pitsbicg_dev(R, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
+                         max_records, info));
+  else
+    PIT_TRY(parareal_dev(R, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
+                         max_records, info));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
   return PIT_OK;
 }
 
@@ -1782,16 +2024,130 @@ int pit_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
                               pit_record* records, int max_records, pit_solve_info* info,
                               void* stream) {
   PIT_DEVICE_SCOPE(ctx);
-  if (!ctx || !lambda_dev) return set_err(PIT_ERR_INVALID_ARGUMENT, "solve: null argument");
-  PIT_TRY(validate_cfg(cfg));
-  if (stream) CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
-  if (lambda_init_dev && lambda_init_dev != lambda_dev)
-    CUDA_TRY(cudaMemcpyAsync(lambda_dev, lambda_init_dev, ctx->nm() * sizeof(double),
-                             cudaMemcpyDeviceToDevice, ctx->stream));
-  PIT_TRY(pitsbicg_dev(ctx, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
-                       max_records, info));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return solve_device(0, false, ctx, cfg, lambda_init_dev, lambda_dev, records, max_records, info,
+                      stream);
+}
+
+// ---- slab-sharded multi-GPU ------------------------------------------------
+
+int pit_comm_nccl_unique_id(unsigned char* id) {
+  if (!id) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_comm_nccl_unique_id: null output");
+  COMM_TRY(pitcomm::unique_id(id, &what_));
   return PIT_OK;
+}
+
+int pit_comm_create_nccl(const unsigned char* id, int rank, int world, int device,
+                         pit_comm** out) {
+  if (!id || !out || world < 1 || rank < 0 || rank >= world)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_comm_create_nccl: bad arguments");
+  *out = nullptr;
+  COMM_TRY(pitcomm::create_nccl(id, rank, world, device, out, &what_));
+  return PIT_OK;
+}
+
+int pit_comm_create_host(const pit_comm_ops* ops, int rank, int world, pit_comm** out) {
+  if (!ops || !out || !ops->send || !ops->recv || !ops->allgather || world < 1 || rank < 0 ||
+      rank >= world)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_comm_create_host: bad arguments");
+  auto c = new pit_comm();
+  c->rank = rank;
+  c->world = world;
+  c->kind = 1;
+  c->ops = *ops;
+  *out = c;
+  return PIT_OK;
+}
+
+int pit_comm_destroy(pit_comm* comm) {
+  pitcomm::destroy(comm);
+  return PIT_OK;
+}
+
+int pit_context_attach_comm(pit_context* ctx, pit_comm* comm) {
+  PIT_DEVICE_SCOPE(ctx);
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (!comm) {
+    ctx->comm = nullptr;
+    ctx->shard_first = 0;
+    ctx->shard_count = ctx->N;
+    return PIT_OK;
+  }
+  if (comm->world > ctx->N)
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_attach_comm: more ranks than slabs (every rank must own a block)");
+  if (comm->kind == 0 && comm->device != ctx->desc.device)
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_attach_comm: the communicator's device is not the context's");
+  const int base = ctx->N / comm->world, extra = ctx->N % comm->world;
+  ctx->shard_first = comm->rank * base + std::min(comm->rank, extra);
+  ctx->shard_count = base + (comm->rank < extra ? 1 : 0);
+  const int maxc = base + (extra ? 1 : 0);
+  const size_t per = (size_t)maxc * 3 + 4;
+  cudaFree(ctx->d_gather);
+  ctx->d_gather = nullptr;
+  if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
+  ctx->h_gather = nullptr;
+  CUDA_TRY(cudaMalloc(&ctx->d_gather, sizeof(double) * per * (comm->world + 1)));
+  CUDA_TRY(cudaMallocHost(&ctx->h_gather, sizeof(double) * per * comm->world));
+  if (!ctx->d_halo) CUDA_TRY(cudaMalloc(&ctx->d_halo, sizeof(double) * ctx->M));
+  if (!ctx->comm_stream)
+    CUDA_TRY(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, -1));
+  for (auto& e : ctx->ev_comm)
+    if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ctx->comm = comm;
+  return PIT_OK;
+}
+
+int pit_context_shard(const pit_context* ctx, int* first, int* count) {
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (first) *first = ctx->shard_first;
+  if (count) *count = ctx->shard_count;
+  return PIT_OK;
+}
+
+int pit_sharded_apply_F_device(pit_context* ctx, const double* L_local, double* out_local,
+                               void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
+  if (!ctx || !L_local || !out_local)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "sharded apply_F: null argument");
+  if (!ctx->comm) return set_err(PIT_ERR_INVALID_ARGUMENT, "sharded apply_F: no communicator");
+  Run R = make_run(ctx, true);
+  if (stream) R.st = (cudaStream_t)stream;
+  // no status read here (stream-ordered, as pit_apply_F_device):
+  // pit_sync_status reports a failing slab
+  return run_fine(R, kApplyF, L_local, nullptr, out_local, nullptr);
+}
+
+int pit_sharded_sync_status(pit_context* ctx, void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
+  if (!ctx) return set_err(PIT_ERR_INVALID_ARGUMENT, "null context");
+  if (!ctx->comm) return pit_sync_status(ctx, stream);
+  Run R = make_run(ctx, true);
+  if (stream) R.st = (cudaStream_t)stream;
+  const int rc = run_reduce(R, 0);  // every rank's status, nothing else
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus),
+                           cudaMemcpyDeviceToHost, R.st));
+  CUDA_TRY(cudaStreamSynchronize(R.st));
+  ctx->busy_mark = ctx->h_status->busy_ns;
+  return rc;
+}
+
+int pit_sharded_pitsbicg_solve_device(pit_context* ctx, const pit_solver_config* cfg,
+                                      const double* lambda_init_local, double* lambda_local,
+                                      pit_record* records, int max_records, pit_solve_info* info,
+                                      void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
+  return solve_device(0, true, ctx, cfg, lambda_init_local, lambda_local, records, max_records,
+                      info, stream);
+}
+
+int pit_sharded_parareal_solve_device(pit_context* ctx, const pit_solver_config* cfg,
+                                      const double* lambda_init_local, double* lambda_local,
+                                      pit_record* records, int max_records, pit_solve_info* info,
+                                      void* stream) {
+  PIT_DEVICE_SCOPE(ctx);
+  return solve_device(1, true, ctx, cfg, lambda_init_local, lambda_local, records, max_records,
+                      info, stream);
 }
 
 // instrumented builds only: per-phase cycle totals of CTA 0 (warps 0, 1)

@@ -77,17 +77,25 @@ __device__ __forceinline__ StepLane step_lane(const StepParams& P,
   StepLane L;
   L.ppos = S::NSEG > 1 ? P.ppos[tid] : 0.0;
   L.qpos = S::NSEG > 1 ? P.qpos[tid] : 0.0;
-  (void)sh;
+  const int lane = tid & 31;
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    L.cf[st] = sh.cf[st][lane];
+    L.cb[st] = sh.cb[st][lane];
+  }
+  L.plane = sh.plane[lane];
+  L.qlane = sh.qlane[lane];
   return L;
 }
 
 // Steps [k0, k1) of one slab's propagation.  The rescale counter restarts
 // from k0 mod R, so cutting a slab into step ranges (piece scheduling) runs
 // exactly the same operation sequence as one uninterrupted pass.
-template <class S, bool SRC>
+template <class S, bool SRC, bool HOIST = false, bool ZREG = false>
 __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepParams& P,
                                          const StepLane& L, StepShared<S::NSEG, S::WARPS>& sh,
-                                         const double* s_zc, int tid, int slab, int k0, int k1) {
+                                         const double* s_zc, int tid, int slab, int k0, int k1,
+                                         const double (*zreg)[S::SUB] = nullptr) {
   const bool ghosts = P.M < S::NSEG * S::LSEG;
 #ifdef PIT_PHASE_TIMING
   long long ph_acc[16] = {};
@@ -110,7 +118,7 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
           const int i = S::point(tid, c, j);
           y[c][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[c][j]);
         }
-      be_solve<S>(y, P, L, sh, s_zc, tid, ghosts PIT_TIMING_ARGS);
+      be_solve<S, HOIST, ZREG>(y, P, L, sh, s_zc, tid, ghosts, zreg PIT_TIMING_ARGS);
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)
 #pragma unroll
@@ -118,9 +126,9 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
       dsk = dsn;
     }
   } else {
-    int cnt = k0 % P.R;
+    int cnt = k0 == 0 ? 0 : k0 % P.R;
     for (int k = k0; k < k1; ++k) {
-      be_solve<S>(y, P, L, sh, s_zc, tid, ghosts PIT_TIMING_ARGS);
+      be_solve<S, HOIST, ZREG>(y, P, L, sh, s_zc, tid, ghosts, zreg PIT_TIMING_ARGS);
       if (++cnt == P.R) {
         cnt = 0;
 #pragma unroll
@@ -575,9 +583,11 @@ __global__ void __launch_bounds__(S::T + 32, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
   double* s_zc = reinterpret_cast<double*>(sh + 1);
-  unsigned char* after = reinterpret_cast<unsigned char*>(s_zc + zc_smem_len<S>(P.narrow));
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(after) + 1023) & ~uintptr_t(1023));
+  // slab buffers 1024-byte aligned (128-byte swizzle atoms); offsets taken in
+  // the shared window so the compiler keeps LDS/STS (not generic LD/ST)
+  const unsigned s0 = smem_u32(smem_raw);
+  const unsigned after = smem_u32(s_zc + zc_smem_len<S>(P.narrow));
+  unsigned char* const base = smem_raw + (((after + 1023u) & ~1023u) - s0);
   const size_t buf_bytes = (size_t)P.M * sizeof(double);
   const int nbuf = X.nbuf;
   uint64_t* vfull = reinterpret_cast<uint64_t*>(base + nbuf * buf_bytes);  // [nbuf]
@@ -596,56 +606,100 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();  // the only CTA-wide barrier
-  auto bufp = [&](int b) { return base + (b % nbuf) * buf_bytes; };
 
   if (io) {
-    if (tid != S::T) return;
+    // I/O warp: lane 0 issues the TMA traffic; the whole warp checks each
+    // finished W block for non-finite values (the compute warps' step
+    // chain carries no check)
+    const int lane = tid - S::T;
     const unsigned bytes = (unsigned)(M * sizeof(double));
-    auto fill = [&](int b) {  // buffer b % nbuf is free: V_b in (or just released)
-      uint64_t* bar = &vfull[b % nbuf];
+    int fill_slot = 0;
+    auto fill = [&](int b) {  // buffer fill_slot is free: V_b in (or just released)
+      uint64_t* bar = &vfull[fill_slot];
+      unsigned char* buf = base + fill_slot * buf_bytes;
       if (A.V) {
         mbar_arrive_expect_tx(bar, bytes);
         for (int r = 0; r < X.rows; r += X.box_rows)
-          tma_load_2d(bufp(b) + r * 128, X.v, 0, b * X.rows + r, bar);
+          tma_load_2d(buf + r * 128, X.v, 0, b * X.rows + r, bar);
       } else {
         mbar_arrive(bar);
       }
+      if (++fill_slot == nbuf) fill_slot = 0;
     };
-    for (int b = 0; b < nbuf && b < A.count; ++b) fill(b);
+    if (lane == 0)
+      for (int b = 0; b < nbuf && b < A.count; ++b) fill(b);
+    bool ok = true;
+    int slot = 0;
+    unsigned phase = 0;
     for (int s = 0; s < A.count; ++s) {
-      mbar_wait(&wfull[s % nbuf], (unsigned)((s / nbuf) & 1));
-      for (int r = 0; r < X.rows; r += X.box_rows)
-        tma_store_2d(X.w, 0, s * X.rows + r, bufp(s) + r * 128);
-      bulk_commit();
-      if (s + nbuf < A.count) {
+      mbar_wait(&wfull[slot], phase);
+      const unsigned char* buf = base + slot * buf_bytes;
+      if (lane == 0) {
+        for (int r = 0; r < X.rows; r += X.box_rows)
+          tma_store_2d(X.w, 0, s * X.rows + r, buf + r * 128);
+        bulk_commit();
+      }
+      if (ok) {
+        // |hi word| >= 0x7ff00000 <=> inf or nan
+        unsigned m = 0;
+        for (int i = 2 * lane; i < M; i += 64) {
+          const double2 v = *reinterpret_cast<const double2*>(buf + 8 * (size_t)i);
+          m = max(m, (unsigned)__double2hiint(v.x) & 0x7fffffffu);
+          m = max(m, (unsigned)__double2hiint(v.y) & 0x7fffffffu);
+        }
+        if (__any_sync(kFull, m >= 0x7ff00000u)) {
+          ok = false;
+          if (lane == 0) {
+            atomicMin(A.status, A.slab0 + s);
+            if (A.fail_info != nullptr) {  // direct solve: no Krylov iterations
+              A.fail_info[0] = __longlong_as_double(0x7ff8000000000000LL);
+              A.fail_info[1] = 0.0;
+              A.fail_info[2] = kFailNonFinite;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && s + nbuf < A.count) {
         bulk_wait_read();  // the store has read the buffer out
         fill(s + nbuf);
       }
+      if (++slot == nbuf) {
+        slot = 0;
+        phase ^= 1u;
+      }
     }
-    bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
     return;
   }
 
   double y[S::NC][S::SUB];
   load_field<S>(y, A.start, tid, M);
   const StepLane L = step_lane<S>(P, *sh, tid);
-  bool ok = true;
-  int bad = 0x7fffffff;
+  // the table-form correction vector of the thread's points in registers
+  // (coarse layouts of few points per thread; others read it from smem)
+  constexpr bool kZreg = S::MPT <= 16 && S::WARPS <= 8;
+  double zreg[kZreg ? S::NC : 1][S::SUB];
+#pragma unroll
+  for (int c = 0; c < (kZreg ? S::NC : 1); ++c)
+#pragma unroll
+    for (int j = 0; j < S::SUB; ++j) zreg[c][j] = P.narrow || !kZreg ? 0.0 : s_zc[S::slot(tid, c, j)];
+  int slot = 0;
+  unsigned phase = 0;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
 #ifdef PIT_PHASE_TIMING
     const long long sw0 = clock64();
 #endif
-    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
+    if (kZreg && !P.narrow)
+      run_slab<S, SRC, true, true>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps, zreg);
+    else
+      run_slab<S, SRC, true, false>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps, zreg);
 #ifdef PIT_PHASE_TIMING
     const long long sw1 = clock64();
 #endif
-    if (ok && !all_finite<S>(y, tid, M)) {
-      ok = false;
-      bad = slab;
-    }
-    unsigned char* buf = bufp(b);
-    mbar_wait(&vfull[b % nbuf], (unsigned)((b / nbuf) & 1));  // V_b landed / buffer free
+    unsigned char* buf = base + slot * buf_bytes;
+    mbar_wait(&vfull[slot], phase);  // V_b landed / buffer free
 #pragma unroll
     for (int c = 0; c < S::NC; ++c)
 #pragma unroll
@@ -662,21 +716,17 @@ __global__ void __launch_bounds__(S::T + 32, 1)
         }
       }
     fence_proxy_async_smem();
-    mbar_arrive(&wfull[b % nbuf]);
+    mbar_arrive(&wfull[slot]);
+    if (++slot == nbuf) {
+      slot = 0;
+      phase ^= 1u;
+    }
 #ifdef PIT_PHASE_TIMING
     if (P.timing && (tid & 31) == 0 && (tid >> 5) < 2) {
       P.timing[(tid >> 5) * 16 + 10] += sw1 - sw0;        // propagation
       P.timing[(tid >> 5) * 16 + 11] += clock64() - sw1;  // V add + W store
     }
 #endif
-  }
-  if (!ok) {
-    atomicMin(A.status, bad);
-    if (A.fail_info != nullptr) {  // direct solve: no Krylov iterations
-      A.fail_info[0] = __longlong_as_double(0x7ff8000000000000LL);
-      A.fail_info[1] = 0.0;
-      A.fail_info[2] = kFailNonFinite;
-    }
   }
 }
 

@@ -11,7 +11,8 @@ enum SlabMode { kApplyF = 0, kResidual = 1, kPropagate = 2 };
 
 // Per-context device status (pinned host mirror), read back in one copy
 // after each operator:
-//   slab     lowest failing slab (INT_MAX = none): SlabError / InnerSolveError
+//   slab, sweep_slab  lowest failing slab (INT_MAX = none) of the fine
+//            batches (SlabError) and of the sequential sweeps (InnerSolveError)
 //   fail[3]  sequential-sweep failure payload of InnerSolveError
 //            (include/pit/errors.hpp:15-21): achieved relative residual,
 //            inner iterations, kind (0 = the Krylov solve missed its
@@ -20,8 +21,8 @@ enum SlabMode { kApplyF = 0, kResidual = 1, kPropagate = 2 };
 //            device analogue of the executor's per-task busy time
 //            (executor.cpp:124-128), feeding RunStats::fine_busy_ms
 struct DevStatus {
-  int slab;
-  int pad;
+  int slab;        // fine batches (SlabError)
+  int sweep_slab;  // sequential sweeps (InnerSolveError)
   double fail[3];
   unsigned long long busy_ns;
 };

@@ -136,18 +136,23 @@ __device__ __forceinline__ void init_step_shared(const StepParams& P,
 }
 
 // Per-thread constants of the step (registers, loaded once per kernel).
+// The HOIST variant of be_solve (the sequential sweeps, one CTA whose step
+// latency is the whole story) also keeps the lane's Kogge-Stone weights and
+// carry weights here instead of re-reading them from shared memory each step.
 struct StepLane {
   double ppos, qpos;
+  double cf[5], cb[5], plane, qlane;
 };
 
 // One step (see the file comment).  The lane-0 / lane-31 carry uses weight 1
 // on a zeroed neighbour value, the Kogge-Stone weight is 0 on lanes without a source
 // lane, and the table-form correction vector is zero-padded: every such
 // extra term is an exact no-op (fma(w, 0, x) == x, fma(0, t, x) == x).
-template <class S>
+template <class S, bool HOIST = false, bool ZREG = false>
 __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepParams& P,
                                          const StepLane& L, StepShared<S::NSEG, S::WARPS>& sh,
-                                         const double* __restrict__ s_zc, int tid, bool ghosts
+                                         const double* __restrict__ s_zc, int tid, bool ghosts,
+                                         const double (*zreg)[S::SUB]
 #ifdef PIT_PHASE_TIMING
                                          , long long (&ph_acc)[16], long long& ph_t
 #endif
@@ -173,7 +178,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
 #pragma unroll
   for (int st = 0; st < (S::KS < 0 ? 5 : S::KS); ++st) {
     if (S::KS < 0 && st >= P.scan_f) break;  // warp-uniform
-    const double cw = sh.cf[st][lane];
+    const double cw = HOIST ? L.cf[st] : sh.cf[st][lane];
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_up_sync(kFull, I[s], 1 << st), I[s]);
   }
@@ -210,7 +215,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     double Sg = 0.0;  // segment carry-in
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) {
-      double C = fma(sh.plane[lane], Wc[s], Ip[s]);
+      double C = fma(HOIST ? L.plane : sh.plane[lane], Wc[s], Ip[s]);
       if (s > 0) {  // segment 0 has no segment carry-in
         Sg = fma(P.Pseg, Sg, Tot[s - 1]);
         C = fma(L.ppos, Sg, C);
@@ -252,7 +257,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
 #pragma unroll
   for (int st = 0; st < (S::KS < 0 ? 5 : S::KS); ++st) {
     if (S::KS < 0 && st >= P.scan_b) break;  // warp-uniform
-    const double cw = sh.cb[st][lane];
+    const double cw = HOIST ? L.cb[st] : sh.cb[st][lane];
 #pragma unroll
     for (int s = 0; s < NSEG; ++s) I[s] = fma(cw, __shfl_down_sync(kFull, I[s], 1 << st), I[s]);
   }
@@ -289,7 +294,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     double Sg = 0.0;  // segment carry from the right
 #pragma unroll
     for (int s = NSEG - 1; s >= 0; --s) {
-      double R = fma(sh.qlane[lane], Wc[s], Ip[s]);
+      double R = fma(HOIST ? L.qlane : sh.qlane[lane], Wc[s], Ip[s]);
       if (s < NSEG - 1) {  // the last segment has no carry from the right
         Sg = fma(P.Qseg, Sg, Tot[s + 1]);
         R = fma(L.qpos, Sg, R);
@@ -331,7 +336,8 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     for (int c = 0; c < NC; ++c)
       if ((c / NSUB) * S::LSEG + tid * S::CH < P.K0) {
 #pragma unroll
-        for (int j = 0; j < SUB; ++j) y[c][j] = fma(cc, s_zc[S::slot(tid, c, j)], y[c][j]);
+        for (int j = 0; j < SUB; ++j)
+          y[c][j] = fma(cc, ZREG ? zreg[c][j] : s_zc[S::slot(tid, c, j)], y[c][j]);
       }
   }
   PIT_PHASE(8);

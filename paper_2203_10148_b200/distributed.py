@@ -390,6 +390,182 @@ class DeviceBackend:
                                           self._st()))
 
 
+# ---------------------------------------------------------------------------
+# The native sharded path: the C ABI's communicator and sharded solver
+# (pit_comm_*, pit_sharded_*; csrc/pit_comm.cpp).  The whole
+# exchange (halo overlapped with the interior slabs, the coarse chain, the
+# partials all-gather) runs inside the library; Python only sets it up.
+# ---------------------------------------------------------------------------
+
+class Communicator:
+    """pit_comm: NCCL (one rank per GPU) or host callbacks over a
+    torch.distributed process group (any backend; the CPU-exchange tests use
+    gloo with several processes on one GPU)."""
+
+    def __init__(self, handle, rank: int, world: int, keep=None):
+        self.handle, self.rank, self.world = handle, rank, world
+        self._keep = keep
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        import ctypes as C
+
+        from . import _lib
+        from .api import _check
+
+        buf = C.create_string_buffer(128)
+        _check(_lib.lib().pit_comm_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, rank: int, world: int, device: int, unique_id: bytes) -> "Communicator":
+        import ctypes as C
+
+        from . import _lib
+        from .api import _check
+
+        h = C.c_void_p()
+        _check(_lib.lib().pit_comm_create_nccl(C.create_string_buffer(unique_id, 128), rank, world,
+                                               device, C.byref(h)))
+        return cls(h, rank, world)
+
+    @classmethod
+    def from_process_group(cls, device: int = 0, group=None, transport: str = "nccl"):
+        """Every rank of `group` calls this: transport "nccl" shares rank 0's
+        NCCL id over the group; "host" routes the exchange through the
+        group's own send/recv/all_gather."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if transport == "host":
+            return cls.host(rank, world, group)
+        obj = [cls.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls.nccl(rank, world, device, obj[0])
+
+    @classmethod
+    def host(cls, rank: int, world: int, group=None) -> "Communicator":
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        from .api import _check
+
+        def view(buf, n):
+            return torch.from_numpy(np.ctypeslib.as_array(buf, shape=(n,)))
+
+        def send(buf, n, peer, _user):
+            try:
+                dist.send(view(buf, n), peer, group=group)
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        def recv(buf, n, peer, _user):
+            try:
+                dist.recv(view(buf, n), peer, group=group)
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        def allgather(buf, n, out, _user):
+            try:
+                parts = [torch.empty(n, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, view(buf, n).clone(), group=group)
+                o = view(out, n * world)
+                for r, t in enumerate(parts):
+                    o[r * n:(r + 1) * n] = t
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        cbs = (_lib.COMM_SEND(send), _lib.COMM_RECV(recv), _lib.COMM_ALLGATHER(allgather))
+        ops = _lib.CommOpsC(cbs[0], cbs[1], cbs[2], None)
+        h = C.c_void_p()
+        _check(_lib.lib().pit_comm_create_host(C.byref(ops), rank, world, C.byref(h)))
+        return cls(h, rank, world, keep=(cbs, ops))
+
+    def close(self):
+        from . import _lib
+
+        if self.handle:
+            _lib.lib().pit_comm_destroy(self.handle)
+            self.handle = None
+
+
+class ShardedContext:
+    """A BlockOperatorContext (the whole problem, on this rank's GPU) with a
+    Communicator attached: the rank owns the contiguous global blocks
+    [first, first+count) and the operators and solvers run sharded through
+    the C ABI (pit_sharded_*)."""
+
+    def __init__(self, ctx, comm: Communicator):
+        import ctypes as C
+
+        from . import _lib
+        from .api import _check
+
+        self.ctx, self.comm = ctx, comm
+        self.L = _lib.lib()
+        _check(self.L.pit_context_attach_comm(ctx.handle, comm.handle))
+        f, c = C.c_int(), C.c_int()
+        _check(self.L.pit_context_shard(ctx.handle, C.byref(f), C.byref(c)))
+        self.first, self.count = f.value, c.value
+
+    def detach(self):
+        self.L.pit_context_attach_comm(self.ctx.handle, None)
+
+    def apply_F(self, L_local, stream=None):
+        """(F L)_n of the rank's blocks; L_local / result: torch CUDA (count, M)."""
+        import torch
+
+        from .api import _check
+
+        out = torch.empty_like(L_local)
+        st = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _check(self.L.pit_sharded_apply_F_device(self.ctx.handle, L_local.data_ptr(),
+                                                 out.data_ptr(), st))
+        _check(self.L.pit_sharded_sync_status(self.ctx.handle, st))
+        return out
+
+    def solve(self, config=None, which: str = "pitsbicg", init_local=None):
+        """Sharded pitsbicg_solve / parareal_solve: (lambda of the rank's
+        blocks as a torch CUDA tensor, ConvergenceHistory) — the history is the
+        same on every rank and bit-identical to the one-GPU solve."""
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+        from .api import (ConvergenceHistory, IterationRecord, SolverConfig, SolveStatus, _check)
+
+        config = config or SolverConfig()
+        config.validate()
+        lam = torch.empty((self.count, self.ctx.M), dtype=torch.float64, device="cuda")
+        cap = config.max_iterations + 2
+        recs = (_lib.RecordC * cap)()
+        info = _lib.SolveInfoC()
+        cfg = config._c()
+        fn = (self.L.pit_sharded_pitsbicg_solve_device if which == "pitsbicg"
+              else self.L.pit_sharded_parareal_solve_device)
+        _check(fn(self.ctx.handle, C.byref(cfg),
+                  init_local.data_ptr() if init_local is not None else None, lam.data_ptr(), recs,
+                  cap, C.byref(info), torch.cuda.current_stream().cuda_stream))
+        hist = ConvergenceHistory()
+        for i in range(info.record_count):
+            r = recs[i]
+            hist.records.append(IterationRecord(r.k, r.residual_norm, r.fine_applications,
+                                                r.coarse_applications, r.wall_ms,
+                                                r.error_vs_reference if r.has_error else None))
+        hist.status = (SolveStatus.Converged if info.status == _lib.PIT_CONVERGED
+                       else SolveStatus.MaxIterations)
+        hist.restarts = info.restarts
+        hist.stats._accumulate(info.stats)
+        return lam, hist
+
+
 def init_from_env(backend: str = "nccl"):
     """torch.distributed init from RANK/WORLD_SIZE/MASTER_* (torchrun)."""
     import os
