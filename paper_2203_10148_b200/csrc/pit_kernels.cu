@@ -608,9 +608,7 @@ __global__ void __launch_bounds__(S::T + 32, 1)
   __syncthreads();  // the only CTA-wide barrier
 
   if (io) {
-    // I/O warp: lane 0 issues the TMA traffic; the whole warp checks each
-    // finished W block for non-finite values (the compute warps' step
-    // chain carries no check)
+    // I/O warp: lane 0 issues the TMA traffic
     const int lane = tid - S::T;
     const unsigned bytes = (unsigned)(M * sizeof(double));
     int fill_slot = 0;
@@ -628,7 +626,6 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     };
     if (lane == 0)
       for (int b = 0; b < nbuf && b < A.count; ++b) fill(b);
-    bool ok = true;
     int slot = 0;
     unsigned phase = 0;
     for (int s = 0; s < A.count; ++s) {
@@ -638,26 +635,6 @@ __global__ void __launch_bounds__(S::T + 32, 1)
         for (int r = 0; r < X.rows; r += X.box_rows)
           tma_store_2d(X.w, 0, s * X.rows + r, buf + r * 128);
         bulk_commit();
-      }
-      if (ok) {
-        // |hi word| >= 0x7ff00000 <=> inf or nan
-        unsigned m = 0;
-        for (int i = 2 * lane; i < M; i += 64) {
-          const double2 v = *reinterpret_cast<const double2*>(buf + 8 * (size_t)i);
-          m = max(m, (unsigned)__double2hiint(v.x) & 0x7fffffffu);
-          m = max(m, (unsigned)__double2hiint(v.y) & 0x7fffffffu);
-        }
-        if (__any_sync(kFull, m >= 0x7ff00000u)) {
-          ok = false;
-          if (lane == 0) {
-            atomicMin(A.status, A.slab0 + s);
-            if (A.fail_info != nullptr) {  // direct solve: no Krylov iterations
-              A.fail_info[0] = __longlong_as_double(0x7ff8000000000000LL);
-              A.fail_info[1] = 0.0;
-              A.fail_info[2] = kFailNonFinite;
-            }
-          }
-        }
       }
       __syncwarp();
       if (lane == 0 && s + nbuf < A.count) {
@@ -686,6 +663,12 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     for (int j = 0; j < S::SUB; ++j) zreg[c][j] = P.narrow || !kZreg ? 0.0 : s_zc[S::slot(tid, c, j)];
   int slot = 0;
   unsigned phase = 0;
+  // non-finite detection off the step chain: pz accumulates fma(w, 0, pz)
+  // over every W value (0 while all are finite, NaN for good after an inf
+  // or nan); it is tested one slab later, when its FMAs have long retired,
+  // and the first failing block is reported
+  double pz = 0.0;
+  int bad = 0x7fffffff;
   for (int b = 0; b < A.count; ++b) {
     const int slab = A.slab0 + b;
 #ifdef PIT_PHASE_TIMING
@@ -721,12 +704,27 @@ __global__ void __launch_bounds__(S::T + 32, 1)
       slot = 0;
       phase ^= 1u;
     }
+    if (bad == 0x7fffffff && !isfinite(pz)) bad = slab - 1;  // blocks up to b-1
+#pragma unroll
+    for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+      for (int j = 0; j < S::SUB; ++j)
+        if (S::point(tid, c, j) < M) pz = fma(y[c][j], 0.0, pz);
 #ifdef PIT_PHASE_TIMING
     if (P.timing && (tid & 31) == 0 && (tid >> 5) < 2) {
       P.timing[(tid >> 5) * 16 + 10] += sw1 - sw0;        // propagation
       P.timing[(tid >> 5) * 16 + 11] += clock64() - sw1;  // V add + W store
     }
 #endif
+  }
+  if (bad == 0x7fffffff && !isfinite(pz)) bad = A.slab0 + A.count - 1;
+  if (bad != 0x7fffffff) {
+    atomicMin(A.status, bad);
+    if (A.fail_info != nullptr) {  // direct solve: no Krylov iterations
+      A.fail_info[0] = __longlong_as_double(0x7ff8000000000000LL);
+      A.fail_info[1] = 0.0;
+      A.fail_info[2] = kFailNonFinite;
+    }
   }
 }
 

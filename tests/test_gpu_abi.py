@@ -88,7 +88,8 @@ def test_run_stats_busy_time_and_worker_count():
         api._check(_lib.lib().pit_context_slots(ctx.handle, C.byref(slots)))
     assert st.fine_applications == 2 * (p.N - 1)
     assert slots.value >= 148
-    # 199 slabs on >= 148 slots: busy time is close to slabs x one slab's time
-    # and below slots x wall time (parallel_efficiency <= 1)
+    # busy time = the summed per-slab kernel times: below slots x wall time
+    # (parallel_efficiency <= 1) and, per slab, the duration of one slab's
+    # 1000 steps (~0.8 ms alone on an SM, a few ms when sharing one)
     assert 0.0 < st.fine_busy_ms <= slots.value * st.fine_parallel_ms
-    assert st.fine_busy_ms > 50 * st.fine_parallel_ms
+    assert 0.3 < st.fine_busy_ms / st.fine_applications < 5.0

@@ -94,4 +94,4 @@ def test_host_transport_multi_rank_bitwise(case, slabs, world, tmp_path):
     assert [tuple(r) for r in g["prows"].tolist()] == [tuple(map(float, r)) for r in rows_of(pref.history)]
     # every rank raised the same SlabError (the lowest failing slab, owned by
     # the last rank)
-    assert set(g["errors"].tolist()) == {f"SlabError {p.N - 1}"}
+    assert set(g["errors"].tolist()) == {f"SlabError {p.N - 2}"}

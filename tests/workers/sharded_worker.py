@@ -37,7 +37,7 @@ def main():
         # the error path: a NaN in one rank's input is reported identically
         # on every rank (lowest failing slab)
         bad = L.copy()
-        bad[p.N - 1, 3] = np.nan
+        bad[p.N - 2, 3] = np.nan  # propagated by slab N-2 (the last slab)
         err = ""
         try:
             sc.apply_F(torch.tensor(bad[sc.first:sc.first + sc.count], device="cuda"))
