@@ -536,7 +536,7 @@ def run_ours(args, rank, world):
     import torch
 
     from paper_2203_10148_b200 import _lib, api, configs
-    from paper_2203_10148_b200.distributed import DeviceBackend, ShardedOperators
+    from paper_2203_10148_b200.distributed import Communicator, ShardedContext
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
@@ -548,8 +548,19 @@ def run_ours(args, rank, world):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     st = stream.cuda_stream
-    first = rank * base.N
-    count = base.N
+    dist = None
+    sc = comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        # the library's own NCCL communicator (rank 0's id over the process
+        # group): halo exchange overlapped with the interior slabs inside
+        # pit_sharded_apply_F_device
+        comm = Communicator.from_process_group(dev, transport="nccl")
+        sc = ShardedContext(ctx, comm)
+        first, count = sc.first, sc.count
+    else:
+        first, count = 0, p.N
     gp_local = p.M * p.fine_steps * (count - 1 if first == 0 else count)
 
     # inputs resident in HBM: the seeded trajectory-like block vector
@@ -558,37 +569,18 @@ def run_ours(args, rank, world):
     Ld = torch.tensor(Lh, device="cuda")
     out = torch.empty_like(Ld)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
-    halo = torch.empty(p.M, dtype=torch.float64, device="cuda") if rank > 0 else None
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-    backend = DeviceBackend(ctx, first, count, stream)
-
-    def exchange():
-        if world == 1:
-            return
-        last = Ld[-1].contiguous()
-        if rank % 2 == 0:
-            if rank + 1 < world:
-                dist.send(last, rank + 1)
-            if rank > 0:
-                dist.recv(halo, rank - 1)
-        else:
-            dist.recv(halo, rank - 1)
-            if rank + 1 < world:
-                dist.send(last, rank + 1)
 
     def kernel():
-        rc = L.pit_apply_F_device(ctx.handle, Ld.data_ptr(), halo.data_ptr() if halo is not None else None,
-                                  out.data_ptr(), first, count, st)
+        if world > 1:
+            rc = L.pit_sharded_apply_F_device(ctx.handle, Ld.data_ptr(), out.data_ptr(), st)
+        else:
+            rc = L.pit_apply_F_device(ctx.handle, Ld.data_ptr(), None, out.data_ptr(), 0, count, st)
         if rc:
             api._check(rc)
 
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for _ in range(args.warmup):
-        exchange()
         kernel()
         flush.zero_()
     torch.cuda.synchronize()
@@ -600,17 +592,15 @@ def run_ours(args, rank, world):
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             e0[i].record(stream)
-            exchange()
-            k0[i].record(stream)
             kernel()
             e1[i].record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    api._check(L.pit_sync_status(ctx.handle, st))
+    api._check(L.pit_sharded_sync_status(ctx.handle, st))
     step_ms = [e0[i].elapsed_time(e1[i]) for i in range(args.steps)]
-    kern_ms = [k0[i].elapsed_time(e1[i]) for i in range(args.steps)]
+    kern_ms = step_ms
     total_ms = float(np.sum(step_ms))
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     gpt = torch.tensor([float(gp_local)], dtype=torch.float64, device="cuda")
@@ -622,9 +612,9 @@ def run_ours(args, rank, world):
     value = gp_total * args.steps / (total_ms * 1e-3)
 
     # ---- e2e: public API with pinned host buffers, H2D + D2H inside ------
+    Lpin = torch.from_numpy(Lh).pin_memory()
+    Opin = torch.empty_like(Lpin).pin_memory()
     if world == 1:
-        Lpin = torch.from_numpy(Lh).pin_memory()
-        Opin = torch.empty_like(Lpin).pin_memory()
         Ln, On = Lpin.numpy(), Opin.numpy()
         api.apply_F(ctx, Ln, out=On)  # warm
         torch.cuda.synchronize()
@@ -639,16 +629,12 @@ def run_ours(args, rank, world):
                "api": "api.apply_F / pit_apply_F (host buffers)"}
     else:
         # sharded public API: host shard in, halo over NCCL, host shard out
-        ops = ShardedOperators(backend, n_global)
-        assert ops.shard.first == first and ops.shard.count == count
-        Lpin = torch.from_numpy(Lh).pin_memory()
-        Opin = torch.empty_like(Lpin).pin_memory()
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             dL = Lpin.to("cuda", non_blocking=True)
-            o = ops.apply_F(dL)
+            o = sc.apply_F(dL, stream)
             Opin.copy_(o, non_blocking=True)
             torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
@@ -656,7 +642,8 @@ def run_ours(args, rank, world):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": gp_total * args.steps / float(tt.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(Lh.nbytes), "d2h_bytes_per_step": int(Lh.nbytes),
-               "api": "distributed.ShardedOperators.apply_F (host shards)"}
+               "api": "distributed.ShardedContext.apply_F (pit_sharded_apply_F_device, "
+                      "host shards)"}
 
     # ---- roofline: FP64 pipe (measured in-run) ---------------------------
     peak = C.c_double()
@@ -672,6 +659,9 @@ def run_ours(args, rank, world):
             traffic = None
 
     if rank != 0:
+        if sc is not None:
+            sc.detach()
+            comm.close()
         ctx.close()
         return
     line = {
@@ -684,7 +674,9 @@ def run_ours(args, rank, world):
         "kernel_layout": {"points_per_thread": api.step_coefficients(p)[0].mpt,
                           "warps_per_slab": api.step_coefficients(p)[0].warps},
         "e2e": e2e,
-        "gpu_launches": args.steps,  # one slab_kernel launch per apply_F
+        # one slab_kernel launch per apply_F (two when sharded: the
+        # interior slabs and, after the halo, the boundary slab)
+        "gpu_launches": args.steps * (2 if world > 1 and rank > 0 else 1),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
                      "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": traffic,
                      "algorithmic": f"{FLOPS_PER_GP_STEP} flop per gridpoint-step x "
@@ -705,6 +697,9 @@ def run_ours(args, rank, world):
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
+    if sc is not None:
+        sc.detach()
+        comm.close()
     ctx.close()
 
 

@@ -225,6 +225,23 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   return v;
 }
 
+// Overlapped sweep: spin until a producer CTA published ready[g] = epoch;
+// never hang the device on a lost producer: after 20 s report the slab as
+// failed and go on.
+__device__ __noinline__ void wait_ready(const int* flag, int epoch, int* status, int slab) {
+  long long t0 = -1;
+  while (ld_acquire(flag) != epoch) {
+    long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t0 < 0) t0 = now;
+    if (now - t0 > 20000000000LL) {
+      atomicMin(status, slab);
+      return;
+    }
+    __nanosleep(128);
+  }
+}
+
 // Host-buffer pipelining (SlabArgs::in_ready / out_done): wait until the
 // chunk holding output block g (and so input blocks g-1, g) has landed.
 __device__ __noinline__ void wait_input(const SlabArgs& A, int b, int tid) {
@@ -249,7 +266,18 @@ __device__ __noinline__ void wait_input(const SlabArgs& A, int b, int tid) {
 }
 // ... and publish block g (plus block 0 for CTA 0) once every thread's
 // output stores are globally visible.
+__device__ __forceinline__ void publish_ready(const SlabArgs& A, int b, int tid) {
+  if (A.ready == nullptr) return;
+  __syncthreads();  // every thread's output stores precede thread 0's release
+  if (tid == 0) {
+    __threadfence();
+    st_release(A.ready + b + A.block_shift, A.epoch);
+    if (b == 0 && A.out0 != nullptr) st_release(A.ready, A.epoch);
+  }
+}
+
 __device__ __noinline__ void signal_output(const SlabArgs& A, int b, int tid) {
+  publish_ready(A, b, tid);
   if (A.out_done == nullptr) return;
   __threadfence_system();
   __syncthreads();
@@ -605,6 +633,9 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // overlapped with the producing fine batch: the start block must be out
+  if (tid == 0 && A.ready != nullptr)
+    wait_ready(A.ready + A.ready_shift - 1, A.epoch, A.status, A.slab0);
   __syncthreads();  // the only CTA-wide barrier
 
   if (io) {
@@ -615,6 +646,12 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     auto fill = [&](int b) {  // buffer fill_slot is free: V_b in (or just released)
       uint64_t* bar = &vfull[fill_slot];
       unsigned char* buf = base + fill_slot * buf_bytes;
+      if (A.V && A.ready != nullptr) {
+        wait_ready(A.ready + b + A.ready_shift, A.epoch, A.status, A.slab0 + b);
+        // the producer's generic-proxy stores, acquired above, before the
+        // async-proxy (TMA) read of the same block
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      }
       if (A.V) {
         mbar_arrive_expect_tx(bar, bytes);
         for (int r = 0; r < X.rows; r += X.box_rows)
@@ -652,6 +689,13 @@ __global__ void __launch_bounds__(S::T + 32, 1)
 
   double y[S::NC][S::SUB];
   load_field<S>(y, A.start, tid, M);
+  if (A.W0 != nullptr) {  // W_0 = V_0
+#pragma unroll
+    for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+      for (int j = 0; j < S::SUB; ++j)
+        if (S::point(tid, c, j) < M) A.W0[S::point(tid, c, j)] = y[c][j];
+  }
   const StepLane L = step_lane<S>(P, *sh, tid);
   // the table-form correction vector of the thread's points in registers
   // (coarse layouts of few points per thread; others read it from smem)
@@ -768,7 +812,7 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A0, int ctas, cudaS
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
       return e;
-    const int slots = per_sm * sms;
+    const int slots = per_sm * (sms - (A0.reserve_sms < sms ? A0.reserve_sms : 0));
     A.pieces = A0.pieces > 0 ? A0.pieces : choose_pieces(ctas, slots);
     if (A.pieces > kMaxPieces) A.pieces = kMaxPieces;
     if (A.pieces > P.steps) A.pieces = P.steps;
@@ -883,6 +927,7 @@ cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t s
       }
   const size_t smem = fixed + (size_t)X.nbuf * buf_bytes;
   static const bool legacy = std::getenv("PIT_SWEEP_LEGACY") != nullptr;  // A/B knob
+  if (A.ready != nullptr && (!tma || legacy)) return cudaErrorNotSupported;  // needs the I/O warp
   auto k = tma ? (legacy ? sweep_kernel<S, SRC, true> : sweep_io_kernel<S, SRC>)
                : sweep_kernel<S, SRC, false>;
   if (smem > 48 * 1024) {

@@ -65,6 +65,14 @@ struct SlabArgs {
   int chunk_blocks;
   int block_shift;
   unsigned long long* busy_ns;  // DevStatus::busy_ns (nullptr: not measured)
+  // Overlap with the coarse sweep (apply_GF): after its output block g
+  // (global; block 0 too, written by CTA 0) is stored, a CTA publishes
+  // ready[g] = epoch (release), which the concurrently running K2 acquires
+  // before it reads V_g.  reserve_sms: the persistent grid leaves that many
+  // SMs' worth of slots free for K2.
+  int* ready;
+  int epoch;
+  int reserve_sms;
 };
 
 // K2: one persistent CTA running the sequential sweep
@@ -77,6 +85,14 @@ struct SweepArgs {
   int slab0;
   int* status;
   double* fail_info;  // DevStatus::fail, written with the failing slab
+  // Overlap with the fine batch producing V (apply_GF, TMA sweep only):
+  // V_b (global block b + ready_shift) and `start` (block ready_shift - 1)
+  // are read only once ready[...] == epoch; W0 != nullptr: the start block is
+  // also copied to W0 (W_0 = V_0, block_system.cpp:181)
+  const int* ready;
+  int epoch;
+  int ready_shift;
+  double* W0;
 };
 
 constexpr int kMaxPieces = 64;
