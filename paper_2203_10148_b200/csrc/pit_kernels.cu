@@ -294,8 +294,11 @@ template <class S, bool SRC>
 __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin))
     slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
-  double* s_zc = reinterpret_cast<double*>(sh + 1);
+  // static, so every access is a direct shared-window address (a pointer
+  // into the dynamic window is converted through SR_CgaCtaId each time)
+  __shared__ StepShared<S::NSEG, S::WARPS> sh_s;
+  auto* sh = &sh_s;
+  double* s_zc = reinterpret_cast<double*>(smem_raw);
   __shared__ int s_unit;
   const int tid = threadIdx.x;
   const int M = P.M;
@@ -435,8 +438,9 @@ __global__ void __launch_bounds__(S::T, 1)
                  const __grid_constant__ SweepTma X) {
   constexpr int STAGE_SLOT = S::T * (S::MPT + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
-  double* s_zc = reinterpret_cast<double*>(sh + 1);
+  __shared__ StepShared<S::NSEG, S::WARPS> sh_s;
+  auto* sh = &sh_s;
+  double* s_zc = reinterpret_cast<double*>(smem_raw);
   unsigned char* after = reinterpret_cast<unsigned char*>(s_zc + zc_smem_len<S>(P.narrow));
   // TMA: two 1024-byte aligned slab buffers of M doubles; slot path: two
   // odd-pitch buffers
@@ -609,8 +613,9 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     sweep_io_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A,
                     const __grid_constant__ SweepTma X) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto* sh = reinterpret_cast<StepShared<S::NSEG, S::WARPS>*>(smem_raw);
-  double* s_zc = reinterpret_cast<double*>(sh + 1);
+  __shared__ StepShared<S::NSEG, S::WARPS> sh_s;
+  auto* sh = &sh_s;
+  double* s_zc = reinterpret_cast<double*>(smem_raw);
   // slab buffers 1024-byte aligned (128-byte swizzle atoms); offsets taken in
   // the shared window so the compiler keeps LDS/STS (not generic LD/ST)
   const unsigned s0 = smem_u32(smem_raw);
@@ -707,6 +712,7 @@ __global__ void __launch_bounds__(S::T + 32, 1)
     for (int j = 0; j < S::SUB; ++j) zreg[c][j] = P.narrow || !kZreg ? 0.0 : s_zc[S::slot(tid, c, j)];
   int slot = 0;
   unsigned phase = 0;
+  const uint32_t base_s = smem_u32(base), vfull_s = smem_u32(vfull), wfull_s = smem_u32(wfull);
   // non-finite detection off the step chain: pz accumulates fma(w, 0, pz)
   // over every W value (0 while all are finite, NaN for good after an inf
   // or nan); it is tested one slab later, when its FMAs have long retired,
@@ -725,25 +731,25 @@ __global__ void __launch_bounds__(S::T + 32, 1)
 #ifdef PIT_PHASE_TIMING
     const long long sw1 = clock64();
 #endif
-    unsigned char* buf = base + slot * buf_bytes;
-    mbar_wait(&vfull[slot], phase);  // V_b landed / buffer free
+    const uint32_t buf = base_s + (uint32_t)(slot * buf_bytes);
+    mbar_wait_s(vfull_s + 8u * slot, phase);  // V_b landed / buffer free
 #pragma unroll
     for (int c = 0; c < S::NC; ++c)
 #pragma unroll
       for (int j = 0; j < S::SUB; j += 2) {
         const int pnt = S::point(tid, c, j);
         if (pnt < M) {
-          double2* q = reinterpret_cast<double2*>(buf + swz_off<S>(pnt));
+          const uint32_t q = buf + (uint32_t)swz_off<S>(pnt);
           if (A.V) {
-            const double2 v = *q;
+            const double2 v = lds_v2(q);
             y[c][j] = y[c][j] + v.x;
             y[c][j + 1] = y[c][j + 1] + v.y;
           }
-          *q = make_double2(y[c][j], y[c][j + 1]);
+          sts_v2(q, y[c][j], y[c][j + 1]);
         }
       }
     fence_proxy_async_smem();
-    mbar_arrive(&wfull[slot]);
+    mbar_arrive_s(wfull_s + 8u * slot);
     if (++slot == nbuf) {
       slot = 0;
       phase ^= 1u;
@@ -795,8 +801,7 @@ inline int choose_pieces(int nblk, int slots) {
 
 template <class S, bool SRC>
 cudaError_t slab_launch(const StepParams& P, const SlabArgs& A0, int ctas, cudaStream_t st) {
-  const size_t smem =
-      sizeof(StepShared<S::NSEG, S::WARPS>) + sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
+  const size_t smem = sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
   auto k = slab_kernel<S, SRC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -837,8 +842,7 @@ cudaError_t slab_launch(const StepParams& P, const SlabArgs& A0, int ctas, cudaS
 // "worker count" for the executor's timing report (executor.cpp:156-171).
 template <class S, bool SRC>
 cudaError_t slab_slots_t(const StepParams& P, int* slots) {
-  const size_t smem =
-      sizeof(StepShared<S::NSEG, S::WARPS>) + sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
+  const size_t smem = sizeof(double) * (size_t)zc_smem_len<S>(P.narrow);
   auto k = slab_kernel<S, SRC>;
   cudaError_t e;
   if (smem > 48 * 1024 &&
@@ -915,13 +919,13 @@ cudaError_t sweep_launch(const StepParams& P, const SweepArgs& A, cudaStream_t s
   }
   const size_t buf_bytes =
       tma ? (size_t)P.M * sizeof(double) : (size_t)S::T * (S::MPT + 1) * sizeof(double);
-  const size_t fixed = sizeof(StepShared<S::NSEG, S::WARPS>) +
-                       sizeof(double) * (size_t)zc_smem_len<S>(P.narrow) + 1024 +
+  const size_t fixed = sizeof(double) * (size_t)zc_smem_len<S>(P.narrow) + 1024 +
                        8 * sizeof(uint64_t);
+  const size_t budget = 227 * 1024 - sizeof(StepShared<S::NSEG, S::WARPS>);  // static part
   X.nbuf = 2;
   if (tma)
     for (int n = 4; n >= 3; --n)
-      if (fixed + n * buf_bytes <= 227 * 1024) {
+      if (fixed + n * buf_bytes <= budget) {
         X.nbuf = n;
         break;
       }
@@ -1068,7 +1072,7 @@ int ew_grid(size_t n) {
   X(16, 1, 1, 16) X(16, 1, 1, 32) X(32, 2, 1, 4) X(32, 2, 1, 8) X(32, 1, 2, 4) X(32, 2, 2, 4) \
   X(64, 2, 2, 1) X(64, 2, 2, 2) X(64, 2, 2, 4) X(64, 4, 1, 2) X(64, 1, 4, 2) X(64, 4, 1, 1)  \
   X(64, 4, 1, 4) X(64, 1, 2, 2) X(32, 2, 2, 8) X(64, 2, 2, 8) X(16, 2, 1, 16) X(16, 2, 2, 8)   \
-  X(64, 4, 1, 8)
+  X(64, 4, 1, 8) X(16, 2, 1, 8) X(16, 4, 1, 8) X(32, 4, 1, 8) X(32, 2, 1, 8) X(32, 4, 1, 4)
 
 #define PIT_SHAPE(MP, NU, NS, W) Shape<(MP) / ((NU) * (NS)), NU, NS, W>
 
@@ -1119,7 +1123,8 @@ cudaError_t launch_sweep(int mpt, int nsub, int nseg, int warps, bool src, const
 #define X(MP, NU, NS, W)                                   \
   if (mpt == MP && nsub == NU && nseg == NS && warps == W) \
     return sweep_launch<Shape<(MP) / ((NU) * (NS)), NU, NS, W, 5>, false>(P, A, st);
-    X(8, 1, 1, 8) X(16, 1, 1, 8) X(16, 1, 1, 16)
+    X(8, 1, 1, 8) X(16, 1, 1, 8) X(16, 1, 1, 16) X(16, 2, 1, 8) X(16, 4, 1, 8) X(32, 4, 1, 8)
+    X(32, 2, 1, 8) X(16, 2, 1, 16) X(32, 4, 1, 4)
 #undef X
   }
 #define X(MP, NU, NS, W)                                                        \
