@@ -137,6 +137,14 @@ struct pit_context {
   cudaStream_t gf_stream = nullptr;
   cudaEvent_t ev_gf[5] = {};
   int gf_overlap = -1;  // -1 untested, 0 off, 1 on
+  // device-resident solver loop (pitsbicg_device_loop): the scalars, the
+  // skip flag every launch of an iteration carries, timing events
+  SolverScalars* d_sc = nullptr;
+  SolverScalars* h_sc = nullptr;  // pinned
+  const int* skip = nullptr;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<size_t, int>> ev_spans;  // (first event index, role)
   unsigned long long busy_mark = 0;  // busy_ns already charged to RunStats
   // SolveOptions::iterate_observer (solvers.hpp:54): called after every
   // history row with the iterate the row describes (host copy)
@@ -486,6 +494,7 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
   A.ready = ready;
   A.epoch = epoch;
   A.reserve_sms = reserve_sms;
+  A.skip = ctx->skip;
   A.mode = mode;
   A.in_ready = in_ready;
   A.out_done = out_done;
@@ -568,6 +577,7 @@ int launch_sweep_any(pit_context* ctx, int role, bool src, const SweepArgs& A, c
     S.mode = kPropagate;
     S.slab0 = A.slab0 + s;
     S.status = A.status;
+    S.skip = A.skip;
     CUDA_TRY(launch_explicit2d(ctx->lay2, ex2_params(ctx), S, 1, st));
   }
   return PIT_OK;
@@ -579,6 +589,7 @@ int run_sweep(pit_context* ctx, int role, bool with_source, const double* V, con
   const size_t M = ctx->M;
   SweepArgs A{};
   bind_status(ctx, &A);
+  A.skip = ctx->skip;
   if (first == 0) {
     // block 0: W_0 = V_0 (G^-1) — the caller seeds block 0 otherwise
     if (add_v && V != W)
@@ -883,6 +894,9 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_ref_diff);
   cudaFree(ctx->d_halo);
   cudaFree(ctx->d_ready);
+  cudaFree(ctx->d_sc);
+  if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->gf_stream) cudaStreamDestroy(ctx->gf_stream);
   for (auto& e : ctx->ev_gf)
     if (e) cudaEventDestroy(e);
@@ -1768,7 +1782,44 @@ bool gf_overlap_ok(pit_context* ctx) {
   return ctx->gf_overlap == 1;
 }
 
-int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_run_stats* st) {
+// timing spans of a deferred (device-loop) iteration, read after its sync
+cudaEvent_t ev_take(pit_context* ctx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_used++];
+}
+int span_begin(pit_context* ctx, int role, cudaStream_t st) {
+  ctx->ev_spans.emplace_back(ctx->ev_used, role);
+  cudaEvent_t e = ev_take(ctx);
+  if (!e) return set_err(PIT_ERR_CUDA, "event pool");
+  CUDA_TRY(cudaEventRecord(e, st));
+  return PIT_OK;
+}
+int span_end(pit_context* ctx, cudaStream_t st) {
+  cudaEvent_t e = ev_take(ctx);
+  if (!e) return set_err(PIT_ERR_CUDA, "event pool");
+  CUDA_TRY(cudaEventRecord(e, st));
+  return PIT_OK;
+}
+void spans_collect(pit_context* ctx, pit_run_stats* st) {
+  for (const auto& sp : ctx->ev_spans) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev_pool[sp.first], ctx->ev_pool[sp.first + 1]);
+    if (sp.second == PIT_FINE)
+      st->fine_parallel_ms += ms;
+    else
+      st->coarse_sequential_ms += ms;
+  }
+  cudaGetLastError();
+  ctx->ev_spans.clear();
+  ctx->ev_used = 0;
+}
+
+int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_run_stats* st,
+                        bool deferred = false) {
   pit_context* ctx = R.ctx;
   const size_t M = ctx->M;
   if (!ctx->d_ready) {
@@ -1784,7 +1835,10 @@ int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_r
   const auto t0 = Clock::now();
   CUDA_TRY(cudaEventRecord(ctx->ev_gf[0], R.st));  // x ready, tmp and out free
   CUDA_TRY(cudaStreamWaitEvent(ctx->gf_stream, ctx->ev_gf[0], 0));
-  CUDA_TRY(cudaEventRecord(ctx->ev_gf[1], R.st));
+  if (deferred)
+    PIT_TRY(span_begin(ctx, PIT_FINE, R.st));
+  else
+    CUDA_TRY(cudaEventRecord(ctx->ev_gf[1], R.st));
   // one CTA per slab in launch order, not piece scheduling: the first wave's
   // blocks are then out after one slab's latency, while pieces would hold
   // every block back to the last piece round (c2 TTT 39.0 vs 42.4 ms)
@@ -1794,6 +1848,7 @@ int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_r
                                  nullptr, nullptr, 0, ctx->d_ready, epoch, 1);
   ctx->pieces = saved_pieces;
   PIT_TRY(rc1);
+  if (deferred) PIT_TRY(span_end(ctx, R.st));
   CUDA_TRY(cudaEventRecord(ctx->ev_gf[2], R.st));
   SweepArgs A{};
   bind_status(ctx, &A);
@@ -1806,7 +1861,11 @@ int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_r
   A.ready = ctx->d_ready;
   A.epoch = epoch;
   A.ready_shift = 1;
-  CUDA_TRY(cudaEventRecord(ctx->ev_gf[3], ctx->gf_stream));
+  A.skip = ctx->skip;
+  if (deferred)
+    PIT_TRY(span_begin(ctx, PIT_COARSE, ctx->gf_stream));
+  else
+    CUDA_TRY(cudaEventRecord(ctx->ev_gf[3], ctx->gf_stream));
   const Role& Rc = ctx->role[PIT_COARSE];
   const cudaError_t le = launch_sweep(Rc.mpt, Rc.nsub, Rc.nseg, Rc.warps, false, Rc.P, A,
                                       ctx->gf_stream);
@@ -1820,8 +1879,10 @@ int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_r
   } else {
     CUDA_TRY(le);
   }
+  if (deferred) PIT_TRY(span_end(ctx, ctx->gf_stream));
   CUDA_TRY(cudaEventRecord(ctx->ev_gf[4], ctx->gf_stream));
   CUDA_TRY(cudaStreamWaitEvent(R.st, ctx->ev_gf[4], 0));
+  if (deferred) return PIT_OK;
   PIT_TRY(check_status(ctx, true));
   PIT_TRY(check_status(ctx, false));
   float k1 = 0.f, k2 = 0.f;
@@ -1963,6 +2024,157 @@ int pitsbicg_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* l
   return finish(PIT_MAX_ITERATIONS);
 }
 
+// G^-1 F x of a device-loop iteration: no status read, timing spans
+int apply_GF_deferred(Run& R, const double* x, double* tmp, double* out) {
+  pit_context* ctx = R.ctx;
+  if (gf_overlap_ok(ctx)) return apply_GF_overlapped(R, x, tmp, out, nullptr, true);
+  PIT_TRY(span_begin(ctx, PIT_FINE, R.st));
+  PIT_TRY(run_slab_batch(ctx, kApplyF, x, nullptr, nullptr, tmp, 0, R.count, R.st));
+  PIT_TRY(span_end(ctx, R.st));
+  PIT_TRY(span_begin(ctx, PIT_COARSE, R.st));
+  PIT_TRY(run_sweep(ctx, PIT_COARSE, false, tmp, nullptr, out, 0, R.count, true, R.st));
+  return span_end(ctx, R.st);
+}
+
+// pitsbicg_solve (src/solvers.cpp:116-220) with the scalar recurrence on the
+// device (single GPU): an iteration's launches are enqueued without waiting
+// — scalars_kernel sums the partials in slab order and takes the reference's
+// branches, setting SolverScalars::stop so that the remaining launches of
+// the iteration skip their work — and the host reads the scalars, the status
+// and the branch once per iteration (instead of after every phase).  The
+// arithmetic, branches and history are those of pitsbicg_dev.
+int pitsbicg_device_loop(Run& R, const pit_solver_config* cfg, bool have_init, double* lam,
+                         double* first_residual_dev, pit_record* rows, int cap,
+                         pit_solve_info* info) {
+  pit_context* ctx = R.ctx;
+  PIT_TRY(ensure_buffers(ctx, R.nl()));
+  if (!ctx->d_sc) {
+    CUDA_TRY(cudaMalloc(&ctx->d_sc, sizeof(SolverScalars)));
+    CUDA_TRY(cudaMallocHost(&ctx->h_sc, sizeof(SolverScalars)));
+  }
+  const int N = ctx->N, M = ctx->M, nb = R.count;
+  const size_t nl = R.nl();
+  double *rhs = ctx->buf[1], *r = ctx->buf[2], *rs = ctx->buf[3], *p = ctx->buf[4],
+         *d = ctx->buf[5], *s = ctx->buf[6], *t = ctx->buf[7], *f = ctx->buf[8];
+  SolverScalars* sc = ctx->d_sc;
+  SolverScalars& hs = *ctx->h_sc;
+  pit_solve_info inf{};
+  inf.min_restart_margin = INFINITY;
+  pit_run_stats& st = inf.stats;
+  Recorder rec{rows, cap, 0, &st, Clock::now(), &R, lam};
+  auto finish = [&](int status) -> int {
+    if (rec.rc) return rec.rc;
+    inf.status = status;
+    inf.total_records = rec.n;
+    inf.record_count = std::min(rec.n, cap);
+    if (info) *info = inf;
+    return PIT_OK;
+  };
+  // the start is pitsbicg_dev's (one host read of ||r|| there)
+  if (!have_init) PIT_TRY(run_initial_guess(R, cfg->initial_guess, lam, &st));
+  PIT_TRY(run_rhs(R, rhs, &st));
+  PIT_TRY(precond_residual(R, lam, rhs, r, &st));
+  if (first_residual_dev) PIT_TRY(run_copy(R, first_residual_dev, r));
+  {
+    const double* A[1] = {r};
+    PIT_TRY(run_dots(R, 1, A, A));
+  }
+  double r_norm = max_sqrt_partials(ctx->h_partials, N, 1, 0);
+  rec(0, r_norm);
+  if (r_norm <= cfg->tolerance) return finish(PIT_CONVERGED);
+  PIT_TRY(run_copy(R, rs, r));
+  PIT_TRY(run_copy(R, p, r));
+  {
+    SolverScalars z{};
+    z.rho = sum_partials(ctx->h_partials, N, 1, 0);  // <r, r~> with r~ = r
+    z.margin = INFINITY;
+    CUDA_TRY(cudaMemcpyAsync(sc, &z, sizeof(z), cudaMemcpyHostToDevice, R.st));
+  }
+  const double tol = cfg->tolerance, eps0 = cfg->restart_tolerance;
+  const long n1 = N - 1;
+  ctx->skip = &sc->stop;
+  struct SkipReset {
+    pit_context* c;
+    ~SkipReset() { c->skip = nullptr; }
+  } skip_reset{ctx};
+  for (int k = 1; k <= cfg->max_iterations; ++k) {
+    CUDA_TRY(cudaMemsetAsync(&sc->flag, 0, 2 * sizeof(int), R.st));  // flag, stop
+    PIT_TRY(apply_GF_deferred(R, p, f, d));
+    {
+      const double* A[1] = {d};
+      const double* B[1] = {rs};
+      CUDA_TRY(launch_dots(M, nb, ctx->weight, 1, A, B, ctx->d_partials, R.st, sc));
+    }
+    CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScAlpha, tol, eps0, R.st));
+    CUDA_TRY(launch_update_s(M, nb, ctx->weight, 0.0, r, d, s, ctx->d_partials, R.st, sc));
+    CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScSnorm, tol, eps0, R.st));
+    PIT_TRY(apply_GF_deferred(R, s, f, t));
+    {
+      const double* A[2] = {t, t};
+      const double* B[2] = {t, s};
+      CUDA_TRY(launch_dots(M, nb, ctx->weight, 2, A, B, ctx->d_partials, R.st, sc));
+    }
+    CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScOmega, tol, eps0, R.st));
+    CUDA_TRY(launch_update_lr(M, nb, ctx->weight, 0.0, 0.0, p, s, t, rs, lam, r, ctx->d_partials,
+                              R.st, sc));
+    CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScR, tol, eps0, R.st));
+    CUDA_TRY(launch_update_p(nl, 0.0, 0.0, d, r, p, R.st, sc));
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_sc, sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, R.st));
+    // one read per iteration: the scalars and the failing-slab status
+    PIT_TRY(check_status(ctx, true));
+    PIT_TRY(check_status(ctx, false));
+    spans_collect(ctx, &st);
+    {
+      const unsigned long long now = ctx->h_status->busy_ns;
+      st.fine_busy_ms += (double)(now - ctx->busy_mark) * 1e-6;
+      ctx->busy_mark = now;
+    }
+    // counters of the applications the iteration actually ran
+    const int flag = hs.flag;
+    const int applies = (flag == kFlagRestartD || flag == kFlagHalf) ? 1 : 2;
+    st.fine_applications += applies * n1;
+    st.coarse_applications += applies * n1;
+    inf.min_restart_margin = std::min(inf.min_restart_margin, hs.margin);
+    auto restart = [&]() -> int {
+      PIT_TRY(run_copy(R, rs, r));
+      PIT_TRY(run_copy(R, p, r));
+      ++inf.restarts;
+      rec(k, r_norm);
+      // r~ = r: <r, r~> becomes <r, r>
+      const double* A[1] = {r};
+      CUDA_TRY(launch_dots(M, nb, ctx->weight, 1, A, A, ctx->d_partials, R.st));
+      CUDA_TRY(cudaMemsetAsync(&sc->flag, 0, 2 * sizeof(int), R.st));
+      CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScRho, tol, eps0, R.st));
+      return PIT_OK;
+    };
+    switch (flag) {
+      case kFlagRestartD:
+      case kFlagRestartT:
+      case kFlagRestartW:
+        PIT_TRY(restart());
+        continue;
+      case kFlagHalf:
+        CUDA_TRY(launch_axpy(nl, 0.0, p, lam, R.st, &sc->alpha));
+        std::swap(ctx->buf[2], ctx->buf[6]);  // r = move(s)
+        rec(k, hs.s_norm);
+        CUDA_TRY(cudaStreamSynchronize(R.st));
+        return finish(PIT_CONVERGED);
+      default:
+        break;
+    }
+    r_norm = hs.r_norm;
+    rec(k, r_norm);
+    if (flag == kFlagConverged) return finish(PIT_CONVERGED);
+    if (flag == kFlagRestartR) {  // the device already set rho = <r, r>
+      PIT_TRY(run_copy(R, rs, r));
+      PIT_TRY(run_copy(R, p, r));
+      ++inf.restarts;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(R.st));
+  return finish(PIT_MAX_ITERATIONS);
+}
+
 // parareal_solve, src/solvers.cpp:73-114.
 int parareal_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* lam,
                  double* first_residual_dev, pit_record* rows, int cap, pit_solve_info* info) {
@@ -2004,6 +2216,15 @@ int parareal_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* l
   return PIT_OK;
 }
 
+// the device-resident loop on one GPU (PIT_HOST_SCALARS=1: the host loop)
+bool device_loop_ok(const Run& R) {
+  static const bool host = [] {
+    const char* e = std::getenv("PIT_HOST_SCALARS");
+    return e && std::atoi(e) != 0;
+  }();
+  return !R.comm && !host;
+}
+
 int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,
                double* lambda_out, double* first_residual_out, pit_record* records,
                int max_records, pit_solve_info* info) {
@@ -2016,7 +2237,10 @@ int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const 
   if (lambda_init)
     CUDA_TRY(cudaMemcpyAsync(lam, lambda_init, ctx->nm() * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
-  if (which == 0)
+  if (which == 0 && device_loop_ok(R))
+    PIT_TRY(pitsbicg_device_loop(R, cfg, lambda_init != nullptr, lam, first, records, max_records,
+                                 info));
+  else if (which == 0)
     PIT_TRY(pitsbicg_dev(R, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
   else
     PIT_TRY(parareal_dev(R, cfg, lambda_init != nullptr, lam, first, records, max_records, info));
@@ -2039,7 +2263,10 @@ int solve_device(int which, bool sharded, pit_context* ctx, const pit_solver_con
   if (lambda_init_dev && lambda_init_dev != lambda_dev)
     CUDA_TRY(cudaMemcpyAsync(lambda_dev, lambda_init_dev, R.nl() * sizeof(double),
                              cudaMemcpyDeviceToDevice, R.st));
-  if (which == 0)
+  if (which == 0 && device_loop_ok(R))
+    PIT_TRY(pitsbicg_device_loop(R, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
+                                 max_records, info));
+  else if (which == 0)
     PIT_TRY(pitsbicg_dev(R, cfg, lambda_init_dev != nullptr, lambda_dev, nullptr, records,
                          max_records, info));
   else

@@ -293,6 +293,7 @@ __device__ __noinline__ void signal_output(const SlabArgs& A, int b, int tid) {
 template <class S, bool SRC>
 __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin))
     slab_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SlabArgs A) {
+  if (A.skip != nullptr && *A.skip) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // static, so every access is a direct shared-window address (a pointer
   // into the dynamic window is converted through SR_CgaCtaId each time)
@@ -436,6 +437,7 @@ template <class S, bool SRC, bool TMA>
 __global__ void __launch_bounds__(S::T, 1)
     sweep_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A,
                  const __grid_constant__ SweepTma X) {
+  if (A.skip != nullptr && *A.skip) return;
   constexpr int STAGE_SLOT = S::T * (S::MPT + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ StepShared<S::NSEG, S::WARPS> sh_s;
@@ -612,6 +614,7 @@ template <class S, bool SRC>
 __global__ void __launch_bounds__(S::T + 32, 1)
     sweep_io_kernel(const __grid_constant__ StepParams P, const __grid_constant__ SweepArgs A,
                     const __grid_constant__ SweepTma X) {
+  if (A.skip != nullptr && *A.skip) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ StepShared<S::NSEG, S::WARPS> sh_s;
   auto* sh = &sh_s;
@@ -971,7 +974,9 @@ struct DotPtrs {
 
 template <int NP>
 __global__ void __launch_bounds__(kVecThreads) dots_kernel(int M, double weight, DotPtrs ptr,
-                                                           double* __restrict__ partials) {
+                                                           double* __restrict__ partials,
+                                                           const SolverScalars* sc) {
+  if (sc != nullptr && sc->stop) return;
   __shared__ double ws[NP][kVecThreads / 32];
   const size_t off = (size_t)blockIdx.x * M;
   double acc[NP];
@@ -991,7 +996,11 @@ __global__ void __launch_bounds__(kVecThreads) dots_kernel(int M, double weight,
 __global__ void __launch_bounds__(kVecThreads)
     update_s_kernel(int M, double weight, double alpha, const double* __restrict__ r,
                     const double* __restrict__ d, double* __restrict__ s,
-                    double* __restrict__ partials) {
+                    double* __restrict__ partials, const SolverScalars* sc) {
+  if (sc != nullptr) {
+    if (sc->stop) return;
+    alpha = sc->alpha;
+  }
   __shared__ double ws[kVecThreads / 32];
   const size_t off = (size_t)blockIdx.x * M;
   const double na = -alpha;
@@ -1010,7 +1019,12 @@ __global__ void __launch_bounds__(kVecThreads)
                      const double* __restrict__ p, const double* __restrict__ s,
                      const double* __restrict__ t, const double* __restrict__ rs,
                      double* __restrict__ lam, double* __restrict__ r,
-                     double* __restrict__ partials) {
+                     double* __restrict__ partials, const SolverScalars* sc) {
+  if (sc != nullptr) {
+    if (sc->stop) return;
+    alpha = sc->alpha;
+    omega = sc->omega;
+  }
   __shared__ double ws[2][kVecThreads / 32];
   const size_t off = (size_t)blockIdx.x * M;
   const double nw = -omega;
@@ -1035,7 +1049,13 @@ __global__ void __launch_bounds__(kVecThreads)
 }
 
 __global__ void update_p_kernel(size_t n, double omega, double beta, const double* __restrict__ d,
-                                const double* __restrict__ r, double* __restrict__ p) {
+                                const double* __restrict__ r, double* __restrict__ p,
+                                const SolverScalars* sc) {
+  if (sc != nullptr) {
+    if (sc->stop) return;
+    omega = sc->omega;
+    beta = sc->beta;
+  }
   const double nw = -omega;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -1043,7 +1063,8 @@ __global__ void update_p_kernel(size_t n, double omega, double beta, const doubl
 }
 
 __global__ void axpy_kernel(size_t n, double a, const double* __restrict__ x,
-                            double* __restrict__ y) {
+                            double* __restrict__ y, const double* a_dev) {
+  if (a_dev != nullptr) a = *a_dev;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     y[i] = fma(a, x[i], y[i]);
@@ -1053,6 +1074,79 @@ __global__ void add_kernel(size_t n, const double* __restrict__ x, double* __res
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     y[i] = y[i] + x[i];
+}
+
+// One thread: the sums and branch tests of pitsbicg_solve's scalar
+// recurrence in the host loop's exact order (sum_partials / max_sqrt_partials
+// in pit_capi.cu, i.e. block_inner_product / block_norm_n_inf).
+__global__ void scalars_kernel(SolverScalars* sc, const double* __restrict__ h, int N, int phase,
+                               double tol, double eps0) {
+  if (sc->stop) return;
+  const int np = (phase == kScOmega || phase == kScR) ? 2 : 1;
+  double s0 = 0.0, s1 = 0.0, w = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double a = h[(size_t)n * np];
+    s0 += a;
+    const double v = sqrt(a);
+    w = (w < v) ? v : w;  // std::max(w, v)
+    if (np == 2) s1 += h[(size_t)n * np + 1];
+  }
+  switch (phase) {
+    case kScRho:
+      sc->rho = s0;
+      break;
+    case kScAlpha:
+      sc->d_dot = s0;
+      if (fabs(s0) < 1e-300) {
+        sc->flag = kFlagRestartD;
+        sc->stop = 1;
+      } else {
+        sc->alpha = sc->rho / s0;
+      }
+      break;
+    case kScSnorm:
+      sc->s_norm = w;
+      if (w <= tol) {
+        sc->flag = kFlagHalf;
+        sc->stop = 1;
+      }
+      break;
+    case kScOmega:
+      sc->tt = s0;
+      sc->ts = s1;
+      if (s0 < 1e-300) {
+        sc->flag = kFlagRestartT;
+        sc->stop = 1;
+      } else {
+        sc->omega = s1 / s0;
+        if (fabs(sc->omega) < 1e-300) {
+          sc->flag = kFlagRestartW;
+          sc->stop = 1;
+        }
+      }
+      break;
+    case kScR: {
+      sc->r_norm = w;
+      sc->rr = s0;
+      sc->r_dot = s1;
+      if (w <= tol) {
+        sc->flag = kFlagConverged;
+        sc->stop = 1;
+        break;
+      }
+      const double m = fabs(s1) / eps0;
+      sc->margin = sc->margin < m ? sc->margin : m;
+      if (fabs(s1) <= eps0) {
+        sc->flag = kFlagRestartR;
+        sc->stop = 1;
+        sc->rho = s0;
+      } else {
+        sc->beta = (sc->alpha / sc->omega) * (s1 / sc->rho);
+        sc->rho = s1;
+      }
+      break;
+    }
+  }
 }
 
 int ew_grid(size_t n) {
@@ -1178,7 +1272,8 @@ cudaError_t measure_fp64_peak(double* tflops) {
 }
 
 cudaError_t launch_dots(int M, int blocks, double weight, int np, const double* const* a,
-                        const double* const* b, double* partials, cudaStream_t st) {
+                        const double* const* b, double* partials, cudaStream_t st,
+                        const SolverScalars* sc) {
   if (blocks <= 0) return cudaSuccess;
   DotPtrs p{};
   for (int k = 0; k < np; ++k) {
@@ -1186,40 +1281,49 @@ cudaError_t launch_dots(int M, int blocks, double weight, int np, const double* 
     p.b[k] = b[k];
   }
   switch (np) {
-    case 1: dots_kernel<1><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials); break;
-    case 2: dots_kernel<2><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials); break;
-    case 3: dots_kernel<3><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials); break;
+    case 1: dots_kernel<1><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials, sc); break;
+    case 2: dots_kernel<2><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials, sc); break;
+    case 3: dots_kernel<3><<<blocks, kVecThreads, 0, st>>>(M, weight, p, partials, sc); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_s(int M, int blocks, double weight, double alpha, const double* r,
-                            const double* d, double* s, double* partials, cudaStream_t st) {
+                            const double* d, double* s, double* partials, cudaStream_t st,
+                            const SolverScalars* sc) {
   if (blocks <= 0) return cudaSuccess;
-  update_s_kernel<<<blocks, kVecThreads, 0, st>>>(M, weight, alpha, r, d, s, partials);
+  update_s_kernel<<<blocks, kVecThreads, 0, st>>>(M, weight, alpha, r, d, s, partials, sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_lr(int M, int blocks, double weight, double alpha, double omega,
                              const double* p, const double* s, const double* t, const double* rs,
-                             double* lam, double* r, double* partials, cudaStream_t st) {
+                             double* lam, double* r, double* partials, cudaStream_t st,
+                             const SolverScalars* sc) {
   if (blocks <= 0) return cudaSuccess;
   update_lr_kernel<<<blocks, kVecThreads, 0, st>>>(M, weight, alpha, omega, p, s, t, rs, lam, r,
-                                                   partials);
+                                                   partials, sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_p(size_t n, double omega, double beta, const double* d, const double* r,
-                            double* p, cudaStream_t st) {
+                            double* p, cudaStream_t st, const SolverScalars* sc) {
   if (!n) return cudaSuccess;
-  update_p_kernel<<<ew_grid(n), 256, 0, st>>>(n, omega, beta, d, r, p);
+  update_p_kernel<<<ew_grid(n), 256, 0, st>>>(n, omega, beta, d, r, p, sc);
   return cudaGetLastError();
 }
 
-cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st) {
+cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st,
+                        const double* a_dev) {
   if (!n) return cudaSuccess;
-  axpy_kernel<<<ew_grid(n), 256, 0, st>>>(n, a, x, y);
+  axpy_kernel<<<ew_grid(n), 256, 0, st>>>(n, a, x, y, a_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scalars(SolverScalars* sc, const double* partials, int N, int phase, double tol,
+                           double eps0, cudaStream_t st) {
+  scalars_kernel<<<1, 1, 0, st>>>(sc, partials, N, phase, tol, eps0);
   return cudaGetLastError();
 }
 

@@ -73,6 +73,9 @@ struct SlabArgs {
   int* ready;
   int epoch;
   int reserve_sms;
+  // device-resident solver loop: the batch is skipped when *skip != 0 (a
+  // branch of the iteration was taken by an earlier scalar kernel)
+  const int* skip;
 };
 
 // K2: one persistent CTA running the sequential sweep
@@ -93,6 +96,7 @@ struct SweepArgs {
   int epoch;
   int ready_shift;
   double* W0;
+  const int* skip;  // as SlabArgs::skip
 };
 
 constexpr int kMaxPieces = 64;
@@ -106,6 +110,27 @@ struct __align__(64) SweepTma {
   int box_rows;          // rows per TMA box (divides rows, <= 256)
   int nbuf;              // slab buffers (3 when shared memory allows, else 2)
 };
+
+// The BiCGStab scalars of pitsbicg_solve (src/solvers.cpp:151-214) kept on
+// the device: one thread sums the per-block partials in slab order, exactly
+// as the host loop does, and sets the branch the reference would take.
+struct SolverScalars {
+  double rho, d_dot, alpha, s_norm, tt, ts, omega, r_norm, rr, r_dot, beta, margin;
+  int flag;  // ScalarFlag
+  int stop;  // != 0: the rest of the iteration's kernels skip their work
+};
+enum ScalarPhase { kScRho = 0, kScAlpha = 1, kScSnorm = 2, kScOmega = 3, kScR = 4 };
+enum ScalarFlag {
+  kFlagNone = 0,
+  kFlagRestartD = 1,    // |<d, r~>| < 1e-300        (solvers.cpp:161-165)
+  kFlagHalf = 2,        // ||s|| <= tol: half step   (171-178)
+  kFlagRestartT = 3,    // <t, t> < 1e-300           (181-185)
+  kFlagRestartW = 4,    // |omega| < 1e-300          (187-190)
+  kFlagConverged = 5,   // ||r|| <= tol              (198-201)
+  kFlagRestartR = 6     // |<r, r~>| <= eps0         (203-209)
+};
+cudaError_t launch_scalars(SolverScalars* sc, const double* partials, int N, int phase, double tol,
+                           double eps0, cudaStream_t st);
 
 // Launchers; return cudaErrorInvalidConfiguration for an uncompiled layout.
 cudaError_t launch_slab(int mpt, int nsub, int nseg, int warps, bool src, const StepParams& P,
@@ -121,20 +146,26 @@ cudaError_t slab_slots(int mpt, int nsub, int nseg, int warps, bool src, const S
 constexpr int kVecThreads = 256;
 // partials[b*np + k] = weight * <a_k, b_k> over block b, k < np (np <= 3)
 cudaError_t launch_dots(int M, int blocks, double weight, int np, const double* const* a,
-                        const double* const* b, double* partials, cudaStream_t st);
+                        const double* const* b, double* partials, cudaStream_t st,
+                        const SolverScalars* sc = nullptr);
 // s = r - alpha*d (fma), partials[b] = weight*<s,s>
+// sc != nullptr: alpha (omega, beta) are read from sc and the kernel is
+// skipped when sc->stop is set
 cudaError_t launch_update_s(int M, int blocks, double weight, double alpha, const double* r,
-                            const double* d, double* s, double* partials, cudaStream_t st);
+                            const double* d, double* s, double* partials, cudaStream_t st,
+                            const SolverScalars* sc = nullptr);
 // lam = fma(alpha,p,lam); lam = fma(omega,s,lam); r = fma(-omega,t,s);
 // partials[2b] = weight*<r,r>, partials[2b+1] = weight*<r,rs>
 cudaError_t launch_update_lr(int M, int blocks, double weight, double alpha, double omega,
                              const double* p, const double* s, const double* t, const double* rs,
-                             double* lam, double* r, double* partials, cudaStream_t st);
+                             double* lam, double* r, double* partials, cudaStream_t st,
+                             const SolverScalars* sc = nullptr);
 // p = fma(fma(-omega, d, p), beta, r)
 cudaError_t launch_update_p(size_t n, double omega, double beta, const double* d, const double* r,
-                            double* p, cudaStream_t st);
+                            double* p, cudaStream_t st, const SolverScalars* sc = nullptr);
 // y = fma(a, x, y)
-cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st);
+cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStream_t st,
+                        const double* a_dev = nullptr);
 // y = y + x
 cudaError_t launch_add(size_t n, const double* x, double* y, cudaStream_t st);
 // measured FP64 DFMA throughput of the current device (TFLOP/s)

@@ -95,6 +95,7 @@ __device__ __forceinline__ double ex_update(const Ex2Params& P, double y, double
 template <int TR, int TC, int CL, int WARPS, bool SCALED>
 __global__ void __launch_bounds__(32 * WARPS, 1)
     explicit2d_kernel(const __grid_constant__ Ex2Params P, const __grid_constant__ SlabArgs A) {
+  if (A.skip != nullptr && *A.skip) return;  // device solver loop: branch taken
   using S = Tile2<TR, TC, CL, WARPS>;
   extern __shared__ __align__(16) double sm2[];
   // top(par, w): first row of warp w's tiles (w == WARPS: CTA below's warp 0)
@@ -410,6 +411,7 @@ __device__ __forceinline__ double stencil_S(const double* Ps, int pitch, int k, 
 __global__ void __launch_bounds__(256, 1)
     cg_sweep2d_kernel(const __grid_constant__ Cg2Params P, const __grid_constant__ SweepArgs A,
                       long long* iters) {
+  if (A.skip != nullptr && *A.skip) return;  // device solver loop: branch taken
   constexpr int RM = kCgRowsMax;
   extern __shared__ __align__(16) double smc[];
   cg::cluster_group cl = cg::this_cluster();

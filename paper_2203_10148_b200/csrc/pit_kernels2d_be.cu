@@ -439,6 +439,7 @@ __device__ __forceinline__ void load_block(const Be2Ctx<PPT>& c, Vec<PPT>& dst, 
 template <int PPT>
 __global__ void __launch_bounds__(kBe2Threads, 1)
     be2d_batch_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SlabArgs A) {
+  if (A.skip != nullptr && *A.skip) return;  // device solver loop: branch taken
   extern __shared__ __align__(16) unsigned char smem_raw[];
   long long tb0 = 0;  // busy time of the slab (DevStatus::busy_ns)
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb0));
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
 template <int PPT>
 __global__ void __launch_bounds__(kBe2Threads, 1)
     be2d_sweep_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SweepArgs A) {
+  if (A.skip != nullptr && *A.skip) return;  // device solver loop: branch taken
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Be2Ctx<PPT> c;
   setup<PPT>(c, P, smem_raw);
