@@ -2080,13 +2080,16 @@ int pitsbicg_device_loop(Run& R, const pit_solver_config* cfg, bool have_init, d
     PIT_TRY(run_dots(R, 1, A, A));
   }
   double r_norm = max_sqrt_partials(ctx->h_partials, N, 1, 0);
+  // <r, r~> with r~ = r, read before rec() (whose error_vs_reference reuses
+  // the partials)
+  const double rho0 = sum_partials(ctx->h_partials, N, 1, 0);
   rec(0, r_norm);
   if (r_norm <= cfg->tolerance) return finish(PIT_CONVERGED);
   PIT_TRY(run_copy(R, rs, r));
   PIT_TRY(run_copy(R, p, r));
   {
     SolverScalars z{};
-    z.rho = sum_partials(ctx->h_partials, N, 1, 0);  // <r, r~> with r~ = r
+    z.rho = rho0;
     z.margin = INFINITY;
     CUDA_TRY(cudaMemcpyAsync(sc, &z, sizeof(z), cudaMemcpyHostToDevice, R.st));
   }

@@ -93,3 +93,19 @@ def test_run_stats_busy_time_and_worker_count():
     # 1000 steps (~0.8 ms alone on an SM, a few ms when sharing one)
     assert 0.0 < st.fine_busy_ms <= slots.value * st.fine_parallel_ms
     assert 0.3 < st.fine_busy_ms / st.fine_applications < 5.0
+
+
+def test_reference_rows_do_not_change_the_solve():
+    # SolveOptions::reference adds error_vs_reference to every row; the
+    # iterates and the history must be those of the plain solve
+    for p in (configs.make("c1"), presets.build_problem(presets.make_preset("diffusion"), 8)):
+        tol = 1e-10 if p.__class__.__name__ == "Problem1D" else 1e-8
+        with api.BlockOperatorContext(p) as ctx:
+            plain = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=tol))
+            seq = api.sequential_fine_solve(ctx)
+            withref = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=tol),
+                                         options=api.SolveOptions(reference=seq))
+        assert np.array_equal(plain.solution, withref.solution)
+        assert [(r.k, r.residual_norm) for r in plain.history.records] == \
+            [(r.k, r.residual_norm) for r in withref.history.records]
+        assert all(r.error_vs_reference is not None for r in withref.history.records)
