@@ -2219,13 +2219,18 @@ int parareal_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* l
   return PIT_OK;
 }
 
-// the device-resident loop on one GPU (PIT_HOST_SCALARS=1: the host loop)
+// The device-resident loop on one GPU, where it is measured to pay: launch-
+// bound solves (c1 1.52 -> 1.39 ms); with K2 overlapped on K1 the host loop
+// is faster (c2 36.0 vs 37.3 ms, profiles/r2p_device_loop.txt), so the large
+// overlapped configs keep it.  PIT_HOST_SCALARS=1/0 forces either.
 bool device_loop_ok(const Run& R) {
-  static const bool host = [] {
+  static const int forced = [] {
     const char* e = std::getenv("PIT_HOST_SCALARS");
-    return e && std::atoi(e) != 0;
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
   }();
-  return !R.comm && !host;
+  if (R.comm || forced == 1) return false;
+  if (forced == 0) return true;
+  return !gf_overlap_ok(R.ctx);
 }
 
 int solve_host(int which, pit_context* ctx, const pit_solver_config* cfg, const double* lambda_init,

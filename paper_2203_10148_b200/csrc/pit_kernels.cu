@@ -1076,21 +1076,38 @@ __global__ void add_kernel(size_t n, const double* __restrict__ x, double* __res
     y[i] = y[i] + x[i];
 }
 
-// One thread: the sums and branch tests of pitsbicg_solve's scalar
-// recurrence in the host loop's exact order (sum_partials / max_sqrt_partials
-// in pit_capi.cu, i.e. block_inner_product / block_norm_n_inf).
-__global__ void scalars_kernel(SolverScalars* sc, const double* __restrict__ h, int N, int phase,
-                               double tol, double eps0) {
+// The sums and branch tests of pitsbicg_solve's scalar recurrence in the
+// host loop's exact order (sum_partials / max_sqrt_partials in pit_capi.cu,
+// i.e. block_inner_product / block_norm_n_inf): the CTA stages the partials
+// (and their square roots) in shared memory in chunks, thread 0 runs the
+// sequential sums over them.
+constexpr int kScChunk = 2048;  // blocks per staged chunk
+__global__ void __launch_bounds__(256) scalars_kernel(SolverScalars* sc, const double* __restrict__ h,
+                                                      int N, int phase, double tol, double eps0) {
   if (sc->stop) return;
+  __shared__ double a0[kScChunk], a1[kScChunk], rt[kScChunk];
   const int np = (phase == kScOmega || phase == kScR) ? 2 : 1;
   double s0 = 0.0, s1 = 0.0, w = 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double a = h[(size_t)n * np];
-    s0 += a;
-    const double v = sqrt(a);
-    w = (w < v) ? v : w;  // std::max(w, v)
-    if (np == 2) s1 += h[(size_t)n * np + 1];
+  for (int c0 = 0; c0 < N; c0 += kScChunk) {
+    const int n = N - c0 < kScChunk ? N - c0 : kScChunk;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double a = h[(size_t)(c0 + i) * np];
+      a0[i] = a;
+      rt[i] = sqrt(a);
+      if (np == 2) a1[i] = h[(size_t)(c0 + i) * np + 1];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < n; ++i) {
+        s0 += a0[i];
+        const double v = rt[i];
+        w = (w < v) ? v : w;  // std::max(w, v)
+        if (np == 2) s1 += a1[i];
+      }
+    }
+    __syncthreads();
   }
+  if (threadIdx.x != 0) return;
   switch (phase) {
     case kScRho:
       sc->rho = s0;
@@ -1323,7 +1340,7 @@ cudaError_t launch_axpy(size_t n, double a, const double* x, double* y, cudaStre
 
 cudaError_t launch_scalars(SolverScalars* sc, const double* partials, int N, int phase, double tol,
                            double eps0, cudaStream_t st) {
-  scalars_kernel<<<1, 1, 0, st>>>(sc, partials, N, phase, tol, eps0);
+  scalars_kernel<<<1, 256, 0, st>>>(sc, partials, N, phase, tol, eps0);
   return cudaGetLastError();
 }
 
