@@ -109,3 +109,37 @@ def test_reference_rows_do_not_change_the_solve():
         assert [(r.k, r.residual_norm) for r in plain.history.records] == \
             [(r.k, r.residual_norm) for r in withref.history.records]
         assert all(r.error_vs_reference is not None for r in withref.history.records)
+
+
+@pytest.mark.parametrize("env", [{"PIT_HOST_SCALARS": "1"},
+                                 {"PIT_HOST_SCALARS": "0", "PIT_GF_OVERLAP": "1"},
+                                 {"PIT_HOST_SCALARS": "1", "PIT_GF_OVERLAP": "1"},
+                                 {"PIT_HOST_SCALARS": "0", "PIT_GF_OVERLAP": "0"}])
+def test_solver_loop_variants_bitwise(env, tmp_path):
+    # the host loop, the device-resident loop, each with and without K2
+    # overlapped on K1: the oracle's bits every time (fresh processes: the
+    # switches are read once per process)
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "lam.npz")
+    code = ("import sys; sys.path.insert(0, '.'); import numpy as np; "
+            "from paper_2203_10148_b200 import api, configs; r = {}\n"
+            "for name, n in (('c2', 9), ('c4', 5), ('c1', 16)):\n"
+            "    p = configs.make(name, slabs=n)\n"
+            "    with api.BlockOperatorContext(p) as ctx:\n"
+            "        s = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))\n"
+            "    r[name] = s.solution; r[name + '_rows'] = np.array([(x.k, x.residual_norm, "
+            "x.fine_applications, x.coarse_applications) for x in s.history.records])\n"
+            f"np.savez({out!r}, **r)\n")
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         timeout=300, env={**os.environ, **env})
+    assert res.returncode == 0, res.stdout + res.stderr
+    g = np.load(out)
+    for name, n in (("c2", 9), ("c4", 5), ("c1", 16)):
+        o = OracleProblem(configs.make(name, slabs=n)).solve(1e-10)
+        assert np.array_equal(g[name], o["lam"]), (env, name)
+        assert [tuple(r) for r in g[name + "_rows"].tolist()] == \
+            [tuple(map(float, r)) for r in o["rows"]], (env, name)
