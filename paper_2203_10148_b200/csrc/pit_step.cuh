@@ -195,9 +195,14 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
       for (int s = 0; s < NSEG; ++s) sh.fw[s][warp] = I[s];
     }
     step_sync<S::T>();
-    for (int v = 0; v < warp; ++v)
+    // unrolled with a predicate (not a warp-dependent trip count), so the
+    // loads of all warp totals issue ahead of the fma chain; the same chain
 #pragma unroll
-      for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.p32, Wc[s], sh.fw[s][v]);
+    for (int v = 0; v < WARPS - 1; ++v)
+      if (v < warp) {
+#pragma unroll
+        for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.p32, Wc[s], sh.fw[s][v]);
+      }
     if (NSEG > 1) {
 #pragma unroll
       for (int s = 0; s < NSEG - 1; ++s) Tot[s] = 0.0;
@@ -274,9 +279,12 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
       for (int s = 0; s < NSEG; ++s) sh.bw[s][warp] = I[s];
     }
     step_sync<S::T>();
-    for (int v = WARPS - 1; v > warp; --v)
 #pragma unroll
-      for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.q32, Wc[s], sh.bw[s][v]);
+    for (int v = WARPS - 1; v >= 1; --v)
+      if (v > warp) {
+#pragma unroll
+        for (int s = 0; s < NSEG; ++s) Wc[s] = fma(P.q32, Wc[s], sh.bw[s][v]);
+      }
     if (NSEG > 1) {
 #pragma unroll
       for (int s = 1; s < NSEG; ++s) Tot[s] = 0.0;
