@@ -117,6 +117,9 @@ struct StepShared {
   double bw[NSEG][WARPS > 1 ? WARPS : 1];
   double b;
   double pad;
+  // replicated corner (REPL): thread 0's backward-carry inputs (Ip, the
+  // sub-chunk end values E[1..NSUB-1], its first sub-chunk before pass 2)
+  double corner[48];
   double plane[32], qlane[32];  // p^lane, q^(31-lane)
   double cf[5][32], cb[5][32];  // Kogge-Stone weights, 0 where a lane has no source lane
 };
@@ -273,7 +276,20 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     Wc[s] = 0.0;
   }
   PIT_PHASE(5);
+  // REPL (table-form corner in registers, one segment): instead of thread 0
+  // broadcasting y_0 behind a third barrier, every thread recomputes thread
+  // 0's backward pass-2 chain for its first point from inputs thread 0
+  // publishes before the backward barrier — the same fma sequence, so the
+  // same bits, with no barrier and no wait on warp 0
+  constexpr bool REPL = ZREG && NSEG == 1 && WARPS > 1 && NSUB - 1 + SUB + 1 <= 48;
   if (WARPS > 1) {
+    if (REPL && tid == 0) {
+      sh.corner[0] = Ip[0];
+#pragma unroll
+      for (int u = 1; u < NSUB; ++u) sh.corner[u] = E[u];
+#pragma unroll
+      for (int j = 0; j < SUB; ++j) sh.corner[NSUB + j] = y[0][j];
+    }
     if (lane == 0) {
 #pragma unroll
       for (int s = 0; s < NSEG; ++s) sh.bw[s][warp] = I[s];
@@ -337,9 +353,23 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
       }
     }
   } else {
-    if (tid == 0) sh.b = y[0][0];
-    step_sync<S::T>();
-    const double cc = P.gneg * sh.b;
+    double y0;
+    if (REPL) {
+      double w0 = 0.0;  // warp 0's Wc
+#pragma unroll
+      for (int v = WARPS - 1; v >= 1; --v) w0 = fma(P.q32, w0, sh.bw[0][v]);
+      double R0 = fma(sh.qlane[0], w0, sh.corner[0]);
+#pragma unroll
+      for (int u = NSUB - 1; u >= 1; --u) R0 = fma(P.qS, R0, sh.corner[u]);
+      y0 = fma(P.nu, R0, sh.corner[NSUB + SUB - 1]);
+#pragma unroll
+      for (int j = SUB - 2; j >= 0; --j) y0 = fma(P.nu, y0, sh.corner[NSUB + j]);
+    } else {
+      if (tid == 0) sh.b = y[0][0];
+      step_sync<S::T>();
+      y0 = sh.b;
+    }
+    const double cc = P.gneg * y0;
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       if ((c / NSUB) * S::LSEG + tid * S::CH < P.K0) {
