@@ -720,6 +720,12 @@ __global__ void __launch_bounds__(S::T + 32, 1)
   int slot = 0;
   unsigned phase = 0;
   const uint32_t base_s = smem_u32(base), vfull_s = smem_u32(vfull), wfull_s = smem_u32(wfull);
+  // the thread's swizzled row offsets in a slab buffer (loop invariant)
+  uint32_t swz[S::NC][S::SUB / 2 > 0 ? S::SUB / 2 : 1];
+#pragma unroll
+  for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+    for (int j = 0; j < S::SUB; j += 2) swz[c][j / 2] = (uint32_t)swz_off<S>(S::point(tid, c, j));
   // non-finite detection off the step chain: pz accumulates fma(w, 0, pz)
   // over every W value (0 while all are finite, NaN for good after an inf
   // or nan); it is tested one slab later, when its FMAs have long retired,
@@ -746,7 +752,7 @@ __global__ void __launch_bounds__(S::T + 32, 1)
       for (int j = 0; j < S::SUB; j += 2) {
         const int pnt = S::point(tid, c, j);
         if (pnt < M) {
-          const uint32_t q = buf + (uint32_t)swz_off<S>(pnt);
+          const uint32_t q = buf + swz[c][j / 2];
           if (A.V) {
             const double2 v = lds_v2(q);
             y[c][j] = y[c][j] + v.x;
@@ -762,11 +768,20 @@ __global__ void __launch_bounds__(S::T + 32, 1)
       phase ^= 1u;
     }
     if (bad == 0x7fffffff && !isfinite(pz)) bad = slab - 1;  // blocks up to b-1
+    {
+      // w * 0 is 0 for a finite w and nan otherwise; summed as a tree (warps
+      // issue in order: a 16-deep fma chain here stalled the next step).
+      // Ghost points hold exact zeros.
+      constexpr int NV = S::NC * S::SUB;
+      double q[NV];
 #pragma unroll
-    for (int c = 0; c < S::NC; ++c)
+      for (int i = 0; i < NV; ++i) q[i] = y[i / S::SUB][i % S::SUB] * 0.0;
 #pragma unroll
-      for (int j = 0; j < S::SUB; ++j)
-        if (S::point(tid, c, j) < M) pz = fma(y[c][j], 0.0, pz);
+      for (int w = 1; w < NV; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < NV; i += 2 * w) q[i] = q[i] + q[i + w];
+      pz = pz + q[0];
+    }
 #ifdef PIT_PHASE_TIMING
     if (P.timing && (tid & 31) == 0 && (tid >> 5) < 2) {
       P.timing[(tid >> 5) * 16 + 10] += sw1 - sw0;        // propagation
