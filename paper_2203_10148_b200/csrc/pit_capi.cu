@@ -146,6 +146,13 @@ struct pit_context {
   size_t ev_used = 0;
   std::vector<std::pair<size_t, int>> ev_spans;  // (first event index, role)
   unsigned long long busy_mark = 0;  // busy_ns already charged to RunStats
+  // one BiCGStab iteration of the device loop as a CUDA graph (launch-bound
+  // solves): the instantiated graph, the buffers / tolerances it was captured
+  // with, timing events around its launches; -1 untested, 0 off, 1 on
+  cudaGraphExec_t it_exec = nullptr;
+  std::vector<unsigned long long> it_key;
+  cudaEvent_t ev_it[2] = {};
+  int graph_mode = -1;
   // SolveOptions::iterate_observer (solvers.hpp:54): called after every
   // history row with the iterate the row describes (host copy)
   pit_iterate_observer observer = nullptr;
@@ -406,10 +413,9 @@ void fill_params(const pit_step_coeffs& c, StepParams* P) {
   P->scan_b = c.scan_b;
 }
 
-int check_status(pit_context* ctx, bool fine_batch) {
-  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+// The failure (if any) recorded in the host mirror of DevStatus, as the
+// reference's exception; the copy and the sync are the caller's.
+int eval_status(pit_context* ctx, bool fine_batch) {
   const int bad = fine_batch ? ctx->h_status->slab : ctx->h_status->sweep_slab;
   if (bad != INT_MAX) {
     const double relres = ctx->h_status->fail[0], iters = ctx->h_status->fail[1];
@@ -445,6 +451,13 @@ int check_status(pit_context* ctx, bool fine_batch) {
     return rc;
   }
   return PIT_OK;
+}
+
+int check_status(pit_context* ctx, bool fine_batch) {
+  CUDA_TRY(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return eval_status(ctx, fine_batch);
 }
 
 void bind_status(pit_context* ctx, SlabArgs* A) {
@@ -896,6 +909,9 @@ int pit_context_destroy(pit_context* ctx) {
   cudaFree(ctx->d_ready);
   cudaFree(ctx->d_sc);
   if (ctx->h_sc) cudaFreeHost(ctx->h_sc);
+  if (ctx->it_exec) cudaGraphExecDestroy(ctx->it_exec);
+  for (cudaEvent_t e : ctx->ev_it)
+    if (e) cudaEventDestroy(e);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->gf_stream) cudaStreamDestroy(ctx->gf_stream);
   for (auto& e : ctx->ev_gf)
@@ -2025,15 +2041,28 @@ int pitsbicg_dev(Run& R, const pit_solver_config* cfg, bool have_init, double* l
 }
 
 // G^-1 F x of a device-loop iteration: no status read, timing spans
-int apply_GF_deferred(Run& R, const double* x, double* tmp, double* out) {
+// (spans = false inside a stream capture: no event records)
+int apply_GF_deferred(Run& R, const double* x, double* tmp, double* out, bool spans = true) {
   pit_context* ctx = R.ctx;
   if (gf_overlap_ok(ctx)) return apply_GF_overlapped(R, x, tmp, out, nullptr, true);
-  PIT_TRY(span_begin(ctx, PIT_FINE, R.st));
+  if (spans) PIT_TRY(span_begin(ctx, PIT_FINE, R.st));
   PIT_TRY(run_slab_batch(ctx, kApplyF, x, nullptr, nullptr, tmp, 0, R.count, R.st));
-  PIT_TRY(span_end(ctx, R.st));
-  PIT_TRY(span_begin(ctx, PIT_COARSE, R.st));
+  if (spans) PIT_TRY(span_end(ctx, R.st));
+  if (spans) PIT_TRY(span_begin(ctx, PIT_COARSE, R.st));
   PIT_TRY(run_sweep(ctx, PIT_COARSE, false, tmp, nullptr, out, 0, R.count, true, R.st));
-  return span_end(ctx, R.st);
+  return spans ? span_end(ctx, R.st) : PIT_OK;
+}
+
+// An iteration of the device loop runs as one CUDA graph launch from the
+// second iteration on, where the fine batch and the coarse sweep run back to
+// back on one stream (no K2-on-K1 overlap: that path forks streams), i.e. on
+// the launch-bound solves the device loop serves.  PIT_NO_GRAPH=1 disables it.
+bool iteration_graph_ok(pit_context* ctx) {
+  if (ctx->graph_mode < 0) {
+    const char* e = std::getenv("PIT_NO_GRAPH");
+    ctx->graph_mode = (e && std::atoi(e) != 0) || gf_overlap_ok(ctx) ? 0 : 1;
+  }
+  return ctx->graph_mode == 1;
 }
 
 // pitsbicg_solve (src/solvers.cpp:116-220) with the scalar recurrence on the
@@ -2100,9 +2129,11 @@ int pitsbicg_device_loop(Run& R, const pit_solver_config* cfg, bool have_init, d
     pit_context* c;
     ~SkipReset() { c->skip = nullptr; }
   } skip_reset{ctx};
-  for (int k = 1; k <= cfg->max_iterations; ++k) {
+  // the launches of one iteration (every pointer and scalar argument is the
+  // same in every iteration, so the sequence can be captured once)
+  auto enqueue_iteration = [&](bool spans) -> int {
     CUDA_TRY(cudaMemsetAsync(&sc->flag, 0, 2 * sizeof(int), R.st));  // flag, stop
-    PIT_TRY(apply_GF_deferred(R, p, f, d));
+    PIT_TRY(apply_GF_deferred(R, p, f, d, spans));
     {
       const double* A[1] = {d};
       const double* B[1] = {rs};
@@ -2111,7 +2142,7 @@ int pitsbicg_device_loop(Run& R, const pit_solver_config* cfg, bool have_init, d
     CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScAlpha, tol, eps0, R.st));
     CUDA_TRY(launch_update_s(M, nb, ctx->weight, 0.0, r, d, s, ctx->d_partials, R.st, sc));
     CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScSnorm, tol, eps0, R.st));
-    PIT_TRY(apply_GF_deferred(R, s, f, t));
+    PIT_TRY(apply_GF_deferred(R, s, f, t, spans));
     {
       const double* A[2] = {t, t};
       const double* B[2] = {t, s};
@@ -2123,10 +2154,77 @@ int pitsbicg_device_loop(Run& R, const pit_solver_config* cfg, bool have_init, d
     CUDA_TRY(launch_scalars(sc, ctx->d_partials, N, kScR, tol, eps0, R.st));
     CUDA_TRY(launch_update_p(nl, 0.0, 0.0, d, r, p, R.st, sc));
     CUDA_TRY(cudaMemcpyAsync(ctx->h_sc, sc, sizeof(SolverScalars), cudaMemcpyDeviceToHost, R.st));
-    // one read per iteration: the scalars and the failing-slab status
-    PIT_TRY(check_status(ctx, true));
-    PIT_TRY(check_status(ctx, false));
-    spans_collect(ctx, &st);
+    return PIT_OK;
+  };
+  // graph of an iteration, (re)captured when the buffers or tolerances differ
+  // from the cached instance's; any failure falls back to plain launches
+  auto iteration_graph = [&]() -> cudaGraphExec_t {
+    unsigned long long bits[2];
+    std::memcpy(&bits[0], &tol, 8);
+    std::memcpy(&bits[1], &eps0, 8);
+    const std::vector<unsigned long long> key = {
+        (unsigned long long)(uintptr_t)lam, (unsigned long long)(uintptr_t)r,
+        (unsigned long long)(uintptr_t)rs,  (unsigned long long)(uintptr_t)p,
+        (unsigned long long)(uintptr_t)d,   (unsigned long long)(uintptr_t)s,
+        (unsigned long long)(uintptr_t)t,   (unsigned long long)(uintptr_t)f,
+        (unsigned long long)(uintptr_t)R.st, bits[0], bits[1], (unsigned long long)nb};
+    if (ctx->it_exec && key == ctx->it_key) return ctx->it_exec;
+    if (ctx->it_exec) {
+      cudaGraphExecDestroy(ctx->it_exec);
+      ctx->it_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(R.st, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    int rc = enqueue_iteration(false);
+    if (rc == PIT_OK &&
+        cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                        R.st) != cudaSuccess)
+      rc = PIT_ERR_CUDA;
+    const cudaError_t ce = cudaStreamEndCapture(R.st, &g);
+    if (rc != PIT_OK || ce != cudaSuccess || !g ||
+        cudaGraphInstantiate(&ctx->it_exec, g, 0) != cudaSuccess)
+      ctx->it_exec = nullptr;
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    if (ctx->it_exec) ctx->it_key = key;
+    return ctx->it_exec;
+  };
+  double fine_share = 0.5;  // of an iteration's device time (first, eager iteration)
+  for (int k = 1; k <= cfg->max_iterations; ++k) {
+    cudaGraphExec_t graph = nullptr;
+    if (k > 1 && iteration_graph_ok(ctx)) {
+      graph = iteration_graph();
+      if (!graph) ctx->graph_mode = 0;  // not capturable here: plain launches from now on
+    }
+    if (graph) {
+      if (!ctx->ev_it[0]) {
+        CUDA_TRY(cudaEventCreate(&ctx->ev_it[0]));
+        CUDA_TRY(cudaEventCreate(&ctx->ev_it[1]));
+      }
+      CUDA_TRY(cudaEventRecord(ctx->ev_it[0], R.st));
+      CUDA_TRY(cudaGraphLaunch(graph, R.st));
+      CUDA_TRY(cudaEventRecord(ctx->ev_it[1], R.st));
+      // one wait per iteration: the scalars and the status came with the graph
+      CUDA_TRY(cudaStreamSynchronize(R.st));
+      PIT_TRY(eval_status(ctx, true));
+      PIT_TRY(eval_status(ctx, false));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev_it[0], ctx->ev_it[1]);
+      st.fine_parallel_ms += fine_share * ms;
+      st.coarse_sequential_ms += (1.0 - fine_share) * ms;
+    } else {
+      const double f0 = st.fine_parallel_ms, c0 = st.coarse_sequential_ms;
+      PIT_TRY(enqueue_iteration(true));
+      // one read per iteration: the scalars and the failing-slab status
+      PIT_TRY(check_status(ctx, true));
+      PIT_TRY(eval_status(ctx, false));
+      spans_collect(ctx, &st);
+      const double df = st.fine_parallel_ms - f0, dc = st.coarse_sequential_ms - c0;
+      if (df + dc > 0.0) fine_share = df / (df + dc);
+    }
     {
       const unsigned long long now = ctx->h_status->busy_ns;
       st.fine_busy_ms += (double)(now - ctx->busy_mark) * 1e-6;
