@@ -70,7 +70,7 @@ __device__ __forceinline__ void load_zc(const StepParams& P, double* s_zc, int t
 template <int MPT, int WARPS, bool SRC>
 struct SlabBounds {
   static constexpr int kThreads = 32 * WARPS;
-  static constexpr int kRegs = MPT <= 16 ? 64 : (MPT <= 32 ? 128 : 168);
+  static constexpr int kRegs = MPT <= 8 ? 96 : (MPT <= 16 ? 64 : (MPT <= 32 ? 128 : 168));
   static constexpr int kMin0 = 65536 / (kThreads * kRegs);
   static constexpr int kMin = SRC ? 1 : (kMin0 < 1 ? 1 : (kMin0 > 16 ? 16 : kMin0));
 };
@@ -153,6 +153,40 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
   if (P.timing && blockIdx.x == 0 && (tid & 31) == 0 && (tid >> 5) < 2)
     for (int k = 0; k < 10; ++k) P.timing[(tid >> 5) * 16 + k] += ph_acc[k];
 #endif
+}
+
+// Layouts of few points per thread (the small grids: c1; M <= 1024)
+// have registers to spare and are bound by the step's latency: they run the
+// HOIST form of the step (scan and carry weights in registers) and keep the
+// table-form correction vector in registers too — the same values from
+// registers instead of shared memory, so the same bits.
+template <class S>
+struct SmallLayout {
+  static constexpr bool hoist = S::MPT <= 8;
+  static constexpr bool zreg = hoist && S::WARPS <= 8;
+};
+template <class S>
+__device__ __forceinline__ void load_zreg(double (&zreg)[SmallLayout<S>::zreg ? S::NC : 1][S::SUB],
+                                          const StepParams& P, const double* s_zc, int tid) {
+#pragma unroll
+  for (int c = 0; c < (SmallLayout<S>::zreg ? S::NC : 1); ++c)
+#pragma unroll
+    for (int j = 0; j < S::SUB; ++j)
+      zreg[c][j] = P.narrow || !SmallLayout<S>::zreg ? 0.0 : s_zc[S::slot(tid, c, j)];
+}
+template <class S, bool SRC>
+__device__ __forceinline__ void run_slab_auto(
+    double (&y)[S::NC][S::SUB], const StepParams& P, const StepLane& L,
+    StepShared<S::NSEG, S::WARPS>& sh, const double* s_zc, int tid, int slab, int k0, int k1,
+    const double (&zreg)[SmallLayout<S>::zreg ? S::NC : 1][S::SUB]) {
+  if constexpr (SmallLayout<S>::hoist) {
+    if (SmallLayout<S>::zreg && !P.narrow)
+      run_slab<S, SRC, true, true>(y, P, L, sh, s_zc, tid, slab, k0, k1, zreg);
+    else
+      run_slab<S, SRC, true, false>(y, P, L, sh, s_zc, tid, slab, k0, k1, zreg);
+  } else {
+    run_slab<S, SRC>(y, P, L, sh, s_zc, tid, slab, k0, k1);
+  }
 }
 
 // Piece state in register order (element (c, j) of thread tid at
@@ -323,10 +357,12 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
     const int slab = A.slab0 + b;
     __syncthreads();
     const StepLane L = step_lane<S>(P, *sh, tid);
+    double zreg[SmallLayout<S>::zreg ? S::NC : 1][S::SUB];
+    load_zreg<S>(zreg, P, s_zc, tid);
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     const long long tr0 = global_ns();
 #endif
-    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
+    run_slab_auto<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps, zreg);
     slab_epilogue<S>(y, A, M, tid, b, slab);
     signal_output(A, b, tid);
     if (A.busy_ns != nullptr && tid == 0)
@@ -342,6 +378,8 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
 
   __syncthreads();
   const StepLane L = step_lane<S>(P, *sh, tid);
+  double zreg[SmallLayout<S>::zreg ? S::NC : 1][S::SUB];
+  load_zreg<S>(zreg, P, s_zc, tid);
   const int units = A.pieces * A.nblk;
   int* head = A.sched;       // next queue position to pop
   int* tail = A.sched + 1;   // next push position
@@ -385,7 +423,7 @@ __global__ void __launch_bounds__(S::T, (SlabBounds<S::MPT, S::WARPS, SRC>::kMin
     __syncthreads();
     const long long tr1 = global_ns();
 #endif
-    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, k0, k1);
+    run_slab_auto<S, SRC>(y, P, L, *sh, s_zc, tid, slab, k0, k1, zreg);
 #if defined(PIT_PHASE_TIMING) || defined(PIT_TRACE)
     __syncthreads();
     const long long tr2 = global_ns();
@@ -503,6 +541,8 @@ __global__ void __launch_bounds__(S::T, 1)
   if (A.V)
     for (int b = 0; b < (TMA ? D : 1) && b < A.count; ++b) prefetch(b);
   const StepLane L = step_lane<S>(P, *sh, tid);
+  double zreg[SmallLayout<S>::zreg ? S::NC : 1][S::SUB];
+  load_zreg<S>(zreg, P, s_zc, tid);
   bool ok = true;
   int bad = 0x7fffffff;
   for (int b = 0; b < A.count; ++b) {
@@ -514,7 +554,7 @@ __global__ void __launch_bounds__(S::T, 1)
 #ifdef PIT_PHASE_TIMING
     const long long sw0 = clock64();
 #endif
-    run_slab<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps);
+    run_slab_auto<S, SRC>(y, P, L, *sh, s_zc, tid, slab, 0, P.steps, zreg);
 #ifdef PIT_PHASE_TIMING
     const long long sw1 = clock64();
 #endif

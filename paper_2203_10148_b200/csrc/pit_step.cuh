@@ -364,6 +364,8 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
       y0 = fma(P.nu, R0, sh.corner[NSUB + SUB - 1]);
 #pragma unroll
       for (int j = SUB - 2; j >= 0; --j) y0 = fma(P.nu, y0, sh.corner[NSUB + j]);
+    } else if (WARPS == 1) {
+      y0 = __shfl_sync(kFull, y[0][0], 0);  // one warp: no shared-memory round trip
     } else {
       if (tid == 0) sh.b = y[0][0];
       step_sync<S::T>();
