@@ -61,7 +61,15 @@ enum {
 };
 
 enum { PIT_FINE = 0, PIT_COARSE = 1 };
-enum { PIT_SOURCE_NONE = 0, PIT_SOURCE_SEPARABLE = 1 };
+/* PIT_SOURCE_SEPARABLE: f(t, x_i) = amp sin(omega t + phase) shape[i].
+ * PIT_SOURCE_TABLE: a general SourceFn (include/pit/pde.hpp:13) sampled by the
+ * caller exactly where Propagator::run samples it (src/propagator.cpp:56-63,
+ * the END of every step): source_table_fine[(n*fine_steps + k-1)*M + i] =
+ * f(breakpoint(n) + k*dt_fine, x_i), n < N, k = 1..fine_steps, and
+ * source_table_coarse likewise with the coarse steps (host arrays, copied;
+ * N*steps*M doubles each, so meant for moderate problems).  Each step adds
+ * fl(dt*f) to the state, the reference's rhs.axpy(dt, sample_source(t)). */
+enum { PIT_SOURCE_NONE = 0, PIT_SOURCE_SEPARABLE = 1, PIT_SOURCE_TABLE = 2 };
 enum { PIT_GUESS_COARSE_SWEEP = 0, PIT_GUESS_ZERO = 1 };
 enum { PIT_CONVERGED = 0, PIT_MAX_ITERATIONS = 1 };
 /* fine propagator scheme: backward Euler (the reference's Propagator,
@@ -125,6 +133,9 @@ typedef struct pit_problem_desc {
   int32_t nonsymmetric;
   double fine_tolerance;
   int64_t fine_max_iterations;
+  /* PIT_SOURCE_TABLE (1D): see the enum above */
+  const double* source_table_fine;
+  const double* source_table_coarse;
 } pit_problem_desc;
 
 typedef struct pit_context pit_context;

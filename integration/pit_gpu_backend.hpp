@@ -16,7 +16,8 @@
 //     (assemble_spatial_operator's 2D rows, pde.cpp:66-100, any velocity),
 //     m <= 50 points per axis; both propagators backward Euler with the
 //     reference's inner solvers (CG if op().symmetric(), else BiCGStab);
-//   * a source, if any, separable f(t,x) = amp*sin(omega*t+phase)*g(x),
+//   * a source, if any: the context's own SourceFn (sampled into tables), or
+//     separable f(t,x) = amp*sin(omega*t+phase)*g(x),
 //     described by a SeparableSource (the std::function itself is opaque;
 //     1D only).
 #pragma once
@@ -65,8 +66,16 @@ inline void check(int rc) {
 
 class Backend {
  public:
+  // A context built with a general SourceFn (pde.hpp:13): pass the same
+  // function; it is sampled where Propagator::run samples it
+  // (propagator.cpp:25-47, 56-63) into the C ABI's PIT_SOURCE_TABLE tables
+  // (N * steps * M doubles per propagator).  The Propagator keeps its
+  // SourceFn private, so the context alone cannot supply it.
+  Backend(const BlockOperatorContext& ctx, const SourceFn& source, int device = 0)
+      : Backend(ctx, nullptr, device, &source) {}
+
   explicit Backend(const BlockOperatorContext& ctx, const SeparableSource* source = nullptr,
-                   int device = 0)
+                   int device = 0, const SourceFn* general = nullptr)
       : ctx_(ctx) {
     const SpatialGrid& g = ctx.fine().op().grid();
     // one spatial operator feeds both device propagators: the reference's
@@ -103,8 +112,9 @@ class Backend {
       }
     }
     const double lo = band[0], di = band[1], up = band[2];
-    if (ctx.fine().has_source() && !source)
-      throw std::invalid_argument("pit::gpu::Backend: a source needs a SeparableSource");
+    if (ctx.fine().has_source() && !source && !(general && *general))
+      throw std::invalid_argument(
+          "pit::gpu::Backend: a source needs its SourceFn or a SeparableSource");
     pit_problem_desc d{};
     d.dimension = 1;
     d.interior = g.interior_per_axis();
@@ -125,6 +135,27 @@ class Backend {
       d.source_omega = source->omega;
       d.source_phase = source->phase;
       d.source_shape = source->shape.data();
+    }
+    std::vector<double> tab[2];
+    if (!source && general && *general && ctx.fine().has_source()) {
+      const Propagator* prop[2] = {&ctx.fine(), &ctx.coarse()};
+      for (int r = 0; r < 2; ++r) {
+        const int steps = prop[r]->steps_per_slab();
+        const double dt = prop[r]->internal_dt();
+        tab[r].resize(static_cast<size_t>(d.slab_count) * steps * d.interior);
+        size_t at = 0;
+        for (int n = 0; n < d.slab_count; ++n) {
+          const double t0 = ctx.partition().breakpoint(n);
+          for (int k = 1; k <= steps; ++k)
+            for (int i = 0; i < d.interior; ++i) {
+              const double x[1] = {g.interior_coord(i)};
+              tab[r][at++] = (*general)(t0 + k * dt, x);
+            }
+        }
+      }
+      d.source_kind = PIT_SOURCE_TABLE;
+      d.source_table_fine = tab[0].data();
+      d.source_table_coarse = tab[1].data();
     }
     d.device = device;
     pit_context* c = nullptr;

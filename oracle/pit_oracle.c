@@ -331,6 +331,26 @@ void orc_stepper_propagate(const orc_stepper* s, const double* in, const double*
   free(scratch);
 }
 
+/* General source (PIT_SOURCE_TABLE): tab[k*M + i] = fl(dt * f(t_k, x_i)) is
+ * added before step k, the reference's rhs.axpy(dt, sample_source(t))
+ * (src/propagator.cpp:60-62); unscaled state every step, as with ds. */
+void orc_stepper_propagate_table(const orc_stepper* s, const double* in, const double* tab,
+                                 double* out) {
+  const int T = 32 * s->warps;
+  double* y = (double*)calloc((size_t)s->Mp, sizeof(double));
+  double* scratch = (double*)calloc((size_t)(2 * T + s->warps + 32), sizeof(double));
+  memcpy(y, in, (size_t)s->M * sizeof(double));
+  for (int k = 0; k < s->steps; ++k) {
+    const double* tk = tab + (size_t)k * s->M;
+    for (int i = 0; i < s->M; ++i) y[i] = y[i] + tk[i];
+    chunked_solve(s, y, scratch);
+    for (int i = 0; i < s->M; ++i) y[i] = y[i] * s->inv;
+  }
+  memcpy(out, y, (size_t)s->M * sizeof(double));
+  free(y);
+  free(scratch);
+}
+
 void orc_thomas_propagate(int M, int steps, double band_lo, double band_diag, double band_up,
                           double dt, const double* in, const double* ds, const double* g,
                           double* out) {
@@ -351,6 +371,8 @@ void orc_thomas_propagate(int M, int steps, double band_lo, double band_diag, do
   for (int k = 0; k < steps; ++k) {
     if (ds)
       for (int i = 0; i < M; ++i) y[i] = y[i] + ds[k] * g[i];
+    else if (g) /* ds == NULL, g != NULL: g is a table [steps][M] of fl(dt*f) */
+      for (int i = 0; i < M; ++i) y[i] = y[i] + g[(size_t)k * M + i];
     y[0] = y[0] * iv[0];
     for (int i = 1; i < M; ++i) y[i] = (y[i] - lam * y[i - 1]) * iv[i];
     for (int i = M - 2; i >= 0; --i) y[i] = y[i] - cp[i] * y[i + 1];
@@ -725,12 +747,24 @@ struct orc_1d {
   double* y0;
   double* shape;
   double* ds[2]; /* [N][steps] */
+  double* tab[2]; /* general source: [N][steps][M] fl(dt*f), or NULL */
 };
 
 static int orc_1d_prop(void* user, int role, int with_source, const double* in, int slab,
                        double* out) {
   orc_1d* o = (orc_1d*)user;
   const double* ds = NULL;
+  if (with_source && o->prob.has_source && o->tab[role]) {
+    const double* tab = o->tab[role] + (size_t)slab * o->steps[role] * o->prob.M;
+    if (o->use_thomas)
+      orc_thomas_propagate(o->prob.M, o->steps[role], o->band[0], o->band[1], o->band[2],
+                           o->dt[role], in, NULL, tab, out);
+    else
+      orc_stepper_propagate_table(&o->st[role], in, tab, out);
+    for (int i = 0; i < o->prob.M; ++i)
+      if (!isfinite(out[i])) return -200 - slab;
+    return 0;
+  }
   if (with_source && o->prob.has_source) ds = o->ds[role] + (size_t)slab * o->steps[role];
   if (o->use_thomas)
     orc_thomas_propagate(o->prob.M, o->steps[role], o->band[0], o->band[1], o->band[2],
@@ -795,8 +829,25 @@ orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double 
   return o;
 }
 
+/* General source tables f(t_k, x_i) of both roles ([N][steps][M], the layout
+ * of pit_problem_desc::source_table_*): stored as fl(dt*f). */
+int orc_1d_set_source_tables(orc_1d* o, const double* fine, const double* coarse) {
+  const double* f[2] = {fine, coarse};
+  for (int r = 0; r < 2; ++r) {
+    const size_t n = (size_t)o->N * o->steps[r] * o->prob.M;
+    free(o->tab[r]);
+    o->tab[r] = (double*)malloc(n * sizeof(double));
+    if (!o->tab[r]) return -1;
+    for (size_t i = 0; i < n; ++i) o->tab[r][i] = o->dt[r] * f[r][i];
+  }
+  o->prob.has_source = 1;
+  return 0;
+}
+
 void orc_1d_destroy(orc_1d* o) {
   if (!o) return;
+  free(o->tab[0]);
+  free(o->tab[1]);
   orc_stepper_free(&o->st[0]);
   orc_stepper_free(&o->st[1]);
   free(o->y0);

@@ -85,7 +85,12 @@ void orc_stepper_free(orc_stepper* s);
 void orc_stepper_propagate(const orc_stepper* s, const double* in, const double* ds,
                            const double* g, double* out);
 
-/* Plain Thomas, the textbook algorithm (no chunking, no deferred scaling). */
+/* ... with a general source: tab[k*M + i] = fl(dt*f(t_k, x_i)) */
+void orc_stepper_propagate_table(const orc_stepper* s, const double* in, const double* tab,
+                                 double* out);
+
+/* Plain Thomas, the textbook algorithm (no chunking, no deferred scaling).
+ * ds == NULL and g != NULL: g is a general-source table [steps][M] of fl(dt*f). */
 void orc_thomas_propagate(int M, int steps, double band_lo, double band_diag, double band_up,
                           double dt, const double* in, const double* ds, const double* g,
                           double* out);
@@ -174,6 +179,8 @@ orc_1d* orc_1d_create(int M, double h, double band_lo, double band_diag, double 
                       int has_source, const double* src_shape, double src_amp,
                       double src_omega, double src_phase, int use_thomas, int mode);
 void orc_1d_destroy(orc_1d* o);
+/* general source (PIT_SOURCE_TABLE): f(t_k, x_i) per role, [N][steps][M] */
+int orc_1d_set_source_tables(orc_1d* o, const double* fine, const double* coarse);
 const orc_problem* orc_1d_problem(orc_1d* o);
 const orc_stepper* orc_1d_stepper(orc_1d* o, int role);
 /* ds table for slab n: dt*amp*sin(omega*t_k + phase), t_k = n*(T/N) + k*dt, k = 1..steps */

@@ -36,6 +36,7 @@ struct RefCtx {
   int M = 0;
   int N = 0;
   std::vector<double> shape;
+  pit::SourceFn src;  // the source both propagators were built with
 };
 
 int fail(const std::exception& e) {
@@ -88,7 +89,10 @@ const char* pitref_last_error() { return g_err.c_str(); }
 // operator comes from assemble_spatial_operator(diffusion, reaction)
 // (pde.cpp:45-64); otherwise a hand-built tridiagonal CSR with the given
 // bands (the route c3's central-difference advection needs, pde.hpp:36-37).
-// Source (has_source): f(t, x_i) = amp * sin(omega*t + phase) * shape[i].
+// Source (has_source == 1): f(t, x_i) = amp * sin(omega*t + phase) * shape[i];
+// has_source == 2: a non-separable test source
+//   f(t, x) = amp * ((1 + t) * x * (1 - x) + sin(omega * t) * cos(phase * x))
+// (shape unused) for the general-source path (PIT_SOURCE_TABLE).
 void* pitref_create_1d(int M, double lo, double hi, double diffusion, double reaction,
                        int use_bands, double band_lo, double band_diag, double band_up,
                        int symmetric, int N, double T, int fine_steps, int coarse_steps,
@@ -126,7 +130,11 @@ void* pitref_create_1d(int M, double lo, double hi, double diffusion, double rea
     }();
     const pit::TimeSlabPartition part(T, N);
     pit::SourceFn src;
-    if (has_source) {
+    if (has_source == 2) {
+      src = [amp, omega, phase](double t, std::span<const double> x) {
+        return amp * ((1.0 + t) * x[0] * (1.0 - x[0]) + std::sin(omega * t) * std::cos(phase * x[0]));
+      };
+    } else if (has_source) {
       r->shape.assign(shape, shape + M);
       const double h = g->spacing();
       const std::vector<double>* sh = &r->shape;
@@ -135,6 +143,7 @@ void* pitref_create_1d(int M, double lo, double hi, double diffusion, double rea
         return amp * std::sin(omega * t + phase) * (*sh)[static_cast<size_t>(i)];
       };
     }
+    r->src = src;
     pit::Propagator fine(op, part, fine_steps, pit::PropagatorRole::Fine, src);
     pit::Propagator coarse(op, part, coarse_steps, pit::PropagatorRole::Coarse, src);
     pit::ScalarField init(g, std::vector<double>(y0, y0 + M));
@@ -279,6 +288,22 @@ int pitref_sequential_fine(void* p, double* out) {
   try {
     auto& r = *static_cast<RefCtx*>(p);
     flat(r, pit::sequential_fine_solve(*r.ctx), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// The values Propagator::sample_source(t) (private; propagator.cpp:25-47)
+// hands to rhs.axpy(dt, .): the context's SourceFn at the M interior nodes.
+int pitref_sample_source(void* p, double t, double* out) {
+  try {
+    auto& r = *static_cast<RefCtx*>(p);
+    const pit::SpatialGrid& g = *r.ctx->grid_ptr();
+    for (int i = 0; i < r.M; ++i) {
+      const double x[1] = {g.interior_coord(i)};
+      out[i] = r.src ? r.src(t, x) : 0.0;
+    }
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

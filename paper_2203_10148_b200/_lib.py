@@ -24,6 +24,7 @@ PIT_FINE = 0
 PIT_COARSE = 1
 PIT_SOURCE_NONE = 0
 PIT_SOURCE_SEPARABLE = 1
+PIT_SOURCE_TABLE = 2
 PIT_GUESS_COARSE_SWEEP = 0
 PIT_GUESS_ZERO = 1
 PIT_CONVERGED = 0
@@ -49,7 +50,8 @@ class ProblemDesc(C.Structure):
                 ("coarse_max_iterations", C.c_int64), ("tile_rows", C.c_int32),
                 ("tile_cols", C.c_int32), ("tile_cluster", C.c_int32), ("tile_warps", C.c_int32),
                 ("stencil", _dp), ("nonsymmetric", C.c_int32), ("fine_tolerance", C.c_double),
-                ("fine_max_iterations", C.c_int64)]
+                ("fine_max_iterations", C.c_int64), ("source_table_fine", _dp),
+                ("source_table_coarse", _dp)]
 
 
 class StepCoeffs2DC(C.Structure):

@@ -92,6 +92,36 @@ class SeparableSource:
 
 
 @dataclass
+class TableSource:
+    """A general pit::SourceFn f(t, x) (include/pit/pde.hpp:13) sampled where
+    Propagator::run samples it (src/propagator.cpp:56-63, the end of every
+    step): fine[n, k-1, i] = f(breakpoint(n) + k*dt_fine, x_i), k = 1 ..
+    fine_steps, and coarse likewise with the coarse steps.  N*steps*M doubles
+    per propagator: for moderate problems (SeparableSource needs no table)."""
+    fine: np.ndarray
+    coarse: np.ndarray
+
+    @staticmethod
+    def sample(f, M: int, N: int, T: float, fine_steps: int, coarse_steps: int,
+               grid_lo: float = 0.0, grid_hi: float = 1.0) -> "TableSource":
+        """Tables of the Python callable f(t, x) (x: array of the M interior
+        coordinates; returns an array of M values)."""
+        h = (grid_hi - grid_lo) / (M + 1)
+        x = np.array([grid_lo + (k + 1) * h for k in range(M)])
+        slab = T / N
+        out = []
+        for steps in (fine_steps, coarse_steps):
+            dt = slab / steps
+            tab = np.empty((N, steps, M))
+            for n in range(N):
+                t0 = n * slab
+                for k in range(1, steps + 1):
+                    tab[n, k - 1] = f(t0 + k * dt, x)
+            out.append(tab)
+        return TableSource(out[0], out[1])
+
+
+@dataclass
 class Problem1D:
     """Everything BlockOperatorContext needs for a 1D problem.
 
@@ -110,7 +140,7 @@ class Problem1D:
     y0: np.ndarray
     grid_lo: float = 0.0
     grid_hi: float = 1.0
-    source: Optional[SeparableSource] = None
+    source: Optional[object] = None  # SeparableSource or TableSource
 
     @property
     def spacing(self) -> float:
@@ -134,7 +164,18 @@ class Problem1D:
         y0 = np.ascontiguousarray(self.y0, dtype=np.float64)
         keep.append(y0)
         d.initial_value = dptr(y0)
-        if self.source is not None:
+        if isinstance(self.source, TableSource):
+            tabs = []
+            for tab, steps in ((self.source.fine, self.fine_steps),
+                               (self.source.coarse, self.coarse_steps)):
+                t = np.ascontiguousarray(tab, dtype=np.float64)
+                if t.shape != (self.N, steps, self.M):
+                    raise ValueError("TableSource: tables are [N, steps, M] per propagator")
+                keep.append(t)
+                tabs.append(t)
+            d.source_kind = _lib.PIT_SOURCE_TABLE
+            d.source_table_fine, d.source_table_coarse = dptr(tabs[0]), dptr(tabs[1])
+        elif self.source is not None:
             sh = np.ascontiguousarray(self.source.shape, dtype=np.float64)
             keep.append(sh)
             d.source_kind = _lib.PIT_SOURCE_SEPARABLE

@@ -95,6 +95,7 @@ struct Role {
   double* d_zc = nullptr;
   double* d_pos = nullptr;  // [3*T]: ppos, qpos, zt
   double* d_ds = nullptr;
+  double* d_tab = nullptr;  // PIT_SOURCE_TABLE: [N*steps][M] fl(dt*f)
   int mpt = 0, nsub = 0, nseg = 0, warps = 0;
 };
 
@@ -234,6 +235,12 @@ int validate_desc(const pit_problem_desc* d) {
   if (d->fine_steps < 1 || d->coarse_steps < 1)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "Propagator: steps_per_slab must be >= 1");
   if (!d->initial_value) return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: null initial value");
+  if (d->source_kind == PIT_SOURCE_TABLE && (!d->source_table_fine || !d->source_table_coarse))
+    return set_err(PIT_ERR_INVALID_ARGUMENT,
+                   "pit_context_create: a table source needs the fine and the coarse table");
+  if (d->source_kind != PIT_SOURCE_NONE && d->source_kind != PIT_SOURCE_SEPARABLE &&
+      d->source_kind != PIT_SOURCE_TABLE)
+    return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: unknown source kind");
   if (d->source_kind == PIT_SOURCE_SEPARABLE && !d->source_shape)
     return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: separable source needs a shape");
   return PIT_OK;
@@ -728,7 +735,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
   ctx->h = grid_spacing(desc);
   // inner_product weight h^d (grid.cpp:113-114)
   ctx->weight = ctx->dim == 2 ? ctx->h * ctx->h : ctx->h;
-  ctx->has_source = desc->source_kind == PIT_SOURCE_SEPARABLE;
+  ctx->has_source = desc->source_kind != PIT_SOURCE_NONE;
   ctx->y0.assign(desc->initial_value, desc->initial_value + ctx->M);
   auto fail = [&](int rc) {
     pit_context_destroy(ctx);
@@ -824,7 +831,25 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
       cudaMemcpy(ctx->d_y0, ctx->y0.data(), sizeof(double) * ctx->M, cudaMemcpyHostToDevice) !=
           cudaSuccess)
     return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
-  if (ctx->has_source) {
+  if (desc->source_kind == PIT_SOURCE_TABLE) {
+    // general source: fl(dt*f) per step and point, as the reference's
+    // rhs.axpy(dt, sample_source(t)) forms it (propagator.cpp:60-62)
+    const double slab = desc->total_time / desc->slab_count;
+    for (int r = 0; r < 2; ++r) {
+      Role& R = ctx->role[r];
+      const double dt = slab / R.c.steps;
+      const double* f = r == PIT_FINE ? desc->source_table_fine : desc->source_table_coarse;
+      const size_t n = (size_t)ctx->N * R.c.steps * ctx->M;
+      std::vector<double> tab(n);
+      for (size_t i = 0; i < n; ++i) tab[i] = dt * f[i];
+      if (cudaMalloc(&R.d_tab, sizeof(double) * n) != cudaSuccess ||
+          cudaMemcpy(R.d_tab, tab.data(), sizeof(double) * n, cudaMemcpyHostToDevice) !=
+              cudaSuccess)
+        return fail(set_err(PIT_ERR_CUDA, "pit_context_create: the source table does not fit "
+                                          "the device (N*steps*M doubles per propagator)"));
+      R.P.tab = R.d_tab;
+    }
+  } else if (ctx->has_source) {
     if (cudaMalloc(&ctx->d_shape, sizeof(double) * ctx->M) != cudaSuccess ||
         cudaMemcpy(ctx->d_shape, desc->source_shape, sizeof(double) * ctx->M,
                    cudaMemcpyHostToDevice) != cudaSuccess)
@@ -886,6 +911,7 @@ int pit_context_destroy(pit_context* ctx) {
     cudaFree(R.d_zc);
     cudaFree(R.d_pos);
     cudaFree(R.d_ds);
+    cudaFree(R.d_tab);
   }
   cudaFree(ctx->d_shape);
   cudaFree(ctx->d_y0);

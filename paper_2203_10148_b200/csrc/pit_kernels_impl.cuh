@@ -110,18 +110,31 @@ __device__ __forceinline__ void run_slab(double (&y)[S::NC][S::SUB], const StepP
 #endif
   if (SRC) {
     // separable source y += dt*s(t_k) g(x): g read through L1 each step (not
-    // held in registers, so wide layouts do not spill)
-    const double* ds = P.ds + (size_t)slab * P.steps;
-    double dsk = ds[k0];
+    // held in registers, so wide layouts do not spill); or a general source
+    // table y += fl(dt*f(t_k, x_i)) (PIT_SOURCE_TABLE)
+    const double* ds = P.tab ? nullptr : P.ds + (size_t)slab * P.steps;
+    const double* tk = P.tab ? P.tab + ((size_t)slab * P.steps + k0) * P.M : nullptr;
+    double dsk = ds ? ds[k0] : 0.0;
     for (int k = k0; k < k1; ++k) {
-      const double dsn = (k + 1 < k1) ? ds[k + 1] : 0.0;
+      const double dsn = (ds && k + 1 < k1) ? ds[k + 1] : 0.0;
+      if (tk) {
 #pragma unroll
-      for (int c = 0; c < S::NC; ++c)
+        for (int c = 0; c < S::NC; ++c)
 #pragma unroll
-        for (int j = 0; j < S::SUB; ++j) {
-          const int i = S::point(tid, c, j);
-          y[c][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[c][j]);
-        }
+          for (int j = 0; j < S::SUB; ++j) {
+            const int i = S::point(tid, c, j);
+            y[c][j] = y[c][j] + (i < P.M ? __ldg(tk + i) : 0.0);
+          }
+        tk += P.M;
+      } else {
+#pragma unroll
+        for (int c = 0; c < S::NC; ++c)
+#pragma unroll
+          for (int j = 0; j < S::SUB; ++j) {
+            const int i = S::point(tid, c, j);
+            y[c][j] = fma(dsk, i < P.M ? __ldg(P.shape + i) : 0.0, y[c][j]);
+          }
+      }
       be_solve<S, HOIST, ZREG>(y, P, L, sh, s_zc, tid, ghosts, zreg PIT_TIMING_ARGS);
 #pragma unroll
       for (int c = 0; c < S::NC; ++c)

@@ -66,6 +66,7 @@ struct StepParams {
   const double* qpos;   // [T] nu^((T-1-t)*NSUB*SUB)  (device)
   const double* shape;  // [M] source shape g(x_i) (device) or nullptr
   const double* ds;     // [slabs*steps] dt*s(t_k) table (device) or nullptr
+  const double* tab;    // [slabs*steps][M] fl(dt*f(t_k, x_i)) general source (device) or nullptr
   long long* timing;    // PIT_PHASE_TIMING builds only: [2 warps][16 phases] cycles
 };
 

@@ -18,6 +18,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "pit_b200.h"
@@ -126,6 +127,10 @@ struct Problem1D {
   bool has_source = false;
   double source_amp = 0.0, source_omega = 0.0, source_phase = 0.0;
   std::vector<double> source_shape;
+  // a general pit::SourceFn f(t, x) (pde.hpp:13), 1D: takes precedence over
+  // the separable description; sampled at the end of every step
+  // (propagator.cpp:56-63) into the C ABI's PIT_SOURCE_TABLE tables
+  std::function<double(double t, double x)> source_fn;
   int device = 0;
 };
 
@@ -187,7 +192,22 @@ class BlockOperatorContext {  // pit::BlockOperatorContext (block_system.hpp:55-
     d.coarse_steps = p.coarse_steps;
     d.initial_value = p.y0.data();
     d.device = p.device;
-    if (p.has_source) {
+    std::vector<double> tab[2];
+    if (p.source_fn) {
+      const double h = (p.grid_hi - p.grid_lo) / (p.M + 1), slab = p.T / p.N;
+      const int steps[2] = {p.fine_steps, p.coarse_steps};
+      for (int r = 0; r < 2; ++r) {
+        const double dt = slab / steps[r];
+        tab[r].reserve(static_cast<size_t>(p.N) * steps[r] * p.M);
+        for (int n = 0; n < p.N; ++n)
+          for (int k = 1; k <= steps[r]; ++k)
+            for (int i = 0; i < p.M; ++i)
+              tab[r].push_back(p.source_fn(n * slab + k * dt, p.grid_lo + (i + 1) * h));
+      }
+      d.source_kind = PIT_SOURCE_TABLE;
+      d.source_table_fine = tab[0].data();
+      d.source_table_coarse = tab[1].data();
+    } else if (p.has_source) {
       d.source_kind = PIT_SOURCE_SEPARABLE;
       d.source_amp = p.source_amp;
       d.source_omega = p.source_omega;

@@ -29,7 +29,7 @@ class OracleProblem:
         cc, _ = api.step_coefficients(p, 1, fine_layout, coarse_layout)
         self.p = p
         self.lib = O.orc()
-        src = p.source
+        src = p.source if isinstance(p.source, api.SeparableSource) else None
         self._keep = [np.ascontiguousarray(p.y0)]
         shape = None
         if src is not None:
@@ -42,6 +42,10 @@ class OracleProblem:
             1 if src else 0, O.ptr(shape) if src else None, src.amp if src else 0.0,
             src.omega if src else 0.0, src.phase if src else 0.0, 1 if use_thomas else 0, mode)
         assert self.o, "orc_1d_create failed"
+        if isinstance(p.source, api.TableSource):
+            tf = np.ascontiguousarray(p.source.fine, dtype=np.float64)
+            tc = np.ascontiguousarray(p.source.coarse, dtype=np.float64)
+            assert self.lib.orc_1d_set_source_tables(self.o, O.ptr(tf), O.ptr(tc)) == 0
         self.prob = self.lib.orc_1d_problem(self.o)
 
     def _init_2d(self, p, mode):

@@ -89,6 +89,7 @@ def orc():
                                       C.c_int, _dp, C.c_double, C.c_double, C.c_double, C.c_int,
                                       C.c_int]
         lib.orc_1d_destroy.argtypes = [C.c_void_p]
+        lib.orc_1d_set_source_tables.argtypes = [C.c_void_p, _dp, _dp]
         lib.orc_1d_problem.restype = C.c_void_p
         lib.orc_1d_problem.argtypes = [C.c_void_p]
         lib.orc_1d_stepper.restype = C.POINTER(OrcStepper)
@@ -184,6 +185,7 @@ def ref():
         lib.pitref_initial_guess.argtypes = [C.c_void_p, _dp]
         lib.pitref_sequential_fine.argtypes = [C.c_void_p, _dp]
         lib.pitref_propagate.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp]
+        lib.pitref_sample_source.argtypes = [C.c_void_p, C.c_double, _dp]
         for name in ("pitref_pitsbicg", "pitref_parareal"):
             getattr(lib, name).argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int,
                                            C.c_int, _dp, _dp, _dp, C.POINTER(C.c_int), _dp,
