@@ -128,7 +128,7 @@ typedef struct pit_problem_desc {
    * isotropic band_diag / band_lo stencil) and solve every step with
    * Jacobi-PCG, or Jacobi-BiCGStab when `nonsymmetric` (ImplicitStepSolver,
    * src/pde.cpp:112-130), to fine/coarse_tolerance (0: 1e-12) within
-   * fine/coarse_max_iterations (0: 10*M).  m <= 50. */
+   * fine/coarse_max_iterations (0: 10*M).  m <= 101 (grid_points <= 103). */
   const double* stencil;
   int32_t nonsymmetric;
   double fine_tolerance;

@@ -14,7 +14,7 @@
 //     constant-coefficient operator such as central-difference advection);
 //   * 2D grid (the desk/paper presets, runner.cpp:75-88): any 5-point CSR
 //     (assemble_spatial_operator's 2D rows, pde.cpp:66-100, any velocity),
-//     m <= 50 points per axis; both propagators backward Euler with the
+//     m <= 101 points per axis; both propagators backward Euler with the
 //     reference's inner solvers (CG if op().symmetric(), else BiCGStab);
 //   * a source, if any: the context's own SourceFn (sampled into tables), or
 //     separable f(t,x) = amp*sin(omega*t+phase)*g(x),

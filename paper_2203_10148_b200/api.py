@@ -259,7 +259,7 @@ class Problem2DImplicit:
     (src/pde.cpp:66-100), 0 where the row has no such entry.  Every step is
     solved by Jacobi-PCG (symmetric operator) or Jacobi-BiCGStab
     (`nonsymmetric`, e.g. the rotation velocity) to the reference's 1e-12
-    within 10 n iterations (ImplicitStepSolver, src/pde.cpp:112-130).  m <= 50."""
+    within 10 n iterations (ImplicitStepSolver, src/pde.cpp:112-130).  m <= 101."""
     m: int
     stencil: np.ndarray
     nonsymmetric: bool

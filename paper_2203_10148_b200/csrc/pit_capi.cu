@@ -201,7 +201,7 @@ int validate_desc(const pit_problem_desc* d) {
   if (d->dimension == 2 && d->fine_scheme == PIT_SCHEME_BACKWARD_EULER) {
     if (!be2d_supported(d->interior))
       return set_err(PIT_ERR_INVALID_ARGUMENT,
-                     "pit_context_create: implicit 2D propagators need m <= 50 points per axis");
+                     "pit_context_create: implicit 2D propagators need m <= 101 points per axis");
     if (!d->stencil && d->band_lo != d->band_up)
       return set_err(PIT_ERR_INVALID_ARGUMENT,
                      "pit_context_create: 2D band operators are isotropic (band_lo == band_up)");

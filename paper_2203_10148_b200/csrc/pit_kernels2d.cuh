@@ -73,7 +73,12 @@ struct Be2Params {
   long long* iters;      // sweeps: cumulative inner iterations (optional)
 };
 constexpr int kBe2Threads = 512;
-constexpr int kBe2MaxPPT = 5;  // points per thread: m*m <= 2560
+// points per thread: up to 5 (m <= 50) everything a thread owns sits in
+// registers and the stencil rows in shared memory; larger grids (m <= 101)
+// run the same code on rounded-up point counts (8, 12, 16, 20) whose
+// vectors the compiler keeps in local memory, read the stencil rows from
+// global memory, and share one operand buffer between x and s^
+constexpr int kBe2MaxPPT = 20;
 size_t be2d_smem_bytes(int m);
 bool be2d_supported(int m);
 cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st);

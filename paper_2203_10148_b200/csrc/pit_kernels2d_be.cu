@@ -37,11 +37,12 @@ constexpr int kT = kBe2Threads, kNW = kBe2Threads / 32;
 template <int PPT>
 struct Be2Ctx {
   static constexpr bool kRegCoef = PPT <= 3;
+  static constexpr bool kBig = PPT > 5;  // stencil rows in global memory, two operand buffers
   int m, M, pitch;
   int ip[PPT];        // padded index of owned point k (or -1)
   int gi[PPT];        // interior index of owned point k
   double cr[6][kRegCoef ? PPT : 1];  // S, W, C, E, N, minv (kRegCoef)
-  const double* cf;   // [6][M] shared memory (!kRegCoef)
+  const double* cf;   // [6][M] shared memory (!kRegCoef), global memory (kBig)
   double* red;        // [2][2][kNW]
   int par;            // reduction slot set
   double *opx, *opp, *ops;  // padded operand buffers (x, p or p^, s^)
@@ -394,14 +395,19 @@ __device__ void setup(Be2Ctx<PPT>& c, const Be2Params& P, unsigned char* smem) {
   c.pitch = P.m + 2;
   const int np = c.pitch * c.pitch;
   double* base = reinterpret_cast<double*>(smem);
+  // big grids: x and s^ share a buffer (each operand is published right
+  // before the stencil that reads it, never two of them at once)
+  constexpr int kBufs = Be2Ctx<PPT>::kBig ? 2 : 3;
   c.opx = base;
   c.opp = base + np;
-  c.ops = base + 2 * (size_t)np;
-  c.red = base + 3 * (size_t)np;
+  c.ops = Be2Ctx<PPT>::kBig ? base : base + 2 * (size_t)np;
+  c.red = base + kBufs * (size_t)np;
   double* cf = c.red + 4 * kNW;
   c.par = 0;
-  for (int i = threadIdx.x; i < 3 * np; i += kT) base[i] = 0.0;  // ghost rings stay 0
-  if constexpr (!Be2Ctx<PPT>::kRegCoef) {
+  for (int i = threadIdx.x; i < kBufs * np; i += kT) base[i] = 0.0;  // ghost rings stay 0
+  if constexpr (Be2Ctx<PPT>::kBig) {
+    c.cf = P.coef;  // [5][M] then minv[M], contiguous (pit_context_create)
+  } else if constexpr (!Be2Ctx<PPT>::kRegCoef) {
     for (int i = threadIdx.x; i < 5 * P.M; i += kT) cf[i] = P.coef[i];
     for (int i = threadIdx.x; i < P.M; i += kT) cf[5 * P.M + i] = P.minv[i];
     c.cf = cf;
@@ -517,7 +523,9 @@ size_t be2d_smem_bytes(int m) {
   // three padded operand buffers, reduction slots, and (more than 3 points
   // per thread) the stencil rows and Jacobi inverse
   const size_t np = (size_t)(m + 2) * (m + 2), M = (size_t)m * m;
-  const bool reg_coef = (M + kBe2Threads - 1) / kBe2Threads <= 3;
+  const size_t ppt = (M + kBe2Threads - 1) / kBe2Threads;
+  if (ppt > 5) return sizeof(double) * (2 * np + 4 * kNW);
+  const bool reg_coef = ppt <= 3;
   return sizeof(double) * (3 * np + 4 * kNW + (reg_coef ? 0 : 6 * M));
 }
 
@@ -525,12 +533,18 @@ bool be2d_supported(int m) {
   return m >= 1 && m * m <= kBe2MaxPPT * kBe2Threads && be2d_smem_bytes(m) <= 227 * 1024;
 }
 
-#define PIT_BE2_PPT(X) X(1) X(2) X(3) X(4) X(5)
+#define PIT_BE2_PPT(X) X(1) X(2) X(3) X(4) X(5) X(8) X(12) X(16) X(20)
+// compiled point count for a grid: exact up to 5, then the next of 8, 12, 16, 20
+static int be2d_ppt(int M) {
+  const int ppt = (M + kBe2Threads - 1) / kBe2Threads;
+  return ppt <= 5 ? ppt : 4 * ((ppt + 3) / 4);
+}
 
 cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st) {
   if (slabs <= 0) return cudaSuccess;
   if (!be2d_supported(P.m)) return cudaErrorInvalidValue;
-  const int ppt = (P.M + kBe2Threads - 1) / kBe2Threads;
+  const int ppt = be2d_ppt(P.M);
+  if (ppt > 5 && P.minv != P.coef + 5 * (size_t)P.M) return cudaErrorInvalidValue;
   const size_t smem = be2d_smem_bytes(P.m);
 #define X(N)                                                                              \
   if (ppt == N) {                                                                         \
@@ -549,7 +563,8 @@ cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, 
 cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st) {
   if (A.count <= 0) return cudaSuccess;
   if (!be2d_supported(P.m)) return cudaErrorInvalidValue;
-  const int ppt = (P.M + kBe2Threads - 1) / kBe2Threads;
+  const int ppt = be2d_ppt(P.M);
+  if (ppt > 5 && P.minv != P.coef + 5 * (size_t)P.M) return cudaErrorInvalidValue;
   const size_t smem = be2d_smem_bytes(P.m);
 #define X(N)                                                                              \
   if (ppt == N) {                                                                         \

@@ -111,11 +111,13 @@ def test_pit_verify_rejects_rotation_in_1d():
     assert verify.main(["--case", "advection_diffusion_reaction", "--dim", "1"]) == 2
 
 
-@pytest.mark.parametrize("m", [1, 3, 22, 23, 39, 45, 50])
+@pytest.mark.parametrize("m", [1, 3, 22, 23, 39, 45, 50, 51, 64, 75, 88, 99, 101])
 @pytest.mark.parametrize("nonsym", [False, True])
 def test_k6_all_thread_layouts_bitwise(m, nonsym):
     # every points-per-thread instantiation (1..5; stencil rows in registers
-    # up to 3, in shared memory beyond) on a random 5-point operator (the
+    # up to 3, in shared memory beyond; 8, 12, 16, 20 for grids above 50
+    # points per axis: stencil rows from global memory, vectors in local
+    # memory, x and s^ sharing an operand buffer) on a random 5-point operator (the
     # rotation preset's structure: diagonally dominant, upwind-like
     # off-diagonals), fine batch and coarse sweep against the oracle
     rng = np.random.default_rng(m * 7 + nonsym)
@@ -160,3 +162,21 @@ def test_device_matches_reference_fixtures(case):
         assert np.allclose([x.residual_norm for x in r.history.records], rows[:, 1], rtol=1e-6,
                            atol=1e-13)
         assert r.history.restarts == int(g[f"{case}_restarts{key}"])
+
+
+def test_grid_points_101_preset_runs_on_the_device():
+    """The reference accepts any grid_points (presets.cpp:36, config.cpp:98-99);
+    grid_points = 101 (m = 99) solves on the device and matches the oracle."""
+    pre = presets.make_preset("advection_diffusion_reaction", "desk")
+    pre.grid_points = 101
+    p = presets.build_problem(pre, 4)
+    o = OracleProblem(p)
+    with api.BlockOperatorContext(p) as ctx:
+        res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-8))
+    r = o.solve(1e-8)
+    assert res.history.records[-1].residual_norm <= 1e-8
+    assert [(x.k, x.residual_norm) for x in res.history.records] == [(a[0], a[1]) for a in r["rows"]]
+    assert np.array_equal(res.solution, r["lam"])
+    with pytest.raises(ValueError):
+        pre.grid_points = 104  # m = 102: beyond the compiled point counts
+        api.BlockOperatorContext(presets.build_problem(pre, 4))
