@@ -129,6 +129,14 @@ typedef struct pit_problem_desc {
    * Jacobi-PCG, or Jacobi-BiCGStab when `nonsymmetric` (ImplicitStepSolver,
    * src/pde.cpp:112-130), to fine/coarse_tolerance (0: 1e-12) within
    * fine/coarse_max_iterations (0: 10*M).  m <= 101 (grid_points <= 103). */
+  /* dimension 1 with `stencil` set: a general tridiagonal operator (any
+   * pit::SpatialOperator the reference's 1D propagators accept through the
+   * CSR constructor, include/pit/pde.hpp:36-37, e.g. variable coefficients):
+   * stencil is [3][M], the sub-diagonal, diagonal and super-diagonal entry of
+   * A per interior node (0 where absent; band_* are ignored).  Every step is
+   * then solved as the reference solves it, Jacobi-PCG or (nonsymmetric)
+   * Jacobi-BiCGStab to fine/coarse_tolerance (K6 on a one-row grid);
+   * M <= 10240, no source. */
   const double* stencil;
   int32_t nonsymmetric;
   double fine_tolerance;

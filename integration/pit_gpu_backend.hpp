@@ -9,9 +9,12 @@
 //   pit::SolveResult r = gpu.pitsbicg_solve(cfg, exec, opts); // == pit::pitsbicg_solve
 //
 // Requirements checked at construction (else std::invalid_argument):
-//   * 1D grid: SpatialOperator a constant-band tridiagonal CSR (what
-//     assemble_spatial_operator builds for 1D, pde.cpp:55-64, or a hand-built
-//     constant-coefficient operator such as central-difference advection);
+//   * 1D grid: SpatialOperator a tridiagonal CSR.  Constant bands (what
+//     assemble_spatial_operator builds for 1D, pde.cpp:55-64, or hand-built
+//     central-difference advection) take the direct solve; any other
+//     tridiagonal operator (variable coefficients, pde.hpp:36-37) is solved
+//     per step by the reference's own inner solvers on the device
+//     (M <= 10240, no source);
 //   * 2D grid (the desk/paper presets, runner.cpp:75-88): any 5-point CSR
 //     (assemble_spatial_operator's 2D rows, pde.cpp:66-100, any velocity),
 //     m <= 101 points per axis; both propagators backward Euler with the
@@ -98,16 +101,21 @@ class Backend {
     const CsrMatrix& A = ctx.fine().op().matrix();
     double band[3] = {0.0, 0.0, 0.0};  // lo, diag, up
     bool seen[3] = {false, false, false};
+    bool constant = true;
+    // per-node sub, diagonal, super entries: a general tridiagonal operator
+    // (variable coefficients) goes to the device's iterative path
+    std::vector<double> tri(3 * static_cast<size_t>(A.n), 0.0);
     for (int i = 0; i < A.n; ++i) {
       for (int k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k) {
         const int off = A.col[k] - i + 1;  // 0 sub, 1 diag, 2 super
         if (off < 0 || off > 2)
           throw std::invalid_argument("pit::gpu::Backend: operator is not tridiagonal");
+        tri[static_cast<size_t>(off) * A.n + i] = A.val[k];
         if (!seen[off]) {
           band[off] = A.val[k];
           seen[off] = true;
         } else if (A.val[k] != band[off]) {
-          throw std::invalid_argument("pit::gpu::Backend: operator bands are not constant");
+          constant = false;
         }
       }
     }
@@ -129,6 +137,15 @@ class Backend {
     d.coarse_steps = ctx.coarse().steps_per_slab();
     const auto y0 = ctx.initial_value().values();
     d.initial_value = y0.data();
+    if (!constant) {
+      // Jacobi-PCG / Jacobi-BiCGStab per step, as the reference's
+      // ImplicitStepSolver (pde.cpp:112-130); no direct solve, no source
+      if (ctx.fine().has_source())
+        throw std::invalid_argument(
+            "pit::gpu::Backend: sources need a constant-coefficient operator");
+      d.stencil = tri.data();
+      d.nonsymmetric = ctx.fine().op().symmetric() ? 0 : 1;
+    }
     if (source) {
       d.source_kind = PIT_SOURCE_SEPARABLE;
       d.source_amp = source->amp;

@@ -66,10 +66,17 @@ void orc_be2_stencil(int m, double lo, double hi, double mu, double r, int rotat
   }
 }
 
+static void role_init_rect(orc_be2_role* R, int m, int my, const double* stencil, double dt,
+                           int steps, double rel_tol, long long cap, int symmetric);
 void orc_be2_role_init(orc_be2_role* R, int m, const double* stencil, double dt, int steps,
                        double rel_tol, long long cap, int symmetric) {
-  const int n = m * m;
+  role_init_rect(R, m, m, stencil, dt, steps, rel_tol, cap, symmetric);
+}
+static void role_init_rect(orc_be2_role* R, int m, int my, const double* stencil, double dt,
+                           int steps, double rel_tol, long long cap, int symmetric) {
+  const int n = m * my;
   R->m = m;
+  R->my = my;
   R->steps = steps;
   R->rel_tol = rel_tol > 0.0 ? rel_tol : 1e-12;
   R->cap = cap > 0 ? cap : 10LL * n;
@@ -127,9 +134,9 @@ static double be2_dot(be2_ws* w, const double* a, const double* b) {
 
 /* (A x)_i, CSR column order south, west, centre, east, north */
 static double be2_row(const orc_be2_role* R, const double* x, int i) {
-  const int m = R->m, n = m * m, ix = i % m, iy = i / m;
+  const int m = R->m, n = m * R->my, ix = i % m, iy = i / m;
   const double xs = iy > 0 ? x[i - m] : 0.0, xw = ix > 0 ? x[i - 1] : 0.0;
-  const double xe = ix < m - 1 ? x[i + 1] : 0.0, xn = iy < m - 1 ? x[i + m] : 0.0;
+  const double xe = ix < m - 1 ? x[i + 1] : 0.0, xn = iy < R->my - 1 ? x[i + m] : 0.0;
   double s = 0.0;
   s = fma(R->coef[i], xs, s);
   s = fma(R->coef[n + i], xw, s);
@@ -311,7 +318,7 @@ done:
 }
 
 int orc_be2_propagate(const orc_be2_role* R, const double* in, double* out, long long* iterations) {
-  const int n = R->m * R->m;
+  const int n = R->m * R->my;
   be2_ws w;
   w.n = n;
   w.pair = (double*)malloc(sizeof(double) * 2 * (size_t)n);
@@ -356,23 +363,40 @@ static int prop_be2(void* user, int role, int with_source, const double* in, int
   return ok ? 0 : 1;
 }
 
+static orc_be2d* create_rect(int m, int my, double lo, double hi, const double* stencil,
+                             int nonsymmetric, int N, double total_time, int fine_steps,
+                             int coarse_steps, double fine_tol, long long fine_cap,
+                             double coarse_tol, long long coarse_cap, const double* y0, int mode) {
+  orc_be2d* o = (orc_be2d*)calloc(1, sizeof(orc_be2d));
+  const double slab = total_time / N;
+  role_init_rect(&o->role[ORC_FINE], m, my, stencil, slab / fine_steps, fine_steps, fine_tol,
+                 fine_cap, !nonsymmetric);
+  role_init_rect(&o->role[ORC_COARSE], m, my, stencil, slab / coarse_steps, coarse_steps,
+                 coarse_tol, coarse_cap, !nonsymmetric);
+  const size_t n = (size_t)m * my;
+  o->y0 = (double*)malloc(n * sizeof(double));
+  memcpy(o->y0, y0, n * sizeof(double));
+  const double h = (hi - lo) / (double)(m + 1);
+  /* inner_product weight h^d (grid.cpp:113-114) */
+  o->prob = orc_problem_new((int)n, N, my == 1 ? h : h * h, 0, mode, o->y0, prop_be2, o);
+  o->prob->parallel = 1;
+  return o;
+}
+
 orc_be2d* orc_be2d_create(int m, double lo, double hi, const double* stencil, int nonsymmetric,
                           int N, double total_time, int fine_steps, int coarse_steps,
                           double fine_tol, long long fine_cap, double coarse_tol,
                           long long coarse_cap, const double* y0, int mode) {
-  orc_be2d* o = (orc_be2d*)calloc(1, sizeof(orc_be2d));
-  const double slab = total_time / N;
-  orc_be2_role_init(&o->role[ORC_FINE], m, stencil, slab / fine_steps, fine_steps, fine_tol,
-                    fine_cap, !nonsymmetric);
-  orc_be2_role_init(&o->role[ORC_COARSE], m, stencil, slab / coarse_steps, coarse_steps,
-                    coarse_tol, coarse_cap, !nonsymmetric);
-  const size_t n = (size_t)m * m;
-  o->y0 = (double*)malloc(n * sizeof(double));
-  memcpy(o->y0, y0, n * sizeof(double));
-  const double h = (hi - lo) / (double)(m + 1);
-  o->prob = orc_problem_new((int)n, N, h * h, 0, mode, o->y0, prop_be2, o);
-  o->prob->parallel = 1;
-  return o;
+  return create_rect(m, m, lo, hi, stencil, nonsymmetric, N, total_time, fine_steps, coarse_steps,
+                     fine_tol, fine_cap, coarse_tol, coarse_cap, y0, mode);
+}
+
+orc_be2d* orc_be2d_create_1d(int M, double lo, double hi, const double* stencil, int nonsymmetric,
+                             int N, double total_time, int fine_steps, int coarse_steps,
+                             double fine_tol, long long fine_cap, double coarse_tol,
+                             long long coarse_cap, const double* y0, int mode) {
+  return create_rect(M, 1, lo, hi, stencil, nonsymmetric, N, total_time, fine_steps, coarse_steps,
+                     fine_tol, fine_cap, coarse_tol, coarse_cap, y0, mode);
 }
 
 void orc_be2d_destroy(orc_be2d* o) {

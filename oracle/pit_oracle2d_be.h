@@ -18,6 +18,7 @@ void orc_be2_stencil(int m, double lo, double hi, double mu, double r, int rotat
 
 typedef struct orc_be2_role {
   int m, steps;
+  int my;       /* rows: m for the 2D presets, 1 for a general 1D operator (m = M columns) */
   double rel_tol;
   long long cap;
   int symmetric;
@@ -32,6 +33,13 @@ void orc_be2_role_free(orc_be2_role* R);
 int orc_be2_propagate(const orc_be2_role* R, const double* in, double* out, long long* iterations);
 
 typedef struct orc_be2d orc_be2d;
+/* A general 1D operator (pit::SpatialOperator over any tridiagonal CSR,
+ * include/pit/pde.hpp:36-37) as a 1-row grid of M columns: stencil[5][M] with
+ * zero south/north rows; inner-product weight h (dimension 1, grid.cpp:113-114). */
+orc_be2d* orc_be2d_create_1d(int M, double lo, double hi, const double* stencil, int nonsymmetric,
+                             int N, double total_time, int fine_steps, int coarse_steps,
+                             double fine_tol, long long fine_cap, double coarse_tol,
+                             long long coarse_cap, const double* y0, int mode);
 orc_be2d* orc_be2d_create(int m, double lo, double hi, const double* stencil, int nonsymmetric,
                           int N, double total_time, int fine_steps, int coarse_steps,
                           double fine_tol, long long fine_cap, double coarse_tol,

@@ -85,6 +85,13 @@ extern "C" {
 
 const char* pitref_last_error() { return g_err.c_str(); }
 
+// 1D context over a general tridiagonal operator given per interior node
+// (sub, diag, sup; 0 = absent) through the SpatialOperator CSR constructor
+// (pde.hpp:36-37): variable coefficients.  No source.
+void* pitref_create_1d_csr(int M, double lo, double hi, const double* sub, const double* diag,
+                           const double* sup, int symmetric, int N, double T, int fine_steps,
+                           int coarse_steps, const double* y0);
+
 // 1D context on [lo, hi] with M interior points.  When use_bands == 0 the
 // operator comes from assemble_spatial_operator(diffusion, reaction)
 // (pde.cpp:45-64); otherwise a hand-built tridiagonal CSR with the given
@@ -307,6 +314,44 @@ int pitref_sample_source(void* p, double t, double* out) {
     return 0;
   } catch (const std::exception& e) {
     return fail(e);
+  }
+}
+
+void* pitref_create_1d_csr(int M, double lo, double hi, const double* sub, const double* diag,
+                           const double* sup, int symmetric, int N, double T, int fine_steps,
+                           int coarse_steps, const double* y0) {
+  try {
+    auto r = std::make_unique<RefCtx>();
+    r->M = M;
+    r->N = N;
+    const pit::GridPtr g = pit::SpatialGrid::make(1, lo, hi, M + 2);
+    pit::CsrMatrix a;
+    a.n = M;
+    a.row_ptr.push_back(0);
+    for (int i = 0; i < M; ++i) {
+      if (i > 0 && sub[i] != 0.0) {
+        a.col.push_back(i - 1);
+        a.val.push_back(sub[i]);
+      }
+      a.col.push_back(i);
+      a.val.push_back(diag[i]);
+      if (i < M - 1 && sup[i] != 0.0) {
+        a.col.push_back(i + 1);
+        a.val.push_back(sup[i]);
+      }
+      a.row_ptr.push_back(static_cast<int>(a.col.size()));
+    }
+    const pit::SpatialOperator op(std::move(a), g, symmetric != 0);
+    const pit::TimeSlabPartition part(T, N);
+    pit::Propagator fine(op, part, fine_steps, pit::PropagatorRole::Fine);
+    pit::Propagator coarse(op, part, coarse_steps, pit::PropagatorRole::Coarse);
+    pit::ScalarField init(g, std::vector<double>(y0, y0 + M));
+    r->ctx = std::make_unique<pit::BlockOperatorContext>(std::move(fine), std::move(coarse),
+                                                          std::move(init));
+    return r.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
   }
 }
 

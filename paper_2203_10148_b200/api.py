@@ -313,6 +313,65 @@ class Problem2DImplicit:
         return d, keep
 
 
+@dataclass
+class Problem1DGeneral:
+    """A 1D problem whose operator is any tridiagonal matrix — what the
+    reference's propagators accept through the SpatialOperator CSR constructor
+    (include/pit/pde.hpp:36-37), e.g. variable coefficients.  `stencil` is
+    [3, M]: the sub-diagonal, diagonal and super-diagonal entry of A per
+    interior node (0 where absent).  Every backward-Euler step is solved as
+    the reference solves it (ImplicitStepSolver, src/pde.cpp:112-130):
+    Jacobi-PCG, or Jacobi-BiCGStab when `nonsymmetric`, to 1e-12.  Constant
+    bands should use Problem1D (the direct solve); M <= 10240; no source."""
+    M: int
+    stencil: np.ndarray
+    nonsymmetric: bool
+    N: int
+    T: float
+    fine_steps: int
+    coarse_steps: int
+    y0: np.ndarray
+    grid_lo: float = 0.0
+    grid_hi: float = 1.0
+    fine_tolerance: float = 1e-12
+    coarse_tolerance: float = 1e-12
+    fine_max_iterations: int = 0
+    coarse_max_iterations: int = 0
+    source: Optional[object] = None  # unsupported (must stay None)
+
+    @property
+    def spacing(self) -> float:
+        return (self.grid_hi - self.grid_lo) / (self.M + 2 - 1)
+
+    def coords(self) -> np.ndarray:
+        h = self.spacing
+        return np.array([self.grid_lo + (k + 1) * h for k in range(self.M)])
+
+    def desc(self, device: int = 0, fine_layout=None, coarse_layout=None):
+        if self.source is not None:
+            raise ValueError("Problem1DGeneral: sources are not supported")
+        d = _lib.ProblemDesc()
+        d.dimension = 1
+        d.interior = self.M
+        d.grid_lo, d.grid_hi = self.grid_lo, self.grid_hi
+        st = np.ascontiguousarray(self.stencil, dtype=np.float64).reshape(-1)
+        if st.size != 3 * self.M:
+            raise ValueError("stencil must be [3, M]")
+        d.slab_count = self.N
+        d.total_time = self.T
+        d.fine_steps, d.coarse_steps = self.fine_steps, self.coarse_steps
+        y0 = np.ascontiguousarray(self.y0, dtype=np.float64).reshape(-1)
+        keep = [y0, st]
+        d.initial_value = dptr(y0)
+        d.stencil = dptr(st)
+        d.nonsymmetric = 1 if self.nonsymmetric else 0
+        d.device = device
+        d.fine_tolerance, d.coarse_tolerance = self.fine_tolerance, self.coarse_tolerance
+        d.fine_max_iterations = self.fine_max_iterations
+        d.coarse_max_iterations = self.coarse_max_iterations
+        return d, keep
+
+
 def heat_2d_bands(diffusion: float, h: float):
     """(neighbour, centre) of the 2D 5-point -mu*Laplacian, as
     assemble_spatial_operator's 2D branch builds them (src/pde.cpp:66-100:

@@ -198,8 +198,20 @@ int validate_desc(const pit_problem_desc* d) {
   if (d->dimension == 1 && d->fine_scheme != PIT_SCHEME_BACKWARD_EULER)
     return set_err(PIT_ERR_INVALID_ARGUMENT,
                    "pit_context_create: 1D fine propagators are backward Euler");
+  if (d->dimension == 1 && d->stencil) {
+    // a general tridiagonal operator: the reference's inner solvers (K6 on a
+    // one-row grid)
+    if (!be2d_supported(d->interior, 1))
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: general 1D operators need M <= 10240");
+    if (d->source_kind != PIT_SOURCE_NONE)
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: no sources with a general 1D operator");
+    if (d->coarse_tolerance < 0.0 || d->fine_tolerance < 0.0)
+      return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: negative inner tolerance");
+  }
   if (d->dimension == 2 && d->fine_scheme == PIT_SCHEME_BACKWARD_EULER) {
-    if (!be2d_supported(d->interior))
+    if (!be2d_supported(d->interior, d->interior))
       return set_err(PIT_ERR_INVALID_ARGUMENT,
                      "pit_context_create: implicit 2D propagators need m <= 101 points per axis");
     if (!d->stencil && d->band_lo != d->band_up)
@@ -437,7 +449,7 @@ int eval_status(pit_context* ctx, bool fine_batch) {
                              cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (fine_batch) {
-      const std::string what = ctx->dim == 2 && ctx->be2
+      const std::string what = ctx->be2
                                    ? "implicit step solve did not converge or produced non-finite "
                                      "values"
                                    : "implicit step produced non-finite values";
@@ -572,7 +584,7 @@ int run_slab_batch(pit_context* ctx, int mode, const double* L, const double* ha
 
 // One sequential sweep launch (SweepArgs semantics) for either dimension.
 int launch_sweep_any(pit_context* ctx, int role, bool src, const SweepArgs& A, cudaStream_t st) {
-  if (ctx->dim == 1) {
+  if (ctx->dim == 1 && !ctx->be2) {
     Role& R = ctx->role[role];
     CUDA_TRY(launch_sweep(R.mpt, R.nsub, R.nseg, R.warps, src, R.P, A, st));
     return PIT_OK;
@@ -741,13 +753,21 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     pit_context_destroy(ctx);
     return rc;
   };
-  ctx->be2 = ctx->dim == 2 && desc->fine_scheme == PIT_SCHEME_BACKWARD_EULER;
+  ctx->be2 = (ctx->dim == 2 && desc->fine_scheme == PIT_SCHEME_BACKWARD_EULER) ||
+             (ctx->dim == 1 && desc->stencil != nullptr);
   if (ctx->be2) {
     // ImplicitStepSolver (pde.cpp:103-110): every entry times dt, then the
     // diagonal + 1; jacobi_inverse_diagonal (sparse.cpp:43-50)
     const int M = ctx->M;
     std::vector<double> st(5 * (size_t)M, 0.0);
-    if (desc->stencil) {
+    if (ctx->dim == 1) {
+      // [3][M] sub, diagonal, super -> west, centre, east of a one-row grid
+      for (int i = 0; i < M; ++i) {
+        st[(size_t)M + i] = i > 0 ? desc->stencil[i] : 0.0;
+        st[2 * (size_t)M + i] = desc->stencil[(size_t)M + i];
+        st[3 * (size_t)M + i] = i < M - 1 ? desc->stencil[2 * (size_t)M + i] : 0.0;
+      }
+    } else if (desc->stencil) {
       st.assign(desc->stencil, desc->stencil + 5 * (size_t)M);
     } else {
       const int m = ctx->m;
@@ -777,6 +797,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
         return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
       Be2Params& P = ctx->bp[r];
       P.m = ctx->m;
+      P.my = ctx->dim == 2 ? ctx->m : 1;
       P.M = M;
       P.steps = steps;
       P.coef = ctx->d_be2[r];
@@ -800,7 +821,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
         cudaMemset(ctx->d_cg_iters, 0, sizeof(long long)) != cudaSuccess)
       return fail(set_err(PIT_ERR_CUDA, "pit_context_create: device allocation failed"));
   }
-  for (int r = 0; r < (ctx->dim == 1 ? 2 : 0); ++r) {
+  for (int r = 0; r < (ctx->dim == 1 && !ctx->be2 ? 2 : 0); ++r) {
     std::vector<double> zc, ppos, qpos, zt;
     Layout lay;
     int rc = role_coeffs(desc, r, &ctx->role[r].c, &zc, &lay, &ppos, &qpos, &zt);
@@ -1316,7 +1337,7 @@ int pit_apply_F(pit_context* ctx, const double* L, double* out, pit_run_stats* s
   if (!ctx || !L || !out) return set_err(PIT_ERR_INVALID_ARGUMENT, "apply_F: null argument");
   ScratchScope scope_{ctx};
   const auto t0 = Clock::now();
-  if (ctx->dim == 1 && ctx->N >= 32 && is_pinned(L) && is_pinned(out)) {
+  if (ctx->dim == 1 && !ctx->be2 && ctx->N >= 32 && is_pinned(L) && is_pinned(out)) {
     PIT_TRY(pipe_setup(ctx));
     if (ctx->pipe == 1) {
       DevVec dL, dO;
@@ -2413,7 +2434,7 @@ int solve_device(int which, bool sharded, pit_context* ctx, const pit_solver_con
 int pit_context_slots(const pit_context* ctx, int* slots) {
   PIT_DEVICE_SCOPE(ctx);
   if (!ctx || !slots) return set_err(PIT_ERR_INVALID_ARGUMENT, "null argument");
-  if (ctx->dim == 1) {
+  if (ctx->dim == 1 && !ctx->be2) {
     const Role& R = ctx->role[PIT_FINE];
     CUDA_TRY(slab_slots(R.mpt, R.nsub, R.nseg, R.warps, false, R.P, slots));
   } else if (ctx->be2) {

@@ -63,7 +63,8 @@ cudaError_t launch_explicit2d(const Layout2D& L, const Ex2Params& P, const SlabA
 // each step solved by Jacobi-PCG (symmetric) or Jacobi-BiCGStab with the
 // reference's control flow (sparse.cpp:60-206).
 struct Be2Params {
-  int m, M;              // points per axis, m*m
+  int m, M;              // columns (points per axis in 2D), unknowns m*my
+  int my;                // rows: m for a 2D grid, 1 for a general 1D operator
   int steps;             // backward-Euler steps per slab
   const double* coef;    // [5][M] device: south, west, centre, east, north of I + dt*A (0 = absent)
   const double* minv;    // [M] device: Jacobi inverse diagonal (jacobi_inverse_diagonal)
@@ -79,8 +80,8 @@ constexpr int kBe2Threads = 512;
 // vectors the compiler keeps in local memory, read the stencil rows from
 // global memory, and share one operand buffer between x and s^
 constexpr int kBe2MaxPPT = 20;
-size_t be2d_smem_bytes(int m);
-bool be2d_supported(int m);
+size_t be2d_smem_bytes(int m, int my);
+bool be2d_supported(int m, int my);
 cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st);
 cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st);
 cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long* iters,

@@ -392,8 +392,11 @@ template <int PPT>
 __device__ void setup(Be2Ctx<PPT>& c, const Be2Params& P, unsigned char* smem) {
   c.m = P.m;
   c.M = P.M;
-  c.pitch = P.m + 2;
-  const int np = c.pitch * c.pitch;
+  // one-row grids (general 1D operators) need no ghost rows: their south /
+  // north coefficients are exact zeros, so pitch 0 makes those operands the
+  // point itself (fma(0, finite, s) == s)
+  c.pitch = P.my == 1 ? 0 : P.m + 2;
+  const int np = P.my == 1 ? P.m + 2 : c.pitch * (P.my + 2);
   double* base = reinterpret_cast<double*>(smem);
   // big grids: x and s^ share a buffer (each operand is published right
   // before the stencil that reads it, never two of them at once)
@@ -519,18 +522,19 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
 
 }  // namespace
 
-size_t be2d_smem_bytes(int m) {
+size_t be2d_smem_bytes(int m, int my) {
   // three padded operand buffers, reduction slots, and (more than 3 points
   // per thread) the stencil rows and Jacobi inverse
-  const size_t np = (size_t)(m + 2) * (m + 2), M = (size_t)m * m;
+  const size_t np = my == 1 ? (size_t)(m + 2) : (size_t)(m + 2) * (my + 2), M = (size_t)m * my;
   const size_t ppt = (M + kBe2Threads - 1) / kBe2Threads;
   if (ppt > 5) return sizeof(double) * (2 * np + 4 * kNW);
   const bool reg_coef = ppt <= 3;
   return sizeof(double) * (3 * np + 4 * kNW + (reg_coef ? 0 : 6 * M));
 }
 
-bool be2d_supported(int m) {
-  return m >= 1 && m * m <= kBe2MaxPPT * kBe2Threads && be2d_smem_bytes(m) <= 227 * 1024;
+bool be2d_supported(int m, int my) {
+  return m >= 1 && my >= 1 && (long long)m * my <= kBe2MaxPPT * kBe2Threads &&
+         be2d_smem_bytes(m, my) <= 227 * 1024;
 }
 
 #define PIT_BE2_PPT(X) X(1) X(2) X(3) X(4) X(5) X(8) X(12) X(16) X(20)
@@ -542,10 +546,10 @@ static int be2d_ppt(int M) {
 
 cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st) {
   if (slabs <= 0) return cudaSuccess;
-  if (!be2d_supported(P.m)) return cudaErrorInvalidValue;
+  if (!be2d_supported(P.m, P.my)) return cudaErrorInvalidValue;
   const int ppt = be2d_ppt(P.M);
   if (ppt > 5 && P.minv != P.coef + 5 * (size_t)P.M) return cudaErrorInvalidValue;
-  const size_t smem = be2d_smem_bytes(P.m);
+  const size_t smem = be2d_smem_bytes(P.m, P.my);
 #define X(N)                                                                              \
   if (ppt == N) {                                                                         \
     auto k = be2d_batch_kernel<N>;                                                        \
@@ -562,10 +566,10 @@ cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, 
 
 cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st) {
   if (A.count <= 0) return cudaSuccess;
-  if (!be2d_supported(P.m)) return cudaErrorInvalidValue;
+  if (!be2d_supported(P.m, P.my)) return cudaErrorInvalidValue;
   const int ppt = be2d_ppt(P.M);
   if (ppt > 5 && P.minv != P.coef + 5 * (size_t)P.M) return cudaErrorInvalidValue;
-  const size_t smem = be2d_smem_bytes(P.m);
+  const size_t smem = be2d_smem_bytes(P.m, P.my);
 #define X(N)                                                                              \
   if (ppt == N) {                                                                         \
     auto k = be2d_sweep_kernel<N>;                                                        \

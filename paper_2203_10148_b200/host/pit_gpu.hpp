@@ -131,6 +131,14 @@ struct Problem1D {
   // the separable description; sampled at the end of every step
   // (propagator.cpp:56-63) into the C ABI's PIT_SOURCE_TABLE tables
   std::function<double(double t, double x)> source_fn;
+  // a general tridiagonal operator (pde.hpp:36-37: any CSR through the
+  // SpatialOperator constructor): [3][M] sub, diagonal, super entries per
+  // interior node; band_* are then ignored and every step is solved by
+  // Jacobi-PCG or (nonsymmetric) Jacobi-BiCGStab as in the reference
+  // (pde.cpp:112-130).  M <= 10240, no source.
+  std::vector<double> stencil;
+  bool nonsymmetric = false;
+  double fine_tolerance = 0.0, coarse_tolerance = 0.0;  // 0: 1e-12
   int device = 0;
 };
 
@@ -192,6 +200,14 @@ class BlockOperatorContext {  // pit::BlockOperatorContext (block_system.hpp:55-
     d.coarse_steps = p.coarse_steps;
     d.initial_value = p.y0.data();
     d.device = p.device;
+    if (!p.stencil.empty()) {
+      if (static_cast<int>(p.stencil.size()) != 3 * p.M)
+        throw std::invalid_argument("Problem1D: stencil must hold 3*M entries");
+      d.stencil = p.stencil.data();
+      d.nonsymmetric = p.nonsymmetric ? 1 : 0;
+      d.fine_tolerance = p.fine_tolerance;
+      d.coarse_tolerance = p.coarse_tolerance;
+    }
     std::vector<double> tab[2];
     if (p.source_fn) {
       const double h = (p.grid_hi - p.grid_lo) / (p.M + 1), slab = p.T / p.N;

@@ -24,6 +24,9 @@ class OracleProblem:
         if isinstance(p, api.Problem2DImplicit):
             self._init_be2d(p, mode)
             return
+        if isinstance(p, api.Problem1DGeneral):
+            self._init_be1d(p, mode)
+            return
         self.dim = 1
         fc, _ = api.step_coefficients(p, 0, fine_layout, coarse_layout)
         cc, _ = api.step_coefficients(p, 1, fine_layout, coarse_layout)
@@ -73,6 +76,23 @@ class OracleProblem:
                                           p.coarse_tolerance, p.coarse_max_iterations,
                                           O.ptr(self._keep[0]), mode)
         assert self.o, "orc_be2d_create failed"
+        self.prob = self.lib.orc_be2d_problem(self.o)
+
+    def _init_be1d(self, p, mode):
+        self.dim = 3  # the K6 mirror on a one-row grid
+        self.p = p
+        self.lib = O.orc()
+        st3 = np.ascontiguousarray(p.stencil, dtype=np.float64).reshape(3, p.M)
+        st = np.zeros((5, p.M))  # south, west, centre, east, north
+        st[1, 1:], st[2], st[3, :-1] = st3[0, 1:], st3[1], st3[2, :-1]
+        st = np.ascontiguousarray(st.reshape(-1))
+        self._keep = [np.ascontiguousarray(p.y0, dtype=np.float64).reshape(-1), st]
+        self.o = self.lib.orc_be2d_create_1d(p.M, p.grid_lo, p.grid_hi, O.ptr(st),
+                                             1 if p.nonsymmetric else 0, p.N, p.T, p.fine_steps,
+                                             p.coarse_steps, p.fine_tolerance,
+                                             p.fine_max_iterations, p.coarse_tolerance,
+                                             p.coarse_max_iterations, O.ptr(self._keep[0]), mode)
+        assert self.o, "orc_be2d_create_1d failed"
         self.prob = self.lib.orc_be2d_problem(self.o)
 
     def coarse_iterations(self):

@@ -143,6 +143,10 @@ def orc():
         lib.orc_be2d_create.argtypes = [C.c_int, C.c_double, C.c_double, _dp, C.c_int, C.c_int,
                                         C.c_double, C.c_int, C.c_int, C.c_double, C.c_longlong,
                                         C.c_double, C.c_longlong, _dp, C.c_int]
+        lib.orc_be2d_create_1d.restype = C.c_void_p
+        lib.orc_be2d_create_1d.argtypes = [C.c_int, C.c_double, C.c_double, _dp, C.c_int, C.c_int,
+                                        C.c_double, C.c_int, C.c_int, C.c_double, C.c_longlong,
+                                        C.c_double, C.c_longlong, _dp, C.c_int]
         lib.orc_be2d_destroy.argtypes = [C.c_void_p]
         lib.orc_be2d_problem.restype = C.c_void_p
         lib.orc_be2d_problem.argtypes = [C.c_void_p]
@@ -184,6 +188,9 @@ def ref():
         lib.pitref_assemble_rhs.argtypes = [C.c_void_p, _dp, C.c_int]
         lib.pitref_initial_guess.argtypes = [C.c_void_p, _dp]
         lib.pitref_sequential_fine.argtypes = [C.c_void_p, _dp]
+        lib.pitref_create_1d_csr.restype = C.c_void_p
+        lib.pitref_create_1d_csr.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp, _dp, C.c_int,
+                                             C.c_int, C.c_double, C.c_int, C.c_int, _dp]
         lib.pitref_propagate.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp]
         lib.pitref_sample_source.argtypes = [C.c_void_p, C.c_double, _dp]
         for name in ("pitref_pitsbicg", "pitref_parareal"):
