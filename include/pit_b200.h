@@ -82,9 +82,11 @@ enum { PIT_SCHEME_BACKWARD_EULER = 0, PIT_SCHEME_EXPLICIT_EULER = 1 };
  * walls (assemble_spatial_operator, src/pde.cpp:55-64: lo = -mu/h^2,
  * diag = 2mu/h^2 + r, up = -mu/h^2; any constant bands are accepted, e.g.
  * central-difference advection), the partition (T, N), steps per slab for
- * the fine and coarse propagators, and an optional separable source
- * f(t, x_i) = amp * sin(omega*t + phase) * shape[i] sampled at step ends
- * (src/propagator.cpp:61-65). */
+ * the fine and coarse propagators, and an optional source sampled at step
+ * ends (src/propagator.cpp:61-65): separable, f(t, x_i) = amp * sin(omega*t +
+ * phase) * shape[i], or a general SourceFn given as tables (PIT_SOURCE_TABLE).
+ * A general tridiagonal operator (variable coefficients) is given per node
+ * through `stencil` and solved iteratively, as the reference does. */
 typedef struct pit_problem_desc {
   int32_t dimension;      /* 1 */
   int32_t interior;       /* M */
