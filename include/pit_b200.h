@@ -130,7 +130,8 @@ typedef struct pit_problem_desc {
    * isotropic band_diag / band_lo stencil) and solve every step with
    * Jacobi-PCG, or Jacobi-BiCGStab when `nonsymmetric` (ImplicitStepSolver,
    * src/pde.cpp:112-130), to fine/coarse_tolerance (0: 1e-12) within
-   * fine/coarse_max_iterations (0: 10*M).  m <= 101 (grid_points <= 103). */
+   * fine/coarse_max_iterations (0: 10*M).  m <= 101 (grid_points <= 103);
+   * a source as PIT_SOURCE_TABLE. */
   /* dimension 1 with `stencil` set: a general tridiagonal operator (any
    * pit::SpatialOperator the reference's 1D propagators accept through the
    * CSR constructor, include/pit/pde.hpp:36-37, e.g. variable coefficients):
@@ -138,7 +139,7 @@ typedef struct pit_problem_desc {
    * A per interior node (0 where absent; band_* are ignored).  Every step is
    * then solved as the reference solves it, Jacobi-PCG or (nonsymmetric)
    * Jacobi-BiCGStab to fine/coarse_tolerance (K6 on a one-row grid);
-   * M <= 10240, no source. */
+   * M <= 10240; a source as PIT_SOURCE_TABLE. */
   const double* stencil;
   int32_t nonsymmetric;
   double fine_tolerance;

@@ -95,7 +95,7 @@ class Backend {
             "pit::gpu::Backend: the fine and coarse propagators must share one spatial operator");
     }
     if (g.dimension() == 2) {
-      init_2d(ctx, g, device);
+      init_2d(ctx, g, device, general);
       return;
     }
     const CsrMatrix& A = ctx.fine().op().matrix();
@@ -140,9 +140,9 @@ class Backend {
     if (!constant) {
       // Jacobi-PCG / Jacobi-BiCGStab per step, as the reference's
       // ImplicitStepSolver (pde.cpp:112-130); no direct solve, no source
-      if (ctx.fine().has_source())
+      if (ctx.fine().has_source() && !(general && *general))
         throw std::invalid_argument(
-            "pit::gpu::Backend: sources need a constant-coefficient operator");
+            "pit::gpu::Backend: a source on a variable-coefficient operator needs its SourceFn");
       d.stencil = tri.data();
       d.nonsymmetric = ctx.fine().op().symmetric() ? 0 : 1;
     }
@@ -155,21 +155,7 @@ class Backend {
     }
     std::vector<double> tab[2];
     if (!source && general && *general && ctx.fine().has_source()) {
-      const Propagator* prop[2] = {&ctx.fine(), &ctx.coarse()};
-      for (int r = 0; r < 2; ++r) {
-        const int steps = prop[r]->steps_per_slab();
-        const double dt = prop[r]->internal_dt();
-        tab[r].resize(static_cast<size_t>(d.slab_count) * steps * d.interior);
-        size_t at = 0;
-        for (int n = 0; n < d.slab_count; ++n) {
-          const double t0 = ctx.partition().breakpoint(n);
-          for (int k = 1; k <= steps; ++k)
-            for (int i = 0; i < d.interior; ++i) {
-              const double x[1] = {g.interior_coord(i)};
-              tab[r][at++] = (*general)(t0 + k * dt, x);
-            }
-        }
-      }
+      sample_tables(ctx, g, *general, tab);
       d.source_kind = PIT_SOURCE_TABLE;
       d.source_table_fine = tab[0].data();
       d.source_table_coarse = tab[1].data();
@@ -184,9 +170,44 @@ class Backend {
 
   // 2D: the per-row south/west/centre/east/north entries of A (0 when the
   // CSR row has none) and the operator's symmetry flag go to the device.
-  void init_2d(const BlockOperatorContext& ctx, const SpatialGrid& g, int device) {
-    if (ctx.fine().has_source())
-      throw std::invalid_argument("pit::gpu::Backend: no sources on 2D grids");
+  // The context's SourceFn sampled where Propagator::run samples it
+  // (propagator.cpp:25-47: every interior node, x fastest; 56-63: the end of
+  // every step) into the C ABI's PIT_SOURCE_TABLE tables.
+  static void sample_tables(const BlockOperatorContext& ctx, const SpatialGrid& g,
+                            const SourceFn& f, std::vector<double> (&tab)[2]) {
+    const Propagator* prop[2] = {&ctx.fine(), &ctx.coarse()};
+    const int m = g.interior_per_axis(), dim = g.dimension(), N = ctx.block_count();
+    const size_t M = dim == 2 ? static_cast<size_t>(m) * m : static_cast<size_t>(m);
+    for (int r = 0; r < 2; ++r) {
+      const int steps = prop[r]->steps_per_slab();
+      const double dt = prop[r]->internal_dt();
+      tab[r].resize(static_cast<size_t>(N) * steps * M);
+      size_t at = 0;
+      for (int n = 0; n < N; ++n) {
+        const double t0 = ctx.partition().breakpoint(n);
+        for (int k = 1; k <= steps; ++k) {
+          const double t = t0 + k * dt;
+          if (dim == 1) {
+            for (int i = 0; i < m; ++i) {
+              const double x[1] = {g.interior_coord(i)};
+              tab[r][at++] = f(t, x);
+            }
+          } else {
+            for (int j = 0; j < m; ++j)
+              for (int i = 0; i < m; ++i) {
+                const double x[2] = {g.interior_coord(i), g.interior_coord(j)};
+                tab[r][at++] = f(t, x);
+              }
+          }
+        }
+      }
+    }
+  }
+
+  void init_2d(const BlockOperatorContext& ctx, const SpatialGrid& g, int device,
+               const SourceFn* general) {
+    if (ctx.fine().has_source() && !(general && *general))
+      throw std::invalid_argument("pit::gpu::Backend: a source on a 2D grid needs its SourceFn");
     const SpatialOperator& op = ctx.fine().op();
     const CsrMatrix& A = op.matrix();
     const int m = g.interior_per_axis(), M = m * m;
@@ -213,6 +234,13 @@ class Backend {
     d.fine_scheme = PIT_SCHEME_BACKWARD_EULER;
     d.stencil = st.data();
     d.nonsymmetric = op.symmetric() ? 0 : 1;
+    std::vector<double> tab[2];
+    if (ctx.fine().has_source()) {
+      sample_tables(ctx, g, *general, tab);
+      d.source_kind = PIT_SOURCE_TABLE;
+      d.source_table_fine = tab[0].data();
+      d.source_table_coarse = tab[1].data();
+    }
     pit_context* c = nullptr;
     check(pit_context_create(&d, &c));
     h_.reset(c);

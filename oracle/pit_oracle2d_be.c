@@ -317,7 +317,14 @@ done:
   return ok;
 }
 
+static int propagate_tab(const orc_be2_role* R, const double* in, double* out,
+                         long long* iterations, const double* tab);
 int orc_be2_propagate(const orc_be2_role* R, const double* in, double* out, long long* iterations) {
+  return propagate_tab(R, in, out, iterations, NULL);
+}
+/* tab: general source fl(dt*f) [steps][n] added before every step, or NULL */
+static int propagate_tab(const orc_be2_role* R, const double* in, double* out,
+                         long long* iterations, const double* tab) {
   const int n = R->m * R->my;
   be2_ws w;
   w.n = n;
@@ -328,6 +335,8 @@ int orc_be2_propagate(const orc_be2_role* R, const double* in, double* out, long
   int ok = 1;
   for (int step = 0; step < R->steps && ok; ++step) {
     long long it = 0;
+    if (tab)
+      for (int i = 0; i < n; ++i) b[i] = b[i] + tab[(size_t)step * n + i];
     ok = R->symmetric ? be2_cg(R, &w, b, x, &it) : be2_bicgstab(R, &w, b, x, &it);
     if (iterations) *iterations += it;
     for (int i = 0; i < n && ok; ++i)
@@ -350,15 +359,20 @@ struct orc_be2d {
   orc_problem* prob;
   double* y0;
   long long coarse_iterations;
+  double* tab[2]; /* general source fl(dt*f) [N][steps][n] per role, or NULL */
+  double dt[2];
+  int N;
 };
 
 static int prop_be2(void* user, int role, int with_source, const double* in, int slab,
                     double* out) {
-  (void)with_source; /* no sources in 2D */
-  (void)slab;
   orc_be2d* o = (orc_be2d*)user;
   long long it = 0;
-  const int ok = orc_be2_propagate(&o->role[role], in, out, &it);
+  const orc_be2_role* R = &o->role[role];
+  const double* tab = NULL;
+  if (with_source && o->tab[role])
+    tab = o->tab[role] + (size_t)slab * R->steps * R->m * R->my;
+  const int ok = propagate_tab(R, in, out, &it, tab);
   if (role == ORC_COARSE) o->coarse_iterations += it;
   return ok ? 0 : 1;
 }
@@ -373,6 +387,9 @@ static orc_be2d* create_rect(int m, int my, double lo, double hi, const double* 
                  fine_cap, !nonsymmetric);
   role_init_rect(&o->role[ORC_COARSE], m, my, stencil, slab / coarse_steps, coarse_steps,
                  coarse_tol, coarse_cap, !nonsymmetric);
+  o->dt[ORC_FINE] = slab / fine_steps;
+  o->dt[ORC_COARSE] = slab / coarse_steps;
+  o->N = N;
   const size_t n = (size_t)m * my;
   o->y0 = (double*)malloc(n * sizeof(double));
   memcpy(o->y0, y0, n * sizeof(double));
@@ -399,8 +416,26 @@ orc_be2d* orc_be2d_create_1d(int M, double lo, double hi, const double* stencil,
                      fine_tol, fine_cap, coarse_tol, coarse_cap, y0, mode);
 }
 
+/* General source tables f(t_k, x_i) of both roles ([N][steps][n]); stored as
+ * fl(dt*f) (PIT_SOURCE_TABLE). */
+int orc_be2d_set_source_tables(orc_be2d* o, const double* fine, const double* coarse) {
+  const double* f[2] = {fine, coarse};
+  for (int r = 0; r < 2; ++r) {
+    const orc_be2_role* R = &o->role[r];
+    const size_t cnt = (size_t)o->N * R->steps * R->m * R->my;
+    free(o->tab[r]);
+    o->tab[r] = (double*)malloc(cnt * sizeof(double));
+    if (!o->tab[r]) return -1;
+    for (size_t i = 0; i < cnt; ++i) o->tab[r][i] = o->dt[r] * f[r][i];
+  }
+  o->prob->has_source = 1;
+  return 0;
+}
+
 void orc_be2d_destroy(orc_be2d* o) {
   if (!o) return;
+  free(o->tab[0]);
+  free(o->tab[1]);
   orc_problem_delete(o->prob);
   orc_be2_role_free(&o->role[0]);
   orc_be2_role_free(&o->role[1]);

@@ -40,6 +40,7 @@ orc_be2d* orc_be2d_create_1d(int M, double lo, double hi, const double* stencil,
                              int N, double total_time, int fine_steps, int coarse_steps,
                              double fine_tol, long long fine_cap, double coarse_tol,
                              long long coarse_cap, const double* y0, int mode);
+int orc_be2d_set_source_tables(orc_be2d* o, const double* fine, const double* coarse);
 orc_be2d* orc_be2d_create(int m, double lo, double hi, const double* stencil, int nonsymmetric,
                           int N, double total_time, int fine_steps, int coarse_steps,
                           double fine_tol, long long fine_cap, double coarse_tol,

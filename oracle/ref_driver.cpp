@@ -90,7 +90,7 @@ const char* pitref_last_error() { return g_err.c_str(); }
 // (pde.hpp:36-37): variable coefficients.  No source.
 void* pitref_create_1d_csr(int M, double lo, double hi, const double* sub, const double* diag,
                            const double* sup, int symmetric, int N, double T, int fine_steps,
-                           int coarse_steps, const double* y0);
+                           int coarse_steps, const double* y0, int test_source);
 
 // 1D context on [lo, hi] with M interior points.  When use_bands == 0 the
 // operator comes from assemble_spatial_operator(diffusion, reaction)
@@ -317,9 +317,11 @@ int pitref_sample_source(void* p, double t, double* out) {
   }
 }
 
+// test_source != 0: the non-separable source of pitref_create_1d (has_source
+// == 2) with amp 2, omega 3, phase 2 pi.
 void* pitref_create_1d_csr(int M, double lo, double hi, const double* sub, const double* diag,
                            const double* sup, int symmetric, int N, double T, int fine_steps,
-                           int coarse_steps, const double* y0) {
+                           int coarse_steps, const double* y0, int test_source) {
   try {
     auto r = std::make_unique<RefCtx>();
     r->M = M;
@@ -343,8 +345,14 @@ void* pitref_create_1d_csr(int M, double lo, double hi, const double* sub, const
     }
     const pit::SpatialOperator op(std::move(a), g, symmetric != 0);
     const pit::TimeSlabPartition part(T, N);
-    pit::Propagator fine(op, part, fine_steps, pit::PropagatorRole::Fine);
-    pit::Propagator coarse(op, part, coarse_steps, pit::PropagatorRole::Coarse);
+    pit::SourceFn src;
+    if (test_source)
+      src = [](double t, std::span<const double> x) {
+        return 2.0 * ((1.0 + t) * x[0] * (1.0 - x[0]) + std::sin(3.0 * t) * std::cos(2.0 * M_PI * x[0]));
+      };
+    r->src = src;
+    pit::Propagator fine(op, part, fine_steps, pit::PropagatorRole::Fine, src);
+    pit::Propagator coarse(op, part, coarse_steps, pit::PropagatorRole::Coarse, src);
     pit::ScalarField init(g, std::vector<double>(y0, y0 + M));
     r->ctx = std::make_unique<pit::BlockOperatorContext>(std::move(fine), std::move(coarse),
                                                           std::move(init));

@@ -121,6 +121,23 @@ class TableSource:
         return TableSource(out[0], out[1])
 
 
+def _attach_tables(d, keep, source, N, fine_steps, coarse_steps, M):
+    """PIT_SOURCE_TABLE fields of a problem description."""
+    if source is None:
+        return
+    if not isinstance(source, TableSource):
+        raise ValueError("this problem class takes its source as a TableSource")
+    tabs = []
+    for tab, steps in ((source.fine, fine_steps), (source.coarse, coarse_steps)):
+        t = np.ascontiguousarray(tab, dtype=np.float64)
+        if t.shape != (N, steps, M):
+            raise ValueError("TableSource: tables are [N, steps, M] per propagator")
+        keep.append(t)
+        tabs.append(t)
+    d.source_kind = _lib.PIT_SOURCE_TABLE
+    d.source_table_fine, d.source_table_coarse = dptr(tabs[0]), dptr(tabs[1])
+
+
 @dataclass
 class Problem1D:
     """Everything BlockOperatorContext needs for a 1D problem.
@@ -274,7 +291,7 @@ class Problem2DImplicit:
     coarse_tolerance: float = 1e-12
     fine_max_iterations: int = 0
     coarse_max_iterations: int = 0
-    source: Optional[SeparableSource] = None  # the presets have f = 0
+    source: Optional[object] = None  # a TableSource (the presets have f = 0)
 
     @property
     def M(self) -> int:
@@ -310,6 +327,7 @@ class Problem2DImplicit:
         d.fine_tolerance, d.coarse_tolerance = self.fine_tolerance, self.coarse_tolerance
         d.fine_max_iterations = self.fine_max_iterations
         d.coarse_max_iterations = self.coarse_max_iterations
+        _attach_tables(d, keep, self.source, self.N, self.fine_steps, self.coarse_steps, self.M)
         return d, keep
 
 
@@ -322,7 +340,8 @@ class Problem1DGeneral:
     interior node (0 where absent).  Every backward-Euler step is solved as
     the reference solves it (ImplicitStepSolver, src/pde.cpp:112-130):
     Jacobi-PCG, or Jacobi-BiCGStab when `nonsymmetric`, to 1e-12.  Constant
-    bands should use Problem1D (the direct solve); M <= 10240; no source."""
+    bands should use Problem1D (the direct solve); M <= 10240; a source, if
+    any, as a TableSource."""
     M: int
     stencil: np.ndarray
     nonsymmetric: bool
@@ -337,7 +356,7 @@ class Problem1DGeneral:
     coarse_tolerance: float = 1e-12
     fine_max_iterations: int = 0
     coarse_max_iterations: int = 0
-    source: Optional[object] = None  # unsupported (must stay None)
+    source: Optional[object] = None  # a TableSource, or None
 
     @property
     def spacing(self) -> float:
@@ -348,8 +367,6 @@ class Problem1DGeneral:
         return np.array([self.grid_lo + (k + 1) * h for k in range(self.M)])
 
     def desc(self, device: int = 0, fine_layout=None, coarse_layout=None):
-        if self.source is not None:
-            raise ValueError("Problem1DGeneral: sources are not supported")
         d = _lib.ProblemDesc()
         d.dimension = 1
         d.interior = self.M
@@ -369,6 +386,7 @@ class Problem1DGeneral:
         d.fine_tolerance, d.coarse_tolerance = self.fine_tolerance, self.coarse_tolerance
         d.fine_max_iterations = self.fine_max_iterations
         d.coarse_max_iterations = self.coarse_max_iterations
+        _attach_tables(d, keep, self.source, self.N, self.fine_steps, self.coarse_steps, self.M)
         return d, keep
 
 

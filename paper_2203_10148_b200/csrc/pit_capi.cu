@@ -204,9 +204,10 @@ int validate_desc(const pit_problem_desc* d) {
     if (!be2d_supported(d->interior, 1))
       return set_err(PIT_ERR_INVALID_ARGUMENT,
                      "pit_context_create: general 1D operators need M <= 10240");
-    if (d->source_kind != PIT_SOURCE_NONE)
+    if (d->source_kind != PIT_SOURCE_NONE && d->source_kind != PIT_SOURCE_TABLE)
       return set_err(PIT_ERR_INVALID_ARGUMENT,
-                     "pit_context_create: no sources with a general 1D operator");
+                     "pit_context_create: a general 1D operator takes its source as tables "
+                     "(PIT_SOURCE_TABLE)");
     if (d->coarse_tolerance < 0.0 || d->fine_tolerance < 0.0)
       return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: negative inner tolerance");
   }
@@ -217,8 +218,9 @@ int validate_desc(const pit_problem_desc* d) {
     if (!d->stencil && d->band_lo != d->band_up)
       return set_err(PIT_ERR_INVALID_ARGUMENT,
                      "pit_context_create: 2D band operators are isotropic (band_lo == band_up)");
-    if (d->source_kind != PIT_SOURCE_NONE)
-      return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: no sources in 2D");
+    if (d->source_kind != PIT_SOURCE_NONE && d->source_kind != PIT_SOURCE_TABLE)
+      return set_err(PIT_ERR_INVALID_ARGUMENT,
+                     "pit_context_create: 2D sources are given as tables (PIT_SOURCE_TABLE)");
     if (d->coarse_tolerance < 0.0 || d->fine_tolerance < 0.0)
       return set_err(PIT_ERR_INVALID_ARGUMENT, "pit_context_create: negative inner tolerance");
   } else if (d->dimension == 2) {
@@ -488,6 +490,20 @@ void bind_status(pit_context* ctx, SweepArgs* A) {
   A->fail_info = ctx->d_status->fail;
 }
 
+int attach_pieces(pit_context* ctx, SlabArgs* A, int ctas);
+// Fine propagation WITH source of a batch of slabs (assemble_rhs): K1's source
+// path, or K6 with the source table.
+int launch_fine_source(pit_context* ctx, SlabArgs& A, int ctas, cudaStream_t st) {
+  if (ctx->be2) {
+    CUDA_TRY(launch_be2d_batch(ctx->bp[PIT_FINE], A, ctas, st, true));
+    return PIT_OK;
+  }
+  Role& R = ctx->role[PIT_FINE];
+  PIT_TRY(attach_pieces(ctx, &A, ctas));
+  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctas, st));
+  return PIT_OK;
+}
+
 // State and scheduler buffers for K1 piece scheduling (grow-only; the
 // launcher decides whether the batch is cut into pieces at all).
 int attach_pieces(pit_context* ctx, SlabArgs* A, int ctas) {
@@ -590,7 +606,7 @@ int launch_sweep_any(pit_context* ctx, int role, bool src, const SweepArgs& A, c
     return PIT_OK;
   }
   if (ctx->be2) {
-    CUDA_TRY(launch_be2d_sweep(ctx->bp[role], A, st));
+    CUDA_TRY(launch_be2d_sweep(ctx->bp[role], A, st, src));
     return PIT_OK;
   }
   if (role == PIT_COARSE) {
@@ -858,9 +874,10 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
     const double slab = desc->total_time / desc->slab_count;
     for (int r = 0; r < 2; ++r) {
       Role& R = ctx->role[r];
-      const double dt = slab / R.c.steps;
+      const int steps_r = r == PIT_FINE ? desc->fine_steps : desc->coarse_steps;
+      const double dt = slab / steps_r;
       const double* f = r == PIT_FINE ? desc->source_table_fine : desc->source_table_coarse;
-      const size_t n = (size_t)ctx->N * R.c.steps * ctx->M;
+      const size_t n = (size_t)ctx->N * steps_r * ctx->M;
       std::vector<double> tab(n);
       for (size_t i = 0; i < n; ++i) tab[i] = dt * f[i];
       if (cudaMalloc(&R.d_tab, sizeof(double) * n) != cudaSuccess ||
@@ -869,6 +886,7 @@ int pit_context_create(const pit_problem_desc* desc, pit_context** out) {
         return fail(set_err(PIT_ERR_CUDA, "pit_context_create: the source table does not fit "
                                           "the device (N*steps*M doubles per propagator)"));
       R.P.tab = R.d_tab;
+      if (ctx->be2) ctx->bp[r].tab = R.d_tab;
     }
   } else if (ctx->has_source) {
     if (cudaMalloc(&ctx->d_shape, sizeof(double) * ctx->M) != cudaSuccess ||
@@ -1120,8 +1138,7 @@ int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, 
   const int skip = first == 0 ? 1 : 0;  // block 0 is y0, set by the caller
   A.out = out + (size_t)skip * ctx->M;
   A.slab0 = first + skip - 1;
-  PIT_TRY(attach_pieces(ctx, &A, count - skip));
-  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, count - skip, st));
+  PIT_TRY(launch_fine_source(ctx, A, count - skip, st));
   return PIT_OK;
 }
 
@@ -1376,8 +1393,7 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
     A.out = d.p + ctx->M;
     A.slab0 = 0;
     bind_status(ctx, &A);
-    PIT_TRY(attach_pieces(ctx, &A, ctx->N - 1));
-    CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+    PIT_TRY(launch_fine_source(ctx, A, ctx->N - 1, ctx->stream));
     PIT_TRY(check_status(ctx, true));
     add_fine(ctx, stats, ms_since(t0));
   }
@@ -1421,8 +1437,7 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
   A.mode = kPropagate;
   A.out = d + ctx->M;
   bind_status(ctx, &A);
-  PIT_TRY(attach_pieces(ctx, &A, ctx->N - 1));
-  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, ctx->N - 1, ctx->stream));
+  PIT_TRY(launch_fine_source(ctx, A, ctx->N - 1, ctx->stream));
   PIT_TRY(check_status(ctx, true));
   add_fine(ctx, stats, ms_since(t0));
   return PIT_OK;
@@ -1558,8 +1573,7 @@ int fine_source(pit_context* ctx, double* out, int first, int count, cudaStream_
   bind_status(ctx, &A);
   A.out = out + (size_t)skip * ctx->M;
   A.slab0 = first + skip - 1;
-  PIT_TRY(attach_pieces(ctx, &A, count - skip));
-  CUDA_TRY(launch_slab(R.mpt, R.nsub, R.nseg, R.warps, true, R.P, A, count - skip, st));
+  PIT_TRY(launch_fine_source(ctx, A, count - skip, st));
   return PIT_OK;
 }
 

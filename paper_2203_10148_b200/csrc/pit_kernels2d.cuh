@@ -72,6 +72,7 @@ struct Be2Params {
   int cap;               // kInnerSolveCapFactor * n (pde.hpp:79)
   int symmetric;         // 1: solve_cg, 0: solve_bicgstab (ImplicitStepSolver::solve)
   long long* iters;      // sweeps: cumulative inner iterations (optional)
+  const double* tab;     // general source fl(dt*f) [N*steps][M] (PIT_SOURCE_TABLE) or nullptr
 };
 constexpr int kBe2Threads = 512;
 // points per thread: up to 5 (m <= 50) everything a thread owns sits in
@@ -82,8 +83,12 @@ constexpr int kBe2Threads = 512;
 constexpr int kBe2MaxPPT = 20;
 size_t be2d_smem_bytes(int m, int my);
 bool be2d_supported(int m, int my);
-cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st);
-cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st);
+// src: add the source table before every step (Propagator::propagate);
+// otherwise the homogeneous map
+cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st,
+                              bool src = false);
+cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st,
+                              bool src = false);
 cudaError_t launch_cg_sweep2d(const Cg2Params& P, const SweepArgs& A, long long* iters,
                               cudaStream_t st);
 

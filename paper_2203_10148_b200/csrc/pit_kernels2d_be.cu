@@ -361,9 +361,15 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
 // pde.cpp:119-128).
 template <int PPT>
 __device__ bool propagate(Be2Ctx<PPT>& c, Vec<PPT>& y, const Be2Params& P, long long* iters,
-                          double* fail_info = nullptr) {
+                          double* fail_info = nullptr, const double* tab = nullptr) {
   Vec<PPT> x;
   for (int step = 0; step < P.steps; ++step) {
+    if (tab != nullptr) {  // rhs = y + dt*f(t_step) (propagator.cpp:60-62)
+      const double* tk = tab + (size_t)step * P.M;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k)
+        if (c.ip[k] >= 0) y[k] = y[k] + tk[threadIdx.x + k * kT];
+    }
     int it = 0;
     double relres = 0.0;
     const bool ok = P.symmetric ? cg_solve(c, y, x, P.rel_tol, P.cap, &it, &relres)
@@ -447,7 +453,8 @@ __device__ __forceinline__ void load_block(const Be2Ctx<PPT>& c, Vec<PPT>& dst, 
 // writes out + b*M (apply_F / residual / propagate epilogues).
 template <int PPT>
 __global__ void __launch_bounds__(kBe2Threads, 1)
-    be2d_batch_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SlabArgs A) {
+    be2d_batch_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SlabArgs A,
+                      const int with_source) {
   if (A.skip != nullptr && *A.skip) return;  // device solver loop: branch taken
   extern __shared__ __align__(16) unsigned char smem_raw[];
   long long tb0 = 0;  // busy time of the slab (DevStatus::busy_ns)
@@ -460,7 +467,9 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
                                           : A.halo;
   Vec<PPT> y;
   load_block(c, y, src);
-  const bool ok = propagate(c, y, P, nullptr);
+  const double* tab =
+      with_source && P.tab != nullptr ? P.tab + (size_t)slab * P.steps * (size_t)M : nullptr;
+  const bool ok = propagate(c, y, P, nullptr, nullptr, tab);
   if (!ok && threadIdx.x == 0) atomicMin(A.status, slab);
   const size_t off = (size_t)b * M;
 #pragma unroll
@@ -495,7 +504,8 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
 // Sequential sweep (SweepArgs semantics of K2): W_b = Prop(W_{b-1}) (+ V_b).
 template <int PPT>
 __global__ void __launch_bounds__(kBe2Threads, 1)
-    be2d_sweep_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SweepArgs A) {
+    be2d_sweep_kernel(const __grid_constant__ Be2Params P, const __grid_constant__ SweepArgs A,
+                      const int with_source) {
   if (A.skip != nullptr && *A.skip) return;  // device solver loop: branch taken
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Be2Ctx<PPT> c;
@@ -504,7 +514,10 @@ __global__ void __launch_bounds__(kBe2Threads, 1)
   Vec<PPT> y;
   load_block(c, y, A.start);
   for (int b = 0; b < A.count; ++b) {
-    if (!propagate(c, y, P, P.iters, A.fail_info)) {
+    const double* tab = with_source && P.tab != nullptr
+                            ? P.tab + (size_t)(A.slab0 + b) * P.steps * (size_t)M
+                            : nullptr;
+    if (!propagate(c, y, P, P.iters, A.fail_info, tab)) {
       if (threadIdx.x == 0) atomicMin(A.status, A.slab0 + b);
       return;
     }
@@ -544,7 +557,8 @@ static int be2d_ppt(int M) {
   return ppt <= 5 ? ppt : 4 * ((ppt + 3) / 4);
 }
 
-cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st) {
+cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, cudaStream_t st,
+                              bool src) {
   if (slabs <= 0) return cudaSuccess;
   if (!be2d_supported(P.m, P.my)) return cudaErrorInvalidValue;
   const int ppt = be2d_ppt(P.M);
@@ -556,7 +570,7 @@ cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, 
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                                          (int)smem);                                      \
     if (e != cudaSuccess) return e;                                                       \
-    k<<<slabs, kBe2Threads, smem, st>>>(P, A);                                            \
+    k<<<slabs, kBe2Threads, smem, st>>>(P, A, src ? 1 : 0);                                            \
     return cudaGetLastError();                                                            \
   }
   PIT_BE2_PPT(X)
@@ -564,7 +578,7 @@ cudaError_t launch_be2d_batch(const Be2Params& P, const SlabArgs& A, int slabs, 
   return cudaErrorInvalidConfiguration;
 }
 
-cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st) {
+cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream_t st, bool src) {
   if (A.count <= 0) return cudaSuccess;
   if (!be2d_supported(P.m, P.my)) return cudaErrorInvalidValue;
   const int ppt = be2d_ppt(P.M);
@@ -576,7 +590,7 @@ cudaError_t launch_be2d_sweep(const Be2Params& P, const SweepArgs& A, cudaStream
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                                          (int)smem);                                      \
     if (e != cudaSuccess) return e;                                                       \
-    k<<<1, kBe2Threads, smem, st>>>(P, A);                                                \
+    k<<<1, kBe2Threads, smem, st>>>(P, A, src ? 1 : 0);                                                \
     return cudaGetLastError();                                                            \
   }
   PIT_BE2_PPT(X)

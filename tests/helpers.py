@@ -76,7 +76,14 @@ class OracleProblem:
                                           p.coarse_tolerance, p.coarse_max_iterations,
                                           O.ptr(self._keep[0]), mode)
         assert self.o, "orc_be2d_create failed"
+        self._tables(p)
         self.prob = self.lib.orc_be2d_problem(self.o)
+
+    def _tables(self, p):
+        if isinstance(p.source, api.TableSource):
+            tf = np.ascontiguousarray(p.source.fine, dtype=np.float64)
+            tc = np.ascontiguousarray(p.source.coarse, dtype=np.float64)
+            assert self.lib.orc_be2d_set_source_tables(self.o, O.ptr(tf), O.ptr(tc)) == 0
 
     def _init_be1d(self, p, mode):
         self.dim = 3  # the K6 mirror on a one-row grid
@@ -93,6 +100,7 @@ class OracleProblem:
                                              p.fine_max_iterations, p.coarse_tolerance,
                                              p.coarse_max_iterations, O.ptr(self._keep[0]), mode)
         assert self.o, "orc_be2d_create_1d failed"
+        self._tables(p)
         self.prob = self.lib.orc_be2d_problem(self.o)
 
     def coarse_iterations(self):

@@ -148,6 +148,7 @@ def orc():
                                         C.c_double, C.c_int, C.c_int, C.c_double, C.c_longlong,
                                         C.c_double, C.c_longlong, _dp, C.c_int]
         lib.orc_be2d_destroy.argtypes = [C.c_void_p]
+        lib.orc_be2d_set_source_tables.argtypes = [C.c_void_p, _dp, _dp]
         lib.orc_be2d_problem.restype = C.c_void_p
         lib.orc_be2d_problem.argtypes = [C.c_void_p]
         lib.orc_be2d_coarse_iterations.restype = C.c_longlong
@@ -190,7 +191,7 @@ def ref():
         lib.pitref_sequential_fine.argtypes = [C.c_void_p, _dp]
         lib.pitref_create_1d_csr.restype = C.c_void_p
         lib.pitref_create_1d_csr.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp, _dp, C.c_int,
-                                             C.c_int, C.c_double, C.c_int, C.c_int, _dp]
+                                             C.c_int, C.c_double, C.c_int, C.c_int, _dp, C.c_int]
         lib.pitref_propagate.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.c_int, _dp]
         lib.pitref_sample_source.argtypes = [C.c_void_p, C.c_double, _dp]
         for name in ("pitref_pitsbicg", "pitref_parareal"):
