@@ -196,3 +196,17 @@ def test_2d_preset_with_source_bitwise_vs_oracle():
         res = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-8))
     r = o.solve(1e-8)
     assert np.array_equal(res.solution, r["lam"])
+
+
+@pytest.mark.gpu
+def test_pit_verify_on_a_general_operator():
+    """run_oracle_checks (src/dense_oracle.cpp, `pit verify`) through the
+    device operators of a variable-coefficient context, with the negative
+    control."""
+    from paper_2203_10148_b200 import verify
+    p = make(40, 3, True)
+    with api.BlockOperatorContext(p) as ctx:
+        rep = verify.run_oracle_checks(ctx, trials=5, tolerance=1e-9)
+        assert all(c.passed for c in rep.checks), [(c.name, c.worst_relative_error) for c in rep.checks]
+        bad = verify.run_oracle_checks(ctx, trials=5, tolerance=1e-9, inject_fault=True)
+        assert not all(c.passed for c in bad.checks)
