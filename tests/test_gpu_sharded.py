@@ -18,6 +18,7 @@ import sys
 import numpy as np
 import pytest
 
+from cases import make_case
 from paper_2203_10148_b200 import api, configs
 
 pytestmark = pytest.mark.gpu
@@ -63,7 +64,8 @@ def _port():
     return port
 
 
-@pytest.mark.parametrize("case,slabs,world", [("c2", 9, 2), ("c4", 7, 3), ("c5", 5, 2)])
+@pytest.mark.parametrize("case,slabs,world", [("c2", 9, 2), ("c4", 7, 3), ("c5", 5, 2),
+                                              ("c1t", 7, 3), ("gen", 6, 2)])
 def test_host_transport_multi_rank_bitwise(case, slabs, world, tmp_path):
     out = str(tmp_path / "res.npz")
     port = _port()
@@ -81,7 +83,7 @@ def test_host_transport_multi_rank_bitwise(case, slabs, world, tmp_path):
             raise
     assert all(pr.returncode == 0 for pr in procs), "\n".join(logs)
     g = np.load(out)
-    p = configs.make(case, slabs=slabs, M=32 if case == "c5" else None)
+    p = make_case(case, slabs)
     with api.BlockOperatorContext(p) as ctx:
         fref = api.apply_F(ctx, g["L"])
         ref = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))

@@ -15,7 +15,9 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from paper_2203_10148_b200 import api, configs  # noqa: E402
+sys.path.insert(0, os.path.dirname(HERE))
+from cases import make_case  # noqa: E402
+from paper_2203_10148_b200 import api  # noqa: E402
 from paper_2203_10148_b200.distributed import Communicator, ShardedContext  # noqa: E402
 
 
@@ -25,7 +27,7 @@ def main():
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     torch.cuda.set_device(0)
-    p = configs.make(case, slabs=slabs, M=32 if case == "c5" else None)
+    p = make_case(case, slabs)
     comm = Communicator.host(rank, world)
     with api.BlockOperatorContext(p) as ctx:
         sc = ShardedContext(ctx, comm)
