@@ -40,12 +40,18 @@ struct Be2Ctx {
   static constexpr bool kBig = PPT > 5;  // stencil rows in global memory, two operand buffers
   int m, M, pitch;
   int ip[PPT];        // padded index of owned point k (or -1)
+  int ir[PPT];        // index the stencil reads for slot k: ip, or a real point's for an empty
+                      // slot (its values are selected to 0: every slot computes, no branches)
   int gi[PPT];        // interior index of owned point k
   double cr[6][kRegCoef ? PPT : 1];  // S, W, C, E, N, minv (kRegCoef)
   const double* cf;   // [6][M] shared memory (!kRegCoef), global memory (kBig)
   double* red;        // [2][2][kNW]
   int par;            // reduction slot set
   double *opx, *opp, *ops;  // padded operand buffers (x, p or p^, s^)
+  __device__ __forceinline__ bool ok(int k) const { return ip[k] >= 0; }
+  // v for an owned point, exact 0 for an empty slot (so the slot's vectors
+  // stay 0 through every linear update and add fma(0, 0, s) == s to the sums)
+  __device__ __forceinline__ double keep(int k, double v) const { return ip[k] >= 0 ? v : 0.0; }
   __device__ __forceinline__ double coef(int j, int k) const {
     if constexpr (kRegCoef) return cr[j][k];
     return cf[(size_t)j * M + gi[k]];
@@ -85,8 +91,7 @@ template <int PPT>
 __device__ __forceinline__ double dot1(Be2Ctx<PPT>& c, const Vec<PPT>& a, const Vec<PPT>& b) {
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) s = fma(a[k], b[k], s);
+  for (int k = 0; k < PPT; ++k) s = fma(a[k], b[k], s);
   return block_sum2(c, s, 0.0).x;
 }
 template <int PPT>
@@ -94,11 +99,10 @@ __device__ __forceinline__ double2 dot2(Be2Ctx<PPT>& c, const Vec<PPT>& a, const
                                         const Vec<PPT>& e, const Vec<PPT>& f) {
   double s = 0.0, t = 0.0;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) {
-      s = fma(a[k], b[k], s);
-      t = fma(e[k], f[k], t);
-    }
+  for (int k = 0; k < PPT; ++k) {
+    s = fma(a[k], b[k], s);
+    t = fma(e[k], f[k], t);
+  }
   return block_sum2(c, s, t);
 }
 
@@ -106,7 +110,7 @@ __device__ __forceinline__ double2 dot2(Be2Ctx<PPT>& c, const Vec<PPT>& a, const
 // (assemble_spatial_operator's row order); op complete (barrier).
 template <int PPT>
 __device__ __forceinline__ double stencil(const Be2Ctx<PPT>& c, int k, const double* op) {
-  const int i = c.ip[k];
+  const int i = c.ir[k];
   double s = 0.0;
   s = fma(c.coef(0, k), op[i - c.pitch], s);
   s = fma(c.coef(1, k), op[i - 1], s);
@@ -131,11 +135,10 @@ __device__ __forceinline__ double true_residual(Be2Ctx<PPT>& c, const Vec<PPT>& 
   __syncthreads();  // x complete
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k)
-    if (c.ip[k] >= 0) {
-      r[k] = b[k] - stencil(c, k, c.opx);
-      s = fma(r[k], r[k], s);
-    }
+  for (int k = 0; k < PPT; ++k) {
+    r[k] = c.keep(k, b[k] - stencil(c, k, c.opx));
+    s = fma(r[k], r[k], s);
+  }
   return sqrt(block_sum2(c, s, 0.0).x);
 }
 
@@ -167,11 +170,10 @@ __device__ bool cg_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, double 
       __syncthreads();  // p complete
       double pq = 0.0;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) {
-          q[k] = stencil(c, k, c.opp);
-          pq = fma(p[k], q[k], pq);
-        }
+      for (int k = 0; k < PPT; ++k) {
+        q[k] = c.keep(k, stencil(c, k, c.opp));
+        pq = fma(p[k], q[k], pq);
+      }
       pq = block_sum2(c, pq, 0.0).x;
       if (pq == 0.0 || !isfinite(pq)) {
         stalled = true;
@@ -269,11 +271,10 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
     __syncthreads();  // ph complete
     double rv = 0.0;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) {
-        v[k] = stencil(c, k, c.opp);
-        rv = fma(rt[k], v[k], rv);
-      }
+    for (int k = 0; k < PPT; ++k) {
+      v[k] = c.keep(k, stencil(c, k, c.opp));
+      rv = fma(rt[k], v[k], rv);
+    }
     rv = block_sum2(c, rv, 0.0).x;
     if (rv == 0.0 || !isfinite(rv)) {
       restart = true;
@@ -283,16 +284,14 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
     alpha = rho / rv;
     double ss = 0.0;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) {
-        s[k] = fma(-alpha, v[k], r[k]);
-        ss = fma(s[k], s[k], ss);
-      }
+    for (int k = 0; k < PPT; ++k) {
+      s[k] = fma(-alpha, v[k], r[k]);
+      ss = fma(s[k], s[k], ss);
+    }
     if (sqrt(block_sum2(c, ss, 0.0).x) <= tol) {
       // half-iteration exit; keep going from the exact residual if spurious
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) x[k] = fma(alpha, ph[c.ip[k]], x[k]);
+      for (int k = 0; k < PPT; ++k) x[k] = fma(alpha, c.keep(k, ph[c.ir[k]]), x[k]);
       ++it;
       res = true_residual(c, b, x, r);
       if (res <= tol) {
@@ -318,22 +317,20 @@ __device__ bool bicgstab_solve(Be2Ctx<PPT>& c, const Vec<PPT>& b, Vec<PPT>& x, d
     __syncthreads();  // sh complete
     double tt = 0.0, ts = 0.0;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) {
-        t[k] = stencil(c, k, c.ops);
-        tt = fma(t[k], t[k], tt);
-        ts = fma(t[k], s[k], ts);
-      }
+    for (int k = 0; k < PPT; ++k) {
+      t[k] = c.keep(k, stencil(c, k, c.ops));
+      tt = fma(t[k], t[k], tt);
+      ts = fma(t[k], s[k], ts);
+    }
     const double2 d = block_sum2(c, tt, ts);
     omega = d.x == 0.0 ? 0.0 : d.y / d.x;
     double rr = 0.0;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k)
-      if (c.ip[k] >= 0) {
-        x[k] = fma(omega, sh[c.ip[k]], fma(alpha, ph[c.ip[k]], x[k]));
-        r[k] = fma(-omega, t[k], s[k]);
-        rr = fma(r[k], r[k], rr);
-      }
+    for (int k = 0; k < PPT; ++k) {
+      x[k] = fma(omega, c.keep(k, sh[c.ir[k]]), fma(alpha, c.keep(k, ph[c.ir[k]]), x[k]));
+      r[k] = fma(-omega, t[k], s[k]);
+      rr = fma(r[k], r[k], rr);
+    }
     ++it;
     res = sqrt(block_sum2(c, rr, 0.0).x);
     if (!isfinite(res)) {
@@ -367,8 +364,7 @@ __device__ bool propagate(Be2Ctx<PPT>& c, Vec<PPT>& y, const Be2Params& P, long 
     if (tab != nullptr) {  // rhs = y + dt*f(t_step) (propagator.cpp:60-62)
       const double* tk = tab + (size_t)step * P.M;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k)
-        if (c.ip[k] >= 0) y[k] = y[k] + tk[threadIdx.x + k * kT];
+      for (int k = 0; k < PPT; ++k) y[k] = y[k] + c.keep(k, tk[c.gi[k]]);
     }
     int it = 0;
     double relres = 0.0;
@@ -430,8 +426,10 @@ __device__ void setup(Be2Ctx<PPT>& c, const Be2Params& P, unsigned char* smem) {
     if (i < P.M) {
       const int ix = i % P.m, iy = i / P.m;
       c.ip[k] = (iy + 1) * c.pitch + ix + 1;
+      c.ir[k] = c.ip[k];
     } else {
       c.ip[k] = -1;
+      c.ir[k] = c.pitch + 1;  // point 0: in bounds with all its neighbours
     }
     if constexpr (Be2Ctx<PPT>::kRegCoef) {
 #pragma unroll
