@@ -276,15 +276,16 @@ def run_reference_arm(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def device_apply_rate(name, reps=3):
+def device_apply_rate(name, reps=3, slabs=None):
     """Best-of-reps device apply_F (inputs resident, dedicated stream) of a
-    full BASELINE config: (gp-steps/s, ms, gp-steps)."""
+    full BASELINE config (or the same per-slab work on `slabs` slabs):
+    (gp-steps/s, ms, gp-steps)."""
     import torch
 
     from paper_2203_10148_b200 import _lib, api, configs
 
     L = _lib.lib()
-    p = configs.make(name)
+    p = configs.make(name, slabs=slabs)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream), api.BlockOperatorContext(p) as ctx:
         x = torch.tensor(np.tile(p.y0, (p.N, 1)), device="cuda")
@@ -475,6 +476,15 @@ def secondary(include_c5_solve=True):
             out["apply_F"][name] = {"gp_steps_per_s": rate, "ms": ms, "gp_steps": gp}
         except Exception as e:  # pragma: no cover
             out["apply_F"][name] = {"error": str(e)}
+    # the same K1 on ten waves of c2 slabs (8881 blocks): the rate the kernel
+    # sustains when finished CTAs are replaced at once; c2's 1023 slabs are
+    # 1.15 waves of 888 resident CTAs
+    try:
+        rate, ms, gp = device_apply_rate("c2", slabs=8881)
+        out["apply_F"]["c2_ten_waves"] = {"gp_steps_per_s": rate, "ms": ms, "gp_steps": gp,
+                                          "slabs": 8880}
+    except Exception as e:  # pragma: no cover
+        out["apply_F"]["c2_ten_waves"] = {"error": str(e)}
     for name in ("c1", "c2", "c3", "c4") + (("c5",) if include_c5_solve else ()):
         try:
             out["time_to_tolerance"][name] = device_time_to_tolerance(name)
