@@ -1131,7 +1131,6 @@ int pit_fine_source_device(pit_context* ctx, double* out, int first, int count, 
   cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
   CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)count * ctx->M * sizeof(double), st));
   if (!ctx->has_source) return PIT_OK;
-  Role& R = ctx->role[PIT_FINE];
   SlabArgs A{};
   A.mode = kPropagate;
   bind_status(ctx, &A);
@@ -1386,7 +1385,6 @@ int pit_assemble_rhs(pit_context* ctx, double* rhs, pit_run_stats* stats) {
   CUDA_TRY(cudaMemcpyAsync(d.p, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
                            ctx->stream));
   if (ctx->has_source) {
-    Role& R = ctx->role[PIT_FINE];
     SlabArgs A{};
     A.mode = kPropagate;
     A.in = nullptr;
@@ -1432,7 +1430,6 @@ int assemble_rhs_dev(pit_context* ctx, double* d, pit_run_stats* stats) {
   CUDA_TRY(cudaMemcpyAsync(d, ctx->d_y0, ctx->M * sizeof(double), cudaMemcpyDeviceToDevice,
                            ctx->stream));
   if (!ctx->has_source) return PIT_OK;
-  Role& R = ctx->role[PIT_FINE];
   SlabArgs A{};
   A.mode = kPropagate;
   A.out = d + ctx->M;
@@ -1567,7 +1564,6 @@ namespace {
 int fine_source(pit_context* ctx, double* out, int first, int count, cudaStream_t st) {
   const int skip = first == 0 ? 1 : 0;
   if (count - skip <= 0) return PIT_OK;
-  Role& R = ctx->role[PIT_FINE];
   SlabArgs A{};
   A.mode = kPropagate;
   bind_status(ctx, &A);
