@@ -81,6 +81,7 @@ __device__ __forceinline__ StepLane step_lane(const StepParams& P,
   StepLane L;
   L.ppos = S::NSEG > 1 ? P.ppos[tid] : 0.0;
   L.qpos = S::NSEG > 1 ? P.qpos[tid] : 0.0;
+  L.zt = (P.narrow && tid < 32 && tid * S::CH < P.K0) ? P.zt[tid] : 0.0;
   const int lane = tid & 31;
 #pragma unroll
   for (int st = 0; st < 5; ++st) {

@@ -145,6 +145,7 @@ __device__ __forceinline__ void init_step_shared(const StepParams& P,
 // carry weights here instead of re-reading them from shared memory each step.
 struct StepLane {
   double ppos, qpos;
+  double zt;  // narrow corner: zc_0 nl^(t*CH) of this thread (0 outside warp 0 / beyond K0)
   double cf[5], cb[5], plane, qlane;
 };
 
@@ -343,7 +344,7 @@ __device__ __forceinline__ void be_solve(double (&y)[S::NC][S::SUB], const StepP
     if (warp == 0) {
       const double cc = P.gneg * __shfl_sync(kFull, y[0][0], 0);
       if (tid * S::CH < P.K0) {
-        const double a = cc * P.zt[tid];
+        const double a = cc * L.zt;  // P.zt[tid], loaded once per kernel
 #pragma unroll
         for (int u = 0; u < NSUB; ++u) {
           if (u * SUB >= P.K0) break;  // warp-uniform: lane 0 has the lowest points

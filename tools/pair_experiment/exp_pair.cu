@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(S::T, 65536 / (S::T * (S::MPT > 32 ? 168 : PAI
     for (int j = 0; j < S::SUB; ++j) y[c][j] = src[S::point(tid, c, j)];
   __syncthreads();
   StepLane L{};
+  L.zt = (P.narrow && tid < 32 && tid * S::CH < P.K0) ? P.zt[tid] : 0.0;
   int cnt = 0;
 #ifdef PIT_PHASE_TIMING
   long long ph_acc[16] = {};
