@@ -62,6 +62,10 @@ struct SlabArgs {
   // written by CTA 0, counts in chunk 0), on which the D2H stream waits.
   const unsigned* in_ready;
   unsigned* out_done;
+  // host_out != nullptr (the caller's pinned output, mapped): instead of a
+  // D2H copy each CTA re-reads its finished block from L2 and streams it to
+  // host memory in coalesced 16-byte stores (host_out is block 0's address)
+  double* host_out;
   int chunk_blocks;
   int block_shift;
   unsigned long long* busy_ns;  // DevStatus::busy_ns (nullptr: not measured)

@@ -249,6 +249,18 @@ __device__ __forceinline__ void slab_epilogue(const double (&y)[S::NC][S::SUB], 
       for (int i = tid; i < M; i += S::T) A.out0[i] = A.rhs0[i] - A.L0[i];
     }
   }
+  if (A.host_out != nullptr) {
+    __syncthreads();  // the block's stores above are visible to the whole CTA
+    double* h = A.host_out + (size_t)(b + A.block_shift) * M;
+    if ((M & 1) == 0) {
+      for (int i = 2 * tid; i < M; i += 2 * S::T)
+        __stcs(reinterpret_cast<double2*>(h + i), __ldcg(reinterpret_cast<const double2*>(out + i)));
+    } else {
+      for (int i = tid; i < M; i += S::T) __stcs(h + i, __ldcg(out + i));
+    }
+    if (b == 0 && A.out0 != nullptr)
+      for (int i = tid; i < M; i += S::T) __stcs(A.host_out + i, __ldcg(A.out0 + i));
+  }
 }
 
 __device__ __forceinline__ long long global_ns() {

@@ -368,15 +368,21 @@ def _pinned(a):
     return t, t.numpy()
 
 
+@pytest.mark.parametrize("direct", ["1", "0"])
 @pytest.mark.parametrize("chunks", ["0", "1", "3", "64"])
-@pytest.mark.parametrize("name,slabs,pieces", [("c2", 40, "0"), ("c2", 37, "3"), ("c4", 33, "1")])
-def test_pipelined_host_apply_F_bitwise(name, slabs, pieces, chunks, monkeypatch):
-    # pit_apply_F on pinned host buffers overlaps the chunked H2D / D2H copies
-    # with K1 (stream memory operations + in-kernel chunk flags); the result
-    # is the sequential path's, bit for bit, for any chunking and scheduling
+@pytest.mark.parametrize("name,slabs,pieces,M", [("c2", 40, "0", None), ("c2", 37, "3", None),
+                                                 ("c4", 33, "1", None), ("c2", 35, "0", 1001)])
+def test_pipelined_host_apply_F_bitwise(name, slabs, pieces, M, chunks, direct, monkeypatch):
+    # pit_apply_F on pinned host buffers overlaps the chunked H2D copies with
+    # K1 (stream memory operations + in-kernel chunk flags) and returns the
+    # output either from the CTAs themselves (stores to the mapped host
+    # buffer, the default) or through chunked D2H copies (PIT_E2E_DIRECT=0);
+    # the result is the sequential path's, bit for bit, for any chunking and
+    # scheduling, even or odd M
     monkeypatch.setenv("PIT_E2E_CHUNKS", chunks)
     monkeypatch.setenv("PIT_PIECES", pieces)
-    p = configs.make(name, slabs=slabs)
+    monkeypatch.setenv("PIT_E2E_DIRECT", direct)
+    p = configs.make(name, slabs=slabs, M=M)
     rng = np.random.default_rng(21)
     L = rng.uniform(-1, 1, (p.N, p.M))
     tl, Lp = _pinned(L)

@@ -34,4 +34,14 @@ for chunks in (os.environ.get("CHUNKS", "16").split(",")):
     ctx.close(); ctx = api.BlockOperatorContext(p)
     f = lambda: lib.pit_apply_F(ctx.handle, _lib.dptr(Lp), _lib.dptr(Op), None)
     ms = t(f); print(f"pit_apply_F pinned chunks={chunks}: {ms:.3f} ms  {p.M*p.fine_steps*(p.N-1)/ms/1e9:.3e} gp-steps/s")
-f = lambda: api.apply_F(ctx, L)
+ref = Op.copy()
+for direct in ("1", "2"):
+    os.environ["PIT_E2E_DIRECT"] = direct
+    for chunks in (os.environ.get("CHUNKS", "16").split(",")):
+        os.environ["PIT_E2E_CHUNKS"] = chunks
+        ctx.close(); ctx = api.BlockOperatorContext(p)
+        Op[:] = 0
+        f = lambda: lib.pit_apply_F(ctx.handle, _lib.dptr(Lp), _lib.dptr(Op), None)
+        ms = t(f)
+        print(f"pit_apply_F direct={direct} chunks={chunks}: {ms:.3f} ms  {p.M*p.fine_steps*(p.N-1)/ms/1e9:.3e} gp-steps/s  same={np.array_equal(Op, ref)}")
+
