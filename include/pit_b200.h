@@ -234,8 +234,10 @@ int pit_coarse_iterations(const pit_context* ctx, int64_t* out);
  * whose parallel_efficiency = fine_busy_ms / (slots * fine_parallel_ms). */
 int pit_context_slots(const pit_context* ctx, int* slots);
 /* Page-locked host buffers (cudaMallocHost): host block vectors here take
- * pit_apply_F's overlapped copy path (staging for C++ bindings whose own
- * storage is pageable, e.g. the reference's BlockVector). */
+ * pit_apply_F's overlapped path — the input goes up in chunks while the
+ * kernel already runs, the output is stored into the (device-mapped) buffer
+ * by the kernel itself (staging for C++ bindings whose own storage is
+ * pageable, e.g. the reference's BlockVector). */
 int pit_host_alloc(size_t bytes, void** out);
 int pit_host_free(void* p);
 /* Coefficients for role PIT_FINE / PIT_COARSE (no device needed). */
