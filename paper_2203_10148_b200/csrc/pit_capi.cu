@@ -1862,6 +1862,15 @@ int validate_cfg(const pit_solver_config* cfg) {
 bool gf_overlap_ok(pit_context* ctx) {
   if (ctx->gf_overlap < 0) {
     const char* e = std::getenv("PIT_GF_OVERLAP");
+    if (ctx->dim == 2 && !ctx->be2) {
+      // config 5 (K4 clusters in slab order, many waves; K5 on its own
+      // cluster): worth it once the batch is more than two waves of clusters
+      const int sms = ctx->sms;
+      const int forced = e ? std::atoi(e) : -1;
+      ctx->gf_overlap = ctx->N >= 3 && forced != 0 &&
+                        (forced == 1 || (long long)(ctx->N - 1) * ctx->lay2.cl > 2LL * sms);
+      return ctx->gf_overlap == 1;
+    }
     ctx->gf_overlap = ctx->dim == 1 && !ctx->be2 && ctx->M % 16 == 0 && ctx->M >= 1024 &&
                       ctx->N >= 3 && ctx->role[PIT_COARSE].nseg == 1 &&
                       ctx->role[PIT_COARSE].mpt % 2 == 0 && !(e && std::atoi(e) == 0);
@@ -1917,8 +1926,10 @@ void spans_collect(pit_context* ctx, pit_run_stats* st) {
   ctx->ev_used = 0;
 }
 
+// mode kApplyF: out = G^-1 (F x), F x staged in tmp; mode kResidual:
+// out = G^-1 (rhs - F x) (preconditioned_residual), in place when tmp == out.
 int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_run_stats* st,
-                        bool deferred = false) {
+                        bool deferred = false, int mode = kApplyF, const double* rhs = nullptr) {
   pit_context* ctx = R.ctx;
   const size_t M = ctx->M;
   if (!ctx->d_ready) {
@@ -1934,6 +1945,42 @@ int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_r
   const auto t0 = Clock::now();
   CUDA_TRY(cudaEventRecord(ctx->ev_gf[0], R.st));  // x ready, tmp and out free
   CUDA_TRY(cudaStreamWaitEvent(ctx->gf_stream, ctx->ev_gf[0], 0));
+  SweepArgs A{};
+  bind_status(ctx, &A);
+  A.start = tmp;  // V_0
+  A.W0 = tmp == out ? nullptr : out;  // W_0 = V_0
+  A.V = tmp + M;
+  A.W = out + M;
+  A.count = R.count - 1;
+  A.slab0 = 0;
+  A.ready = ctx->d_ready;
+  A.epoch = epoch;
+  A.ready_shift = 1;
+  A.skip = ctx->skip;
+  auto launch_coarse = [&]() -> int {
+    if (deferred)
+      PIT_TRY(span_begin(ctx, PIT_COARSE, ctx->gf_stream));
+    else
+      CUDA_TRY(cudaEventRecord(ctx->ev_gf[3], ctx->gf_stream));
+    if (ctx->dim == 2) {
+      CUDA_TRY(launch_cg_sweep2d(cg2_params(ctx), A, ctx->d_cg_iters, ctx->gf_stream));
+      return deferred ? span_end(ctx, ctx->gf_stream) : PIT_OK;
+    }
+    const Role& Rc = ctx->role[PIT_COARSE];
+    const cudaError_t le = launch_sweep(Rc.mpt, Rc.nsub, Rc.nseg, Rc.warps, false, Rc.P, A,
+                                        ctx->gf_stream);
+    if (le == cudaErrorNotSupported) {
+      // this layout / alignment has no I/O-warp sweep: serial from now on
+      cudaGetLastError();
+      ctx->gf_overlap = 0;
+      CUDA_TRY(cudaStreamWaitEvent(ctx->gf_stream, ctx->ev_gf[2], 0));
+      PIT_TRY(run_sweep(ctx, PIT_COARSE, false, tmp, nullptr, out, 0, R.count, true,
+                        ctx->gf_stream));
+    } else {
+      CUDA_TRY(le);
+    }
+    return deferred ? span_end(ctx, ctx->gf_stream) : PIT_OK;
+  };
   if (deferred)
     PIT_TRY(span_begin(ctx, PIT_FINE, R.st));
   else
@@ -1943,42 +1990,19 @@ int apply_GF_overlapped(Run& R, const double* x, double* tmp, double* out, pit_r
   // every block back to the last piece round (c2 TTT 39.0 vs 42.4 ms)
   const int saved_pieces = ctx->pieces;
   if (ctx->pieces == 0) ctx->pieces = 1;
-  const int rc1 = run_slab_batch(ctx, kApplyF, x, nullptr, nullptr, tmp, 0, R.count, R.st,
+  const int rc1 = run_slab_batch(ctx, mode, x, nullptr, rhs, tmp, 0, R.count, R.st,
                                  nullptr, nullptr, 0, ctx->d_ready, epoch, 1);
   ctx->pieces = saved_pieces;
   PIT_TRY(rc1);
   if (deferred) PIT_TRY(span_end(ctx, R.st));
   CUDA_TRY(cudaEventRecord(ctx->ev_gf[2], R.st));
-  SweepArgs A{};
-  bind_status(ctx, &A);
-  A.start = tmp;  // V_0
-  A.W0 = out;     // W_0 = V_0
-  A.V = tmp + M;
-  A.W = out + M;
-  A.count = R.count - 1;
-  A.slab0 = 0;
-  A.ready = ctx->d_ready;
-  A.epoch = epoch;
-  A.ready_shift = 1;
-  A.skip = ctx->skip;
-  if (deferred)
-    PIT_TRY(span_begin(ctx, PIT_COARSE, ctx->gf_stream));
-  else
-    CUDA_TRY(cudaEventRecord(ctx->ev_gf[3], ctx->gf_stream));
-  const Role& Rc = ctx->role[PIT_COARSE];
-  const cudaError_t le = launch_sweep(Rc.mpt, Rc.nsub, Rc.nseg, Rc.warps, false, Rc.P, A,
-                                      ctx->gf_stream);
-  if (le == cudaErrorNotSupported) {
-    // this layout / alignment has no I/O-warp sweep: serial from now on
-    cudaGetLastError();
-    ctx->gf_overlap = 0;
-    CUDA_TRY(cudaStreamWaitEvent(ctx->gf_stream, ctx->ev_gf[2], 0));
-    PIT_TRY(run_sweep(ctx, PIT_COARSE, false, tmp, nullptr, out, 0, R.count, true,
-                      ctx->gf_stream));
-  } else {
-    CUDA_TRY(le);
-  }
-  if (deferred) PIT_TRY(span_end(ctx, ctx->gf_stream));
+  // The sweep is launched after the fine batch in 1D and 2D alike: a first
+  // launch of a kernel may wait for outstanding work (lazy module loading),
+  // and the batch never waits on the sweep, so this order cannot deadlock.
+  // Config 5: K5's cluster (high-priority stream) gets its SMs as K4's first
+  // wave of clusters retires, then follows K4 block by block (it needs V_b
+  // only after slab b's CG solves).
+  PIT_TRY(launch_coarse());
   CUDA_TRY(cudaEventRecord(ctx->ev_gf[4], ctx->gf_stream));
   CUDA_TRY(cudaStreamWaitEvent(R.st, ctx->ev_gf[4], 0));
   if (deferred) return PIT_OK;
@@ -2004,6 +2028,8 @@ int apply_GF(Run& R, const double* x, double* tmp, double* out, pit_run_stats* s
 // preconditioned_residual (solvers.cpp:66-71): G^-1 (rhs - F lam)
 int precond_residual(Run& R, const double* lam, const double* rhs, double* out,
                      pit_run_stats* st) {
+  if (!R.comm && gf_overlap_ok(R.ctx))
+    return apply_GF_overlapped(R, lam, out, out, st, false, kResidual, rhs);
   PIT_TRY(run_fine(R, kResidual, lam, rhs, out, st));
   return run_chain(R, PIT_COARSE, false, out, out, true, st);
 }

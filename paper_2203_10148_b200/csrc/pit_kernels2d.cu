@@ -40,6 +40,32 @@ __device__ __forceinline__ void cl_sync() {
   cl_wait();
 }
 
+// G^-1 F overlap (SlabArgs::ready / SweepArgs::ready): block flags written by
+// K4's clusters and read by the concurrently running K5
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// one thread: spin until *flag == epoch; never hang the device on a lost
+// producer — give up after 20 s and report the slab as failed
+__device__ __noinline__ void wait_block_ready(const int* flag, int epoch, int* status, int slab) {
+  long long t0 = -1;
+  while (ld_acquire_gpu(flag) != epoch) {
+    long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t0 < 0) t0 = now;
+    if (now - t0 > 20000000000LL) {
+      atomicMin(status, slab);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
 // y' = fma(ac, y, an * ((w + e) + (n + s)))
 __device__ __forceinline__ double ex_point(double ac, double an, double y, double w, double e,
                                            double n, double s) {
@@ -351,6 +377,18 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     atomicAdd(A.busy_ns, (unsigned long long)(t1 - tb0));
   }
+  if (A.ready != nullptr) {
+    // every CTA's output stores precede the cluster barrier (release /
+    // acquire at cluster scope), which precedes thread 0's release at gpu
+    // scope (cumulativity): the sweep's acquire of ready[g] sees the block
+    __threadfence();
+    cl_sync();
+    if (c == 0 && tid == 0) {
+      __threadfence();
+      st_release_gpu(A.ready + b + A.block_shift, A.epoch);
+      if (b == 0 && A.out0 != nullptr) st_release_gpu(A.ready, A.epoch);
+    }
+  }
 }
 
 template <class K>
@@ -507,8 +545,16 @@ __global__ void __launch_bounds__(256, 1)
   };
 
   double x[RM], r[RM], q[RM];
+  if (A.ready != nullptr) {  // the start block comes from the running fine batch
+    if (t == 0) wait_block_ready(A.ready + A.ready_shift - 1, A.epoch, A.status, A.slab0);
+    __syncthreads();
+  }
 #pragma unroll
-  for (int k = 0; k < RM; ++k) Bs[k * NT + t] = valid[k] ? A.start[gidx(k)] : 0.0;
+  for (int k = 0; k < RM; ++k) {
+    const double v = valid[k] ? A.start[gidx(k)] : 0.0;
+    Bs[k * NT + t] = v;
+    if (A.W0 != nullptr && valid[k]) A.W0[gidx(k)] = v;  // W_0 = V_0 (block_system.cpp:181)
+  }
 
   long long total_it = 0;
 #ifdef PIT_PHASE_TIMING
@@ -661,6 +707,12 @@ __global__ void __launch_bounds__(256, 1)
     }
     const double* V = A.V ? A.V + (size_t)s * m * m : nullptr;
     double* Wb = A.W + (size_t)s * m * m;
+    if (A.ready != nullptr && V != nullptr) {
+      // V_s is needed only now, after the slab's CG solves: the wait hides
+      // behind them whenever the fine batch is ahead of the sweep
+      if (t == 0) wait_block_ready(A.ready + s + A.ready_shift, A.epoch, A.status, slab);
+      __syncthreads();
+    }
 #pragma unroll
     for (int k = 0; k < RM; ++k) {
       const double v = valid[k] ? (V ? x[k] + V[gidx(k)] : x[k]) : 0.0;

@@ -55,11 +55,39 @@ def test_overlapped_apply_GF_repeatable(monkeypatch):
     monkeypatch.setenv("PIT_GF_OVERLAP", "1")
     p = configs.make("c2", slabs=40)
     p.fine_steps = 60
-    r = OracleProblem(p).solve(1e-10)
+    o = OracleProblem(p)
+    r = o.solve(1e-10)
+    L = np.random.default_rng(8).uniform(-1, 1, (p.N, p.M))
+    rhs = o.assemble_rhs()
+    pr = o.preconditioned_residual(L, rhs)
     with api.BlockOperatorContext(p) as ctx:
         for _ in range(8):
             s = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
             assert np.array_equal(s.solution, r["lam"])
+            # G^-1 (rhs - F lam) takes the same overlapped path, in place
+            assert np.array_equal(api.preconditioned_residual(ctx, L, rhs), pr)
+
+
+@pytest.mark.parametrize("m,slabs,fs", [(48, 12, 128), (256, 6, 64)])
+def test_overlapped_apply_GF_2d_bitwise_and_repeatable(m, slabs, fs, monkeypatch):
+    # config 5: K5's cluster follows K4's clusters block by block through the
+    # ready flags (engages by itself from two waves of clusters; forced here)
+    monkeypatch.setenv("PIT_GF_OVERLAP", "1")
+    p = configs.make("c5", slabs=slabs, M=m)
+    p.fine_steps = fs
+    p.T = p.N * fs * (p.spacing ** 2 / 8.0)
+    o = OracleProblem(p)
+    r = o.solve(1e-10)
+    L = np.random.default_rng(9).uniform(-1, 1, (p.N, p.M))
+    rhs = o.assemble_rhs()
+    pr = o.preconditioned_residual(L, rhs)
+    with api.BlockOperatorContext(p) as ctx:
+        for _ in range(4):
+            s = api.pitsbicg_solve(ctx, api.SolverConfig(tolerance=1e-10))
+            assert [(x.k, x.residual_norm) for x in s.history.records] == \
+                [(a[0], a[1]) for a in r["rows"]]
+            assert np.array_equal(s.solution, r["lam"])
+            assert np.array_equal(api.preconditioned_residual(ctx, L, rhs), pr)
 
 
 def test_cluster_kernels_repeatable():
